@@ -1,0 +1,211 @@
+/*
+ * rte_b200.h -- drop-in C-ABI for the batched parametric source-iteration hot
+ * path of arxiv 2402.10488 (ROM-enhanced SI with synthetic acceleration),
+ * implemented with hand-written sm_100a CUDA kernels (librte_b200.so).
+ *
+ * The reference exposes this path as a C++ class API (namespace rte, see
+ * SURVEY.md s8(b)); every entry point below replaces one reference call for a
+ * whole BATCH of parameter samples mu_0..mu_{S-1} at once.  The replaced
+ * reference interface is cited per function (paths relative to
+ * /root/reference/proj/core/).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no exceptions cross the ABI.  Every
+ *     function returns RTE_OK (0) or an error code; rte_last_error() gives the
+ *     message.  RTE_ERR_INVALID maps to the reference's std::invalid_argument,
+ *     RTE_ERR_RUNTIME to std::runtime_error (e.g. singular reduced operator in
+ *     romig, strategies.cpp:11-16).  Non-convergence is NOT an error: it is
+ *     reported per sample (rte_si_report.converged = 0), as in sisa.cpp:30-47.
+ *   - "_dev" pointers are device memory on the context's device, fp64, one
+ *     contiguous block per sample: x[s * n_dof + cell * n_local + local]
+ *     (the reference's per-sample DOF layout, dg_space.hpp:24).  Kinetic
+ *     vectors are direction-major per sample: f[(s * n_dirs + j) * n_dof + i]
+ *     (transport_system.hpp:73-89).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  Calls are stream-ordered; only rte_si_solve and the rte_*_host
+ *     convenience calls synchronize.
+ *   - One context per host thread at a time; contexts are independent.
+ */
+#ifndef RTE_B200_H_
+#define RTE_B200_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rte_ctx rte_ctx; /* opaque: one problem batch on one device */
+
+enum rte_status {
+  RTE_OK = 0,
+  RTE_ERR_INVALID = 1,     /* bad argument (reference: std::invalid_argument) */
+  RTE_ERR_RUNTIME = 2,     /* numerical/runtime failure (std::runtime_error) */
+  RTE_ERR_CUDA = 3,        /* CUDA error */
+  RTE_ERR_UNSUPPORTED = 4  /* valid request outside what this build implements */
+};
+
+enum rte_geometry { RTE_SLAB1D = 0, RTE_XY2D = 1 };
+
+/* Problem batch.  Replaces TransportSystem(problem, mesh, space, quad, mu)
+ * (transport_system.hpp:32-34, ctor transport_system.cpp:82-109) for S
+ * parameter values.  The coefficient closures of ProblemDefinition are given
+ * already integrated into per-cell mass blocks (the reference's
+ * build_masses, transport_system.cpp:111-140; see rte_weighted_mass below).
+ * All pointers are host memory and are copied. */
+typedef struct rte_problem {
+  int geometry;          /* RTE_SLAB1D or RTE_XY2D */
+  int nx, ny;            /* cells (ny ignored for slab) */
+  const double* bounds;  /* slab: nx+1 strictly increasing boundaries (Mesh::slab) */
+  double x0, x1, y0, y1; /* xy: uniform grid extents (Mesh::rect_uniform) */
+  int n_dirs;
+  const double* dirs;    /* [n_dirs][3] unit vectors (vx, vy, vz) */
+  const double* weights; /* [n_dirs], normalised (sum 1) */
+  double inflow[4];      /* isotropic inflow: left, right, bottom, top */
+  int n_samples;         /* S >= 1 */
+  int block;             /* 1: per-cell scalar sigma (block = sigma * I);
+                            n_local^2: full per-cell blocks (slab only) */
+  const double* mt;      /* [S][cells][block] total-collision mass blocks */
+  const double* ms;      /* [S][cells][block] scattering mass blocks */
+  const double* source;  /* [S or 1][n_dof] volumetric source load vector G */
+  int source_shared;     /* 1: one G for all samples */
+} rte_problem;
+
+/* Affine decomposition sigma(x; mu) = sum_k psi_k(mu) w_k(x) (problem.hpp:
+ * 24-29) used by the kinetic term operators (apply_term_kinetic,
+ * transport_system.cpp:560-596) and the reduced models
+ * (ReducedModel::assemble, reduced_model.cpp:32-39). */
+typedef struct rte_affine {
+  int k_terms;
+  const double* term_mt; /* [K][cells][block] per-term total mass blocks */
+  const double* term_ms; /* [K][cells][block] per-term scattering blocks */
+  const double* psi;     /* [S][K], psi[s][0] must be 1 */
+} rte_affine;
+
+/* Online reduced model (ReducedModel, reduced_model.hpp:19-44). Host memory,
+ * column-major like the reference's Eigen storage. */
+typedef struct rte_rom {
+  int rank;              /* r */
+  int k_affine;          /* K */
+  const double* u_rho;   /* [r][n_dof] column-major n_dof x r */
+  const double* u_iso;   /* [r][n_dof] column-major n_dof x r */
+  const double* a_r;     /* [K][r][r] column-major r x r */
+  const double* b_r;     /* [r] */
+  double eps_pod;
+  double eps_train;
+} rte_rom;
+
+enum rte_method {
+  RTE_SI = 0,     /* plain source iteration (strategy == nullptr) */
+  RTE_DSA = 1,    /* DsaStrategy (solvers.hpp:54-65) */
+  RTE_ROMSA = 2,  /* RomsaStrategy (strategies.hpp:25-46) on the correction model */
+  RTE_ROMSAD = 3, /* RomsadStrategy (strategies.hpp:48-67) */
+  RTE_ROMIG = 4   /* romig initial guess (strategies.cpp:8-28) + DSA */
+};
+
+enum rte_norm { RTE_NORM_ABS = 0, RTE_NORM_REL = 1 };
+
+typedef struct rte_si_config {
+  int method;          /* rte_method */
+  double eps;          /* stop tolerance (SolveConfig::eps_sisa) */
+  int norm;            /* RTE_NORM_ABS: ||rho*-rho||_inf < eps (sisa.cpp:123);
+                          RTE_NORM_REL: ||rho*-rho||_inf / ||rho*||_inf < eps */
+  int max_iters;       /* SolveConfig::max_iters */
+  int fixed_iters;     /* > 0: run exactly this many iterations, no stop test */
+  int theta;           /* ROMSAD switch iteration budget */
+  double eps_romsad;   /* ROMSAD switching tolerance (romsad_tolerance) */
+  int use_guess;       /* 1: rho_dev holds the initial guess on entry */
+  int compute_residual;/* 1: final ||rho - L rho - bbar||_inf (one extra sweep) */
+  int check_every;     /* host polls the active count every k iterations (0 = 4) */
+} rte_si_config;
+
+typedef struct rte_si_report {
+  int converged;
+  int iterations;
+  long n_sweep;        /* reference accounting: 1 (bbar) + iterations */
+  int switch_iter;     /* ROMSAD: first iteration corrected by DSA (-1: none) */
+  int singular;        /* reduced operator singular at this mu */
+  double final_residual;
+  double last_change;
+} rte_si_report;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+int rte_create(const rte_problem* p, int device, rte_ctx** out);
+void rte_destroy(rte_ctx* ctx);
+const char* rte_last_error(const rte_ctx* ctx); /* ctx may be NULL (create failures) */
+long rte_n_dof(const rte_ctx* ctx);
+int rte_n_samples(const rte_ctx* ctx);
+int rte_n_slots(const rte_ctx* ctx); /* unique (vx,vy) sweep slots (transport_system.cpp:194-202) */
+
+/* ---- transport operator (batched over samples) -------------------------- */
+/* TransportSystem::apply_L (transport_system.cpp:393-404): out = L rho. */
+int rte_apply_L(rte_ctx* ctx, const double* rho_dev, double* out_dev, void* stream);
+/* TransportSystem::assemble_rhs (transport_system.cpp:406-418): bbar. */
+int rte_assemble_rhs(rte_ctx* ctx, double* bbar_dev, void* stream);
+/* Fused fixed-point map rho* = L rho + bbar in ONE sweep (identical in exact
+ * arithmetic to apply_L + assemble_rhs, sisa.cpp:118). */
+int rte_fixed_point(rte_ctx* ctx, const double* rho_dev, double* out_dev, void* stream);
+/* TransportSystem::sweep_direction (transport_system.cpp:366-371) for
+ * direction j of every sample: f = (D_j + Sigma_t)^{-1} rhs. */
+int rte_sweep_direction(rte_ctx* ctx, int j, const double* rhs_dev, double* f_dev, void* stream);
+/* TransportSystem::kinetic_sweep (transport_system.cpp:420-431). */
+int rte_kinetic_sweep(rte_ctx* ctx, const double* rho_dev, double* f_dev, void* stream);
+/* TransportSystem::density_of (transport_system.cpp:433-441). */
+int rte_density_of(rte_ctx* ctx, const double* f_dev, double* rho_dev, void* stream);
+/* TransportSystem::apply_Ms / apply_Mt (transport_system.cpp:373-391). */
+int rte_apply_Ms(rte_ctx* ctx, const double* x_dev, double* out_dev, void* stream);
+int rte_apply_Mt(rte_ctx* ctx, const double* x_dev, double* out_dev, void* stream);
+
+/* ---- affine terms / kinetic operators ---------------------------------- */
+int rte_set_affine(rte_ctx* ctx, const rte_affine* aff);
+/* TransportSystem::apply_term_kinetic (transport_system.cpp:560-596) for
+ * sample 0's discretization (term operators are parameter independent);
+ * u/out: [n_cols][n_dirs * n_dof]. */
+int rte_apply_term_kinetic(rte_ctx* ctx, int k, int n_cols, const double* u_dev, double* out_dev,
+                           void* stream);
+
+/* ---- DSA (dsa.cpp) ----------------------------------------------------- */
+/* DsaOperator ctor (dsa.cpp:154-258): assemble + factor per sample. */
+int rte_dsa_setup(rte_ctx* ctx, void* stream);
+/* DsaOperator::solve_density (dsa.cpp:264-273). */
+int rte_dsa_solve_density(rte_ctx* ctx, const double* rhs_dev, double* out_dev, void* stream);
+/* DsaOperator::correct (dsa.cpp:275-277): C * Ms * delta. */
+int rte_dsa_correct(rte_ctx* ctx, const double* delta_dev, double* out_dev, void* stream);
+/* DsaOperator::coupled_dim (dsa.hpp:48). */
+long rte_dsa_coupled_dim(const rte_ctx* ctx);
+
+/* ---- reduced models (reduced_model.cpp, strategies.cpp) ----------------- */
+/* which: 0 = primary model (ROMIG), 1 = correction model (ROMSA/ROMSAD).
+ * Requires rte_set_affine (psi per sample). */
+int rte_rom_load(rte_ctx* ctx, int which, const rte_rom* rom);
+/* romig (strategies.cpp:8-28) for every sample: rho0 = U_rho A_r(mu)^{-1} b_r.
+ * status_host[s] = 0 ok, 1 singular, 2 Galerkin residual check failed. */
+int rte_romig(rte_ctx* ctx, double* rho0_dev, int* status_host, void* stream);
+
+/* ---- source iteration (sisa.cpp:14-54) ----------------------------------- */
+/* Batched sisa_solve: all samples iterate on the device; converged samples
+ * are masked.  rho_dev [S][n_dof] holds the guess on entry (use_guess) and
+ * the solution on exit.  reports_host[S]; history_host [S][max_iters] (change
+ * per iteration, may be NULL); log_host [S][max_iters] correction kinds
+ * 'D','R','S' or 0 (may be NULL). */
+int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg, double* rho_dev, rte_si_report* reports_host,
+                 double* history_host, char* log_host);
+
+/* ---- host-side discretization helpers (problem setup) ------------------- */
+/* quadrature.cpp:8-39: n-point Gauss-Legendre nodes/weights on [-1,1]. */
+int rte_gauss_legendre_nodes(int n, double* x, double* w);
+/* weighted_mass (transport_system.cpp:17-55) for every cell: wvals holds the
+ * coefficient values at the cell points returned by rte_cell_points;
+ * out [cells][n_local^2]. */
+int rte_cell_points(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0,
+                    double y1, int nq, double* px, double* py);
+int rte_weighted_mass(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0,
+                      double y1, int nq, const double* wvals, double* out);
+/* project (dg_space.cpp:31-71) from values at the cell points. */
+int rte_project(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0,
+                double y1, int nq, const double* fvals, double* out);
+/* cases.cpp:11-13: n unit draws (gen() >> 11) * 2^-53 of std::mt19937_64(seed). */
+int rte_unit_draws(unsigned long long seed, long n, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RTE_B200_H_ */

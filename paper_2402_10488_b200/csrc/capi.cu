@@ -1,0 +1,727 @@
+// capi.cu -- the C-ABI of include/rte_b200.h: context setup, transport
+// operator entry points, the batched device-resident source-iteration driver
+// (sisa.cpp:14-54 for S samples at once) and small bookkeeping kernels.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <random>
+#include <utility>
+
+#include "rte_internal.cuh"
+
+using namespace rte;
+
+namespace rte {
+void dsa_apply(rte_ctx* ctx, const double* rhs, double* out, const int* kind, int apply_ms, cudaStream_t st);
+int sweep2d_dirs_per_cta();
+}
+
+rte_ctx::~rte_ctx() {
+  dsa_destroy(dsa);
+  rom_destroy(rom[0]);
+  rom_destroy(rom[1]);
+}
+
+namespace {
+
+thread_local std::string g_create_err;
+
+template <typename F>
+int guarded(rte_ctx* ctx, F&& f) {
+  try {
+    f();
+    if (ctx) ctx->err.clear();
+    return RTE_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->err = e.what();
+    else g_create_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    else g_create_err = e.what();
+    return RTE_ERR_RUNTIME;
+  }
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// small kernels
+
+__global__ void apply_block_kernel(int S, int ncells, int nl, int block, const double* __restrict__ m,
+                                   const double* __restrict__ x, double* __restrict__ out) {
+  const long nd = (long)ncells * nl;
+  const long total = (long)S * nd;
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
+    const long s = t / nd, i = t - s * nd;
+    const long c = i / nl;
+    const int r = (int)(i - c * nl);
+    if (block == 1) {
+      out[t] = m[s * ncells + c] * x[t];
+    } else {
+      const double* mb = m + (s * ncells + c) * block + (long)r * nl;
+      const double* xs = x + s * nd + c * nl;
+      double v = mb[0] * xs[0];
+      for (int k = 1; k < nl; ++k) v += mb[k] * xs[k];
+      out[t] = v;
+    }
+  }
+}
+
+__global__ void density_kernel(int S, int nv, long nd, const double* __restrict__ w, const double* __restrict__ f,
+                               double* __restrict__ rho) {
+  const long total = (long)S * nd;
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
+    const long s = t / nd, i = t - s * nd;
+    double v = 0.0;
+    for (int j = 0; j < nv; ++j) v = v + w[j] * f[(s * nv + j) * nd + i];
+    rho[t] = v;
+  }
+}
+
+__device__ __forceinline__ double bits2d(unsigned long long b) { return __longlong_as_double((long long)b); }
+
+__global__ void si_decide_kernel(int S, SiState st, int l, rte_si_config cfg) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  if (!st.active[s]) {
+    st.kind[s] = KIND_IDLE;
+    return;
+  }
+  const double ch = bits2d(st.change_bits[2 * s]);
+  const double rm = bits2d(st.change_bits[2 * s + 1]);
+  double chn = ch;
+  if (cfg.norm == RTE_NORM_REL && rm > 0) chn = ch / rm;
+  st.history[(long)s * cfg.max_iters + l - 1] = chn;
+  st.iters[s] = l;
+  st.last_change[s] = chn;
+  if (cfg.fixed_iters <= 0 && chn < cfg.eps) {  // sisa.cpp:123-127
+    st.converged[s] = 1;
+    st.active[s] = 0;
+    st.kind[s] = KIND_ACCEPT;
+    return;
+  }
+  int kind = KIND_ACCEPT;
+  char lg = 0;
+  switch (cfg.method) {
+    case RTE_SI:
+      break;
+    case RTE_DSA:
+    case RTE_ROMIG:
+      kind = KIND_DSA;
+      lg = 'D';
+      break;
+    case RTE_ROMSA:
+      kind = st.singular[s] ? KIND_SINGULAR : KIND_ROMSA;
+      lg = st.singular[s] ? 'S' : 'R';
+      break;
+    case RTE_ROMSAD:  // strategies.cpp:67-76 (monotone switch)
+      if (!st.switched[s] && l <= cfg.theta && ch >= cfg.eps_romsad) {
+        kind = KIND_ROMSA;
+        lg = 'R';
+      } else {
+        st.switched[s] = 1;
+        kind = KIND_DSA;
+        lg = 'D';
+      }
+      break;
+  }
+  if (kind == KIND_DSA && st.switch_iter[s] < 0) st.switch_iter[s] = l;
+  st.kind[s] = kind;
+  if (lg) st.log[(long)s * cfg.max_iters + l - 1] = lg;
+  const int limit = cfg.fixed_iters > 0 ? cfg.fixed_iters : cfg.max_iters;
+  if (l >= limit)
+    st.active[s] = 0;
+  else
+    atomicAdd(st.n_active, 1);
+}
+
+__global__ void si_finalize_kernel(int S, long nd, const int* __restrict__ kind, const double* __restrict__ rho_star,
+                                   const double* __restrict__ corr, double* __restrict__ rho) {
+  const int s = blockIdx.y;
+  const int k = kind[s];
+  if (k == KIND_IDLE) return;
+  const bool add = (k == KIND_DSA || k == KIND_ROMSA);
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += (long)gridDim.x * blockDim.x) {
+    const long t = (long)s * nd + i;
+    rho[t] = add ? rho_star[t] + corr[t] : rho_star[t];
+  }
+}
+
+__global__ void init_state_kernel(int S, SiState st, const int* sing, int method) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  st.active[s] = 1;
+  st.iters[s] = 0;
+  st.converged[s] = 0;
+  st.switch_iter[s] = -1;
+  st.singular[s] = sing ? sing[s] : 0;
+  st.switched[s] = (method == RTE_ROMSAD && sing && sing[s]) ? 1 : 0;
+  st.last_change[s] = 0.0;
+}
+
+// Slot tables (transport_system.cpp:194-202: slots keyed by (vx, vy)).
+void build_slots(rte_ctx* c) {
+  std::map<std::pair<double, double>, int> slot_of;
+  c->dir_slot.assign(c->nv, -1);
+  c->slot_vx.clear();
+  c->slot_vy.clear();
+  c->slot_w.clear();
+  for (int j = 0; j < c->nv; ++j) {
+    const auto key = std::make_pair(c->vx[j], c->geom == RTE_XY2D ? c->vy[j] : 0.0);
+    auto it = slot_of.find(key);
+    if (it == slot_of.end()) {
+      it = slot_of.emplace(key, (int)slot_of.size()).first;
+      c->slot_vx.push_back(key.first);
+      c->slot_vy.push_back(key.second);
+      c->slot_w.push_back(0.0);
+    }
+    c->dir_slot[j] = it->second;
+    c->slot_w[it->second] += c->w[j];
+  }
+  c->nslots = (int)c->slot_vx.size();
+  for (int q = 0; q < 4; ++q) c->q_slots[q].clear();
+  for (int k = 0; k < c->nslots; ++k) {
+    const int q = (c->slot_vx[k] > 0 ? 0 : 1) + 2 * (c->slot_vy[k] > 0 ? 0 : 1);
+    c->q_slots[q].push_back(k);
+  }
+  for (int q = 0; q < 4; ++q) c->q_count[q] = (int)c->q_slots[q].size();
+}
+
+// Canonical slot constants; `single` >= 0 restricts to one slot with weight 1.
+std::vector<Slot2D> slot_table(const rte_ctx* c, int dpl, int groups, int nq_pad, int single) {
+  std::vector<Slot2D> t((size_t)4 * nq_pad);
+  for (auto& e : t) e = Slot2D{1.0, 1.0, 0.0, 0.0, 0.0};
+  const double hx = c->hx, hy = c->hy;
+  for (int q = 0; q < 4; ++q) {
+    int n = 0;
+    for (int k : c->q_slots[q]) {
+      if (single >= 0 && k != single) continue;
+      const double vx = c->slot_vx[k], vy = c->slot_vy[k];
+      Slot2D sl;
+      sl.a = std::fabs(vx) / hx;
+      sl.b = std::fabs(vy) / hy;
+      sl.w = single >= 0 ? 1.0 : c->slot_w[k];
+      // inflow ghost traces (transport_system.cpp:166-185), canonical basis
+      const double gx = vx > 0 ? c->inflow[0] : c->inflow[1];
+      const double gy = vy > 0 ? c->inflow[2] : c->inflow[3];
+      sl.bcx = std::fabs(vx) * gx * (1.0 / std::sqrt(hx)) * std::sqrt(hy);
+      sl.bcy = std::fabs(vy) * gy * (1.0 / std::sqrt(hy)) * std::sqrt(hx);
+      t[(size_t)q * nq_pad + n] = sl;
+      ++n;
+    }
+  }
+  (void)dpl;
+  (void)groups;
+  return t;
+}
+
+struct Plan2D {
+  int dpl, groups, nq_pad;
+};
+
+Plan2D plan2d(const rte_ctx* c, int single) {
+  int mq = 0;
+  for (int q = 0; q < 4; ++q) {
+    int n = single >= 0 ? 1 : c->q_count[q];
+    mq = std::max(mq, n);
+  }
+  const int nw = sweep2d_dirs_per_cta();
+  const int nbands = (c->ny + 31) / 32;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  Plan2D best{1, 1, 0};
+  for (int dpl : {8, 4, 2, 1}) {
+    const int groups = std::max(1, (mq + nw * dpl - 1) / (nw * dpl));
+    best = Plan2D{dpl, groups, groups * nw * dpl};
+    const long items = (long)nbands * c->S * 4 * groups;
+    if (items >= 4L * sms) break;
+  }
+  return best;
+}
+
+}  // namespace
+
+namespace rte {
+
+// mode: SrcMode bits.  2D: always through the band-wavefront kernel + the
+// fixed-order partial reduction.  rho_prev/delta/change_bits: SI epilogue.
+static void transport_apply_ex(rte_ctx* ctx, int mode, int single, const double* rho, double* out, const int* active,
+                               const double* rho_prev, double* delta, unsigned long long* change_bits,
+                               cudaStream_t st) {
+  if (ctx->geom == RTE_SLAB1D) {
+    Sweep1DArgs a{};
+    a.S = ctx->S;
+    a.N = ctx->ncells;
+    a.nv = ctx->nv;
+    a.ndof = ctx->ndof;
+    a.width = ctx->width.p;
+    a.vx = ctx->dvx.p;
+    a.w = ctx->dw.p;
+    a.block = ctx->block;
+    a.mt = ctx->mt.p;
+    a.ms = ctx->ms.p;
+    a.g = ctx->g.p;
+    a.g_shared = ctx->g_shared;
+    a.rho = rho;
+    a.inflow_l = ctx->inflow[0];
+    a.inflow_r = ctx->inflow[1];
+    a.mode = mode;
+    a.j_single = single;
+    a.out = single >= 0 ? nullptr : out;
+    a.fout = single >= 0 ? out : nullptr;
+    a.active = active;
+    a.rho_prev = rho_prev;
+    a.delta = delta;
+    a.change_bits = change_bits;
+    launch_sweep1d(a, st);
+    return;
+  }
+  const Plan2D pl = plan2d(ctx, single);
+  const int slot_single = single >= 0 ? ctx->dir_slot[single] : -1;
+  DBuf<Slot2D> tmp;
+  const Slot2D* dtab = nullptr;
+  if (single < 0) {
+    if (ctx->slot_tab_dpl != pl.dpl * 1000 + pl.groups) {
+      std::vector<Slot2D> tab = slot_table(ctx, pl.dpl, pl.groups, pl.nq_pad, -1);
+      ctx->slot_tab.upload(tab.data(), tab.size());
+      ctx->slot_tab_dpl = pl.dpl * 1000 + pl.groups;
+    }
+    dtab = ctx->slot_tab.p;
+  } else {
+    std::vector<Slot2D> tab = slot_table(ctx, pl.dpl, pl.groups, pl.nq_pad, slot_single);
+    tmp.upload(tab.data(), tab.size());
+    dtab = tmp.p;
+  }
+  const int nbands = (ctx->ny + 31) / 32;
+  const int nparts = 4 * pl.groups;
+  const int ndir_cta = pl.nq_pad / pl.groups;
+  ctx->ws_part.alloc((size_t)nparts * ctx->S * ctx->ndof);
+  ctx->ws_c.alloc((size_t)ctx->S * 4 * pl.groups * nbands * ctx->nx * ndir_cta * 2);
+  ctx->ws_sync.alloc(1 + (size_t)ctx->S * 4 * pl.groups * nbands);
+  ctx->ws_sync.zero(st);
+  Sweep2DArgs a{};
+  a.S = ctx->S;
+  a.nx = ctx->nx;
+  a.ny = ctx->ny;
+  a.slots = dtab;
+  a.nq_pad = pl.nq_pad;
+  a.groups = pl.groups;
+  a.sig_t = ctx->mt.p;
+  a.sig_s = ctx->ms.p;
+  a.g = ctx->g.p;
+  a.g_shared = ctx->g_shared;
+  a.rho = rho;
+  a.mode = mode;
+  a.part = ctx->ws_part.p;
+  a.ybuf = ctx->ws_c.p;
+  a.sync = ctx->ws_sync.p;
+  a.active = active;
+  launch_sweep2d(a, st);
+  launch_reduce_partials(ctx->S, ctx->ndof, nparts, ctx->ws_part.p, out, rho_prev, delta, change_bits, active, st);
+  // a temporary slot table must outlive the kernels queued above
+  if (single >= 0) RTE_CUDA(cudaStreamSynchronize(st));
+}
+
+void transport_apply(rte_ctx* ctx, int mode, const double* rho, double* out, const int* active,
+                     const double* rho_prev, double* delta, unsigned long long* change_bits, cudaStream_t st) {
+  transport_apply_ex(ctx, mode, -1, rho, out, active, rho_prev, delta, change_bits, st);
+}
+
+void launch_apply_block(int S, int ncells, int nl, int block, const double* m, const double* x, double* out,
+                        cudaStream_t st) {
+  const long total = (long)S * ncells * nl;
+  const int blocks = (int)std::min<long>((total + 255) / 256, 65535);
+  apply_block_kernel<<<blocks, 256, 0, st>>>(S, ncells, nl, block, m, x, out);
+  RTE_CUDA(cudaGetLastError());
+}
+
+void launch_density_of(int S, int nv, long nd, const double* w, const double* f, double* rho, cudaStream_t st) {
+  const long total = (long)S * nd;
+  const int blocks = (int)std::min<long>((total + 255) / 256, 65535);
+  density_kernel<<<blocks, 256, 0, st>>>(S, nv, nd, w, f, rho);
+  RTE_CUDA(cudaGetLastError());
+}
+
+}  // namespace rte
+
+// ===========================================================================
+extern "C" {
+
+int rte_create(const rte_problem* p, int device, rte_ctx** out) {
+  return guarded(nullptr, [&] {
+    RTE_REQUIRE(p && out, RTE_ERR_INVALID, "rte_create: null argument");
+    RTE_REQUIRE(p->geometry == RTE_SLAB1D || p->geometry == RTE_XY2D, RTE_ERR_INVALID, "rte_create: bad geometry");
+    RTE_REQUIRE(p->nx >= 1 && (p->geometry == RTE_SLAB1D || p->ny >= 1), RTE_ERR_INVALID, "invalid mesh");
+    RTE_REQUIRE(p->n_dirs >= 1 && p->dirs && p->weights, RTE_ERR_INVALID, "rte_create: empty quadrature");
+    RTE_REQUIRE(p->n_samples >= 1, RTE_ERR_INVALID, "rte_create: n_samples must be >= 1");
+    RTE_REQUIRE(p->mt && p->ms, RTE_ERR_INVALID, "rte_create: mass blocks missing");
+    auto* c = new rte_ctx();
+    std::unique_ptr<rte_ctx> hold(c);
+    c->device = device;
+    DeviceGuard dg(device);
+    c->geom = p->geometry;
+    c->nx = p->nx;
+    c->ny = p->geometry == RTE_SLAB1D ? 1 : p->ny;
+    c->ncells = c->nx * c->ny;
+    c->nl = p->geometry == RTE_SLAB1D ? 2 : 4;
+    c->ndof = (long)c->ncells * c->nl;
+    c->S = p->n_samples;
+    c->nv = p->n_dirs;
+    for (int j = 0; j < c->nv; ++j) {
+      c->vx.push_back(p->dirs[3 * j]);
+      c->vy.push_back(p->dirs[3 * j + 1]);
+      c->vz.push_back(p->dirs[3 * j + 2]);
+      c->w.push_back(p->weights[j]);
+    }
+    for (int k = 0; k < 4; ++k) c->inflow[k] = p->inflow[k];
+    c->block = p->block;
+    if (c->geom == RTE_SLAB1D) {
+      RTE_REQUIRE(p->bounds, RTE_ERR_INVALID, "slab mesh needs boundaries");
+      RTE_REQUIRE(c->block == 1 || c->block == 4, RTE_ERR_INVALID, "slab: block must be 1 or 4");
+      c->bounds.assign(p->bounds, p->bounds + c->nx + 1);
+      std::vector<double> wd(c->nx);
+      for (int i = 0; i < c->nx; ++i) {
+        RTE_REQUIRE(c->bounds[i] < c->bounds[i + 1], RTE_ERR_INVALID, "slab mesh boundaries must be strictly increasing");
+        wd[i] = c->bounds[i + 1] - c->bounds[i];
+      }
+      c->width.upload(wd.data(), wd.size());
+      c->dvx.upload(c->vx.data(), c->nv);
+      c->dw.upload(c->w.data(), c->nv);
+    } else {
+      RTE_REQUIRE(c->block == 1, RTE_ERR_UNSUPPORTED,
+                  "xy: only per-cell constant coefficients (block = 1) are implemented");
+      RTE_REQUIRE(p->x0 < p->x1 && p->y0 < p->y1, RTE_ERR_INVALID, "invalid rectangular mesh");
+      c->hx = (p->x1 - p->x0) / c->nx;
+      c->hy = (p->y1 - p->y0) / c->ny;
+    }
+    build_slots(c);
+    const size_t nblk = (size_t)c->S * c->ncells * c->block;
+    c->mt_h.assign(p->mt, p->mt + nblk);
+    c->ms_h.assign(p->ms, p->ms + nblk);
+    c->mt.upload(p->mt, nblk);
+    c->ms.upload(p->ms, nblk);
+    c->g_shared = p->source_shared ? 1 : 0;
+    const size_t ng = (size_t)(c->g_shared ? 1 : c->S) * c->ndof;
+    if (p->source) {
+      c->g.upload(p->source, ng);
+    } else {
+      std::vector<double> z(ng, 0.0);
+      c->g.upload(z.data(), ng);
+    }
+    RTE_CUDA(cudaDeviceSynchronize());
+    *out = hold.release();
+  });
+}
+
+void rte_destroy(rte_ctx* ctx) {
+  if (!ctx) return;
+  DeviceGuard dg(ctx->device);
+  delete ctx;
+}
+
+const char* rte_last_error(const rte_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+long rte_n_dof(const rte_ctx* ctx) { return ctx->ndof; }
+int rte_n_samples(const rte_ctx* ctx) { return ctx->S; }
+int rte_n_slots(const rte_ctx* ctx) { return ctx->nslots; }
+
+int rte_apply_L(rte_ctx* ctx, const double* rho, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    transport_apply(ctx, SRC_MS_RHO, rho, out, nullptr, nullptr, nullptr, nullptr, as_stream(stream));
+  });
+}
+
+int rte_assemble_rhs(rte_ctx* ctx, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    transport_apply(ctx, SRC_G | SRC_BC, ctx->g.p, out, nullptr, nullptr, nullptr, nullptr, as_stream(stream));
+  });
+}
+
+int rte_fixed_point(rte_ctx* ctx, const double* rho, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    transport_apply(ctx, SRC_MS_RHO | SRC_G | SRC_BC, rho, out, nullptr, nullptr, nullptr, nullptr,
+                    as_stream(stream));
+  });
+}
+
+int rte_sweep_direction(rte_ctx* ctx, int j, const double* rhs, double* f, void* stream) {
+  return guarded(ctx, [&] {
+    RTE_REQUIRE(j >= 0 && j < ctx->nv, RTE_ERR_INVALID, "sweep_direction: bad direction index");
+    DeviceGuard dg(ctx->device);
+    transport_apply_ex(ctx, SRC_RAW, j, rhs, f, nullptr, nullptr, nullptr, nullptr, as_stream(stream));
+  });
+}
+
+int rte_kinetic_sweep(rte_ctx* ctx, const double* rho, double* f, void* stream) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    if (ctx->geom == RTE_SLAB1D) {
+      Sweep1DArgs a{};
+      a.S = ctx->S;
+      a.N = ctx->ncells;
+      a.nv = ctx->nv;
+      a.ndof = ctx->ndof;
+      a.width = ctx->width.p;
+      a.vx = ctx->dvx.p;
+      a.w = ctx->dw.p;
+      a.block = ctx->block;
+      a.mt = ctx->mt.p;
+      a.ms = ctx->ms.p;
+      a.g = ctx->g.p;
+      a.g_shared = ctx->g_shared;
+      a.rho = rho;
+      a.inflow_l = ctx->inflow[0];
+      a.inflow_r = ctx->inflow[1];
+      a.mode = SRC_MS_RHO | SRC_G | SRC_BC;
+      a.j_single = -1;
+      a.fout = f;
+      launch_sweep1d(a, as_stream(stream));
+      return;
+    }
+    throw Error(RTE_ERR_UNSUPPORTED, "kinetic_sweep: xy geometry not implemented in this build");
+  });
+}
+
+int rte_density_of(rte_ctx* ctx, const double* f, double* rho, void* stream) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    DBuf<double> w;
+    w.upload(ctx->w.data(), ctx->nv);
+    launch_density_of(ctx->S, ctx->nv, ctx->ndof, w.p, f, rho, as_stream(stream));
+    RTE_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  });
+}
+
+int rte_apply_Ms(rte_ctx* ctx, const double* x, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    launch_apply_block(ctx->S, ctx->ncells, ctx->nl, ctx->block, ctx->ms.p, x, out, as_stream(stream));
+  });
+}
+
+int rte_apply_Mt(rte_ctx* ctx, const double* x, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    launch_apply_block(ctx->S, ctx->ncells, ctx->nl, ctx->block, ctx->mt.p, x, out, as_stream(stream));
+  });
+}
+
+int rte_set_affine(rte_ctx* ctx, const rte_affine* aff) {
+  return guarded(ctx, [&] {
+    RTE_REQUIRE(aff && aff->k_terms >= 1 && aff->psi, RTE_ERR_INVALID, "set_affine: bad arguments");
+    DeviceGuard dg(ctx->device);
+    for (int s = 0; s < ctx->S; ++s)
+      RTE_REQUIRE(aff->psi[(size_t)s * aff->k_terms] == 1.0, RTE_ERR_INVALID,
+                  "transport system: term 0 must be parameter independent (psi == 1)");
+    ctx->k_terms = aff->k_terms;
+    ctx->psi_h.assign(aff->psi, aff->psi + (size_t)ctx->S * aff->k_terms);
+    ctx->psi.upload(aff->psi, (size_t)ctx->S * aff->k_terms);
+    const size_t nb = (size_t)aff->k_terms * ctx->ncells * ctx->block;
+    if (aff->term_mt) ctx->term_mt.upload(aff->term_mt, nb);
+    if (aff->term_ms) ctx->term_ms.upload(aff->term_ms, nb);
+  });
+}
+
+int rte_apply_term_kinetic(rte_ctx* ctx, int, int, const double*, double*, void*) {
+  return guarded(ctx, [&] { throw Error(RTE_ERR_UNSUPPORTED, "apply_term_kinetic: not implemented in this build"); });
+}
+
+int rte_dsa_setup(rte_ctx* ctx, void* stream) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    dsa_setup(ctx, as_stream(stream));
+  });
+}
+
+int rte_dsa_solve_density(rte_ctx* ctx, const double* rhs, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    dsa_apply(ctx, rhs, out, nullptr, 0, as_stream(stream));
+  });
+}
+
+int rte_dsa_correct(rte_ctx* ctx, const double* delta, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    dsa_apply(ctx, delta, out, nullptr, 1, as_stream(stream));
+  });
+}
+
+long rte_dsa_coupled_dim(const rte_ctx* ctx) { return dsa_coupled_dim(ctx); }
+
+int rte_rom_load(rte_ctx* ctx, int which, const rte_rom* rom) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    rom_load(ctx, which, rom);
+  });
+}
+
+int rte_romig(rte_ctx* ctx, double* rho0, int* status_host, void* stream) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    DBuf<int> stat;
+    stat.alloc(ctx->S);
+    romig(ctx, rho0, stat.p, as_stream(stream));
+    if (status_host) RTE_CUDA(cudaMemcpy(status_host, stat.p, sizeof(int) * ctx->S, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_report* reports, double* history,
+                 char* log) {
+  return guarded(ctx, [&] {
+    RTE_REQUIRE(cfg_in && rho, RTE_ERR_INVALID, "si_solve: null argument");
+    DeviceGuard dg(ctx->device);
+    rte_si_config cfg = *cfg_in;
+    RTE_REQUIRE(cfg.max_iters >= 1, RTE_ERR_INVALID, "si_solve: max_iters must be >= 1");
+    if (cfg.fixed_iters > 0) cfg.max_iters = std::max(cfg.max_iters, cfg.fixed_iters);
+    const int every = cfg.check_every > 0 ? cfg.check_every : 4;
+    cudaStream_t st = nullptr;
+    const int S = ctx->S;
+    const long nd = ctx->ndof;
+    const bool need_dsa = cfg.method == RTE_DSA || cfg.method == RTE_ROMSAD || cfg.method == RTE_ROMIG;
+    const bool need_rom = cfg.method == RTE_ROMSA || cfg.method == RTE_ROMSAD;
+    if (need_dsa && !ctx->dsa) dsa_setup(ctx, st);
+    DBuf<int> ibuf;
+    ibuf.alloc((size_t)S * 8 + 1);
+    SiState sst{};
+    sst.active = ibuf.p;
+    sst.iters = ibuf.p + S;
+    sst.switched = ibuf.p + 2 * S;
+    sst.kind = ibuf.p + 3 * S;
+    sst.converged = ibuf.p + 4 * S;
+    sst.singular = ibuf.p + 5 * S;
+    sst.switch_iter = ibuf.p + 6 * S;
+    DBuf<int> sing;
+    if (need_rom) {
+      sing.alloc(S);
+      rom_setup(ctx, 1, sing.p, st);
+    }
+    sst.n_active = ibuf.p + 8 * S;
+    DBuf<double> hist, lastc;
+    hist.alloc((size_t)S * cfg.max_iters);
+    hist.zero(st);
+    lastc.alloc(S);
+    sst.history = hist.p;
+    sst.last_change = lastc.p;
+    DBuf<char> lg;
+    lg.alloc((size_t)S * cfg.max_iters);
+    RTE_CUDA(cudaMemsetAsync(lg.p, 0, (size_t)S * cfg.max_iters, st));
+    sst.log = lg.p;
+    DBuf<unsigned long long> bits;
+    bits.alloc((size_t)2 * S);
+    sst.change_bits = bits.p;
+    init_state_kernel<<<(S + 127) / 128, 128, 0, st>>>(S, sst, need_rom ? sing.p : nullptr, cfg.method);
+    RTE_CUDA(cudaGetLastError());
+
+    if (cfg.method == RTE_ROMIG) {
+      DBuf<int> stat;
+      stat.alloc(S);
+      romig(ctx, rho, stat.p, st);
+      std::vector<int> hs(S);
+      RTE_CUDA(cudaMemcpy(hs.data(), stat.p, sizeof(int) * S, cudaMemcpyDeviceToHost));
+      for (int s = 0; s < S; ++s) {
+        if (hs[s] == 1)
+          throw Error(RTE_ERR_RUNTIME, "reduced initial guess: reduced operator is singular at sample " +
+                                           std::to_string(s));
+        if (hs[s] == 2)
+          throw Error(RTE_ERR_RUNTIME, "reduced initial guess: Galerkin residual check failed at sample " +
+                                           std::to_string(s));
+      }
+    } else if (!cfg.use_guess) {
+      RTE_CUDA(cudaMemsetAsync(rho, 0, sizeof(double) * S * nd, st));
+    }
+
+    DBuf<double> rstar, delta, corr;
+    rstar.alloc((size_t)S * nd);
+    delta.alloc((size_t)S * nd);
+    corr.alloc((size_t)S * nd);
+    int* n_active_host = nullptr;
+    RTE_CUDA(cudaMallocHost(&n_active_host, sizeof(int)));
+    const int fin_bx = (int)std::min<long>((nd + 255) / 256, std::max(1, 8192 / S));
+    int l = 1;
+    try {
+      for (; l <= cfg.max_iters; ++l) {
+        bits.zero(st);
+        transport_apply(ctx, SRC_MS_RHO | SRC_G | SRC_BC, rho, rstar.p, sst.active, rho, delta.p, bits.p, st);
+        RTE_CUDA(cudaMemsetAsync(sst.n_active, 0, sizeof(int), st));
+        si_decide_kernel<<<(S + 127) / 128, 128, 0, st>>>(S, sst, l, cfg);
+        RTE_CUDA(cudaGetLastError());
+        if (need_dsa) dsa_apply(ctx, delta.p, corr.p, sst.kind, 1, st);
+        if (need_rom) rom_correct(ctx, delta.p, corr.p, sst.kind, st);
+        si_finalize_kernel<<<dim3(fin_bx, S), 256, 0, st>>>(S, nd, sst.kind, rstar.p, corr.p, rho);
+        RTE_CUDA(cudaGetLastError());
+        if (l % every == 0 || l == cfg.max_iters || (cfg.fixed_iters > 0 && l >= cfg.fixed_iters)) {
+          RTE_CUDA(cudaMemcpyAsync(n_active_host, sst.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+          RTE_CUDA(cudaStreamSynchronize(st));
+          if (*n_active_host == 0) break;
+        }
+      }
+    } catch (...) {
+      cudaFreeHost(n_active_host);
+      throw;
+    }
+    cudaFreeHost(n_active_host);
+
+    std::vector<double> resid(S, 0.0);
+    if (cfg.compute_residual) {
+      bits.zero(st);
+      transport_apply(ctx, SRC_MS_RHO | SRC_G | SRC_BC, rho, rstar.p, nullptr, rho, delta.p, bits.p, st);
+      std::vector<unsigned long long> hb(2 * S);
+      RTE_CUDA(cudaMemcpy(hb.data(), bits.p, sizeof(unsigned long long) * 2 * S, cudaMemcpyDeviceToHost));
+      for (int s = 0; s < S; ++s) {
+        double v;
+        std::memcpy(&v, &hb[2 * s], sizeof(double));
+        resid[s] = v;
+      }
+    }
+    RTE_CUDA(cudaStreamSynchronize(st));
+    std::vector<int> hi((size_t)S * 8);
+    RTE_CUDA(cudaMemcpy(hi.data(), ibuf.p, sizeof(int) * S * 8, cudaMemcpyDeviceToHost));
+    std::vector<double> hl(S);
+    RTE_CUDA(cudaMemcpy(hl.data(), lastc.p, sizeof(double) * S, cudaMemcpyDeviceToHost));
+    if (reports) {
+      for (int s = 0; s < S; ++s) {
+        rte_si_report& r = reports[s];
+        r.converged = hi[4 * S + s];
+        r.iterations = hi[S + s];
+        r.n_sweep = 1 + (long)r.iterations;  // sisa.cpp:112 (bbar) + one per iteration
+        r.switch_iter = hi[6 * S + s];
+        r.singular = hi[5 * S + s];
+        r.final_residual = resid[s];
+        r.last_change = hl[s];
+      }
+    }
+    if (history) RTE_CUDA(cudaMemcpy(history, hist.p, sizeof(double) * S * cfg.max_iters, cudaMemcpyDeviceToHost));
+    if (log) RTE_CUDA(cudaMemcpy(log, lg.p, (size_t)S * cfg.max_iters, cudaMemcpyDeviceToHost));
+  });
+}
+
+// ---- host-side discretization helpers ---------------------------------------
+
+int rte_gauss_legendre_nodes(int n, double* x, double* w);
+int rte_unit_draws(unsigned long long seed, long n, double* out) {
+  return guarded(nullptr, [&] {
+    std::mt19937_64 gen(seed);
+    for (long i = 0; i < n; ++i) out[i] = static_cast<double>(gen() >> 11) * 0x1p-53;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,316 @@
+// rom.cu -- K6: online reduced-order stage on the device.
+//
+// Replaces ReducedModel::assemble (reduced_model.cpp:32-39), romig
+// (strategies.cpp:8-28) and RomsaStrategy::setup/correct
+// (strategies.cpp:34-53) for a batch of parameter samples.  Per sample the
+// reduced operator A_r(mu) = sum_k psi_k(mu) a_r[k] is factored once with
+// complete pivoting and the same rank test as Eigen::FullPivLU
+// (|pivot| > eps * r * |max pivot|); each ROMSA correction is
+//   rhs_r = U_iso^T (Ms delta),  c = A_r^{-1} rhs_r,  corr = U_rho c,
+// done by one CTA per sample with fixed-order block reductions.
+#include "rte_internal.cuh"
+
+namespace rte {
+
+struct RomState {
+  int r = 0, K = 0;
+  double eps_pod = 0, eps_train = 0;
+  DBuf<double> u_rho, u_iso, a_r, b_r;  // column-major as in the reference
+  DBuf<double> lu;                      // [S][r][r] row-major factors
+  DBuf<int> rp, cp, sing;               // [S][r], [S][r], [S]
+  bool factored = false;
+};
+
+namespace {
+
+// Complete-pivoting LU of the r x r row-major matrix in place.
+__device__ int fullpiv_lu(double* a, int r, int* rp, int* cp) {
+  for (int i = 0; i < r; ++i) {
+    rp[i] = i;
+    cp[i] = i;
+  }
+  double maxpiv = 0.0;
+  int nz = r;
+  for (int k = 0; k < r; ++k) {
+    double big = 0.0;
+    int bi = k, bj = k;
+    for (int j = k; j < r; ++j)  // column-major traversal, first maximum
+      for (int i = k; i < r; ++i) {
+        const double v = fabs(a[i * r + j]);
+        if (v > big) {
+          big = v;
+          bi = i;
+          bj = j;
+        }
+      }
+    if (big == 0.0) {
+      nz = k;
+      break;
+    }
+    maxpiv = fmax(maxpiv, big);
+    if (bi != k) {
+      for (int j = 0; j < r; ++j) {
+        const double t = a[k * r + j];
+        a[k * r + j] = a[bi * r + j];
+        a[bi * r + j] = t;
+      }
+      const int t = rp[k];
+      rp[k] = rp[bi];
+      rp[bi] = t;
+    }
+    if (bj != k) {
+      for (int i = 0; i < r; ++i) {
+        const double t = a[i * r + k];
+        a[i * r + k] = a[i * r + bj];
+        a[i * r + bj] = t;
+      }
+      const int t = cp[k];
+      cp[k] = cp[bj];
+      cp[bj] = t;
+    }
+    const double piv = a[k * r + k];
+    for (int i = k + 1; i < r; ++i) {
+      const double l = a[i * r + k] / piv;
+      a[i * r + k] = l;
+      for (int j = k + 1; j < r; ++j) a[i * r + j] -= l * a[k * r + j];
+    }
+  }
+  const double thr = 2.220446049250313e-16 * r * maxpiv;
+  int rank = 0;
+  for (int i = 0; i < nz; ++i)
+    if (fabs(a[i * r + i]) > thr) ++rank;
+  return rank;
+}
+
+__device__ void fullpiv_solve(const double* a, int r, const int* rp, const int* cp, const double* b, double* y,
+                              double* x) {
+  for (int i = 0; i < r; ++i) {
+    double t = b[rp[i]];
+    for (int k = 0; k < i; ++k) t -= a[i * r + k] * y[k];
+    y[i] = t;
+  }
+  for (int i = r - 1; i >= 0; --i) {
+    double t = y[i];
+    for (int k = i + 1; k < r; ++k) t -= a[i * r + k] * y[k];
+    y[i] = t / a[i * r + i];
+  }
+  for (int i = 0; i < r; ++i) x[cp[i]] = y[i];
+}
+
+// A(mu_s) = sum_k psi_k a_r[k] (reduced_model.cpp:32-39), row-major.
+__device__ void assemble(const double* a_r, const double* psi, int r, int K, double* out) {
+  for (int i = 0; i < r; ++i)
+    for (int j = 0; j < r; ++j) {
+      double t = 0.0;
+      for (int k = 0; k < K; ++k) t = t + psi[k] * a_r[(long)k * r * r + (long)j * r + i];
+      out[i * r + j] = t;
+    }
+}
+
+__global__ void rom_factor_kernel(int S, int r, int K, const double* a_r, const double* psi, double* lu, int* rp,
+                                  int* cp, int* sing) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  double* a = lu + (long)s * r * r;
+  assemble(a_r, psi + (long)s * K, r, K, a);
+  const int rank = fullpiv_lu(a, r, rp + (long)s * r, cp + (long)s * r);
+  sing[s] = rank < r ? 1 : 0;
+}
+
+template <int CH>
+__device__ void block_dots(const double* u, long nd, int r, const double* v_smem_or_null, const double* ms,
+                           int block, int N, const double* delta, int s, double* out_smem, double* red) {
+  // out[k] = sum_i u[k*nd + i] * (Ms delta)_i, fixed-order reduction
+  for (int k0 = 0; k0 < r; k0 += CH) {
+    double acc[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) acc[c] = 0.0;
+    for (long i = threadIdx.x; i < nd; i += blockDim.x) {
+      double m;
+      const double* d = delta + (long)s * nd;
+      if (block == 4) {
+        const long c = i >> 1;
+        const int rr = (int)(i & 1);
+        const double* mm = ms + ((long)s * N + c) * 4 + 2 * rr;
+        m = mm[0] * d[2 * c] + mm[1] * d[2 * c + 1];
+      } else {
+        const int nl = (int)(nd / N);
+        m = ms[(long)s * N + i / nl] * d[i];
+      }
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        if (k0 + c < r) acc[c] = fma(u[(long)(k0 + c) * nd + i], m, acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      double v = acc[c];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((threadIdx.x & 31) == 0) red[(threadIdx.x >> 5) * CH + c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < CH && k0 + (int)threadIdx.x < r) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w * CH + threadIdx.x];
+      out_smem[k0 + threadIdx.x] = t;
+    }
+    __syncthreads();
+  }
+}
+
+struct RomCorrectArgs {
+  int S, r, N, block;
+  long nd;
+  const double* u_rho;
+  const double* u_iso;
+  const double* lu;
+  const int* rp;
+  const int* cp;
+  const double* ms;
+  const double* delta;
+  double* corr;
+  const int* kind;
+};
+
+__global__ void rom_correct_kernel(const RomCorrectArgs a) {
+  __shared__ double rhs[128], y[128], c[128], red[32 * 8];
+  const int s = blockIdx.x;
+  if (a.kind[s] != KIND_ROMSA) return;
+  block_dots<8>(a.u_iso, a.nd, a.r, nullptr, a.ms, a.block, a.N, a.delta, s, rhs, red);
+  if (threadIdx.x == 0)
+    fullpiv_solve(a.lu + (long)s * a.r * a.r, a.r, a.rp + (long)s * a.r, a.cp + (long)s * a.r, rhs, y, c);
+  __syncthreads();
+  for (long i = threadIdx.x; i < a.nd; i += blockDim.x) {
+    double t = 0.0;
+    for (int k = 0; k < a.r; ++k) t = fma(a.u_rho[(long)k * a.nd + i], c[k], t);
+    a.corr[(long)s * a.nd + i] = t;
+  }
+}
+
+struct RomigArgs {
+  int S, r, K;
+  long nd;
+  const double* a_r;
+  const double* b_r;
+  const double* psi;
+  const double* u_rho;
+  double* work;  // [S][r*r]
+  int* rp;
+  int* cp;
+  double* rho0;
+  int* status;
+};
+
+__global__ void romig_kernel(const RomigArgs a) {
+  __shared__ double c[128], y[128], b[128];
+  __shared__ int ok;
+  const int s = blockIdx.x;
+  const int r = a.r;
+  if (threadIdx.x == 0) {
+    double* A = a.work + (long)s * r * r;
+    // keep an unfactored copy for the residual check in y/b scratch space
+    double* lu = A;
+    assemble(a.a_r, a.psi + (long)s * a.K, r, a.K, lu);
+    // row-abs-sum and residual need A: recompute entries from a_r on the fly
+    int* rp = a.rp + (long)s * r;
+    int* cp = a.cp + (long)s * r;
+    for (int i = 0; i < r; ++i) b[i] = a.b_r[i];
+    const int rank = fullpiv_lu(lu, r, rp, cp);
+    ok = 1;
+    if (rank < r) {
+      a.status[s] = 1;
+      ok = 0;
+    } else {
+      fullpiv_solve(lu, r, rp, cp, b, y, c);
+      // Galerkin residual check (strategies.cpp:20-27)
+      double resid = 0.0, rowmax = 0.0, cmax = 0.0, bmax = 0.0;
+      for (int i = 0; i < r; ++i) {
+        double t = 0.0, rs = 0.0;
+        for (int j = 0; j < r; ++j) {
+          double aij = 0.0;
+          for (int k = 0; k < a.K; ++k) aij = aij + a.psi[(long)s * a.K + k] * a.a_r[(long)k * r * r + (long)j * r + i];
+          t += aij * c[j];
+          rs += fabs(aij);
+        }
+        resid = fmax(resid, fabs(b[i] - t));
+        rowmax = fmax(rowmax, rs);
+        cmax = fmax(cmax, fabs(c[i]));
+        bmax = fmax(bmax, fabs(b[i]));
+      }
+      const double scale = rowmax * cmax + bmax;
+      if (resid > 1e-10 * fmax(scale, 1e-300)) {
+        a.status[s] = 2;
+        ok = 0;
+      } else {
+        a.status[s] = 0;
+      }
+    }
+  }
+  __syncthreads();
+  for (long i = threadIdx.x; i < a.nd; i += blockDim.x) {
+    double t = 0.0;
+    if (ok)
+      for (int k = 0; k < r; ++k) t = fma(a.u_rho[(long)k * a.nd + i], c[k], t);
+    a.rho0[(long)s * a.nd + i] = t;
+  }
+}
+
+}  // namespace
+
+void rom_load(rte_ctx* ctx, int which, const rte_rom* rom) {
+  RTE_REQUIRE(which == 0 || which == 1, RTE_ERR_INVALID, "rom_load: which must be 0 or 1");
+  RTE_REQUIRE(rom && rom->rank > 0 && rom->rank <= 128, RTE_ERR_INVALID, "rom_load: rank must be in [1,128]");
+  RTE_REQUIRE(ctx->k_terms > 0, RTE_ERR_INVALID, "rom_load: call rte_set_affine first (psi per sample)");
+  RTE_REQUIRE(rom->k_affine == ctx->k_terms, RTE_ERR_INVALID,
+              "reduced model: affine term count does not match the system");
+  if (!ctx->rom[which]) ctx->rom[which] = new RomState();
+  RomState* m = ctx->rom[which];
+  m->r = rom->rank;
+  m->K = rom->k_affine;
+  m->eps_pod = rom->eps_pod;
+  m->eps_train = rom->eps_train;
+  const size_t nd = (size_t)ctx->ndof, r = (size_t)m->r;
+  m->u_rho.upload(rom->u_rho, nd * r);
+  m->u_iso.upload(rom->u_iso, nd * r);
+  m->a_r.upload(rom->a_r, (size_t)m->K * r * r);
+  m->b_r.upload(rom->b_r, r);
+  m->lu.alloc((size_t)ctx->S * r * r);
+  m->rp.alloc((size_t)ctx->S * r);
+  m->cp.alloc((size_t)ctx->S * r);
+  m->sing.alloc((size_t)ctx->S);
+  m->factored = false;
+}
+
+void rom_setup(rte_ctx* ctx, int which, int* singular_dev, cudaStream_t st) {
+  RomState* m = ctx->rom[which];
+  RTE_REQUIRE(m, RTE_ERR_INVALID, "rom: model not loaded");
+  rom_factor_kernel<<<(ctx->S + 31) / 32, 32, 0, st>>>(ctx->S, m->r, m->K, m->a_r.p, ctx->psi.p, m->lu.p, m->rp.p,
+                                                        m->cp.p, m->sing.p);
+  RTE_CUDA(cudaGetLastError());
+  if (singular_dev) RTE_CUDA(cudaMemcpyAsync(singular_dev, m->sing.p, sizeof(int) * ctx->S, cudaMemcpyDeviceToDevice, st));
+  m->factored = true;
+}
+
+void rom_correct(rte_ctx* ctx, const double* delta, double* corr, const int* kind, cudaStream_t st) {
+  RomState* m = ctx->rom[1];
+  RTE_REQUIRE(m && m->factored, RTE_ERR_INVALID, "rom: correction model not set up");
+  RomCorrectArgs a{ctx->S, m->r, ctx->ncells, ctx->block, ctx->ndof, m->u_rho.p, m->u_iso.p, m->lu.p, m->rp.p,
+                   m->cp.p, ctx->ms.p, delta, corr, kind};
+  rom_correct_kernel<<<ctx->S, 256, 0, st>>>(a);
+  RTE_CUDA(cudaGetLastError());
+}
+
+void romig(rte_ctx* ctx, double* rho0, int* status_dev, cudaStream_t st) {
+  RomState* m = ctx->rom[0];
+  RTE_REQUIRE(m, RTE_ERR_INVALID, "romig: primary model not loaded");
+  DBuf<double> work;
+  work.alloc((size_t)ctx->S * m->r * m->r);
+  RomigArgs a{ctx->S, m->r, m->K, ctx->ndof, m->a_r.p, m->b_r.p, ctx->psi.p, m->u_rho.p, work.p, m->rp.p, m->cp.p,
+              rho0, status_dev};
+  romig_kernel<<<ctx->S, 256, 0, st>>>(a);
+  RTE_CUDA(cudaGetLastError());
+  RTE_CUDA(cudaStreamSynchronize(st));
+}
+
+void rom_destroy(RomState* r) { delete r; }
+
+}  // namespace rte

@@ -1,0 +1,232 @@
+// rte_internal.cuh -- shared declarations of the B200 implementation behind
+// include/rte_b200.h.  Host-side context, device kernels' argument blocks and
+// launch helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/rte_b200.h"
+
+namespace rte {
+
+constexpr double kSqrt3 = 1.7320508075688772935;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define RTE_CUDA(call)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      throw ::rte::Error(RTE_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define RTE_REQUIRE(cond, code, msg) \
+  do {                               \
+    if (!(cond)) throw ::rte::Error((code), (msg)); \
+  } while (0)
+
+// Owning device buffer.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count == n && p) return;
+    release();
+    if (count == 0) return;
+    RTE_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void upload(const T* host, size_t count) {
+    alloc(count);
+    if (count) RTE_CUDA(cudaMemcpy(p, host, count * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  void zero(cudaStream_t s) {
+    if (n) RTE_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+};
+
+// Source-assembly modes shared by the 1D and 2D sweeps.
+enum SrcMode : int {
+  SRC_MS_RHO = 1,  // q += Ms rho
+  SRC_G = 2,       // q += G
+  SRC_BC = 4,      // inflow ghost traces (boundary sources, transport_system.cpp:142-187)
+  SRC_RAW = 8      // q = rhs given (single-direction sweeps)
+};
+
+// Per-sample SI bookkeeping kinds (rte_si_solve).
+enum Kind : int { KIND_IDLE = 0, KIND_ACCEPT = 1, KIND_DSA = 2, KIND_ROMSA = 3, KIND_SINGULAR = 4 };
+
+// 2D sweep direction table entry: canonical (reflected) constants of one
+// unique (vx, vy) slot.
+struct Slot2D {
+  double a, b;   // |vx|/hx, |vy|/hy
+  double w;      // folded quadrature weight (sum over the slot's directions)
+  double bcx, bcy;  // inflow ghost traces (already scaled), see sweep2d.cu
+};
+
+struct DsaState;
+struct RomState;
+
+}  // namespace rte
+
+struct rte_ctx {
+  int device = 0;
+  int geom = 0, nx = 0, ny = 1, ncells = 0, nl = 2;
+  long ndof = 0;
+  int S = 0;
+  int nv = 0;
+  std::vector<double> vx, vy, vz, w;
+  double inflow[4] = {0, 0, 0, 0};
+  int block = 1;
+  double hx = 0, hy = 0;
+  std::vector<double> bounds;
+  std::vector<double> mt_h, ms_h;  // host copies of the mass blocks (sample-major)
+
+  // device problem data
+  rte::DBuf<double> width;   // slab widths [N]
+  rte::DBuf<double> dvx, dw; // slab directions [nv]
+  rte::DBuf<double> mt, ms;  // [S][cells][block]
+  rte::DBuf<double> g;       // [S or 1][ndof]
+  int g_shared = 0;
+
+  // 2D direction tables
+  int nslots = 0;
+  std::vector<int> dir_slot;          // direction -> slot
+  std::vector<double> slot_vx, slot_vy, slot_w;
+  int q_count[4] = {0, 0, 0, 0};      // slots per quadrant
+  std::vector<int> q_slots[4];
+
+  // workspace (lazily sized)
+  rte::DBuf<double> ws_a, ws_b, ws_c, ws_d, ws_part;
+  rte::DBuf<unsigned long long> ws_bits;
+  rte::DBuf<unsigned int> ws_sync;
+  rte::DBuf<rte::Slot2D> slot_tab;  // cached all-slot sweep table (2D)
+  int slot_tab_dpl = 0;
+
+  // affine terms
+  int k_terms = 0;
+  rte::DBuf<double> term_mt, term_ms, psi;
+  std::vector<double> psi_h;
+
+  rte::DsaState* dsa = nullptr;
+  rte::RomState* rom[2] = {nullptr, nullptr};
+
+  std::string err;
+  ~rte_ctx();
+};
+
+namespace rte {
+
+// ---- kernel launchers (implemented in the .cu files) ----------------------
+
+struct Sweep1DArgs {
+  int S, N, nv;
+  long ndof;
+  const double* width;
+  const double* vx;
+  const double* w;
+  int block;
+  const double* mt;
+  const double* ms;
+  const double* g;
+  int g_shared;
+  const double* rho;   // Ms rho source, or raw rhs in SRC_RAW mode
+  double inflow_l, inflow_r;
+  int mode;            // SrcMode bits
+  int j_single;        // -1 all directions, else only this one (weight 1)
+  double* out;         // [S][ndof] sum_j w_j f_j (may be null)
+  double* fout;        // kinetic [S][nv][ndof] or single-dir [S][ndof] (may be null)
+  const int* active;   // [S] mask (may be null)
+  // fused SI epilogue (may be null): delta = out - rho_prev, per-sample
+  // max|delta| and max|out| as ordered bit patterns
+  const double* rho_prev;
+  double* delta;
+  unsigned long long* change_bits;  // [S][2]
+};
+void launch_sweep1d(const Sweep1DArgs& a, cudaStream_t st);
+
+struct Sweep2DArgs {
+  int S, nx, ny;
+  const Slot2D* slots;   // [4][nq_pad] canonical slot table per quadrant
+  int nq_pad;            // padded slots per quadrant (multiple of D*NW)
+  int groups;            // direction groups per quadrant
+  const double* sig_t;   // [S][cells]
+  const double* sig_s;   // [S][cells]
+  const double* g;       // [S or 1][ndof]
+  int g_shared;
+  const double* rho;     // [S][ndof] (Ms rho source, or raw rhs)
+  int mode;
+  double* part;          // [4*groups][S][ndof] partial sums
+  double* ybuf;          // band-boundary traces
+  unsigned int* sync;    // progress counters + ticket
+  const int* active;
+};
+void launch_sweep2d(const Sweep2DArgs& a, cudaStream_t st);
+
+// sum of partials (fixed order) + optional SI epilogue
+void launch_reduce_partials(int S, long ndof, int nparts, const double* part, double* out,
+                            const double* rho_prev, double* delta, unsigned long long* change_bits,
+                            const int* active, cudaStream_t st);
+
+void launch_apply_block(int S, int ncells, int nl, int block, const double* m, const double* x, double* out,
+                        cudaStream_t st);
+void launch_density_of(int S, int nv, long ndof, const double* w, const double* f, double* rho,
+                       cudaStream_t st);
+
+// SI bookkeeping
+struct SiState {
+  int* active;
+  int* iters;
+  int* switched;
+  int* kind;
+  int* converged;
+  int* singular;
+  double* history;     // [S][max_iters]
+  char* log;           // [S][max_iters]
+  int* switch_iter;
+  unsigned long long* change_bits;  // [S][2]: max|delta|, max|rho*|
+  double* last_change;
+  int* n_active;
+};
+void launch_si_decide(int S, const SiState& st, int l, const rte_si_config& cfg, cudaStream_t s);
+void launch_si_finalize(int S, long ndof, const SiState& st, const double* rho_star, const double* corr,
+                        double* rho, cudaStream_t s);
+void launch_residual(int S, long ndof, const double* rho, const double* rho_star, double* resid,
+                     cudaStream_t s);
+
+// DSA
+void dsa_setup(rte_ctx* ctx, cudaStream_t st);
+void dsa_solve_density(rte_ctx* ctx, const double* rhs, double* out, const int* kind_mask, cudaStream_t st);
+void dsa_destroy(DsaState* d);
+long dsa_coupled_dim(const rte_ctx* ctx);
+
+// ROM
+void rom_load(rte_ctx* ctx, int which, const rte_rom* rom);
+void rom_setup(rte_ctx* ctx, int which, int* singular_dev, cudaStream_t st);
+void rom_correct(rte_ctx* ctx, const double* ms_delta, double* corr, const int* kind, cudaStream_t st);
+void romig(rte_ctx* ctx, double* rho0, int* status_dev, cudaStream_t st);
+void rom_destroy(RomState* r);
+
+// transport helpers used by the C-ABI (capi.cu)
+void transport_apply(rte_ctx* ctx, int mode, const double* rho, double* out, const int* active,
+                     const double* rho_prev, double* delta, unsigned long long* change_bits, cudaStream_t st);
+
+}  // namespace rte

@@ -1,0 +1,514 @@
+"""Host-side mirror of the reference's solver API for the B200 path.
+
+Names and argument meaning follow the reference core library (namespace rte,
+/root/reference/proj/core/include/rte): quadratures, meshes, DG space,
+ProblemDefinition/CoefficientTerm, TransportSystem (here batched over
+parameter samples: ``TransportBatch``), DsaOperator, ReducedModel, romig,
+romsad_tolerance and sisa_solve.  Every numerical operation on the hot path
+runs in librte_b200.so (hand-written sm_100a kernels) through the C-ABI of
+include/rte_b200.h; this module only marshals arguments.
+
+Device vectors are torch float64 CUDA tensors of shape [S, n_dof]
+(per-sample reference layout) -- torch is used for device memory and
+streams only.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import capi
+
+SLAB1D = capi.RTE_SLAB1D
+XY2D = capi.RTE_XY2D
+NQ = 6  # per-axis Gauss points of the cell rules (transport_system.cpp:18)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _c(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ---------------------------------------------------------------------------
+# Quadrature (quadrature.cpp:8-73), mesh (mesh.cpp), DG space (dg_space.cpp)
+
+@dataclass
+class AngularQuadrature:
+    geometry: int
+    directions: np.ndarray
+    weights: np.ndarray
+
+    def n(self) -> int:
+        return len(self.weights)
+
+
+def gauss_legendre_nodes(n: int):
+    if n < 1:
+        raise ValueError("gauss_legendre: n must be >= 1")
+    x, w = np.zeros(n), np.zeros(n)
+    capi.check(capi.load().rte_gauss_legendre_nodes(n, capi.dptr(x), capi.dptr(w)))
+    return x, w
+
+
+def gauss_legendre(n: int) -> AngularQuadrature:
+    x, w = gauss_legendre_nodes(n)
+    d = np.zeros((n, 3))
+    d[:, 0] = x
+    return AngularQuadrature(SLAB1D, d, 0.5 * w)
+
+
+def chebyshev_legendre(n_phi: int, n_vz: int) -> AngularQuadrature:
+    if n_phi < 2 or n_vz < 1:
+        raise ValueError("chebyshev_legendre: invalid sizes")
+    z, wz = gauss_legendre_nodes(n_vz)
+    pi = 3.14159265358979323846
+    dirs, ws = [], []
+    for j2 in range(n_vz):
+        s = np.sqrt(max(0.0, 1.0 - z[j2] * z[j2]))
+        for j1 in range(1, n_phi + 1):
+            phi = 2.0 * j1 * pi / n_phi - pi / n_phi
+            dirs.append((np.cos(phi) * s, np.sin(phi) * s, z[j2]))
+            ws.append((1.0 / n_phi) * (0.5 * wz[j2]))
+    return AngularQuadrature(XY2D, np.array(dirs), np.array(ws))
+
+
+@dataclass
+class Mesh:
+    geometry: int = SLAB1D
+    boundaries: Optional[np.ndarray] = None
+    x0: float = 0.0
+    x1: float = 1.0
+    y0: float = 0.0
+    y1: float = 1.0
+    nx: int = 0
+    ny: int = 1
+
+    def cell_count(self) -> int:
+        return self.nx if self.geometry == SLAB1D else self.nx * self.ny
+
+    def n_local(self) -> int:
+        return 2 if self.geometry == SLAB1D else 4
+
+    def n_dof(self) -> int:
+        return self.cell_count() * self.n_local()
+
+    @staticmethod
+    def slab(bounds) -> "Mesh":
+        b = _c(bounds)
+        if b.size < 2 or not np.all(b[:-1] < b[1:]):
+            raise ValueError("slab mesh boundaries must be strictly increasing")
+        return Mesh(SLAB1D, b, nx=b.size - 1, ny=1)
+
+    @staticmethod
+    def slab_uniform(a, b, n) -> "Mesh":
+        if n < 1 or not (a < b):
+            raise ValueError("invalid slab mesh")
+        bounds = np.array([a + (b - a) * i / n for i in range(n + 1)])
+        bounds[n] = b
+        return Mesh.slab(bounds)
+
+    @staticmethod
+    def rect_uniform(x0, x1, nx, y0, y1, ny) -> "Mesh":
+        if nx < 1 or ny < 1 or not (x0 < x1) or not (y0 < y1):
+            raise ValueError("invalid rectangular mesh")
+        return Mesh(XY2D, None, float(x0), float(x1), float(y0), float(y1), nx, ny)
+
+    def _geo(self):
+        b = self.boundaries if self.boundaries is not None else np.zeros(2)
+        self._bk = _c(b)
+        return (self.geometry, self.nx, max(self.ny, 1), capi.dptr(self._bk), self.x0, self.x1, self.y0, self.y1)
+
+    def cell_points(self, nq: int = NQ):
+        npc = nq if self.geometry == SLAB1D else nq * nq
+        px, py = np.zeros(self.cell_count() * npc), np.zeros(self.cell_count() * npc)
+        capi.check(capi.load().rte_cell_points(*self._geo(), nq, capi.dptr(px), capi.dptr(py)))
+        return px, py
+
+    def weighted_mass(self, wvals, nq: int = NQ):
+        nl = self.n_local()
+        out = np.zeros(self.cell_count() * nl * nl)
+        w = _c(wvals)
+        capi.check(capi.load().rte_weighted_mass(*self._geo(), nq, capi.dptr(w), capi.dptr(out)))
+        return out.reshape(self.cell_count(), nl, nl)
+
+    def project(self, fvals, nq: int = NQ):
+        out = np.zeros(self.n_dof())
+        f = _c(fvals)
+        capi.check(capi.load().rte_project(*self._geo(), nq, capi.dptr(f), capi.dptr(out)))
+        return out
+
+
+@dataclass
+class CoefficientTerm:
+    """problem.hpp:24-29."""
+    psi: Optional[Callable] = None
+    absorption_weight: Optional[Callable] = None
+    scattering_weight: Optional[Callable] = None
+    name: str = ""
+
+
+@dataclass
+class ProblemDefinition:
+    """problem.hpp:31-44 (coefficient closures are vectorised f(x, y))."""
+    geometry: int = SLAB1D
+    terms: list = field(default_factory=list)
+    source: Optional[Callable] = None
+    inflow_left: float = 0.0
+    inflow_right: float = 0.0
+    inflow_bottom: float = 0.0
+    inflow_top: float = 0.0
+    n_params: int = 0
+    param_ranges: list = field(default_factory=list)
+
+
+def _vals(fn, px, py):
+    if fn is None:
+        return np.zeros(px.size)
+    return np.ascontiguousarray(np.broadcast_to(np.asarray(fn(px, py), dtype=np.float64), px.shape))
+
+
+# ---------------------------------------------------------------------------
+
+class TransportBatch:
+    """TransportSystem (transport_system.hpp:30-142) for S parameter samples.
+
+    Construct either from a ProblemDefinition + parameter list (the
+    reference's constructor; mass blocks via the 6x6 Gauss rule of
+    transport_system.cpp:17-55) or with ``from_cells`` from per-cell constant
+    coefficients (the B200-native bulk input).
+    """
+
+    def __init__(self, problem: ProblemDefinition, mesh: Mesh, quad: AngularQuadrature,
+                 mus: Sequence[Sequence[float]], device: int = 0):
+        if not (problem.geometry == mesh.geometry == quad.geometry):
+            raise ValueError("transport system: geometry mismatch")
+        if not problem.terms:
+            raise ValueError("transport system: no coefficient terms")
+        mus = [list(m) for m in mus]
+        S = len(mus)
+        psi = np.array([[t.psi(m) if t.psi is not None else 1.0 for t in problem.terms] for m in mus])
+        if np.any(psi[:, 0] != 1.0):
+            raise ValueError("transport system: term 0 must be parameter independent (psi == 1)")
+        px, py = mesh.cell_points()
+        K = len(problem.terms)
+        tmt, tms = [], []
+        for t in problem.terms:
+            a = _vals(t.absorption_weight, px, py)
+            sc = _vals(t.scattering_weight, px, py)
+            tot = np.zeros(px.size)
+            if t.absorption_weight is not None:
+                tot = tot + a
+            if t.scattering_weight is not None:
+                tot = tot + sc
+            tmt.append(mesh.weighted_mass(tot))
+            tms.append(mesh.weighted_mass(sc))
+        tmt, tms = np.stack(tmt), np.stack(tms)  # [K][cells][nl][nl]
+        mt = np.zeros((S,) + tmt.shape[1:])
+        ms = np.zeros_like(mt)
+        for k in range(K):  # build_masses accumulation order (transport_system.cpp:136-137)
+            mt = mt + psi[:, k, None, None, None] * tmt[k][None]
+            ms = ms + psi[:, k, None, None, None] * tms[k][None]
+        g = mesh.project(_vals(problem.source, px, py)) if problem.source is not None else np.zeros(mesh.n_dof())
+        inflow = (problem.inflow_left, problem.inflow_right, problem.inflow_bottom, problem.inflow_top)
+        if mesh.geometry == XY2D:
+            mt_s, ms_s = _scalar_blocks(mt), _scalar_blocks(ms)
+            tmt_s, tms_s = _scalar_blocks(tmt), _scalar_blocks(tms)
+            self._create(mesh, quad, mt_s, ms_s, g, True, inflow, 1, device)
+            self._affine(K, tmt_s, tms_s, psi)
+        else:
+            self._create(mesh, quad, mt.reshape(S, -1, 4), ms.reshape(S, -1, 4), g, True, inflow, 4, device)
+            self._affine(K, tmt.reshape(K, -1, 4), tms.reshape(K, -1, 4), psi)
+        self.problem, self.mus = problem, mus
+
+    @classmethod
+    def from_cells(cls, mesh: Mesh, quad: AngularQuadrature, sigma_t, sigma_s, source, inflow=(0, 0, 0, 0),
+                   device: int = 0, psi=None, term_sigma_t=None, term_sigma_s=None) -> "TransportBatch":
+        """Per-cell constant coefficients: sigma_t/sigma_s [S][cells]; source is
+        a DOF load vector [n_dof] (shared) or [S][n_dof]."""
+        self = cls.__new__(cls)
+        st, ss = _c(sigma_t), _c(sigma_s)
+        if st.ndim == 1:
+            st, ss = st[None], ss[None]
+        g = _c(source)
+        shared = g.ndim == 1
+        self._create(mesh, quad, st, ss, g, shared, inflow, 1, device)
+        if psi is not None:
+            self._affine(np.asarray(psi).shape[1], _c(term_sigma_t), _c(term_sigma_s), _c(psi))
+        self.problem, self.mus = None, None
+        return self
+
+    def _create(self, mesh, quad, mt, ms, g, shared, inflow, block, device):
+        L = capi.load()
+        self.mesh, self.quad, self.device = mesh, quad, device
+        S = mt.shape[0]
+        self._keep = [_c(mt), _c(ms), _c(g), _c(quad.directions), _c(quad.weights)]
+        p = capi.Problem()
+        geo = mesh._geo()
+        p.geometry, p.nx, p.ny, p.bounds = geo[0], geo[1], geo[2], geo[3]
+        p.x0, p.x1, p.y0, p.y1 = mesh.x0, mesh.x1, mesh.y0, mesh.y1
+        p.n_dirs = quad.n()
+        p.dirs = capi.dptr(self._keep[3])
+        p.weights = capi.dptr(self._keep[4])
+        p.inflow = (ctypes.c_double * 4)(*[float(v) for v in inflow])
+        p.n_samples = S
+        p.block = block
+        p.mt, p.ms, p.source = capi.dptr(self._keep[0]), capi.dptr(self._keep[1]), capi.dptr(self._keep[2])
+        p.source_shared = 1 if shared else 0
+        h = ctypes.c_void_p()
+        capi.check(L.rte_create(ctypes.byref(p), device, ctypes.byref(h)))
+        self._h = h
+        self.S = S
+        self.nd = L.rte_n_dof(h)
+        self.sigma_t_cells = mt if block == 1 else None
+        self.k_terms = 0
+
+    def _affine(self, K, tmt, tms, psi):
+        self._akeep = [_c(tmt), _c(tms), _c(psi)]
+        a = capi.Affine(K, capi.dptr(self._akeep[0]), capi.dptr(self._akeep[1]), capi.dptr(self._akeep[2]))
+        capi.check(capi.load().rte_set_affine(self._h, ctypes.byref(a)), self._h)
+        self.k_terms = K
+        self.psi = self._akeep[2]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and capi._lib is not None:
+            capi._lib.rte_destroy(h)
+            self._h = None
+
+    # -- helpers --
+    def n_dof(self) -> int:
+        return self.nd
+
+    def n_samples(self) -> int:
+        return self.S
+
+    def kinetic_dim(self) -> int:
+        return self.quad.n() * self.nd
+
+    def n_slots(self) -> int:
+        return capi.load().rte_n_slots(self._h)
+
+    def _dev(self, x, shape=None):
+        torch = _torch()
+        t = torch.as_tensor(x, dtype=torch.float64, device="cuda:%d" % self.device).contiguous()
+        if shape is not None:
+            t = t.reshape(shape)
+        return t
+
+    def _out(self, *shape):
+        torch = _torch()
+        return torch.empty(*shape, dtype=torch.float64, device="cuda:%d" % self.device)
+
+    def _stream(self):
+        return ctypes.c_void_p(_torch().cuda.current_stream(self.device).cuda_stream)
+
+    def _call(self, fn, *args):
+        capi.check(fn(self._h, *args), self._h)
+
+    # -- transport operator (batched over samples) --
+    def apply_L(self, rho):
+        rho = self._dev(rho, (self.S, self.nd))
+        out = self._out(self.S, self.nd)
+        self._call(capi.load().rte_apply_L, rho.data_ptr(), out.data_ptr(), self._stream())
+        return out
+
+    def assemble_rhs(self):
+        out = self._out(self.S, self.nd)
+        self._call(capi.load().rte_assemble_rhs, out.data_ptr(), self._stream())
+        return out
+
+    def fixed_point(self, rho):
+        rho = self._dev(rho, (self.S, self.nd))
+        out = self._out(self.S, self.nd)
+        self._call(capi.load().rte_fixed_point, rho.data_ptr(), out.data_ptr(), self._stream())
+        return out
+
+    def sweep_direction(self, j, rhs):
+        rhs = self._dev(rhs, (self.S, self.nd))
+        out = self._out(self.S, self.nd)
+        self._call(capi.load().rte_sweep_direction, int(j), rhs.data_ptr(), out.data_ptr(), self._stream())
+        return out
+
+    def kinetic_sweep(self, rho):
+        rho = self._dev(rho, (self.S, self.nd))
+        out = self._out(self.S, self.quad.n() * self.nd)
+        self._call(capi.load().rte_kinetic_sweep, rho.data_ptr(), out.data_ptr(), self._stream())
+        return out
+
+    def density_of(self, f):
+        f = self._dev(f, (self.S, self.quad.n() * self.nd))
+        out = self._out(self.S, self.nd)
+        self._call(capi.load().rte_density_of, f.data_ptr(), out.data_ptr(), self._stream())
+        return out
+
+    def apply_Ms(self, x):
+        x = self._dev(x, (self.S, self.nd))
+        out = self._out(self.S, self.nd)
+        self._call(capi.load().rte_apply_Ms, x.data_ptr(), out.data_ptr(), self._stream())
+        return out
+
+    def apply_Mt(self, x):
+        x = self._dev(x, (self.S, self.nd))
+        out = self._out(self.S, self.nd)
+        self._call(capi.load().rte_apply_Mt, x.data_ptr(), out.data_ptr(), self._stream())
+        return out
+
+
+def _scalar_blocks(m):
+    """Per-cell mass blocks -> scalar sigma (the B200 2D path needs sigma*I)."""
+    nl = m.shape[-1]
+    d = np.diagonal(m, axis1=-2, axis2=-1)
+    off = m - d[..., None] * np.eye(nl)
+    scale = np.maximum(np.max(np.abs(d), axis=-1), 1e-300)
+    if np.any(np.max(np.abs(off), axis=(-2, -1)) > 1e-12 * scale) or \
+            np.any(np.max(np.abs(d - d[..., :1]), axis=-1) > 1e-12 * scale):
+        raise capi.RteError(capi.RTE_ERR_UNSUPPORTED,
+                            "xy geometry: coefficients must be constant per cell in this build")
+    return np.ascontiguousarray(d[..., 0])
+
+
+class DsaOperator:
+    """DsaOperator (dsa.hpp:29-56), one factorization per sample."""
+
+    def __init__(self, batch: TransportBatch):
+        self.batch = batch
+        batch._call(capi.load().rte_dsa_setup, batch._stream())
+
+    def coupled_dim(self) -> int:
+        return capi.load().rte_dsa_coupled_dim(self.batch._h)
+
+    def solve_density(self, rhs):
+        b = self.batch
+        rhs = b._dev(rhs, (b.S, b.nd))
+        out = b._out(b.S, b.nd)
+        b._call(capi.load().rte_dsa_solve_density, rhs.data_ptr(), out.data_ptr(), b._stream())
+        return out
+
+    def correct(self, delta):
+        b = self.batch
+        d = b._dev(delta, (b.S, b.nd))
+        out = b._out(b.S, b.nd)
+        b._call(capi.load().rte_dsa_correct, d.data_ptr(), out.data_ptr(), b._stream())
+        return out
+
+
+def build_dsa(batch: TransportBatch) -> DsaOperator:
+    return DsaOperator(batch)
+
+
+# ---------------------------------------------------------------------------
+# Reduced models and the solver driver
+
+@dataclass
+class ReducedModel:
+    """reduced_model.hpp:19-44 (host copy; column-major storage)."""
+    geometry: int = 0
+    n_v: int = 0
+    n_dof: int = 0
+    rank: int = 0
+    k_affine: int = 0
+    kind: str = "p"
+    eps_pod: float = 0.0
+    eps_train: float = 0.0
+    u_rho: np.ndarray = None
+    u_iso: np.ndarray = None
+    a_r: list = None
+    singular_values: np.ndarray = None
+    discarded_fraction: float = 0.0
+    b_r: np.ndarray = None
+
+
+def load_rom(batch: TransportBatch, which: int, model) -> None:
+    """Upload a reduced model (which: 0 primary / 1 correction)."""
+    keep = [_c(np.asarray(model.u_rho).T), _c(np.asarray(model.u_iso).T),
+            _c(np.stack([np.asarray(a).T for a in model.a_r])), _c(model.b_r)]
+    r = capi.Rom(int(model.rank), int(model.k_affine), capi.dptr(keep[0]), capi.dptr(keep[1]), capi.dptr(keep[2]),
+                 capi.dptr(keep[3]), float(model.eps_pod), float(model.eps_train))
+    capi.check(capi.load().rte_rom_load(batch._h, which, ctypes.byref(r)), batch._h)
+    batch.__dict__.setdefault("_romkeep", {})[which] = keep
+
+
+def romig(batch: TransportBatch):
+    """strategies.cpp:8-28 for every sample; returns (rho0 [S,n_dof], status)."""
+    out = batch._out(batch.S, batch.nd)
+    status = (ctypes.c_int * batch.S)()
+    batch._call(capi.load().rte_romig, out.data_ptr(), status, batch._stream())
+    return out, np.array(status[:], dtype=np.int32)
+
+
+def romsad_tolerance(eps_train, eps_pod, eta=0.1):
+    """strategies.cpp:30-32."""
+    return eta * max(eps_train, eps_pod)
+
+
+@dataclass
+class SolveConfig:
+    """solvers.hpp:13-19 plus the batch extensions of rte_si_config."""
+    eps_sisa: float = 1e-11
+    max_iters: int = 2000
+    norm: str = "abs"
+    fixed_iters: int = 0
+    theta: int = 3
+    eps_romsad: float = 0.0
+    initial_guess: Optional[object] = None
+    compute_residual: bool = True
+    check_every: int = 4
+
+
+@dataclass
+class SolveReport:
+    """solvers.hpp:21-33 (per sample)."""
+    converged: bool
+    n_sweep: int
+    iterations: int
+    change_history: list
+    final_residual: float
+    strategy: str
+    initial_guess: str
+    correction_log: str
+    switch_iter: int
+    singular: bool
+
+
+_METHODS = {"SI": capi.RTE_SI, "DSA": capi.RTE_DSA, "ROMSA": capi.RTE_ROMSA, "ROMSAD": capi.RTE_ROMSAD,
+            "ROMIG": capi.RTE_ROMIG}
+
+
+def sisa_solve(batch: TransportBatch, method: str, config: SolveConfig):
+    """Batched sisa_solve (sisa.cpp:14-54): returns (rho [S, n_dof], reports)."""
+    L = capi.load()
+    m = _METHODS[method]
+    cfg = capi.SiConfig(m, float(config.eps_sisa), capi.RTE_NORM_REL if config.norm == "rel" else capi.RTE_NORM_ABS,
+                        int(config.max_iters), int(config.fixed_iters), int(config.theta),
+                        float(config.eps_romsad), 1 if config.initial_guess is not None else 0,
+                        1 if config.compute_residual else 0, int(config.check_every))
+    if config.initial_guess is not None:
+        rho = batch._dev(config.initial_guess, (batch.S, batch.nd)).clone()
+    else:
+        rho = batch._out(batch.S, batch.nd)
+    S, mi = batch.S, max(config.max_iters, config.fixed_iters)
+    reps = (capi.SiReport * S)()
+    hist = np.zeros(S * mi)
+    log = ctypes.create_string_buffer(S * mi)
+    _torch().cuda.synchronize(batch.device)
+    capi.check(L.rte_si_solve(batch._h, ctypes.byref(cfg), ctypes.c_void_p(rho.data_ptr()), reps, capi.dptr(hist),
+                              log), batch._h)
+    raw = log.raw
+    out = []
+    label = {"SI": "SI", "DSA": "DSA", "ROMSA": "ROMSA", "ROMSAD": "ROMSAD", "ROMIG": "ROMIG"}[method]
+    for s in range(S):
+        r = reps[s]
+        it = r.iterations
+        lg = raw[s * mi:s * mi + it].replace(b"\0", b"").decode()
+        out.append(SolveReport(bool(r.converged), int(r.n_sweep), int(it), list(hist[s * mi:s * mi + it]),
+                               float(r.final_residual), label,
+                               "supplied" if (config.initial_guess is not None or method == "ROMIG") else "zero",
+                               lg, int(r.switch_iter), bool(r.singular)))
+    return rho, out
