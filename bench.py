@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the batched parametric source-iteration hot path on B200.
+
+Workload (BASELINE.json configs[4], the 2D sweep-throughput stress config):
+[0,1]^2 at 1024x1024 cells, 256 unique directions (CL(32,16): 8 polar x 32
+azimuthal per hemisphere, +/-vz folded), 16 samples with per-cell
+sigma_t ~ logU[0.1,100] and c ~ U[0.5,0.99] drawn from seed, q = 1, vacuum.
+One step = one source iteration over the whole batch: the upwind sweep of
+every (cell, direction, sample) with the fused source update and scalar-flux
+reduction, the per-sample change norm, and the DSA correction when the build
+provides it for XY geometry (see config.dsa).  Metric: cell*direction*sample
+sweep updates per second (updates counted over unique directions).
+
+Contract: `python bench.py --gpus N --steps K --warmup W [--impl reference]`
+prints one JSON line (rank 0).  Multi-GPU: samples shard across ranks (weak
+scaling, no collective on the data path); timing is on the device, max over
+ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOP_PER_UPDATE = 66      # FP64 instructions of the on-the-fly cell solve (sweep2d.cu)
+BYTES_PER_UPDATE = 40     # sigma_t + 4 source moments (operand-stream accounting)
+PHI, VZ = 32, 16          # CL(32,16) -> 256 unique (vx, vy) slots
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi clock / throttle sampling during the timed region."""
+
+    def __init__(self, device):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), "--query-gpu=" + q,
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world, device):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda:%d" % device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+def run_b200(args, rank, world, device):
+    import torch
+    from paper_2402_10488_b200 import capi, configs, rte
+    torch.cuda.set_device(device)
+    L = capi.load()
+    nx, S = args.nx, args.samples
+    mesh = rte.Mesh.rect_uniform(0, 1, nx, 0, 1, nx)
+    quad = rte.chebyshev_legendre(PHI, VZ)
+    st, ss = configs.c5_coefficients(nx, S, seed=configs.SEEDS["c5"] + rank)
+    px, py = mesh.cell_points()
+    g = mesh.project(np.ones(px.size))
+    batch = rte.TransportBatch.from_cells(mesh, quad, st, ss, g, device=device)
+    slots = batch.n_slots()
+    upd_step = nx * nx * slots * S
+    # DSA availability for XY geometry in this build
+    dsa_ok = True
+    try:
+        rte.DsaOperator(batch)
+    except capi.RteError:
+        dsa_ok = False
+    method = "DSA" if dsa_ok else "SI"
+
+    def solve(iters, guess):
+        cfg = rte.SolveConfig(fixed_iters=iters, max_iters=iters, compute_residual=False,
+                              initial_guess=guess, check_every=max(iters, 1))
+        return rte.sisa_solve(batch, method, cfg)
+
+    rho, _ = solve(args.warmup, None)
+    torch.cuda.synchronize()
+    L.rte_profile_enable(batch._h, 1)
+    L.rte_profile_read(batch._h, None, None)
+    clocks = Clocks(device)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rho, reps = solve(args.steps, rho)
+    e1.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    ck = clocks.stop()
+    ms_total = e0.elapsed_time(e1)
+    ms_k = (ctypes.c_double * 5)()
+    n_k = (ctypes.c_long * 5)()
+    capi.check(L.rte_profile_read(batch._h, ms_k, n_k), batch._h)
+    L.rte_profile_enable(batch._h, 0)
+    ms_max = max_over_ranks(ms_total, world, device)
+    value = upd_step * args.steps * world / (ms_max * 1e-3)
+
+    # end-to-end through the C-ABI with host buffers: create (H2D of the
+    # problem), K iterations, D2H of the result.
+    e2e = None
+    if not args.no_e2e:
+        st_p = torch.from_numpy(st).pin_memory()
+        ss_p = torch.from_numpy(ss).pin_memory()
+        out_h = torch.empty((S, batch.n_dof()), dtype=torch.float64).pin_memory()
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        b2 = rte.TransportBatch.from_cells(mesh, quad, st_p.numpy(), ss_p.numpy(), g, device=device)
+        if dsa_ok:
+            rte.DsaOperator(b2)
+        cfg = rte.SolveConfig(fixed_iters=args.steps, max_iters=args.steps, compute_residual=False,
+                              check_every=args.steps)
+        r2, _ = rte.sisa_solve(b2, method, cfg)
+        out_h.copy_(r2)
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks(time.perf_counter() - t0, world, device)
+        del b2, r2
+        h2d = st.nbytes + ss.nbytes + g.nbytes
+        e2e = {"value": upd_step * args.steps * world / t_e2e, "unit": "updates/s",
+               "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(out_h.numel() * 8 / args.steps),
+               "job": "rte_create(host arrays) + rte_dsa_setup + rte_si_solve(%d its) + D2H rho" % args.steps}
+
+    sweep_ms = ms_k[0] / max(n_k[0], 1)
+    hbm_peak, peak_kind = peaks()
+    achieved = upd_step * BYTES_PER_UPDATE / (sweep_ms * 1e-3) / 1e9
+    tf = ctypes.c_double()
+    capi.check(L.rte_probe_dfma(device, ctypes.byref(tf)))
+    fp64_ach = upd_step * FLOP_PER_UPDATE / (sweep_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "sweep2d_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    gpu_launches = int(sum(n_k[k] for k in range(5)))
+    line = {
+        "metric": "sweep cell*direction*sample updates/s (1 SI%s iteration per step)" % ("-DSA" if dsa_ok else ""),
+        "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded mt19937_64, BASELINE configs[4])",
+        "config": {"workload": "c5_2d_sweep_stress", "cells": "%dx%d" % (nx, nx), "directions_unique": slots,
+                   "quadrature": "CL(%d,%d) folded" % (PHI, VZ), "samples_per_gpu": S,
+                   "dsa": "device" if dsa_ok else "not in this build (step = sweep + source update only)",
+                   "l2": "inputs (%.1f GB per step) exceed the 126 MB L2" % (S * nx * nx * 4 * 8 * 3 / 1e9)},
+        "e2e": e2e,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic,
+                     "kernel": "sweep2d_kernel", "per_launch_ms": sweep_ms, "bytes_per_update": BYTES_PER_UPDATE,
+                     "peak_kind": peak_kind,
+                     "fp64": {"achieved_tflops": fp64_ach, "peak_tflops": tf.value, "frac": fp64_ach / tf.value,
+                              "flop_per_update": FLOP_PER_UPDATE, "peak_kind": "measured DFMA probe"}},
+        "kernel_ms": {k: ms_k[i] for i, k in enumerate(capi.PROF_KINDS)},
+        "kernel_launches": {k: int(n_k[i]) for i, k in enumerate(capi.PROF_KINDS)},
+        "gpu_launches": gpu_launches,
+        "clocks": ck,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_reference(args, budget_s=args.cpu_seconds)
+    return line
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm: the oracle restatement of the reference's apply_L
+# (sweep + source update, transport_system.cpp:393-404) on a bounded sample.
+
+def _cpu_worker(payload):
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    from oracle import rte_oracle as ro
+    win, st, ss, reps = payload
+    h = 1.0 / 1024
+    mesh = ro.Mesh.rect_uniform(0.0, win * h, win, 0.0, win * h, win)
+
+    def cell(x, y):
+        ix = np.clip(np.floor(np.asarray(x) / h).astype(np.int64), 0, win - 1)
+        iy = np.clip(np.floor(np.asarray(y) / h).astype(np.int64), 0, win - 1)
+        return ix + win * iy
+    t0 = ro.CoefficientTerm(absorption_weight=lambda x, y: (st - ss)[cell(x, y)],
+                            scattering_weight=lambda x, y: ss[cell(x, y)])
+    p = ro.ProblemDefinition(ro.XY2D, [t0], lambda x, y: 1.0)
+    sys_ = ro.TransportSystem(p, mesh, ro.build_dg_space(mesh), ro.chebyshev_legendre(PHI, VZ), [])
+    rho = np.ones(sys_.n_dof())
+    t = time.perf_counter()
+    for _ in range(reps):
+        rho = sys_.apply_L(rho) + 1e-3
+    return time.perf_counter() - t
+
+
+def cpu_reference(args, budget_s=20.0):
+    import multiprocessing as mp
+    from paper_2402_10488_b200 import configs
+    win = 64
+    st, ss = configs.c5_coefficients(1024, 1, seed=configs.SEEDS["c5"])
+    st = st[0].reshape(1024, 1024)
+    ss = ss[0].reshape(1024, 1024)
+    cores = min(os.cpu_count() or 1, 64)
+    # one calibration apply_L to size the sample to ~budget_s of CPU time
+    probe = _cpu_worker((win, st[:win, :win].ravel().copy(), ss[:win, :win].ravel().copy(), 1))
+    reps = max(1, int(budget_s / max(probe, 1e-3) / 2))
+    jobs = []
+    for k in range(cores):
+        oy, ox = (k * win) % 1024, ((k * win) // 1024 * win) % 1024
+        jobs.append((win, st[oy:oy + win, ox:ox + win].ravel().copy(), ss[oy:oy + win, ox:ox + win].ravel().copy(),
+                     reps))
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(cores) as pool:
+        times = pool.map(_cpu_worker, jobs)
+    wall = time.perf_counter() - t0
+    upd = win * win * (PHI * VZ // 2) * reps * cores
+    return {"value": upd / max(times), "unit": "updates/s", "cores": cores, "kind": "port",
+            "sample": "%d x apply_L (sweep + source update, all %d directions swept as the reference does; updates "
+                      "counted over the %d unique slots) on %d independent %dx%d windows of C5 sample 0, one per "
+                      "process; single-sweep time %.3f s" % (reps, PHI * VZ, PHI * VZ // 2, cores, win, win, probe),
+            "wall_s": wall}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    cb = cpu_reference(args, budget_s=args.cpu_seconds)
+    return {"metric": "sweep cell*direction*sample updates/s", "value": cb["value"], "unit": "updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+            "data": "synthetic (seeded mt19937_64, BASELINE configs[4])",
+            "config": {"workload": "c5_2d_sweep_stress", "cells": "1024x1024", "directions_unique": PHI * VZ // 2,
+                       "samples_per_gpu": 16},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "reference C++ not buildable here (Eigen3/LAPACKE absent); CPU oracle restatement timed"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--nx", type=int, default=1024)
+    ap.add_argument("--samples", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    args = ap.parse_args()
+    rank, world, local = dist_init()
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_b200(args, rank, world, local)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -189,6 +189,19 @@ int rte_romig(rte_ctx* ctx, double* rho0_dev, int* status_host, void* stream);
 int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg, double* rho_dev, rte_si_report* reports_host,
                  double* history_host, char* log_host);
 
+/* ---- measurement ---------------------------------------------------------- */
+/* Per-context kernel timing with CUDA events recorded on the launching stream
+ * around every kernel the context issues, by category.  Off by default. */
+enum rte_prof_kind { RTE_PROF_SWEEP = 0, RTE_PROF_REDUCE = 1, RTE_PROF_DSA = 2, RTE_PROF_ROM = 3,
+                     RTE_PROF_OTHER = 4, RTE_PROF_KINDS = 5 };
+int rte_profile_enable(rte_ctx* ctx, int on);
+/* Synchronizes, returns summed milliseconds and launch counts per kind since
+ * the last read, and clears them. */
+int rte_profile_read(rte_ctx* ctx, double* ms_by_kind, long* launches_by_kind);
+/* FP64 FMA throughput probe (independent DFMA chains on every SM): the
+ * denominator for fp64_fraction.  Returns TFLOP/s (2 flops per FMA). */
+int rte_probe_dfma(int device, double* tflops);
+
 /* ---- host-side discretization helpers (problem setup) ------------------- */
 /* quadrature.cpp:8-39: n-point Gauss-Legendre nodes/weights on [-1,1]. */
 int rte_gauss_legendre_nodes(int n, double* x, double* w);

@@ -16,6 +16,7 @@ RTE_OK, RTE_ERR_INVALID, RTE_ERR_RUNTIME, RTE_ERR_CUDA, RTE_ERR_UNSUPPORTED = 0,
 RTE_SLAB1D, RTE_XY2D = 0, 1
 RTE_SI, RTE_DSA, RTE_ROMSA, RTE_ROMSAD, RTE_ROMIG = 0, 1, 2, 3, 4
 RTE_NORM_ABS, RTE_NORM_REL = 0, 1
+PROF_KINDS = ("sweep", "reduce", "dsa", "rom", "other")
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _ip = ctypes.POINTER(ctypes.c_int)
@@ -78,6 +79,9 @@ SIGNATURES = [
     ("rte_romig", ctypes.c_int, [_vp, _vp, _ip, _vp]),
     ("rte_si_solve", ctypes.c_int, [_vp, ctypes.POINTER(SiConfig), _vp, ctypes.POINTER(SiReport), _dp,
                                     ctypes.c_char_p]),
+    ("rte_profile_enable", ctypes.c_int, [_vp, ctypes.c_int]),
+    ("rte_profile_read", ctypes.c_int, [_vp, _dp, ctypes.POINTER(ctypes.c_long)]),
+    ("rte_probe_dfma", ctypes.c_int, [ctypes.c_int, _dp]),
     ("rte_gauss_legendre_nodes", ctypes.c_int, [ctypes.c_int, _dp, _dp]),
     ("rte_cell_points", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, ctypes.c_double,
                                        ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, _dp, _dp]),

@@ -1,0 +1,71 @@
+"""Seeded synthetic inputs for the BASELINE.json configs.
+
+RNG: std::mt19937_64(seed) with unit draw (gen() >> 11) * 2^-53, exactly as
+the reference's cases.cpp:11-13 (exported by librte_b200.so as
+rte_unit_draws, and restated by the oracle).  Maps: uniform [a,b] ->
+a + (b-a) u; log-uniform [a,b] -> exp(ln a + (ln b - ln a) u).  Training
+samples are drawn first, then test samples; parameter components in the order
+listed in BASELINE.json; an exact collision with an earlier draw is re-drawn
+(cases.cpp:297-313).  No public dataset is involved.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import capi
+
+SEEDS = {"c2": 20260820, "c4": 20260821, "c5": 20260822}
+
+
+def unit_draws(seed: int, n: int) -> np.ndarray:
+    out = np.zeros(n)
+    capi.check(capi.load().rte_unit_draws(int(seed), int(n), capi.dptr(out)))
+    return out
+
+
+def logu(a, b, u):
+    return np.exp(math.log(a) + (math.log(b) - math.log(a)) * u)
+
+
+def uni(a, b, u):
+    return a + (b - a) * u
+
+
+def sample_params(seed: int, ranges, n_train: int, n_test: int):
+    """Training then test parameter vectors; ranges = [(kind, a, b)] with kind
+    'u' (uniform) or 'log' (log-uniform); collisions re-drawn."""
+    need = (n_train + n_test) * len(ranges) * 4 + 64
+    u = iter(unit_draws(seed, need))
+    out = []
+    while len(out) < n_train + n_test:
+        p = [logu(a, b, next(u)) if k == "log" else uni(a, b, next(u)) for (k, a, b) in ranges]
+        if p not in out:
+            out.append(p)
+    return out[:n_train], out[n_train:]
+
+
+def c2_params(n_train=32, n_test=512, seed=SEEDS["c2"]):
+    """configs[1]: mu = (eps ~ logU[1e-3,1], c ~ U[0.9,0.9999])."""
+    return sample_params(seed, [("log", 1e-3, 1.0), ("u", 0.9, 0.9999)], n_train, n_test)
+
+
+def c4_params(n_train=40, n_test=64, seed=SEEDS["c4"]):
+    """configs[3]: mu = (sigma_pin ~ U[1,10], eps ~ logU[1e-3,1e-1], c ~ U[0.9,0.9999])."""
+    return sample_params(seed, [("u", 1.0, 10.0), ("log", 1e-3, 1e-1), ("u", 0.9, 0.9999)], n_train, n_test)
+
+
+def c5_coefficients(nx: int = 1024, samples: int = 16, seed: int = SEEDS["c5"]):
+    """configs[4]: per sample, cell-major draws: sigma_t ~ logU[0.1,100] for all
+    cells, then c ~ U[0.5,0.99] for all cells.  Returns (sigma_t, sigma_s)."""
+    n = nx * nx
+    u = unit_draws(seed, 2 * n * samples)
+    st = np.empty((samples, n))
+    ss = np.empty((samples, n))
+    for s in range(samples):
+        a = u[2 * n * s:2 * n * s + n]
+        b = u[2 * n * s + n:2 * n * (s + 1)]
+        st[s] = logu(0.1, 100.0, a)
+        ss[s] = uni(0.5, 0.99, b) * st[s]
+    return st, ss

@@ -255,6 +255,44 @@ Plan2D plan2d(const rte_ctx* c, int single) {
   return best;
 }
 
+// Independent DFMA chains: 8 per thread, enough warps to saturate the pipe.
+__global__ void dfma_probe_kernel(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;
+}
+
+double probe_dfma_tflops() {
+  int dev = 0, sms = 0;
+  RTE_CUDA(cudaGetDevice(&dev));
+  RTE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  DBuf<double> out;
+  out.alloc(1);
+  const int threads = 512, blocks = sms * 4, iters = 4096;
+  cudaEvent_t e0, e1;
+  RTE_CUDA(cudaEventCreate(&e0));
+  RTE_CUDA(cudaEventCreate(&e1));
+  dfma_probe_kernel<<<blocks, threads>>>(out.p, iters, 0.999999, 1e-7);
+  RTE_CUDA(cudaEventRecord(e0));
+  for (int r = 0; r < 5; ++r) dfma_probe_kernel<<<blocks, threads>>>(out.p, iters, 0.999999, 1e-7);
+  RTE_CUDA(cudaEventRecord(e1));
+  RTE_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  RTE_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double fmas = 5.0 * blocks * threads * (double)iters * 8;
+  return 2.0 * fmas / (ms * 1e-3) / 1e12;
+}
+
 }  // namespace
 
 namespace rte {
@@ -289,6 +327,7 @@ static void transport_apply_ex(rte_ctx* ctx, int mode, int single, const double*
     a.rho_prev = rho_prev;
     a.delta = delta;
     a.change_bits = change_bits;
+    ProfScope ps(ctx, RTE_PROF_SWEEP, st);
     launch_sweep1d(a, st);
     return;
   }
@@ -332,8 +371,14 @@ static void transport_apply_ex(rte_ctx* ctx, int mode, int single, const double*
   a.ybuf = ctx->ws_c.p;
   a.sync = ctx->ws_sync.p;
   a.active = active;
-  launch_sweep2d(a, st);
-  launch_reduce_partials(ctx->S, ctx->ndof, nparts, ctx->ws_part.p, out, rho_prev, delta, change_bits, active, st);
+  {
+    ProfScope ps(ctx, RTE_PROF_SWEEP, st);
+    launch_sweep2d(a, st);
+  }
+  {
+    ProfScope ps(ctx, RTE_PROF_REDUCE, st);
+    launch_reduce_partials(ctx->S, ctx->ndof, nparts, ctx->ws_part.p, out, rho_prev, delta, change_bits, active, st);
+  }
   // a temporary slot table must outlive the kernels queued above
   if (single >= 0) RTE_CUDA(cudaStreamSynchronize(st));
 }
@@ -649,7 +694,9 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
       RTE_CUDA(cudaMemsetAsync(rho, 0, sizeof(double) * S * nd, st));
     }
 
-    DBuf<double> rstar, delta, corr;
+    DBuf<double>& rstar = ctx->ws_a;
+    DBuf<double>& delta = ctx->ws_b;
+    DBuf<double>& corr = ctx->ws_d;
     rstar.alloc((size_t)S * nd);
     delta.alloc((size_t)S * nd);
     corr.alloc((size_t)S * nd);
@@ -662,12 +709,24 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
         bits.zero(st);
         transport_apply(ctx, SRC_MS_RHO | SRC_G | SRC_BC, rho, rstar.p, sst.active, rho, delta.p, bits.p, st);
         RTE_CUDA(cudaMemsetAsync(sst.n_active, 0, sizeof(int), st));
-        si_decide_kernel<<<(S + 127) / 128, 128, 0, st>>>(S, sst, l, cfg);
-        RTE_CUDA(cudaGetLastError());
-        if (need_dsa) dsa_apply(ctx, delta.p, corr.p, sst.kind, 1, st);
-        if (need_rom) rom_correct(ctx, delta.p, corr.p, sst.kind, st);
-        si_finalize_kernel<<<dim3(fin_bx, S), 256, 0, st>>>(S, nd, sst.kind, rstar.p, corr.p, rho);
-        RTE_CUDA(cudaGetLastError());
+        {
+          ProfScope ps(ctx, RTE_PROF_OTHER, st);
+          si_decide_kernel<<<(S + 127) / 128, 128, 0, st>>>(S, sst, l, cfg);
+          RTE_CUDA(cudaGetLastError());
+        }
+        if (need_dsa) {
+          ProfScope ps(ctx, RTE_PROF_DSA, st);
+          dsa_apply(ctx, delta.p, corr.p, sst.kind, 1, st);
+        }
+        if (need_rom) {
+          ProfScope ps(ctx, RTE_PROF_ROM, st);
+          rom_correct(ctx, delta.p, corr.p, sst.kind, st);
+        }
+        {
+          ProfScope ps(ctx, RTE_PROF_OTHER, st, 2);
+          si_finalize_kernel<<<dim3(fin_bx, S), 256, 0, st>>>(S, nd, sst.kind, rstar.p, corr.p, rho);
+          RTE_CUDA(cudaGetLastError());
+        }
         if (l % every == 0 || l == cfg.max_iters || (cfg.fixed_iters > 0 && l >= cfg.fixed_iters)) {
           RTE_CUDA(cudaMemcpyAsync(n_active_host, sst.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
           RTE_CUDA(cudaStreamSynchronize(st));
@@ -711,6 +770,40 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
     }
     if (history) RTE_CUDA(cudaMemcpy(history, hist.p, sizeof(double) * S * cfg.max_iters, cudaMemcpyDeviceToHost));
     if (log) RTE_CUDA(cudaMemcpy(log, lg.p, (size_t)S * cfg.max_iters, cudaMemcpyDeviceToHost));
+  });
+}
+
+// ---- measurement ------------------------------------------------------------
+
+int rte_profile_enable(rte_ctx* ctx, int on) {
+  return guarded(ctx, [&] { ctx->prof = on != 0; });
+}
+
+int rte_profile_read(rte_ctx* ctx, double* ms, long* n) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    for (auto& e : ctx->prof_ev) {
+      RTE_CUDA(cudaEventSynchronize(e.b));
+      float t = 0;
+      RTE_CUDA(cudaEventElapsedTime(&t, e.a, e.b));
+      ctx->prof_ms[e.kind] += t;
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    ctx->prof_ev.clear();
+    for (int k = 0; k < RTE_PROF_KINDS; ++k) {
+      if (ms) ms[k] = ctx->prof_ms[k];
+      if (n) n[k] = ctx->prof_n[k];
+      ctx->prof_ms[k] = 0;
+      ctx->prof_n[k] = 0;
+    }
+  });
+}
+
+int rte_probe_dfma(int device, double* tflops) {
+  return guarded(nullptr, [&] {
+    DeviceGuard dg(device);
+    *tflops = probe_dfma_tflops();
   });
 }
 

@@ -284,8 +284,8 @@ void dsa_apply(rte_ctx* ctx, const double* rhs, double* out, const int* kind, in
     dsa2d_solve(ctx, rhs, out, kind, apply_ms, st);
     return;
   }
-  ctx->ws_d.alloc((size_t)ctx->S * ctx->ncells * 4);
-  Dsa1DSolve a{ctx->S, ctx->ncells, ctx->block, ctx->dsa->fac.p, ctx->ms.p, rhs, out, ctx->ws_d.p, kind, apply_ms};
+  ctx->ws_e.alloc((size_t)ctx->S * ctx->ncells * 4);
+  Dsa1DSolve a{ctx->S, ctx->ncells, ctx->block, ctx->dsa->fac.p, ctx->ms.p, rhs, out, ctx->ws_e.p, kind, apply_ms};
   dsa1d_solve<<<(ctx->S + 31) / 32, 32, 0, st>>>(a);
   RTE_CUDA(cudaGetLastError());
 }

@@ -115,7 +115,7 @@ struct rte_ctx {
   std::vector<int> q_slots[4];
 
   // workspace (lazily sized)
-  rte::DBuf<double> ws_a, ws_b, ws_c, ws_d, ws_part;
+  rte::DBuf<double> ws_a, ws_b, ws_c, ws_d, ws_e, ws_part;
   rte::DBuf<unsigned long long> ws_bits;
   rte::DBuf<unsigned int> ws_sync;
   rte::DBuf<rte::Slot2D> slot_tab;  // cached all-slot sweep table (2D)
@@ -126,6 +126,13 @@ struct rte_ctx {
   rte::DBuf<double> term_mt, term_ms, psi;
   std::vector<double> psi_h;
 
+  // profiling (rte_profile_enable)
+  bool prof = false;
+  struct ProfEv { int kind; cudaEvent_t a, b; };
+  std::vector<ProfEv> prof_ev;
+  double prof_ms[RTE_PROF_KINDS] = {0, 0, 0, 0, 0};
+  long prof_n[RTE_PROF_KINDS] = {0, 0, 0, 0, 0};
+
   rte::DsaState* dsa = nullptr;
   rte::RomState* rom[2] = {nullptr, nullptr};
 
@@ -134,6 +141,30 @@ struct rte_ctx {
 };
 
 namespace rte {
+
+// RAII scope that brackets the kernels launched inside it with CUDA events
+// on `st` when the context profiles (rte_profile_enable).
+struct ProfScope {
+  rte_ctx* c;
+  int kind;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  int launches;
+  ProfScope(rte_ctx* ctx, int k, cudaStream_t s, int n = 1) : c(ctx), kind(k), st(s), launches(n) {
+    if (c && c->prof) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (c && c->prof) {
+      cudaEventRecord(b, st);
+      c->prof_ev.push_back({kind, a, b});
+      c->prof_n[kind] += launches;
+    }
+  }
+};
 
 // ---- kernel launchers (implemented in the .cu files) ----------------------
 

@@ -278,8 +278,9 @@ class TransportBatch:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and capi._lib is not None:
-            capi._lib.rte_destroy(h)
+        lib = getattr(capi, "_lib", None) if capi is not None else None
+        if h is not None and lib is not None:
+            lib.rte_destroy(h)
             self._h = None
 
     # -- helpers --
