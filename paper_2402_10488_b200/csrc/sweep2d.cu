@@ -34,11 +34,13 @@
 namespace rte {
 namespace {
 
-constexpr int kNW = 8;  // warps per CTA
-constexpr int kC = 8;   // steps per synchronisation chunk
+constexpr int kNW = 8;   // warps per CTA (direction subgroups)
+constexpr int kC = 4;    // steps per synchronisation chunk
+constexpr int kRC = 40;  // ring slots (columns): >= 31 + 2 * kC
+constexpr int kRP = 162; // ring slot pitch in doubles (5 comps x 32 rows, padded to even)
 
 struct DirConst {
-  double a, b, w, e1, e2, tb, be, bcx, bcy, pad;
+  double a, b, w, c4b, k1, a2, k2, a12, k6, tb, be, bcx, bcy, pad0, pad1, pad2;
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -49,35 +51,54 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Canonical cell solve.  In: q (reflected source moments), X (incoming x-face
-// traces per y-mode, pre-scaled by a), Y (incoming y-face traces per x-mode,
-// pre-scaled by b).  Out: f and the outgoing traces.
-__device__ __forceinline__ void solve_cell(const DirConst& dc, double sig, const double q[4], double X0,
+// 1/x for x > 0 (normal): hardware approximation + two Newton steps (~1 ulp).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Canonical cell solve (see file header).  q: reflected source moments;
+// X: incoming x-face traces per y-mode (pre-scaled by a); Y: incoming
+// y-face traces per x-mode (pre-scaled by b).
+__device__ __forceinline__ void solve_cell(const DirConst& dc, double sig, double sig2, const double q[4], double X0,
                                            double X1, double Y0, double Y1, double f[4], double& Xo0,
                                            double& Xo1, double& Yo0, double& Yo1) {
   const double s3 = kSqrt3;
-  const double r00 = q[0] + X0 + Y0;
+  const double r00 = (q[0] + Y0) + X0;
   const double r01 = fma(-s3, X0, q[1] + Y1);
   const double r10 = fma(-s3, Y0, q[2] + X1);
-  const double r11 = fma(-s3, X1, fma(-s3, Y1, q[3]));
+  const double r11 = fma(-s3, X1 + Y1, q[3]);
+  // Delta = del I + al K with del = sig^2 + 4 b sig + 6(b^2 - a^2),
+  // al = 2 a sig + 4 a b + 4 a^2; det(Delta) = del (del + 4 al) + 6 al^2.
+  const double del = fma(dc.c4b, sig, sig2 + dc.k1);
+  const double al = fma(dc.a2, sig, dc.k2);
+  const double al6 = fma(dc.a12, sig, dc.k6);
+  const double u4 = fma(4.0, al, del);
+  const double inv = fast_rcp(fma(del, u4, al6 * al));
+  const double c1 = u4 * inv, c2 = -al * inv;
   const double p = sig + dc.b;
   const double tt = p + dc.tb;
-  const double del = fma(p, tt, dc.e1);
-  const double al = fma(2.0 * dc.a, p, dc.e2);
-  const double u4 = fma(4.0, al, del);
-  const double det = fma(del, u4, 6.0 * al * al);
-  const double inv = 1.0 / det;
-  const double c1 = u4 * inv, c2 = -al * inv;
-  // K r
   const double k00 = fma(s3, r01, r00), k01 = fma(3.0, r01, -s3 * r00);
   const double k10 = fma(s3, r11, r10), k11 = fma(3.0, r11, -s3 * r10);
-  // g0 = tt r0 + a K r0 - be r1 ; g1 = p r1 + a K r1 + be r0
   const double g00 = fma(tt, r00, fma(dc.a, k00, -dc.be * r10));
   const double g01 = fma(tt, r01, fma(dc.a, k01, -dc.be * r11));
   const double g10 = fma(p, r10, fma(dc.a, k10, dc.be * r00));
   const double g11 = fma(p, r11, fma(dc.a, k11, dc.be * r01));
-  // f = c1 g + c2 K g
   const double h00 = fma(s3, g01, g00), h01 = fma(3.0, g01, -s3 * g00);
   const double h10 = fma(s3, g11, g10), h11 = fma(3.0, g11, -s3 * g10);
   f[0] = fma(c1, g00, c2 * h00);
@@ -90,11 +111,96 @@ __device__ __forceinline__ void solve_cell(const DirConst& dc, double sig, const
   Yo1 = dc.b * fma(s3, f[3], f[1]);
 }
 
+struct Smem {
+  double* red;    // [kC][kNW][4][32]
+  double* ring;   // [kRC][kRP]: comps 0..3 = reflected q, 4 = sigma_t; row fastest
+  double* stage;  // [kC*32][10]: raw rho(4), G(4), sigma_t, sigma_s of the next columns
+  double* ystg;   // [2][kC][ndir][2]
+  DirConst* tab;  // [ndir]
+};
+
+template <int D>
+__device__ __forceinline__ void issue_chunk_loads(const Sweep2DArgs& a, const Smem& sm, int c0, int band,
+                                                  int qx, int qy, int s, const double2* ybelow, int ybuf_slot) {
+  const int nx = a.nx, ny = a.ny;
+  const long ncell = (long)nx * ny, nd = 4 * ncell;
+  const int t = threadIdx.x;
+  // raw cell data: 128 cells, two threads per cell
+  {
+    const int cell = t & (kC * 32 - 1);
+    const int part = t / (kC * 32);
+    const int col = c0 + (cell >> 5), row = band * 32 + (cell & 31);
+    if (part < 2 && col < nx && row < ny) {
+      const int ix = qx ? nx - 1 - col : col;
+      const int iy = qy ? ny - 1 - row : row;
+      const long pc = (long)iy * nx + ix;
+      double* dst = sm.stage + cell * 10;
+      if (part == 0) {
+        const double* src = a.rho + (long)s * nd + 4 * pc;
+        cp_async16(dst, src);
+        cp_async16(dst + 2, src + 2);
+        cp_async8(dst + 8, a.sig_t + (long)s * ncell + pc);
+      } else {
+        const double* src = a.g + (a.g_shared ? 0 : (long)s * nd) + 4 * pc;
+        cp_async16(dst + 4, src);
+        cp_async16(dst + 6, src + 2);
+        cp_async8(dst + 9, a.sig_s + (long)s * ncell + pc);
+      }
+    }
+  }
+  // band-boundary traces from the band below
+  if (band > 0) {
+    constexpr int ndir = kNW * D;
+    for (int i = t; i < kC * ndir; i += blockDim.x) {
+      const int kk = i / ndir, dd = i - kk * ndir;
+      const int col = c0 + kk;
+      if (col < nx) cp_async16(sm.ystg + (((ybuf_slot * kC + kk) * ndir + dd) << 1), ybelow + (long)col * ndir + dd);
+    }
+  }
+  cp_async_commit();
+}
+
+// stage -> ring (reflected source moments + sigma_t) for columns c0..c0+kC-1
+__device__ __forceinline__ void convert_chunk(const Sweep2DArgs& a, const Smem& sm, int c0, int band, double sx,
+                                              double sy) {
+  const int t = threadIdx.x;
+  if (t >= kC * 32) return;
+  const int col = c0 + (t >> 5), row = t & 31;
+  const bool ok = col < a.nx && band * 32 + row < a.ny;
+  const double* r = sm.stage + t * 10;
+  double q0 = 0, q1 = 0, q2 = 0, q3 = 0, sg = 1.0;
+  if (ok) {
+    sg = r[8];
+    if (a.mode & SRC_RAW) {
+      q0 = r[0]; q1 = r[1]; q2 = r[2]; q3 = r[3];
+    } else {
+      if (a.mode & SRC_MS_RHO) {
+        const double ss = r[9];
+        q0 = ss * r[0]; q1 = ss * r[1]; q2 = ss * r[2]; q3 = ss * r[3];
+      }
+      if (a.mode & SRC_G) {
+        q0 += r[4]; q1 += r[5]; q2 += r[6]; q3 += r[7];
+      }
+    }
+  }
+  double* dst = sm.ring + (col % kRC) * kRP + row;
+  dst[0] = q0;
+  dst[32] = sx * q1;
+  dst[64] = sy * q2;
+  dst[96] = sx * sy * q3;
+  dst[128] = sg;
+}
+
 template <int D>
 __global__ void __launch_bounds__(kNW * 32, 2) sweep2d_kernel(const Sweep2DArgs a) {
-  extern __shared__ double sm[];
-  double* red = sm;  // [kC][kNW][32][4]
-  DirConst* tab = reinterpret_cast<DirConst*>(sm + kC * kNW * 32 * 4);  // [kNW*D]
+  extern __shared__ double smraw[];
+  constexpr int ndir = kNW * D;
+  Smem sm;
+  sm.red = smraw;
+  sm.ring = sm.red + kC * kNW * 4 * 32;
+  sm.stage = sm.ring + kRC * kRP;
+  sm.ystg = sm.stage + kC * 32 * 10;
+  sm.tab = reinterpret_cast<DirConst*>(sm.ystg + 2 * kC * ndir * 2);
   __shared__ int item_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nx = a.nx, ny = a.ny;
@@ -102,7 +208,6 @@ __global__ void __launch_bounds__(kNW * 32, 2) sweep2d_kernel(const Sweep2DArgs 
   const int nbands = (ny + 31) / 32;
   const int per_band = a.S * 4 * a.groups;
   const int total = nbands * per_band;
-  const int ndir = kNW * D;
   unsigned* ticket = a.sync;
   unsigned* progress = a.sync + 1;
 
@@ -124,104 +229,91 @@ __global__ void __launch_bounds__(kNW * 32, 2) sweep2d_kernel(const Sweep2DArgs 
     }
     const int qx = qd & 1, qy = qd >> 1;
     const double sx = qx ? -1.0 : 1.0, sy = qy ? -1.0 : 1.0;
-
-    // direction table of this item
     for (int i = threadIdx.x; i < ndir; i += blockDim.x) {
       const Slot2D sl = a.slots[qd * a.nq_pad + grp * ndir + i];
       DirConst d;
       d.a = sl.a;
       d.b = sl.b;
       d.w = sl.w;
-      d.e1 = 3.0 * sl.b * sl.b - 6.0 * sl.a * sl.a;
-      d.e2 = 2.0 * sl.a * sl.b + 4.0 * sl.a * sl.a;
+      d.c4b = 4.0 * sl.b;
+      d.k1 = 6.0 * (sl.b * sl.b - sl.a * sl.a);
+      d.a2 = 2.0 * sl.a;
+      d.k2 = 4.0 * sl.a * sl.b + 4.0 * sl.a * sl.a;
+      d.a12 = 12.0 * sl.a;
+      d.k6 = 6.0 * d.k2;
       d.tb = 2.0 * sl.b;
       d.be = kSqrt3 * sl.b;
       d.bcx = (a.mode & SRC_BC) ? sl.bcx : 0.0;
       d.bcy = (a.mode & SRC_BC) ? sl.bcy : 0.0;
-      tab[i] = d;
-    }
-    __syncthreads();
-
-    const int yr = band * 32 + lane;  // canonical row
-    const bool row_ok = yr < ny;
-    const int iy = qy ? ny - 1 - yr : yr;
-    double X[D][2], Y[D][2];
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      X[d][0] = tab[warp * D + d].bcx;
-      X[d][1] = 0.0;
-      Y[d][0] = 0.0;
-      Y[d][1] = 0.0;
+      sm.tab[i] = d;
     }
     const double2* ybelow =
         reinterpret_cast<const double2*>(a.ybuf) + ((long)(ibase * nbands + band - 1) * nx) * ndir;
     double2* yabove = reinterpret_cast<double2*>(a.ybuf) + ((long)(ibase * nbands + band) * nx) * ndir;
-    const double* gsrc = a.g + (a.g_shared ? 0 : (long)s * nd);
-    const double* rho = a.rho + (long)s * nd;
-    const double* sgt = a.sig_t + (long)s * ncell;
-    const double* sgs = a.sig_s + (long)s * ncell;
     double* part = a.part + ((long)(qd * a.groups + grp) * a.S + s) * nd;
+    const unsigned* prod = progress + ibase * nbands + band - 1;
 
+    // prologue: columns [0, kC)
+    if (band > 0 && threadIdx.x == 0) {
+      const unsigned need = (unsigned)min(nx, kC);
+      while (ld_acquire(prod) < need) __nanosleep(64);
+    }
+    __syncthreads();
+    issue_chunk_loads<D>(a, sm, 0, band, qx, qy, s, ybelow, 0);
+    cp_async_wait_all();
+    __syncthreads();
+    convert_chunk(a, sm, 0, band, sx, sy);
+
+    const int yr = band * 32 + lane;
+    const bool row_ok = yr < ny;
+    double X[D][2], Y[D][2];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      X[d][0] = sm.tab[warp * D + d].bcx;
+      X[d][1] = 0.0;
+      Y[d][0] = 0.0;
+      Y[d][1] = 0.0;
+    }
     const int nsteps = nx + 31;
+    int ys = 0;  // ystg slot holding the current chunk
     for (int k0 = 0; k0 < nsteps; k0 += kC) {
-      if (band > 0) {
-        if (threadIdx.x == 0) {
-          const unsigned need = (unsigned)min(nx, k0 + kC);
-          const unsigned* pc = progress + ibase * nbands + band - 1;
-          while (ld_acquire(pc) < need) __nanosleep(100);
-        }
-        __syncthreads();
+      if (band > 0 && threadIdx.x == 0) {
+        const unsigned need = (unsigned)min(nx, k0 + 2 * kC);
+        while (ld_acquire(prod) < need) __nanosleep(64);
       }
+      __syncthreads();
+      if (k0 + kC < nx) issue_chunk_loads<D>(a, sm, k0 + kC, band, qx, qy, s, ybelow, ys ^ 1);
 #pragma unroll 1
       for (int kk = 0; kk < kC; ++kk) {
         const int x = k0 + kk - lane;
         const bool ok = row_ok && x >= 0 && x < nx;
-        double q[4] = {0.0, 0.0, 0.0, 0.0};
-        double sig = 1.0;
-        long cell = 0;
-        if (ok) {
-          const int ix = qx ? nx - 1 - x : x;
-          cell = (long)iy * nx + ix;
-          sig = sgt[cell];
-          if (a.mode & SRC_RAW) {
-            const double2 r01 = *reinterpret_cast<const double2*>(rho + 4 * cell);
-            const double2 r23 = *reinterpret_cast<const double2*>(rho + 4 * cell + 2);
-            q[0] = r01.x; q[1] = r01.y; q[2] = r23.x; q[3] = r23.y;
-          } else {
-            if (a.mode & SRC_MS_RHO) {
-              const double ss = sgs[cell];
-              const double2 r01 = *reinterpret_cast<const double2*>(rho + 4 * cell);
-              const double2 r23 = *reinterpret_cast<const double2*>(rho + 4 * cell + 2);
-              q[0] = ss * r01.x; q[1] = ss * r01.y; q[2] = ss * r23.x; q[3] = ss * r23.y;
-            }
-            if (a.mode & SRC_G) {
-              const double2 g01 = *reinterpret_cast<const double2*>(gsrc + 4 * cell);
-              const double2 g23 = *reinterpret_cast<const double2*>(gsrc + 4 * cell + 2);
-              q[0] += g01.x; q[1] += g01.y; q[2] += g23.x; q[3] += g23.y;
-            }
-          }
-          q[1] *= sx;
-          q[2] *= sy;
-          q[3] *= sx * sy;
-        }
+        const double* rg = sm.ring + (((x % kRC) + kRC) % kRC) * kRP + lane;
+        double q[4];
+        q[0] = rg[0];
+        q[1] = rg[32];
+        q[2] = rg[64];
+        q[3] = rg[96];
+        const double sig = ok ? rg[128] : 1.0;
+        if (!ok) q[0] = q[1] = q[2] = q[3] = 0.0;
+        const double sig2 = sig * sig;
+        const double* yst = sm.ystg + ((ys * kC + kk) * ndir + warp * D) * 2;
         double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-          const DirConst& dc = tab[warp * D + d];
+          const DirConst& dc = sm.tab[warp * D + d];
           double Y0 = __shfl_up_sync(0xffffffffu, Y[d][0], 1);
           double Y1 = __shfl_up_sync(0xffffffffu, Y[d][1], 1);
           if (lane == 0) {
             if (band == 0) {
               Y0 = dc.bcy;
               Y1 = 0.0;
-            } else if (x >= 0 && x < nx) {
-              const double2 yb = __ldcg(ybelow + (long)x * ndir + warp * D + d);
-              Y0 = yb.x;
-              Y1 = yb.y;
+            } else {
+              Y0 = yst[2 * d];
+              Y1 = yst[2 * d + 1];
             }
           }
           double f[4], xo0, xo1, yo0, yo1;
-          solve_cell(dc, sig, q, X[d][0], X[d][1], Y0, Y1, f, xo0, xo1, yo0, yo1);
+          solve_cell(dc, sig, sig2, q, X[d][0], X[d][1], Y0, Y1, f, xo0, xo1, yo0, yo1);
           Y[d][0] = yo0;
           Y[d][1] = yo1;
           if (ok) {
@@ -234,47 +326,60 @@ __global__ void __launch_bounds__(kNW * 32, 2) sweep2d_kernel(const Sweep2DArgs 
             if (lane == 31 && band + 1 < nbands) __stcg(yabove + (long)x * ndir + warp * D + d, make_double2(yo0, yo1));
           }
         }
-        double* rr = red + ((kk * kNW + warp) * 32 + lane) * 4;
+        double* rr = sm.red + ((kk * kNW + warp) * 4) * 32 + lane;
         rr[0] = acc0;
-        rr[1] = acc1;
-        rr[2] = acc2;
-        rr[3] = acc3;
+        rr[32] = acc1;
+        rr[64] = acc2;
+        rr[96] = acc3;
       }
+      cp_async_wait_all();
       __syncthreads();
       // fixed-order reduction over the warps (direction subgroups) of the chunk
-      for (int t = threadIdx.x; t < kC * 32; t += blockDim.x) {
-        const int kk = t >> 5, ln = t & 31;
-        const int x = k0 + kk - ln;
-        const int yy = band * 32 + ln;
-        if (x >= 0 && x < nx && yy < ny) {
-          double v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-          for (int w = 0; w < kNW; ++w) {
-            const double* rr = red + ((kk * kNW + w) * 32 + ln) * 4;
-            v0 += rr[0];
-            v1 += rr[1];
-            v2 += rr[2];
-            v3 += rr[3];
+      {
+        const int t = threadIdx.x;
+        if (t < kC * 32) {
+          const int kk = t >> 5, ln = t & 31;
+          const int x = k0 + kk - ln;
+          const int yy = band * 32 + ln;
+          if (x >= 0 && x < nx && yy < ny) {
+            double v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+            for (int w = 0; w < kNW; ++w) {
+              const double* rr = sm.red + ((kk * kNW + w) * 4) * 32 + ln;
+              v0 += rr[0];
+              v1 += rr[32];
+              v2 += rr[64];
+              v3 += rr[96];
+            }
+            const int ix = qx ? nx - 1 - x : x;
+            const int iyy = qy ? ny - 1 - yy : yy;
+            double* o = part + 4 * ((long)iyy * nx + ix);
+            __stcs(reinterpret_cast<double2*>(o), make_double2(v0, sx * v1));
+            __stcs(reinterpret_cast<double2*>(o + 2), make_double2(sy * v2, sx * sy * v3));
           }
-          const int ix = qx ? nx - 1 - x : x;
-          const int iyy = qy ? ny - 1 - yy : yy;
-          double* o = part + 4 * ((long)iyy * nx + ix);
-          *reinterpret_cast<double2*>(o) = make_double2(v0, sx * v1);
-          *reinterpret_cast<double2*>(o + 2) = make_double2(sy * v2, sx * sy * v3);
         }
       }
-      __syncthreads();
+      if (k0 + kC < nx) convert_chunk(a, sm, k0 + kC, band, sx, sy);
+      ys ^= 1;
       if (threadIdx.x == 0 && band + 1 < nbands) {
         __threadfence();
         const int avail = min(nx, max(0, k0 + kC - 31));
         st_release(progress + ibase * nbands + band, (unsigned)avail);
       }
     }
+    __syncthreads();
   }
 }
 
 template <int D>
+size_t smem_bytes() {
+  return sizeof(double) * ((size_t)kC * kNW * 4 * 32 + (size_t)kRC * kRP + (size_t)kC * 32 * 10 +
+                           (size_t)2 * kC * kNW * D * 2) +
+         sizeof(DirConst) * kNW * D;
+}
+
+template <int D>
 void launch_d(const Sweep2DArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)kC * kNW * 32 * 4 * 8 + (size_t)kNW * D * sizeof(DirConst);
+  const size_t smem = smem_bytes<D>();
   static int max_ctas = -1;
   if (max_ctas < 0) {
     RTE_CUDA(cudaFuncSetAttribute(sweep2d_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
