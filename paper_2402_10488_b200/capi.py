@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librte_b200.so")
+LIB_PATH = os.environ.get("RTE_B200_LIB", os.path.join(HERE, "librte_b200.so"))
 
 RTE_OK, RTE_ERR_INVALID, RTE_ERR_RUNTIME, RTE_ERR_CUDA, RTE_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 RTE_SLAB1D, RTE_XY2D = 0, 1

@@ -34,7 +34,13 @@
 namespace rte {
 namespace {
 
-constexpr int kNW = 8;   // warps per CTA (direction subgroups)
+#ifndef RTE_SWEEP_NW
+#define RTE_SWEEP_NW 8
+#endif
+#ifndef RTE_SWEEP_MINB
+#define RTE_SWEEP_MINB 2
+#endif
+constexpr int kNW = RTE_SWEEP_NW;  // warps per CTA (direction subgroups)
 constexpr int kC = 4;    // steps per synchronisation chunk
 constexpr int kRC = 40;  // ring slots (columns): >= 31 + 2 * kC
 constexpr int kRP = 162; // ring slot pitch in doubles (5 comps x 32 rows, padded to even)
@@ -192,7 +198,7 @@ __device__ __forceinline__ void convert_chunk(const Sweep2DArgs& a, const Smem& 
 }
 
 template <int D>
-__global__ void __launch_bounds__(kNW * 32, 2) sweep2d_kernel(const Sweep2DArgs a) {
+__global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const Sweep2DArgs a) {
   extern __shared__ double smraw[];
   constexpr int ndir = kNW * D;
   Smem sm;
@@ -297,34 +303,34 @@ __global__ void __launch_bounds__(kNW * 32, 2) sweep2d_kernel(const Sweep2DArgs 
         if (!ok) q[0] = q[1] = q[2] = q[3] = 0.0;
         const double sig2 = sig * sig;
         const double* yst = sm.ystg + ((ys * kC + kk) * ndir + warp * D) * 2;
+        const bool lane0 = lane == 0;
+        const bool from_below = lane0 && band > 0;
         double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+        // Branch-free direction loop: the D chains are independent and the
+        // compiler interleaves them (no reconvergence points inside).
 #pragma unroll
         for (int d = 0; d < D; ++d) {
           const DirConst& dc = sm.tab[warp * D + d];
+          const double ys0 = yst[2 * d], ys1 = yst[2 * d + 1];
           double Y0 = __shfl_up_sync(0xffffffffu, Y[d][0], 1);
           double Y1 = __shfl_up_sync(0xffffffffu, Y[d][1], 1);
-          if (lane == 0) {
-            if (band == 0) {
-              Y0 = dc.bcy;
-              Y1 = 0.0;
-            } else {
-              Y0 = yst[2 * d];
-              Y1 = yst[2 * d + 1];
-            }
-          }
+          Y0 = lane0 ? (from_below ? ys0 : dc.bcy) : Y0;
+          Y1 = lane0 ? (from_below ? ys1 : 0.0) : Y1;
           double f[4], xo0, xo1, yo0, yo1;
           solve_cell(dc, sig, sig2, q, X[d][0], X[d][1], Y0, Y1, f, xo0, xo1, yo0, yo1);
           Y[d][0] = yo0;
           Y[d][1] = yo1;
-          if (ok) {
-            X[d][0] = xo0;
-            X[d][1] = xo1;
-            acc0 = fma(dc.w, f[0], acc0);
-            acc1 = fma(dc.w, f[1], acc1);
-            acc2 = fma(dc.w, f[2], acc2);
-            acc3 = fma(dc.w, f[3], acc3);
-            if (lane == 31 && band + 1 < nbands) __stcg(yabove + (long)x * ndir + warp * D + d, make_double2(yo0, yo1));
-          }
+          X[d][0] = ok ? xo0 : X[d][0];
+          X[d][1] = ok ? xo1 : X[d][1];
+          const double wv = ok ? dc.w : 0.0;
+          acc0 = fma(wv, f[0], acc0);
+          acc1 = fma(wv, f[1], acc1);
+          acc2 = fma(wv, f[2], acc2);
+          acc3 = fma(wv, f[3], acc3);
+        }
+        if (lane == 31 && ok && band + 1 < nbands) {
+#pragma unroll
+          for (int d = 0; d < D; ++d) __stcg(yabove + (long)x * ndir + warp * D + d, make_double2(Y[d][0], Y[d][1]));
         }
         double* rr = sm.red + ((kk * kNW + warp) * 4) * 32 + lane;
         rr[0] = acc0;
