@@ -169,6 +169,13 @@ int rte_dsa_setup(rte_ctx* ctx, void* stream);
 int rte_dsa_solve_density(rte_ctx* ctx, const double* rhs_dev, double* out_dev, void* stream);
 /* DsaOperator::correct (dsa.cpp:275-277): C * Ms * delta. */
 int rte_dsa_correct(rte_ctx* ctx, const double* delta_dev, double* out_dev, void* stream);
+/* XY geometry: the coupled system is solved iteratively (BiCGStab with a
+ * multigrid V-cycle preconditioner) to relative residual `tol` (default
+ * 1e-12) within `max_iters` (default 1000); <= 0 keeps the current value.
+ * The reference uses a direct SparseLU (dsa.cpp:253). */
+int rte_dsa_set_tolerance(rte_ctx* ctx, double tol, int max_iters);
+/* Krylov iterations of the last XY DSA solve (0 for slab: direct). */
+int rte_dsa_last_iterations(const rte_ctx* ctx);
 /* DsaOperator::coupled_dim (dsa.hpp:48). */
 long rte_dsa_coupled_dim(const rte_ctx* ctx);
 

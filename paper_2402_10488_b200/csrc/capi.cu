@@ -612,6 +612,17 @@ int rte_dsa_correct(rte_ctx* ctx, const double* delta, double* out, void* stream
 
 long rte_dsa_coupled_dim(const rte_ctx* ctx) { return dsa_coupled_dim(ctx); }
 
+int rte_dsa_set_tolerance(rte_ctx* ctx, double tol, int max_iters) {
+  return guarded(ctx, [&] {
+    RTE_REQUIRE(ctx->geom == RTE_XY2D, RTE_ERR_INVALID, "dsa: tolerance applies to the xy (iterative) solver only");
+    DeviceGuard dg(ctx->device);
+    if (!ctx->dsa) dsa_setup(ctx, nullptr);
+    dsa2d_set_tolerance(ctx, tol, max_iters);
+  });
+}
+
+int rte_dsa_last_iterations(const rte_ctx* ctx) { return ctx->geom == RTE_XY2D ? dsa2d_last_iters(ctx) : 0; }
+
 int rte_rom_load(rte_ctx* ctx, int which, const rte_rom* rom) {
   return guarded(ctx, [&] {
     DeviceGuard dg(ctx->device);

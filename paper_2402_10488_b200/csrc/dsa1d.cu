@@ -20,15 +20,6 @@
 
 namespace rte {
 
-struct DsaState {
-  int nf = 2;
-  long dim = 0;
-  double m1 = 0, m2 = 0, m3 = 0;
-  DBuf<double> fac;  // slab: [S][N][48]
-  // 2D state lives in dsa2d.cu
-  void* impl2d = nullptr;
-};
-
 namespace {
 
 // 4x4 inverse by Gauss-Jordan with partial pivoting (row-major).

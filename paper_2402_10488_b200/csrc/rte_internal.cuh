@@ -41,6 +41,20 @@ struct DBuf {
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
   ~DBuf() { release(); }
   void release() {
     if (p) cudaFree(p);
@@ -82,7 +96,13 @@ struct Slot2D {
   double bcx, bcy;  // inflow ghost traces (already scaled), see sweep2d.cu
 };
 
-struct DsaState;
+struct DsaState {
+  int nf = 2;
+  long dim = 0;
+  double m1 = 0, m2 = 0, m3 = 0;
+  DBuf<double> fac;         // slab: [S][N][48] block-Thomas factors
+  void* impl2d = nullptr;   // xy: multigrid/Krylov state (dsa2d.cu)
+};
 struct RomState;
 
 }  // namespace rte
@@ -247,6 +267,8 @@ void launch_residual(int S, long ndof, const double* rho, const double* rho_star
 void dsa_setup(rte_ctx* ctx, cudaStream_t st);
 void dsa_solve_density(rte_ctx* ctx, const double* rhs, double* out, const int* kind_mask, cudaStream_t st);
 void dsa_destroy(DsaState* d);
+int dsa2d_last_iters(const rte_ctx* ctx);
+void dsa2d_set_tolerance(rte_ctx* ctx, double tol, int maxit);
 long dsa_coupled_dim(const rte_ctx* ctx);
 
 // ROM

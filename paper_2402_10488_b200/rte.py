@@ -385,6 +385,13 @@ class DsaOperator:
     def coupled_dim(self) -> int:
         return capi.load().rte_dsa_coupled_dim(self.batch._h)
 
+    def set_tolerance(self, tol: float, max_iters: int = 0) -> None:
+        """XY only: relative residual of the iterative coupled solve."""
+        self.batch._call(capi.load().rte_dsa_set_tolerance, float(tol), int(max_iters))
+
+    def last_iterations(self) -> int:
+        return capi.load().rte_dsa_last_iterations(self.batch._h)
+
     def solve_density(self, rhs):
         b = self.batch
         rhs = b._dev(rhs, (b.S, b.nd))

@@ -186,3 +186,61 @@ def test_2d_sweep_is_deterministic():
     a = batch.fixed_point(rho).cpu().numpy()
     b = batch.fixed_point(rho).cpu().numpy()
     assert np.array_equal(a, b)
+
+
+DSA_CASES_2D = CASES_2D + [
+    ("c3_32", lambda m: prob2d_const(m, 10 * 0.001, 10 * 0.999, lambda x, y: 1.0), 32, 32, (16, 8), [[]],
+     (0.0, 1.0, 0.0, 1.0)),
+    ("thin_random_32", None, 32, 32, (8, 4), [[]], (0.0, 1.0, 0.0, 1.0)),
+]
+
+
+def _thin_random(mod, nx=32):
+    rng = np.random.default_rng(5)
+    st = np.exp(np.log(0.1) + (np.log(100.0) - np.log(0.1)) * rng.uniform(size=(nx, nx))) * nx / 1024
+    c = 0.5 + 0.49 * rng.uniform(size=(nx, nx))
+
+    def idx(x, y):
+        ix = np.clip(np.floor(np.asarray(x) * nx).astype(int), 0, nx - 1)
+        iy = np.clip(np.floor(np.asarray(y) * nx).astype(int), 0, nx - 1)
+        return iy, ix
+    t0 = mod.CoefficientTerm(absorption_weight=lambda x, y: ((1 - c) * st)[idx(x, y)],
+                             scattering_weight=lambda x, y: (c * st)[idx(x, y)])
+    return mod.ProblemDefinition(mod.XY2D, [t0], lambda x, y: 1.0)
+
+
+def _dsa_case(case):
+    name, fn, nx, ny, cl, mus, ext = case
+    if fn is None:
+        fn = _thin_random
+    return pair_2d(fn, nx, ny, cl, mus, ext)
+
+
+@pytest.mark.parametrize("case", DSA_CASES_2D, ids=[c[0] for c in DSA_CASES_2D])
+def test_2d_dsa_parity(case):
+    osys, batch = _dsa_case(case)
+    R = rte()
+    dsa = R.DsaOperator(batch)
+    assert dsa.coupled_dim() == 3 * osys[0].n_dof()
+    rhs = np.random.default_rng(9).uniform(-1, 1, (len(osys), osys[0].n_dof()))
+    x = dsa.solve_density(rhs).cpu().numpy()
+    c = dsa.correct(rhs).cpu().numpy()
+    assert dsa.last_iterations() > 0
+    for s, o in enumerate(osys):
+        od = ro.build_dsa(o)
+        assert rel_l2(x[s], od.solve_density(rhs[s])) < 1e-9
+        assert rel_l2(c[s], od.correct(rhs[s])) < 1e-9
+
+
+@pytest.mark.parametrize("case", [DSA_CASES_2D[0], DSA_CASES_2D[3]], ids=["box_inflow", "c3_32"])
+def test_2d_dsa_solve_parity(case):
+    osys, batch = _dsa_case(case)
+    R = rte()
+    eps = 1e-10
+    rho, reps = R.sisa_solve(batch, "DSA", R.SolveConfig(eps_sisa=eps, max_iters=500))
+    o_rho, o_rep = ro.sisa_solve(osys[0], ro.DsaStrategy(ro.build_dsa(osys[0])), ro.SolveConfig(eps_sisa=eps,
+                                                                                              max_iters=500))
+    assert reps[0].converged and o_rep.converged
+    assert reps[0].iterations == o_rep.iterations, (reps[0].iterations, o_rep.iterations)
+    assert rel_l2(rho.cpu().numpy()[0], o_rho) < CONV_TOL
+    np.testing.assert_allclose(reps[0].change_history, o_rep.change_history, rtol=1e-5, atol=1e-13)
