@@ -780,7 +780,7 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
     Level& lv = d->L[l];
     if (l > 0) {
       const Level& f = d->L[l - 1];
-      k_galerkin_diag<<<nblocks((long)S * lv.nc), 128, 0, st>>>(S, f.nx, f.ny, f.D.p, d->P.p,
+      k_galerkin_diag<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, f.nx, f.ny, f.D.p, d->P.p,
                                                                  d->Dint.p + (l - 1) * NB2, lv.D.p);
       RTE_CUDA(cudaGetLastError());
     }
@@ -795,7 +795,7 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
     DBuf<double> A;
     A.alloc((size_t)S * n * n);
     d->coarse_inv.alloc((size_t)S * n * n);
-    k_dense_coarse<<<nblocks((long)S * lc.nc), 64, 0, st>>>(S, lc.nx, lc.ny, lc.D.p, lc.nbr.p, A.p);
+    k_dense_coarse<<<nblocks((long)S * lc.nc, 64), 64, 0, st>>>(S, lc.nx, lc.ny, lc.D.p, lc.nbr.p, A.p);
     RTE_CUDA(cudaGetLastError());
     k_dense_inverse<<<S, 1024, 0, st>>>(n, A.p, d->coarse_inv.p);
     RTE_CUDA(cudaGetLastError());
