@@ -58,6 +58,9 @@ struct Dsa2D {
   int maxit = 1000;
   int nu = 2;
   int last_iters = 0;
+  int nblk = 64;
+  const double* sgt = nullptr;
+  const double* sgs = nullptr;
 };
 
 constexpr int kDotBlocks = 64;
@@ -129,6 +132,98 @@ Mat galerkin(const Mat& A, const Mat& Pl, const Mat& Pr) {
 // device kernels
 
 __constant__ double c_dconst[NB2];
+__constant__ double c_m2x3, c_m2y3;
+
+// Fine-level diagonal block D_c = Dconst + diag(sigma_a I4, 3 m2x sigma_t I4,
+// 3 m2y sigma_t I4).  Its rho-rho and J-J blocks are diagonal (the jump parts
+// of dsa.cpp:288-297 are diagonal per axis), so D_c is applied and solved on
+// the fly from (sigma_t, sigma_a) without storing 12x12 blocks.
+__device__ __forceinline__ void fine_block_mv(double sgt, double sga, const double* __restrict__ x, double* y) {
+#pragma unroll
+  for (int r = 0; r < NB; ++r) {
+    double acc = y[r];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc = fma(c_dconst[r * NB + c], x[c], acc);
+    y[r] = acc;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    y[i] = fma(sga, x[i], y[i]);
+    y[4 + i] = fma(c_m2x3 * sgt, x[4 + i], y[4 + i]);
+    y[8 + i] = fma(c_m2y3 * sgt, x[8 + i], y[8 + i]);
+  }
+}
+
+// x = D_c^{-1} r by eliminating Jx, Jy (diagonal T blocks) and a 4x4 Schur
+// solve with partial pivoting.
+__device__ __forceinline__ void fine_block_solve(double sgt, double sga, const double* r, double* x) {
+  double it1[4], it2[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    it1[k] = 1.0 / (c_dconst[(4 + k) * NB + 4 + k] + c_m2x3 * sgt);
+    it2[k] = 1.0 / (c_dconst[(8 + k) * NB + 8 + k] + c_m2y3 * sgt);
+  }
+  double S[4][5];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double v = c_dconst[i * NB + j] + (i == j ? sga : 0.0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v -= c_dconst[i * NB + 4 + k] * it1[k] * c_dconst[(4 + k) * NB + j];
+        v -= c_dconst[i * NB + 8 + k] * it2[k] * c_dconst[(8 + k) * NB + j];
+      }
+      S[i][j] = v;
+    }
+    double b = r[i];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      b -= c_dconst[i * NB + 4 + k] * it1[k] * r[4 + k];
+      b -= c_dconst[i * NB + 8 + k] * it2[k] * r[8 + k];
+    }
+    S[i][4] = b;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    int p = k;
+#pragma unroll
+    for (int i = k + 1; i < 4; ++i)
+      if (fabs(S[i][k]) > fabs(S[p][k])) p = i;
+    if (p != k)
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        const double t = S[k][j];
+        S[k][j] = S[p][j];
+        S[p][j] = t;
+      }
+    const double id = 1.0 / S[k][k];
+#pragma unroll
+    for (int i = k + 1; i < 4; ++i) {
+      const double f = S[i][k] * id;
+#pragma unroll
+      for (int j = k; j < 5; ++j) S[i][j] -= f * S[k][j];
+    }
+  }
+#pragma unroll
+  for (int i = 3; i >= 0; --i) {
+    double v = S[i][4];
+#pragma unroll
+    for (int j = i + 1; j < 4; ++j) v -= S[i][j] * x[j];
+    x[i] = v / S[i][i];
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    double vx = r[4 + k], vy = r[8 + k];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      vx -= c_dconst[(4 + k) * NB + j] * x[j];
+      vy -= c_dconst[(8 + k) * NB + j] * x[j];
+    }
+    x[4 + k] = vx * it1[k];
+    x[8 + k] = vy * it2[k];
+  }
+}
 
 // Fine diagonal blocks: constant part + sigma terms (dsa.cpp:288-297).
 __global__ void k_fine_diag(int S, long nc, const double* __restrict__ st, const double* __restrict__ ss,
@@ -192,7 +287,8 @@ __global__ void k_inv12(long n, const double* __restrict__ D, double* __restrict
 }
 
 // Coarse diagonal blocks: D_C = sum_pos P_pos^T D_c P_pos + Dint (Galerkin).
-__global__ void k_galerkin_diag(int S, int fnx, int fny, const double* __restrict__ Df, const double* __restrict__ P,
+__global__ void k_galerkin_diag(int S, int fnx, int fny, const double* __restrict__ Df, const double* __restrict__ sgt,
+                                const double* __restrict__ sgs, const double* __restrict__ P,
                                 const double* __restrict__ Dint, double* __restrict__ Dc) {
   const int cnx = fnx / 2, cny = fny / 2;
   const long ncc = (long)cnx * cny;
@@ -205,7 +301,21 @@ __global__ void k_galerkin_diag(int S, int fnx, int fny, const double* __restric
   for (int py = 0; py < 2; ++py)
     for (int px = 0; px < 2; ++px) {
       const long c = (long)(2 * cy + py) * fnx + 2 * cx + px;
-      const double* d = Df + (s * (long)fnx * fny + c) * NB2;
+      double dloc[NB2];
+      const double* d;
+      if (Df) {
+        d = Df + (s * (long)fnx * fny + c) * NB2;
+      } else {
+        const long fi = s * (long)fnx * fny + c;
+        const double st = sgt[fi], sa = sgt[fi] - sgs[fi];
+        for (int e = 0; e < NB2; ++e) dloc[e] = c_dconst[e];
+        for (int i = 0; i < 4; ++i) {
+          dloc[i * NB + i] += sa;
+          dloc[(4 + i) * NB + 4 + i] += c_m2x3 * st;
+          dloc[(8 + i) * NB + 8 + i] += c_m2y3 * st;
+        }
+        d = dloc;
+      }
       const double* E = P + (px + 2 * py) * 16;  // 4x4 fine x coarse
       // out[f1 blk][f2 blk] += E^T d[f1][f2] E
       for (int f1 = 0; f1 < 3; ++f1)
@@ -248,7 +358,8 @@ __device__ __forceinline__ void face_terms(const double* __restrict__ nbr, const
 }
 
 // y = K x (mode 0) or y = b - K x (mode 1)
-__global__ void k_apply(int S, int nx, int ny, const double* __restrict__ D, const double* __restrict__ nbr,
+__global__ void k_apply(int S, int nx, int ny, const double* __restrict__ D, const double* __restrict__ sgt,
+                        const double* __restrict__ sgs, const double* __restrict__ nbr,
                         const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ y, int mode,
                         const int* __restrict__ act) {
   const long nc = (long)nx * ny;
@@ -261,7 +372,10 @@ __global__ void k_apply(int S, int nx, int ny, const double* __restrict__ D, con
   double acc[NB];
 #pragma unroll
   for (int r = 0; r < NB; ++r) acc[r] = 0.0;
-  blk_mv_acc(D + t * NB2, xs + c * NB, acc);
+  if (D)
+    blk_mv_acc(D + t * NB2, xs + c * NB, acc);
+  else
+    fine_block_mv(sgt[t], sgt[t] - sgs[t], xs + c * NB, acc);
   face_terms(nbr, xs, nx, ny, ix, iy, c, acc);
   double* yo = y + t * NB;
   if (mode == 1) {
@@ -275,7 +389,8 @@ __global__ void k_apply(int S, int nx, int ny, const double* __restrict__ D, con
 }
 
 // red-black block Gauss-Seidel half sweep: x_c = Dinv_c (b_c - sum_nbr C x_nbr)
-__global__ void k_gs(int S, int nx, int ny, int color, const double* __restrict__ Dinv, const double* __restrict__ nbr,
+__global__ void k_gs(int S, int nx, int ny, int color, const double* __restrict__ Dinv, const double* __restrict__ sgt,
+                     const double* __restrict__ sgs, const double* __restrict__ nbr,
                      double* __restrict__ x, const double* __restrict__ b, const int* __restrict__ act, int zero_init) {
   const long nc = (long)nx * ny;
   const long half = (nc + 1) / 2;
@@ -314,9 +429,14 @@ __global__ void k_gs(int S, int nx, int ny, int color, const double* __restrict_
 #pragma unroll
     for (int r = 0; r < NB; ++r) rr[r] = bi[r] - acc[r];
     double out[NB];
+    if (Dinv) {
 #pragma unroll
-    for (int r = 0; r < NB; ++r) out[r] = 0.0;
-    blk_mv_acc(Dinv + (s * nc + c) * NB2, rr, out);
+      for (int r = 0; r < NB; ++r) out[r] = 0.0;
+      blk_mv_acc(Dinv + (s * nc + c) * NB2, rr, out);
+    } else {
+      const long fi = s * nc + c;
+      fine_block_solve(sgt[fi], sgt[fi] - sgs[fi], rr, out);
+    }
     double* xo = x + (s * nc + c) * NB;
 #pragma unroll
     for (int r = 0; r < NB; ++r) xo[r] = out[r];
@@ -472,10 +592,12 @@ __global__ void k_dense_apply(int n, const double* __restrict__ Ainv, const doub
   if (act && !act[s]) return;
   const double* a = Ainv + (long)s * n * n;
   const double* bs = b + (long)s * n;
-  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = wid; r < n; r += nw) {
     double acc = 0.0;
-    for (int c = 0; c < n; ++c) acc = fma(a[(long)r * n + c], bs[c], acc);
-    x[(long)s * n + r] = acc;
+    for (int c = lane; c < n; c += 32) acc = fma(a[(long)r * n + c], bs[c], acc);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) x[(long)s * n + r] = acc;
   }
 }
 
@@ -708,6 +830,11 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   }
   std::vector<Mat> nbr = {nbx(clx, hclx), nbx(crx, hcrx), nby(cly, hcly), nby(cry, hcry)};
   RTE_CUDA(cudaMemcpyToSymbol(c_dconst, Dc.data(), sizeof(double) * NB2));
+  const double m2x3 = 3 * m2x, m2y3 = 3 * m2y;
+  RTE_CUDA(cudaMemcpyToSymbol(c_m2x3, &m2x3, sizeof(double)));
+  RTE_CUDA(cudaMemcpyToSymbol(c_m2y3, &m2y3, sizeof(double)));
+  d->sgt = ctx->mt.p;
+  d->sgs = ctx->ms.p;
 
   // prolongation blocks (4x4 E2 per position) for the device
   std::vector<Mat> P12(4);
@@ -734,8 +861,10 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
     lv.nbr_h.resize(4 * NB2);
     for (int k = 0; k < 4; ++k) std::copy(nbr[k].begin(), nbr[k].end(), lv.nbr_h.begin() + k * NB2);
     lv.nbr.upload(lv.nbr_h.data(), lv.nbr_h.size());
-    lv.D.alloc((size_t)S * lv.nc * NB2);
-    lv.Dinv.alloc((size_t)S * lv.nc * NB2);
+    if (!d->L.empty() && &lv != &d->L.front()) {
+      lv.D.alloc((size_t)S * lv.nc * NB2);
+      lv.Dinv.alloc((size_t)S * lv.nc * NB2);
+    }
     lv.x.alloc((size_t)S * lv.nc * NB);
     lv.b.alloc((size_t)S * lv.nc * NB);
     lv.r.alloc((size_t)S * lv.nc * NB);
@@ -771,20 +900,21 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
     ny /= 2;
   }
   d->Dint.upload(dint_all.data(), dint_all.size());
-  // fine diagonal blocks + inverses; Galerkin coarse diagonals
+  // coarse diagonal blocks (Galerkin) and their inverses; level 0 is matrix-free
   const Level& l0 = d->L[0];
-  k_fine_diag<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, ctx->mt.p, ctx->ms.p, 3 * m2x, 3 * m2y,
-                                                          d->L[0].D.p);
-  RTE_CUDA(cudaGetLastError());
-  for (size_t l = 0; l < d->L.size(); ++l) {
+  for (size_t l = 1; l < d->L.size(); ++l) {
     Level& lv = d->L[l];
-    if (l > 0) {
-      const Level& f = d->L[l - 1];
-      k_galerkin_diag<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, f.nx, f.ny, f.D.p, d->P.p,
-                                                                 d->Dint.p + (l - 1) * NB2, lv.D.p);
-      RTE_CUDA(cudaGetLastError());
-    }
+    const Level& f = d->L[l - 1];
+    k_galerkin_diag<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, f.nx, f.ny, l == 1 ? nullptr : f.D.p, d->sgt,
+                                                                   d->sgs, d->P.p, d->Dint.p + (l - 1) * NB2, lv.D.p);
+    RTE_CUDA(cudaGetLastError());
     k_inv12<<<nblocks((long)S * lv.nc, 64), 64, 0, st>>>((long)S * lv.nc, lv.D.p, lv.Dinv.p);
+    RTE_CUDA(cudaGetLastError());
+  }
+  if (d->L.size() == 1 && l0.nc <= kMaxCoarseCells) {
+    // tiny grid: the dense coarsest solve needs explicit level-0 blocks
+    d->L[0].D.alloc((size_t)S * l0.nc * NB2);
+    k_fine_diag<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, ctx->mt.p, ctx->ms.p, m2x3, m2y3, d->L[0].D.p);
     RTE_CUDA(cudaGetLastError());
   }
   Level& lc = d->L.back();
@@ -805,7 +935,8 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   const size_t nv = (size_t)S * l0.nc * NB;
   for (DBuf<double>* b : {&d->r, &d->rh, &d->p, &d->v, &d->s, &d->t, &d->x, &d->ph, &d->sh}) b->alloc(nv);
   d->scal.alloc((size_t)S * 16);
-  d->part.alloc((size_t)S * kDotBlocks * 4);
+  d->nblk = (int)std::min<long>(512, std::max<long>(16, (long)l0.nc * NB / 4096));
+  d->part.alloc((size_t)S * d->nblk * 4);
   d->act.alloc(S);
   d->nact.alloc(1);
   RTE_CUDA(cudaStreamSynchronize(st));
@@ -817,9 +948,10 @@ static void smooth(Dsa2D* d, int l, const double* b, double* x, const int* act, 
   const int S = d->S;
   const long half = (lv.nc + 1) / 2;
   const int c0 = reverse ? 1 : 0;
-  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, c0, lv.Dinv.p, lv.nbr.p, x, b, act,
-                                                      zero_init ? 1 : 0);
-  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, 1 - c0, lv.Dinv.p, lv.nbr.p, x, b, act, 0);
+  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, c0, lv.Dinv.p, d->sgt, d->sgs, lv.nbr.p, x, b,
+                                                      act, zero_init ? 1 : 0);
+  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, 1 - c0, lv.Dinv.p, d->sgt, d->sgs, lv.nbr.p, x,
+                                                      b, act, 0);
 }
 
 static void vcycle(Dsa2D* d, int l, const double* b, double* x, const int* act, cudaStream_t st) {
@@ -837,7 +969,8 @@ static void vcycle(Dsa2D* d, int l, const double* b, double* x, const int* act, 
     return;
   }
   for (int k = 0; k < d->nu; ++k) smooth(d, l, b, x, act, k == 0, false, st);
-  k_apply<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, lv.D.p, lv.nbr.p, x, b, lv.r.p, 1, act);
+  k_apply<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, lv.D.p, d->sgt, d->sgs, lv.nbr.p, x, b,
+                                                          lv.r.p, 1, act);
   Level& lc = d->L[l + 1];
   k_restrict<<<nblocks((long)S * lc.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, d->P.p, lv.r.p, lc.b.p, act);
   vcycle(d, l + 1, lc.b.p, lc.x.p, act, st);
@@ -856,7 +989,7 @@ static void dots(Dsa2D* d, long n, std::initializer_list<std::pair<const double*
     ++q;
   }
   a.nq = q;
-  k_dots<<<dim3(kDotBlocks, d->S), 256, 0, st>>>(d->S, n, a, d->part.p, d->act.p);
+  k_dots<<<dim3(d->nblk, d->S), 256, 0, st>>>(d->S, n, a, d->part.p, d->act.p);
   RTE_CUDA(cudaGetLastError());
 }
 
@@ -866,7 +999,7 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   const int S = d->S;
   Level& l0 = d->L[0];
   const long n = l0.nc * NB;
-  const dim3 vgrid(kDotBlocks, S);
+  const dim3 vgrid(d->nblk, S);
   // b -> l0.b ; x = 0 ; r = b ; rh = r
   k_pack_rhs<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, rhs, ctx->ms.p, apply_ms, l0.b.p, kind);
   RTE_CUDA(cudaMemsetAsync(d->x.p, 0, sizeof(double) * S * n, st));
@@ -883,7 +1016,7 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     k_dots<<<vgrid, 256, 0, st>>>(S, n, a, d->part.p, nullptr);
   }
   std::vector<int> mask_h;
-  k_bicg_init<<<(S + 127) / 128, 128, 0, st>>>(S, kDotBlocks, d->part.p, d->scal.p, d->act.p, nullptr);
+  k_bicg_init<<<(S + 127) / 128, 128, 0, st>>>(S, d->nblk, d->part.p, d->scal.p, d->act.p, nullptr);
   RTE_CUDA(cudaGetLastError());
   if (kind) {
     // samples not selected for DSA: b was packed as zero -> inactive after init
@@ -894,21 +1027,21 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   int it = 0;
   for (; it < d->maxit; ++it) {
     dots(d, n, {{d->rh.p, d->r.p}}, st);
-    k_bicg_p<<<vgrid, 256, 0, st>>>(S, n, kDotBlocks, d->part.p, d->scal.p, d->r.p, d->p.p, d->v.p, d->act.p);
+    k_bicg_p<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->r.p, d->p.p, d->v.p, d->act.p);
     vcycle(d, 0, d->p.p, d->ph.p, d->act.p, st);
-    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, l0.D.p, l0.nbr.p, d->ph.p, nullptr, d->v.p,
-                                                            0, d->act.p);
+    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, l0.D.p, d->sgt, d->sgs, l0.nbr.p, d->ph.p,
+                                                            nullptr, d->v.p, 0, d->act.p);
     dots(d, n, {{d->rh.p, d->v.p}}, st);
-    k_bicg_s<<<vgrid, 256, 0, st>>>(S, n, kDotBlocks, d->part.p, d->scal.p, d->r.p, d->v.p, d->s.p, d->act.p);
+    k_bicg_s<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->r.p, d->v.p, d->s.p, d->act.p);
     vcycle(d, 0, d->s.p, d->sh.p, d->act.p, st);
-    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, l0.D.p, l0.nbr.p, d->sh.p, nullptr, d->t.p,
-                                                            0, d->act.p);
+    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, l0.D.p, d->sgt, d->sgs, l0.nbr.p, d->sh.p,
+                                                            nullptr, d->t.p, 0, d->act.p);
     dots(d, n, {{d->t.p, d->s.p}, {d->t.p, d->t.p}}, st);
-    k_bicg_x<<<vgrid, 256, 0, st>>>(S, n, kDotBlocks, d->part.p, d->scal.p, d->x.p, d->ph.p, d->sh.p, d->r.p, d->s.p,
+    k_bicg_x<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->x.p, d->ph.p, d->sh.p, d->r.p, d->s.p,
                                     d->t.p, d->act.p);
     dots(d, n, {{d->r.p, d->r.p}}, st);
     RTE_CUDA(cudaMemsetAsync(d->nact.p, 0, sizeof(int), st));
-    k_bicg_check<<<(S + 127) / 128, 128, 0, st>>>(S, kDotBlocks, d->part.p, d->scal.p, d->act.p, tol2, d->maxit,
+    k_bicg_check<<<(S + 127) / 128, 128, 0, st>>>(S, d->nblk, d->part.p, d->scal.p, d->act.p, tol2, d->maxit,
                                                   d->nact.p);
     RTE_CUDA(cudaGetLastError());
     if ((it & 3) == 3) {

@@ -1,0 +1,25 @@
+"""One 2D DSA solve (for launch lists): python scripts/dsa_once.py NX S TOL"""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2402_10488_b200 import rte, configs
+nx = int(sys.argv[1]); S = int(sys.argv[2]); tol = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-12
+kind = sys.argv[4] if len(sys.argv) > 4 else "c3"
+mesh = rte.Mesh.rect_uniform(0, 1, nx, 0, 1, nx)
+quad = rte.chebyshev_legendre(16, 8)
+n = nx * nx
+if kind == "c3":
+    st, ss = np.full((S, n), 10.0), np.full((S, n), 9.99)
+else:
+    st, ss = configs.c5_coefficients(nx, S)
+px, py = mesh.cell_points()
+g = mesh.project(np.ones(px.size))
+b = rte.TransportBatch.from_cells(mesh, quad, st, ss, g)
+d = rte.DsaOperator(b)
+d.set_tolerance(tol, 2000)
+rhs = torch.rand(S, b.n_dof(), dtype=torch.float64, device="cuda")
+for k in range(2):
+    torch.cuda.synchronize(); t0 = time.time()
+    x = d.solve_density(rhs)
+    torch.cuda.synchronize()
+    print("solve %.3f s, krylov iterations %d" % (time.time() - t0, d.last_iterations()), flush=True)
