@@ -30,7 +30,8 @@ namespace {
 
 constexpr int NB = 12;  // unknowns per cell
 constexpr int NB2 = NB * NB;
-constexpr int kMaxCoarseCells = 64;
+constexpr int kMaxCoarseCells = 16;
+constexpr int kMaxLevels = 16;
 
 struct Level {
   int nx, ny;
@@ -133,6 +134,43 @@ Mat galerkin(const Mat& A, const Mat& Pl, const Mat& Pr) {
 
 __constant__ double c_dconst[NB2];
 __constant__ double c_m2x3, c_m2y3;
+// Face couplings per level and direction (W, E, S, N): every face block is
+// axis-lifted, [[L(Mrr), L(Mrj), 0], [L(Mjr), L(Mjj), 0], [0, 0, L(Mo)]] for x
+// faces (j = Jx, o = Jy) and the mirrored pattern for y faces, at all levels
+// (Galerkin preserves it since sum_s E_s^T E_s = I).  5 matrices of 2x2.
+__constant__ double c_face[kMaxLevels][4][5][4];
+
+__device__ __forceinline__ void lift_mv(const double* M, const double* v, double* y, int axis) {
+  // y += L_axis(M) v on one 4-mode field
+  if (axis == 0) {
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const double v0 = v[2 * b], v1 = v[2 * b + 1];
+      y[2 * b] = fma(M[0], v0, fma(M[1], v1, y[2 * b]));
+      y[2 * b + 1] = fma(M[2], v0, fma(M[3], v1, y[2 * b + 1]));
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const double v0 = v[a], v1 = v[a + 2];
+      y[a] = fma(M[0], v0, fma(M[1], v1, y[a]));
+      y[a + 2] = fma(M[2], v0, fma(M[3], v1, y[a + 2]));
+    }
+  }
+}
+
+__device__ __forceinline__ void face_mv(int lev, int dir, const double* __restrict__ xn, double* y) {
+  const int axis = dir >> 1;
+  const int j = axis == 0 ? 4 : 8, o = axis == 0 ? 8 : 4;
+  double v[NB];
+#pragma unroll
+  for (int r = 0; r < NB; ++r) v[r] = xn[r];
+  lift_mv(c_face[lev][dir][0], v, y, axis);
+  lift_mv(c_face[lev][dir][1], v + j, y, axis);
+  lift_mv(c_face[lev][dir][2], v, y + j, axis);
+  lift_mv(c_face[lev][dir][3], v + j, y + j, axis);
+  lift_mv(c_face[lev][dir][4], v + o, y + o, axis);
+}
 
 // Fine-level diagonal block D_c = Dconst + diag(sigma_a I4, 3 m2x sigma_t I4,
 // 3 m2y sigma_t I4).  Its rho-rho and J-J blocks are diagonal (the jump parts
@@ -155,7 +193,7 @@ __device__ __forceinline__ void fine_block_mv(double sgt, double sga, const doub
 }
 
 // x = D_c^{-1} r by eliminating Jx, Jy (diagonal T blocks) and a 4x4 Schur
-// solve with partial pivoting.
+// solve.
 __device__ __forceinline__ void fine_block_solve(double sgt, double sga, const double* r, double* x) {
   double it1[4], it2[4];
 #pragma unroll
@@ -184,19 +222,10 @@ __device__ __forceinline__ void fine_block_solve(double sgt, double sga, const d
     }
     S[i][4] = b;
   }
+  // S = A + (1/3) B^T T^{-1} B is symmetric positive definite (A diagonal
+  // positive, B antisymmetric, T diagonal positive): no pivoting needed.
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    int p = k;
-#pragma unroll
-    for (int i = k + 1; i < 4; ++i)
-      if (fabs(S[i][k]) > fabs(S[p][k])) p = i;
-    if (p != k)
-#pragma unroll
-      for (int j = 0; j < 5; ++j) {
-        const double t = S[k][j];
-        S[k][j] = S[p][j];
-        S[p][j] = t;
-      }
     const double id = 1.0 / S[k][k];
 #pragma unroll
     for (int i = k + 1; i < 4; ++i) {
@@ -349,17 +378,17 @@ __device__ __forceinline__ void blk_mv_acc(const double* __restrict__ M, const d
 }
 
 // off-diagonal (face) contributions sum_nbr C_dir x_nbr
-__device__ __forceinline__ void face_terms(const double* __restrict__ nbr, const double* __restrict__ xs, int nx, int ny,
-                                           int ix, int iy, long c, double* y) {
-  if (ix > 0) blk_mv_acc(nbr + 0 * NB2, xs + (c - 1) * NB, y);
-  if (ix < nx - 1) blk_mv_acc(nbr + 1 * NB2, xs + (c + 1) * NB, y);
-  if (iy > 0) blk_mv_acc(nbr + 2 * NB2, xs + (c - nx) * NB, y);
-  if (iy < ny - 1) blk_mv_acc(nbr + 3 * NB2, xs + (c + nx) * NB, y);
+__device__ __forceinline__ void face_terms(int lev, const double* __restrict__ xs, int nx, int ny, int ix, int iy,
+                                           long c, double* y) {
+  if (ix > 0) face_mv(lev, 0, xs + (c - 1) * NB, y);
+  if (ix < nx - 1) face_mv(lev, 1, xs + (c + 1) * NB, y);
+  if (iy > 0) face_mv(lev, 2, xs + (c - nx) * NB, y);
+  if (iy < ny - 1) face_mv(lev, 3, xs + (c + nx) * NB, y);
 }
 
 // y = K x (mode 0) or y = b - K x (mode 1)
 __global__ void k_apply(int S, int nx, int ny, const double* __restrict__ D, const double* __restrict__ sgt,
-                        const double* __restrict__ sgs, const double* __restrict__ nbr,
+                        const double* __restrict__ sgs, int lev,
                         const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ y, int mode,
                         const int* __restrict__ act) {
   const long nc = (long)nx * ny;
@@ -376,7 +405,7 @@ __global__ void k_apply(int S, int nx, int ny, const double* __restrict__ D, con
     blk_mv_acc(D + t * NB2, xs + c * NB, acc);
   else
     fine_block_mv(sgt[t], sgt[t] - sgs[t], xs + c * NB, acc);
-  face_terms(nbr, xs, nx, ny, ix, iy, c, acc);
+  face_terms(lev, xs, nx, ny, ix, iy, c, acc);
   double* yo = y + t * NB;
   if (mode == 1) {
     const double* bi = b + t * NB;
@@ -390,7 +419,7 @@ __global__ void k_apply(int S, int nx, int ny, const double* __restrict__ D, con
 
 // red-black block Gauss-Seidel half sweep: x_c = Dinv_c (b_c - sum_nbr C x_nbr)
 __global__ void k_gs(int S, int nx, int ny, int color, const double* __restrict__ Dinv, const double* __restrict__ sgt,
-                     const double* __restrict__ sgs, const double* __restrict__ nbr,
+                     const double* __restrict__ sgs, int lev,
                      double* __restrict__ x, const double* __restrict__ b, const int* __restrict__ act, int zero_init) {
   const long nc = (long)nx * ny;
   const long half = (nc + 1) / 2;
@@ -424,7 +453,7 @@ __global__ void k_gs(int S, int nx, int ny, int color, const double* __restrict_
     const double* bi = b + (s * nc + c) * NB;
 #pragma unroll
     for (int r = 0; r < NB; ++r) acc[r] = 0.0;
-    if (!zero_init) face_terms(nbr, xs, nx, ny, ix, iy, c, acc);
+    if (!zero_init) face_terms(lev, xs, nx, ny, ix, iy, c, acc);
     double rr[NB];
 #pragma unroll
     for (int r = 0; r < NB; ++r) rr[r] = bi[r] - acc[r];
@@ -900,6 +929,38 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
     ny /= 2;
   }
   d->Dint.upload(dint_all.data(), dint_all.size());
+  RTE_REQUIRE(d->L.size() <= (size_t)kMaxLevels, RTE_ERR_UNSUPPORTED, "dsa: too many multigrid levels");
+  {
+    std::vector<double> cf((size_t)kMaxLevels * 4 * 5 * 4, 0.0);
+    for (size_t l = 0; l < d->L.size(); ++l)
+      for (int dir = 0; dir < 4; ++dir) {
+        const double* B = d->L[l].nbr_h.data() + dir * NB2;
+        const int axis = dir >> 1;
+        const int j = axis == 0 ? 1 : 2, o = axis == 0 ? 2 : 1;
+        const int fr[5] = {0, 0, j, j, o}, fc[5] = {0, j, 0, j, o};
+        // exact lifted pattern check; extract the 2x2 factor
+        Mat chk = zeros(NB, NB);
+        for (int m = 0; m < 5; ++m) {
+          double M[4];
+          for (int k = 0; k < 2; ++k)
+            for (int q = 0; q < 2; ++q) {
+              const int lr = axis == 0 ? k : 2 * k, lc = axis == 0 ? q : 2 * q;
+              M[2 * k + q] = B[(size_t)(4 * fr[m] + lr) * NB + 4 * fc[m] + lc];
+            }
+          double Lm[16];
+          lift(M, axis, Lm);
+          put(chk, fr[m], fc[m], Lm, 1.0);
+          for (int e = 0; e < 4; ++e) cf[(((l * 4) + dir) * 5 + m) * 4 + e] = M[e];
+        }
+        double err = 0, mag = 0;
+        for (int e = 0; e < NB2; ++e) {
+          err = std::max(err, std::fabs(chk[e] - B[e]));
+          mag = std::max(mag, std::fabs(B[e]));
+        }
+        RTE_REQUIRE(err <= 1e-12 * mag, RTE_ERR_RUNTIME, "dsa: face coupling lost its lifted structure");
+      }
+    RTE_CUDA(cudaMemcpyToSymbol(c_face, cf.data(), sizeof(double) * cf.size()));
+  }
   // coarse diagonal blocks (Galerkin) and their inverses; level 0 is matrix-free
   const Level& l0 = d->L[0];
   for (size_t l = 1; l < d->L.size(); ++l) {
@@ -948,9 +1009,9 @@ static void smooth(Dsa2D* d, int l, const double* b, double* x, const int* act, 
   const int S = d->S;
   const long half = (lv.nc + 1) / 2;
   const int c0 = reverse ? 1 : 0;
-  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, c0, lv.Dinv.p, d->sgt, d->sgs, lv.nbr.p, x, b,
+  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, c0, lv.Dinv.p, d->sgt, d->sgs, l, x, b,
                                                       act, zero_init ? 1 : 0);
-  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, 1 - c0, lv.Dinv.p, d->sgt, d->sgs, lv.nbr.p, x,
+  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, 1 - c0, lv.Dinv.p, d->sgt, d->sgs, l, x,
                                                       b, act, 0);
 }
 
@@ -969,7 +1030,7 @@ static void vcycle(Dsa2D* d, int l, const double* b, double* x, const int* act, 
     return;
   }
   for (int k = 0; k < d->nu; ++k) smooth(d, l, b, x, act, k == 0, false, st);
-  k_apply<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, lv.D.p, d->sgt, d->sgs, lv.nbr.p, x, b,
+  k_apply<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, lv.D.p, d->sgt, d->sgs, l, x, b,
                                                           lv.r.p, 1, act);
   Level& lc = d->L[l + 1];
   k_restrict<<<nblocks((long)S * lc.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, d->P.p, lv.r.p, lc.b.p, act);
@@ -1029,12 +1090,12 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     dots(d, n, {{d->rh.p, d->r.p}}, st);
     k_bicg_p<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->r.p, d->p.p, d->v.p, d->act.p);
     vcycle(d, 0, d->p.p, d->ph.p, d->act.p, st);
-    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, l0.D.p, d->sgt, d->sgs, l0.nbr.p, d->ph.p,
+    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, l0.D.p, d->sgt, d->sgs, 0, d->ph.p,
                                                             nullptr, d->v.p, 0, d->act.p);
     dots(d, n, {{d->rh.p, d->v.p}}, st);
     k_bicg_s<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->r.p, d->v.p, d->s.p, d->act.p);
     vcycle(d, 0, d->s.p, d->sh.p, d->act.p, st);
-    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, l0.D.p, d->sgt, d->sgs, l0.nbr.p, d->sh.p,
+    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, l0.D.p, d->sgt, d->sgs, 0, d->sh.p,
                                                             nullptr, d->t.p, 0, d->act.p);
     dots(d, n, {{d->t.p, d->s.p}, {d->t.p, d->t.p}}, st);
     k_bicg_x<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->x.p, d->ph.p, d->sh.p, d->r.p, d->s.p,
