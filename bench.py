@@ -131,7 +131,8 @@ def run_b200(args, rank, world, device):
     # DSA availability for XY geometry in this build
     dsa_ok = True
     try:
-        rte.DsaOperator(batch)
+        dsa = rte.DsaOperator(batch)
+        dsa.set_tolerance(args.dsa_tol, 2000)
     except capi.RteError:
         dsa_ok = False
     method = "DSA" if dsa_ok else "SI"
@@ -175,7 +176,7 @@ def run_b200(args, rank, world, device):
         t0 = time.perf_counter()
         b2 = rte.TransportBatch.from_cells(mesh, quad, st_p.numpy(), ss_p.numpy(), g, device=device)
         if dsa_ok:
-            rte.DsaOperator(b2)
+            rte.DsaOperator(b2).set_tolerance(args.dsa_tol, 2000)
         cfg = rte.SolveConfig(fixed_iters=args.steps, max_iters=args.steps, compute_residual=False,
                               check_every=args.steps)
         r2, _ = rte.sisa_solve(b2, method, cfg)
@@ -209,7 +210,8 @@ def run_b200(args, rank, world, device):
         "dtype": "f64", "data": "synthetic (seeded mt19937_64, BASELINE configs[4])",
         "config": {"workload": "c5_2d_sweep_stress", "cells": "%dx%d" % (nx, nx), "directions_unique": slots,
                    "quadrature": "CL(%d,%d) folded" % (PHI, VZ), "samples_per_gpu": S,
-                   "dsa": "device" if dsa_ok else "not in this build (step = sweep + source update only)",
+                   "dsa": ("device BiCGStab+multigrid to rel. residual %g" % args.dsa_tol) if dsa_ok
+                   else "not in this build (step = sweep + source update only)",
                    "l2": "inputs (%.1f GB per step) exceed the 126 MB L2" % (S * nx * nx * 4 * 8 * 3 / 1e9)},
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -219,6 +221,7 @@ def run_b200(args, rank, world, device):
                      "fp64": {"achieved_tflops": fp64_ach, "peak_tflops": tf.value, "frac": fp64_ach / tf.value,
                               "flop_per_update": FLOP_PER_UPDATE, "peak_kind": "measured DFMA probe"}},
         "kernel_ms": {k: ms_k[i] for i, k in enumerate(capi.PROF_KINDS)},
+        "sweep_only_updates_per_s": upd_step / (sweep_ms * 1e-3),
         "kernel_launches": {k: int(n_k[i]) for i, k in enumerate(capi.PROF_KINDS)},
         "gpu_launches": gpu_launches,
         "clocks": ck,
@@ -301,7 +304,8 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--dsa-tol", type=float, default=1e-8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--nx", type=int, default=1024)

@@ -1,0 +1,190 @@
+// rte_b200.hpp -- header-only C++ host API over the C-ABI (rte_b200.h).
+//
+// Mirrors the reference core library's entry points for the hot path
+// (namespace rte, /root/reference/proj/core/include/rte): problem setup
+// (TransportSystem ctor, transport_system.hpp:32-34), the DSA operator
+// (dsa.hpp:29-56), reduced models (reduced_model.hpp:19-44) and the solver
+// driver sisa_solve (solvers.hpp:70-72) with SolveConfig / SolveReport
+// (solvers.hpp:13-33) -- batched over parameter samples.  Errors are thrown
+// as std::invalid_argument / std::runtime_error like the reference.
+//
+// Link: -lrte_b200 (paper_2402_10488_b200/librte_b200.so) -lcudart.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "rte_b200.h"
+
+namespace rte_b200 {
+
+inline void check(int code, const rte_ctx* ctx) {
+  if (code == RTE_OK) return;
+  const std::string msg = rte_last_error(ctx);
+  if (code == RTE_ERR_INVALID) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+struct AngularQuadrature {  // quadrature.hpp:19-35
+  int geometry = RTE_SLAB1D;
+  std::vector<std::array<double, 3>> directions;
+  std::vector<double> weights;
+  int n() const { return static_cast<int>(weights.size()); }
+};
+
+inline AngularQuadrature gauss_legendre(int n) {  // quadrature.cpp:41-52
+  std::vector<double> x(n), w(n);
+  check(rte_gauss_legendre_nodes(n, x.data(), w.data()), nullptr);
+  AngularQuadrature q;
+  for (int j = 0; j < n; ++j) {
+    q.directions.push_back({x[j], 0.0, 0.0});
+    q.weights.push_back(0.5 * w[j]);
+  }
+  return q;
+}
+
+inline AngularQuadrature chebyshev_legendre(int n_phi, int n_vz) {  // quadrature.cpp:54-73
+  std::vector<double> z(n_vz), wz(n_vz);
+  check(rte_gauss_legendre_nodes(n_vz, z.data(), wz.data()), nullptr);
+  AngularQuadrature q;
+  q.geometry = RTE_XY2D;
+  const double pi = 3.14159265358979323846;
+  for (int j2 = 0; j2 < n_vz; ++j2) {
+    const double s = std::sqrt(std::max(0.0, 1.0 - z[j2] * z[j2]));
+    for (int j1 = 1; j1 <= n_phi; ++j1) {
+      const double phi = 2.0 * j1 * pi / n_phi - pi / n_phi;
+      q.directions.push_back({std::cos(phi) * s, std::sin(phi) * s, z[j2]});
+      q.weights.push_back((1.0 / n_phi) * (0.5 * wz[j2]));
+    }
+  }
+  return q;
+}
+
+// Device buffer of S x n doubles (sample-major).
+class DeviceVector {
+ public:
+  DeviceVector() = default;
+  DeviceVector(long n) : n_(n) {
+    if (cudaMalloc(&p_, sizeof(double) * n) != cudaSuccess) throw std::runtime_error("cudaMalloc failed");
+  }
+  ~DeviceVector() {
+    if (p_) cudaFree(p_);
+  }
+  DeviceVector(DeviceVector&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; }
+  DeviceVector(const DeviceVector&) = delete;
+  double* data() { return p_; }
+  const double* data() const { return p_; }
+  long size() const { return n_; }
+  std::vector<double> to_host() const {
+    std::vector<double> h(n_);
+    cudaMemcpy(h.data(), p_, sizeof(double) * n_, cudaMemcpyDeviceToHost);
+    return h;
+  }
+  void from_host(const std::vector<double>& h) {
+    cudaMemcpy(p_, h.data(), sizeof(double) * n_, cudaMemcpyHostToDevice);
+  }
+
+ private:
+  double* p_ = nullptr;
+  long n_ = 0;
+};
+
+// TransportSystem (transport_system.hpp:30-142) for S samples, built from
+// per-cell coefficients (slab: full 2x2 blocks or scalars; xy: scalars).
+class TransportBatch {
+ public:
+  TransportBatch(const rte_problem& p, int device = 0) {
+    check(rte_create(&p, device, &ctx_), nullptr);
+  }
+  ~TransportBatch() { rte_destroy(ctx_); }
+  TransportBatch(const TransportBatch&) = delete;
+  rte_ctx* handle() const { return ctx_; }
+  long n_dof() const { return rte_n_dof(ctx_); }
+  int n_samples() const { return rte_n_samples(ctx_); }
+
+  void apply_L(const DeviceVector& rho, DeviceVector& out) const {  // transport_system.cpp:393
+    check(rte_apply_L(ctx_, rho.data(), out.data(), nullptr), ctx_);
+  }
+  void assemble_rhs(DeviceVector& out) const {  // transport_system.cpp:406
+    check(rte_assemble_rhs(ctx_, out.data(), nullptr), ctx_);
+  }
+  void apply_Ms(const DeviceVector& x, DeviceVector& out) const {  // transport_system.cpp:373
+    check(rte_apply_Ms(ctx_, x.data(), out.data(), nullptr), ctx_);
+  }
+
+ private:
+  rte_ctx* ctx_ = nullptr;
+};
+
+class DsaOperator {  // dsa.hpp:29-56
+ public:
+  explicit DsaOperator(TransportBatch& b) : b_(&b) { check(rte_dsa_setup(b.handle(), nullptr), b.handle()); }
+  void correct(const DeviceVector& delta, DeviceVector& out) const {
+    check(rte_dsa_correct(b_->handle(), delta.data(), out.data(), nullptr), b_->handle());
+  }
+  void solve_density(const DeviceVector& rhs, DeviceVector& out) const {
+    check(rte_dsa_solve_density(b_->handle(), rhs.data(), out.data(), nullptr), b_->handle());
+  }
+  long coupled_dim() const { return rte_dsa_coupled_dim(b_->handle()); }
+
+ private:
+  TransportBatch* b_;
+};
+
+struct SolveConfig {  // solvers.hpp:13-19 (+ batch options)
+  double eps_sisa = 1e-11;
+  int max_iters = 2000;
+  int method = RTE_DSA;
+  int norm = RTE_NORM_ABS;
+  int theta = 3;
+  double eps_romsad = 0.0;
+  int fixed_iters = 0;
+  const std::vector<double>* initial_guess = nullptr;  // S * n_dof, host
+};
+
+struct SolveReport {  // solvers.hpp:21-33 (per sample)
+  bool converged = false;
+  long n_sweep = 0;
+  int iterations = 0;
+  std::vector<double> change_history;
+  double final_residual = 0;
+  std::string correction_log;
+  int switch_iter = -1;
+};
+
+// sisa_solve (solvers.hpp:70-72) for all samples: returns rho [S * n_dof].
+inline std::pair<std::vector<double>, std::vector<SolveReport>> sisa_solve(TransportBatch& b, const SolveConfig& c) {
+  const int S = b.n_samples();
+  const long nd = b.n_dof();
+  DeviceVector rho((long)S * nd);
+  if (c.initial_guess) rho.from_host(*c.initial_guess);
+  rte_si_config cfg{c.method, c.eps_sisa, c.norm, c.max_iters, c.fixed_iters, c.theta, c.eps_romsad,
+                    c.initial_guess ? 1 : 0, 1, 4};
+  const int mi = std::max(c.max_iters, c.fixed_iters);
+  std::vector<rte_si_report> reps(S);
+  std::vector<double> hist((size_t)S * mi);
+  std::vector<char> log((size_t)S * mi);
+  check(rte_si_solve(b.handle(), &cfg, rho.data(), reps.data(), hist.data(), log.data()), b.handle());
+  std::vector<SolveReport> out(S);
+  for (int s = 0; s < S; ++s) {
+    SolveReport& r = out[s];
+    r.converged = reps[s].converged != 0;
+    r.n_sweep = reps[s].n_sweep;
+    r.iterations = reps[s].iterations;
+    r.change_history.assign(hist.begin() + (long)s * mi, hist.begin() + (long)s * mi + r.iterations);
+    r.final_residual = reps[s].final_residual;
+    r.switch_iter = reps[s].switch_iter;
+    for (int l = 0; l < r.iterations; ++l)
+      if (log[(size_t)s * mi + l]) r.correction_log.push_back(log[(size_t)s * mi + l]);
+  }
+  return {rho.to_host(), out};
+}
+
+}  // namespace rte_b200
