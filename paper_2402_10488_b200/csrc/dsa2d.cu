@@ -36,7 +36,8 @@ constexpr int kMaxLevels = 16;
 struct Level {
   int nx, ny;
   long nc;
-  DBuf<double> D, Dinv;       // [S][nc][144]
+  DBuf<double> D, Dinv;       // [S][nc][144] fp64 (setup only)
+  DBuf<float> Df, Dinvf;      // [S][nc][144] fp32 copies used by the V-cycle (preconditioner)
   DBuf<double> x, b, r;       // [S][nc][12]
   DBuf<double> nbr;           // [4][144] W, E, S, N face-coupling blocks (constant)
   std::vector<double> nbr_h;
@@ -367,6 +368,21 @@ __global__ void k_galerkin_diag(int S, int fnx, int fny, const double* __restric
   for (int e = 0; e < NB2; ++e) Dc[t * NB2 + e] = out[e];
 }
 
+__device__ __forceinline__ void blk_mv_accf(const float* __restrict__ M, const double* __restrict__ x, double* y) {
+#pragma unroll
+  for (int r = 0; r < NB; ++r) {
+    double acc = y[r];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc = fma((double)M[r * NB + c], x[c], acc);
+    y[r] = acc;
+  }
+}
+
+__global__ void k_to_f32(long n, const double* __restrict__ a, float* __restrict__ b) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) b[t] = (float)a[t];
+}
+
 __device__ __forceinline__ void blk_mv_acc(const double* __restrict__ M, const double* __restrict__ x, double* y) {
 #pragma unroll
   for (int r = 0; r < NB; ++r) {
@@ -387,7 +403,7 @@ __device__ __forceinline__ void face_terms(int lev, const double* __restrict__ x
 }
 
 // y = K x (mode 0) or y = b - K x (mode 1)
-__global__ void k_apply(int S, int nx, int ny, const double* __restrict__ D, const double* __restrict__ sgt,
+__global__ void k_apply(int S, int nx, int ny, const float* __restrict__ D, const double* __restrict__ sgt,
                         const double* __restrict__ sgs, int lev,
                         const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ y, int mode,
                         const int* __restrict__ act) {
@@ -402,7 +418,7 @@ __global__ void k_apply(int S, int nx, int ny, const double* __restrict__ D, con
 #pragma unroll
   for (int r = 0; r < NB; ++r) acc[r] = 0.0;
   if (D)
-    blk_mv_acc(D + t * NB2, xs + c * NB, acc);
+    blk_mv_accf(D + t * NB2, xs + c * NB, acc);
   else
     fine_block_mv(sgt[t], sgt[t] - sgs[t], xs + c * NB, acc);
   face_terms(lev, xs, nx, ny, ix, iy, c, acc);
@@ -418,7 +434,7 @@ __global__ void k_apply(int S, int nx, int ny, const double* __restrict__ D, con
 }
 
 // red-black block Gauss-Seidel half sweep: x_c = Dinv_c (b_c - sum_nbr C x_nbr)
-__global__ void k_gs(int S, int nx, int ny, int color, const double* __restrict__ Dinv, const double* __restrict__ sgt,
+__global__ void k_gs(int S, int nx, int ny, int color, const float* __restrict__ Dinv, const double* __restrict__ sgt,
                      const double* __restrict__ sgs, int lev,
                      double* __restrict__ x, const double* __restrict__ b, const int* __restrict__ act, int zero_init) {
   const long nc = (long)nx * ny;
@@ -461,7 +477,7 @@ __global__ void k_gs(int S, int nx, int ny, int color, const double* __restrict_
     if (Dinv) {
 #pragma unroll
       for (int r = 0; r < NB; ++r) out[r] = 0.0;
-      blk_mv_acc(Dinv + (s * nc + c) * NB2, rr, out);
+      blk_mv_accf(Dinv + (s * nc + c) * NB2, rr, out);
     } else {
       const long fi = s * nc + c;
       fine_block_solve(sgt[fi], sgt[fi] - sgs[fi], rr, out);
@@ -992,6 +1008,22 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
     RTE_CUDA(cudaGetLastError());
     RTE_CUDA(cudaStreamSynchronize(st));
   }
+  // fp32 copies of the coarse blocks for the V-cycle (the V-cycle is only a
+  // preconditioner: the outer BiCGStab residuals stay fp64), fp64 released
+  for (size_t l = 1; l < d->L.size(); ++l) {
+    Level& lv = d->L[l];
+    const long nb = (long)S * lv.nc * NB2;
+    lv.Df.alloc(nb);
+    lv.Dinvf.alloc(nb);
+    k_to_f32<<<nblocks(nb), 256, 0, st>>>(nb, lv.D.p, lv.Df.p);
+    k_to_f32<<<nblocks(nb), 256, 0, st>>>(nb, lv.Dinv.p, lv.Dinvf.p);
+    RTE_CUDA(cudaGetLastError());
+  }
+  RTE_CUDA(cudaStreamSynchronize(st));
+  for (size_t l = 1; l < d->L.size(); ++l) {
+    d->L[l].D.release();
+    d->L[l].Dinv.release();
+  }
   // Krylov workspace
   const size_t nv = (size_t)S * l0.nc * NB;
   for (DBuf<double>* b : {&d->r, &d->rh, &d->p, &d->v, &d->s, &d->t, &d->x, &d->ph, &d->sh}) b->alloc(nv);
@@ -1009,9 +1041,9 @@ static void smooth(Dsa2D* d, int l, const double* b, double* x, const int* act, 
   const int S = d->S;
   const long half = (lv.nc + 1) / 2;
   const int c0 = reverse ? 1 : 0;
-  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, c0, lv.Dinv.p, d->sgt, d->sgs, l, x, b,
+  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, c0, lv.Dinvf.p, d->sgt, d->sgs, l, x, b,
                                                       act, zero_init ? 1 : 0);
-  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, 1 - c0, lv.Dinv.p, d->sgt, d->sgs, l, x,
+  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, 1 - c0, lv.Dinvf.p, d->sgt, d->sgs, l, x,
                                                       b, act, 0);
 }
 
@@ -1030,7 +1062,7 @@ static void vcycle(Dsa2D* d, int l, const double* b, double* x, const int* act, 
     return;
   }
   for (int k = 0; k < d->nu; ++k) smooth(d, l, b, x, act, k == 0, false, st);
-  k_apply<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, lv.D.p, d->sgt, d->sgs, l, x, b,
+  k_apply<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, lv.Df.p, d->sgt, d->sgs, l, x, b,
                                                           lv.r.p, 1, act);
   Level& lc = d->L[l + 1];
   k_restrict<<<nblocks((long)S * lc.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, d->P.p, lv.r.p, lc.b.p, act);
@@ -1090,12 +1122,12 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     dots(d, n, {{d->rh.p, d->r.p}}, st);
     k_bicg_p<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->r.p, d->p.p, d->v.p, d->act.p);
     vcycle(d, 0, d->p.p, d->ph.p, d->act.p, st);
-    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, l0.D.p, d->sgt, d->sgs, 0, d->ph.p,
+    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, nullptr, d->sgt, d->sgs, 0, d->ph.p,
                                                             nullptr, d->v.p, 0, d->act.p);
     dots(d, n, {{d->rh.p, d->v.p}}, st);
     k_bicg_s<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->r.p, d->v.p, d->s.p, d->act.p);
     vcycle(d, 0, d->s.p, d->sh.p, d->act.p, st);
-    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, l0.D.p, d->sgt, d->sgs, 0, d->sh.p,
+    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, nullptr, d->sgt, d->sgs, 0, d->sh.p,
                                                             nullptr, d->t.p, 0, d->act.p);
     dots(d, n, {{d->t.p, d->s.p}, {d->t.p, d->t.p}}, st);
     k_bicg_x<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->x.p, d->ph.p, d->sh.p, d->r.p, d->s.p,
