@@ -160,12 +160,14 @@ __device__ __forceinline__ void lift_mv(const double* M, const double* v, double
   }
 }
 
-__device__ __forceinline__ void face_mv(int lev, int dir, const double* __restrict__ xn, double* y) {
+// Vectors are component-major per sample (SoA): x[s][r][cell], so a warp's
+// loads of one component of consecutive cells coalesce.
+__device__ __forceinline__ void face_mv(int lev, int dir, const double* __restrict__ xs, long nc, long cn, double* y) {
   const int axis = dir >> 1;
   const int j = axis == 0 ? 4 : 8, o = axis == 0 ? 8 : 4;
   double v[NB];
 #pragma unroll
-  for (int r = 0; r < NB; ++r) v[r] = xn[r];
+  for (int r = 0; r < NB; ++r) v[r] = xs[r * nc + cn];
   lift_mv(c_face[lev][dir][0], v, y, axis);
   lift_mv(c_face[lev][dir][1], v + j, y, axis);
   lift_mv(c_face[lev][dir][2], v, y + j, axis);
@@ -396,10 +398,11 @@ __device__ __forceinline__ void blk_mv_acc(const double* __restrict__ M, const d
 // off-diagonal (face) contributions sum_nbr C_dir x_nbr
 __device__ __forceinline__ void face_terms(int lev, const double* __restrict__ xs, int nx, int ny, int ix, int iy,
                                            long c, double* y) {
-  if (ix > 0) face_mv(lev, 0, xs + (c - 1) * NB, y);
-  if (ix < nx - 1) face_mv(lev, 1, xs + (c + 1) * NB, y);
-  if (iy > 0) face_mv(lev, 2, xs + (c - nx) * NB, y);
-  if (iy < ny - 1) face_mv(lev, 3, xs + (c + nx) * NB, y);
+  const long nc = (long)nx * ny;
+  if (ix > 0) face_mv(lev, 0, xs, nc, c - 1, y);
+  if (ix < nx - 1) face_mv(lev, 1, xs, nc, c + 1, y);
+  if (iy > 0) face_mv(lev, 2, xs, nc, c - nx, y);
+  if (iy < ny - 1) face_mv(lev, 3, xs, nc, c + nx, y);
 }
 
 // y = K x (mode 0) or y = b - K x (mode 1)
@@ -414,22 +417,25 @@ __global__ void k_apply(int S, int nx, int ny, const float* __restrict__ D, cons
   if (act && !act[s]) return;
   const int ix = (int)(c % nx), iy = (int)(c / nx);
   const double* xs = x + s * nc * NB;
-  double acc[NB];
+  double acc[NB], xl[NB];
 #pragma unroll
-  for (int r = 0; r < NB; ++r) acc[r] = 0.0;
+  for (int r = 0; r < NB; ++r) {
+    acc[r] = 0.0;
+    xl[r] = xs[r * nc + c];
+  }
   if (D)
-    blk_mv_accf(D + t * NB2, xs + c * NB, acc);
+    blk_mv_accf(D + t * NB2, xl, acc);
   else
-    fine_block_mv(sgt[t], sgt[t] - sgs[t], xs + c * NB, acc);
+    fine_block_mv(sgt[t], sgt[t] - sgs[t], xl, acc);
   face_terms(lev, xs, nx, ny, ix, iy, c, acc);
-  double* yo = y + t * NB;
+  double* yo = y + s * nc * NB + c;
   if (mode == 1) {
-    const double* bi = b + t * NB;
+    const double* bi = b + s * nc * NB + c;
 #pragma unroll
-    for (int r = 0; r < NB; ++r) yo[r] = bi[r] - acc[r];
+    for (int r = 0; r < NB; ++r) yo[r * nc] = bi[r * nc] - acc[r];
   } else {
 #pragma unroll
-    for (int r = 0; r < NB; ++r) yo[r] = acc[r];
+    for (int r = 0; r < NB; ++r) yo[r * nc] = acc[r];
   }
 }
 
@@ -466,13 +472,13 @@ __global__ void k_gs(int S, int nx, int ny, int color, const float* __restrict__
     c = (long)iy * nx + ix;
     const double* xs = x + s * nc * NB;
     double acc[NB];
-    const double* bi = b + (s * nc + c) * NB;
+    const double* bi = b + s * nc * NB + c;
 #pragma unroll
     for (int r = 0; r < NB; ++r) acc[r] = 0.0;
     if (!zero_init) face_terms(lev, xs, nx, ny, ix, iy, c, acc);
     double rr[NB];
 #pragma unroll
-    for (int r = 0; r < NB; ++r) rr[r] = bi[r] - acc[r];
+    for (int r = 0; r < NB; ++r) rr[r] = bi[r * nc] - acc[r];
     double out[NB];
     if (Dinv) {
 #pragma unroll
@@ -482,9 +488,9 @@ __global__ void k_gs(int S, int nx, int ny, int color, const float* __restrict__
       const long fi = s * nc + c;
       fine_block_solve(sgt[fi], sgt[fi] - sgs[fi], rr, out);
     }
-    double* xo = x + (s * nc + c) * NB;
+    double* xo = x + s * nc * NB + c;
 #pragma unroll
-    for (int r = 0; r < NB; ++r) xo[r] = out[r];
+    for (int r = 0; r < NB; ++r) xo[r * nc] = out[r];
   }
 }
 
@@ -504,18 +510,19 @@ __global__ void k_restrict(int S, int fnx, int fny, const double* __restrict__ P
   for (int py = 0; py < 2; ++py)
     for (int px = 0; px < 2; ++px) {
       const long c = (long)(2 * cy + py) * fnx + 2 * cx + px;
-      const double* r = rf + (s * (long)fnx * fny + c) * NB;
+      const long nf = (long)fnx * fny;
+      const double* r = rf + s * nf * NB + c;
       const double* E = P + (px + 2 * py) * 16;
       for (int f = 0; f < 3; ++f)
         for (int k = 0; k < 4; ++k) {
           double acc = out[4 * f + k];
-          for (int l = 0; l < 4; ++l) acc = fma(E[4 * l + k], r[4 * f + l], acc);
+          for (int l = 0; l < 4; ++l) acc = fma(E[4 * l + k], r[(4 * f + l) * nf], acc);
           out[4 * f + k] = acc;
         }
     }
-  double* o = bc + t * NB;
+  double* o = bc + s * ncc * NB + C;
 #pragma unroll
-  for (int r = 0; r < NB; ++r) o[r] = out[r];
+  for (int r = 0; r < NB; ++r) o[r * ncc] = out[r];
 }
 
 // x_c += P_pos x_C
@@ -530,13 +537,14 @@ __global__ void k_prolong_add(int S, int fnx, int fny, const double* __restrict_
   const int cnx = fnx / 2;
   const long C = (long)(iy / 2) * cnx + ix / 2;
   const double* E = P + ((ix & 1) + 2 * (iy & 1)) * 16;
-  const double* xcs = xc + (s * (long)(fnx / 2) * (fny / 2) + C) * NB;
-  double* o = xf + t * NB;
+  const long ncc = (long)(fnx / 2) * (fny / 2);
+  const double* xcs = xc + s * ncc * NB + C;
+  double* o = xf + s * nf * NB + c;
   for (int f = 0; f < 3; ++f)
     for (int l = 0; l < 4; ++l) {
-      double acc = o[4 * f + l];
-      for (int k = 0; k < 4; ++k) acc = fma(E[4 * l + k], xcs[4 * f + k], acc);
-      o[4 * f + l] = acc;
+      double acc = o[(4 * f + l) * nf];
+      for (int k = 0; k < 4; ++k) acc = fma(E[4 * l + k], xcs[(4 * f + k) * ncc], acc);
+      o[(4 * f + l) * nf] = acc;
     }
 }
 
@@ -549,14 +557,16 @@ __global__ void k_dense_coarse(int S, int nx, int ny, const double* __restrict__
   const long s = t / nc, c = t - s * nc;
   const int ix = (int)(c % nx), iy = (int)(c / nx);
   double* As = A + s * n * n;
+  // SoA ordering of the coarsest vector: index(cell, r) = r * nc + cell
+  auto col = [&](long cell, int q) { return (long)q * nc + cell; };
   for (int r = 0; r < NB; ++r) {
-    double* row = As + (c * NB + r) * n;
+    double* row = As + col(c, r) * n;
     for (long j = 0; j < n; ++j) row[j] = 0.0;
-    for (int q = 0; q < NB; ++q) row[c * NB + q] = D[t * NB2 + r * NB + q];
-    if (ix > 0) for (int q = 0; q < NB; ++q) row[(c - 1) * NB + q] = nbr[0 * NB2 + r * NB + q];
-    if (ix < nx - 1) for (int q = 0; q < NB; ++q) row[(c + 1) * NB + q] = nbr[1 * NB2 + r * NB + q];
-    if (iy > 0) for (int q = 0; q < NB; ++q) row[(c - nx) * NB + q] = nbr[2 * NB2 + r * NB + q];
-    if (iy < ny - 1) for (int q = 0; q < NB; ++q) row[(c + nx) * NB + q] = nbr[3 * NB2 + r * NB + q];
+    for (int q = 0; q < NB; ++q) row[col(c, q)] = D[t * NB2 + r * NB + q];
+    if (ix > 0) for (int q = 0; q < NB; ++q) row[col(c - 1, q)] = nbr[0 * NB2 + r * NB + q];
+    if (ix < nx - 1) for (int q = 0; q < NB; ++q) row[col(c + 1, q)] = nbr[1 * NB2 + r * NB + q];
+    if (iy > 0) for (int q = 0; q < NB; ++q) row[col(c - nx, q)] = nbr[2 * NB2 + r * NB + q];
+    if (iy < ny - 1) for (int q = 0; q < NB; ++q) row[col(c + nx, q)] = nbr[3 * NB2 + r * NB + q];
   }
 }
 
@@ -783,11 +793,12 @@ __global__ void k_pack_rhs(int S, long nc, const double* __restrict__ in, const 
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long)S * nc) return;
   const long s = t / nc;
+  const long c = t - s * nc;
   const bool on = !kind || kind[s] == KIND_DSA;
   const double m = apply_ms ? ss[t] : 1.0;
-  double* o = b + t * NB;
-  for (int r = 0; r < 4; ++r) o[r] = on ? m * in[t * 4 + r] : 0.0;
-  for (int r = 4; r < NB; ++r) o[r] = 0.0;
+  double* o = b + s * nc * NB + c;
+  for (int r = 0; r < 4; ++r) o[r * nc] = on ? m * in[t * 4 + r] : 0.0;
+  for (int r = 4; r < NB; ++r) o[r * nc] = 0.0;
 }
 
 __global__ void k_unpack(int S, long nc, const double* __restrict__ x, double* __restrict__ out,
@@ -796,7 +807,8 @@ __global__ void k_unpack(int S, long nc, const double* __restrict__ x, double* _
   if (t >= (long)S * nc) return;
   const long s = t / nc;
   if (kind && kind[s] != KIND_DSA) return;
-  for (int r = 0; r < 4; ++r) out[t * 4 + r] = x[t * NB + r];
+  const long c = t - s * nc;
+  for (int r = 0; r < 4; ++r) out[t * 4 + r] = x[s * nc * NB + r * nc + c];
 }
 
 inline int nblocks(long n, int bs = 256) { return (int)((n + bs - 1) / bs); }
