@@ -370,19 +370,27 @@ __global__ void k_galerkin_diag(int S, int fnx, int fny, const double* __restric
   for (int e = 0; e < NB2; ++e) Dc[t * NB2 + e] = out[e];
 }
 
-__device__ __forceinline__ void blk_mv_accf(const float* __restrict__ M, const double* __restrict__ x, double* y) {
+// Coarse-level blocks are stored element-major in fp32: M[s][e][cell]
+// (e = r * 12 + c), so a warp's loads of one element coalesce.  `M` points at
+// (sample s, element 0, cell c); `stride` = cells per sample of the level.
+__device__ __forceinline__ void blk_mv_accf(const float* __restrict__ M, long stride, const double* __restrict__ x,
+                                            double* y) {
 #pragma unroll
   for (int r = 0; r < NB; ++r) {
     double acc = y[r];
 #pragma unroll
-    for (int c = 0; c < NB; ++c) acc = fma((double)M[r * NB + c], x[c], acc);
+    for (int c = 0; c < NB; ++c) acc = fma((double)M[(r * NB + c) * stride], x[c], acc);
     y[r] = acc;
   }
 }
 
-__global__ void k_to_f32(long n, const double* __restrict__ a, float* __restrict__ b) {
+// [S][nc][144] fp64 -> [S][144][nc] fp32
+__global__ void k_to_f32(int S, long nc, const double* __restrict__ a, float* __restrict__ b) {
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < n) b[t] = (float)a[t];
+  if (t >= (long)S * nc * NB2) return;
+  const long s = t / (nc * NB2), rem = t - s * nc * NB2;
+  const long e = rem / nc, c = rem - e * nc;
+  b[t] = (float)a[(s * nc + c) * NB2 + e];
 }
 
 __device__ __forceinline__ void blk_mv_acc(const double* __restrict__ M, const double* __restrict__ x, double* y) {
@@ -424,7 +432,7 @@ __global__ void k_apply(int S, int nx, int ny, const float* __restrict__ D, cons
     xl[r] = xs[r * nc + c];
   }
   if (D)
-    blk_mv_accf(D + t * NB2, xl, acc);
+    blk_mv_accf(D + s * nc * NB2 + c, nc, xl, acc);
   else
     fine_block_mv(sgt[t], sgt[t] - sgs[t], xl, acc);
   face_terms(lev, xs, nx, ny, ix, iy, c, acc);
@@ -483,7 +491,7 @@ __global__ void k_gs(int S, int nx, int ny, int color, const float* __restrict__
     if (Dinv) {
 #pragma unroll
       for (int r = 0; r < NB; ++r) out[r] = 0.0;
-      blk_mv_accf(Dinv + (s * nc + c) * NB2, rr, out);
+      blk_mv_accf(Dinv + s * nc * NB2 + c, nc, rr, out);
     } else {
       const long fi = s * nc + c;
       fine_block_solve(sgt[fi], sgt[fi] - sgs[fi], rr, out);
@@ -1027,8 +1035,8 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
     const long nb = (long)S * lv.nc * NB2;
     lv.Df.alloc(nb);
     lv.Dinvf.alloc(nb);
-    k_to_f32<<<nblocks(nb), 256, 0, st>>>(nb, lv.D.p, lv.Df.p);
-    k_to_f32<<<nblocks(nb), 256, 0, st>>>(nb, lv.Dinv.p, lv.Dinvf.p);
+    k_to_f32<<<nblocks(nb), 256, 0, st>>>(S, lv.nc, lv.D.p, lv.Df.p);
+    k_to_f32<<<nblocks(nb), 256, 0, st>>>(S, lv.nc, lv.Dinv.p, lv.Dinvf.p);
     RTE_CUDA(cudaGetLastError());
   }
   RTE_CUDA(cudaStreamSynchronize(st));
