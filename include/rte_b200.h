@@ -162,6 +162,41 @@ int rte_set_affine(rte_ctx* ctx, const rte_affine* aff);
 int rte_apply_term_kinetic(rte_ctx* ctx, int k, int n_cols, const double* u_dev, double* out_dev,
                            void* stream);
 
+/* collect_snapshots (snapshots.cpp:118-194) for every sample: training
+ * SI-DSA in kinetic form, stopping on ||drho||_inf < eps_train.  Stores
+ * f^(l) for l <= window in f_iter_dev [S][window][n_dirs*n_dof], drho^(l) in
+ * drho_dev [S][window][n_dof] and the last (converged) f in f_conv_dev
+ * [S][n_dirs*n_dof].  converged_host[S], n_iter_host[S] (w_mu =
+ * min(n_iter, window)). */
+int rte_collect_snapshots(rte_ctx* ctx, int window, double eps_train, int max_iters, double* f_iter_dev,
+                          double* f_conv_dev, double* drho_dev, int* converged_host, int* n_iter_host);
+
+/* Training matrices from rte_collect_snapshots output (PrimarySource /
+ * CorrectionSource, snapshots.cpp:316-376): kind 0 = converged solutions,
+ * kind 1 = correction columns f - f^(l), l <= min(n_iter, window,
+ * window_limit); converged samples only.  out_dev (may be NULL to count)
+ * [n_cols][n_dirs*n_dof]; *n_cols receives the column count. */
+int rte_snapshot_columns(rte_ctx* ctx, int window, const double* f_iter_dev, const double* f_conv_dev,
+                         const int* n_iter_host, const int* converged_host, int kind, int window_limit,
+                         double* out_dev, int* n_cols);
+
+/* ---- POD and Galerkin projections (pod.cpp, reduced_model.cpp) ----------- */
+/* POD of F (m x n column-major, device; m >= n, n <= 128): all n singular
+ * values to sigma_host (descending) and the first rank_max left singular
+ * vectors to U_dev (m x rank_max, column-major).  Shifted CholeskyQR3 on the
+ * device + one-sided Jacobi SVD of the n x n factor (replaces dgesdd / TSQR,
+ * pod.cpp:81-94, 173-276). */
+int rte_pod(int device, long m, int n, const double* F_dev, int rank_max, double* U_dev, double* sigma_host,
+            void* stream);
+/* truncation_rank (pod.cpp:117-139). */
+int rte_truncation_rank(const double* sigma, int n, double eps_pod);
+/* build_reduced_model (reduced_model.cpp:106-199) on the device from a basis
+ * U_dev (n_dirs*n_dof x r, column-major) with the context's (sample-
+ * independent) term operators; outputs in the rte_rom layout to host arrays.
+ * RTE_ERR_RUNTIME if ||U^T U - I||_max > 1e-10 (reduced_model.cpp:189-194). */
+int rte_build_rom(rte_ctx* ctx, int r, const double* U_dev, double* u_rho_host, double* u_iso_host,
+                  double* a_r_host, double* b_r_host);
+
 /* ---- DSA (dsa.cpp) ----------------------------------------------------- */
 /* DsaOperator ctor (dsa.cpp:154-258): assemble + factor per sample. */
 int rte_dsa_setup(rte_ctx* ctx, void* stream);

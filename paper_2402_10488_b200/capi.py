@@ -71,6 +71,13 @@ SIGNATURES = [
     ("rte_apply_Mt", ctypes.c_int, [_vp, _vp, _vp, _vp]),
     ("rte_set_affine", ctypes.c_int, [_vp, ctypes.POINTER(Affine)]),
     ("rte_apply_term_kinetic", ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
+    ("rte_collect_snapshots", ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, _vp, _vp, _vp, _ip,
+                                             _ip]),
+    ("rte_snapshot_columns", ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _ip, _ip, ctypes.c_int, ctypes.c_int, _vp,
+                                            _ip]),
+    ("rte_pod", ctypes.c_int, [ctypes.c_int, ctypes.c_long, ctypes.c_int, _vp, ctypes.c_int, _vp, _dp, _vp]),
+    ("rte_truncation_rank", ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_double]),
+    ("rte_build_rom", ctypes.c_int, [_vp, ctypes.c_int, _vp, _dp, _dp, _dp, _dp]),
     ("rte_dsa_setup", ctypes.c_int, [_vp, _vp]),
     ("rte_dsa_solve_density", ctypes.c_int, [_vp, _vp, _vp, _vp]),
     ("rte_dsa_correct", ctypes.c_int, [_vp, _vp, _vp, _vp]),

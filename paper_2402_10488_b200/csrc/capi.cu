@@ -206,7 +206,7 @@ void build_slots(rte_ctx* c) {
 // Canonical slot constants; `single` >= 0 restricts to one slot with weight 1.
 std::vector<Slot2D> slot_table(const rte_ctx* c, int dpl, int groups, int nq_pad, int single) {
   std::vector<Slot2D> t((size_t)4 * nq_pad);
-  for (auto& e : t) e = Slot2D{1.0, 1.0, 0.0, 0.0, 0.0};
+  for (auto& e : t) e = Slot2D{1.0, 1.0, 0.0, 0.0, 0.0, -1, -1};
   const double hx = c->hx, hy = c->hy;
   for (int q = 0; q < 4; ++q) {
     int n = 0;
@@ -222,6 +222,14 @@ std::vector<Slot2D> slot_table(const rte_ctx* c, int dpl, int groups, int nq_pad
       const double gy = vy > 0 ? c->inflow[2] : c->inflow[3];
       sl.bcx = std::fabs(vx) * gx * (1.0 / std::sqrt(hx)) * std::sqrt(hy);
       sl.bcy = std::fabs(vy) * gy * (1.0 / std::sqrt(hy)) * std::sqrt(hx);
+      sl.dir0 = sl.dir1 = -1;
+      for (int j = 0; j < c->nv; ++j)
+        if (c->dir_slot[j] == k) {
+          if (sl.dir0 < 0)
+            sl.dir0 = j;
+          else if (sl.dir1 < 0)
+            sl.dir1 = j;
+        }
       t[(size_t)q * nq_pad + n] = sl;
       ++n;
     }
@@ -301,7 +309,7 @@ namespace rte {
 // fixed-order partial reduction.  rho_prev/delta/change_bits: SI epilogue.
 static void transport_apply_ex(rte_ctx* ctx, int mode, int single, const double* rho, double* out, const int* active,
                                const double* rho_prev, double* delta, unsigned long long* change_bits,
-                               cudaStream_t st) {
+                               cudaStream_t st, double* fout = nullptr) {
   if (ctx->geom == RTE_SLAB1D) {
     Sweep1DArgs a{};
     a.S = ctx->S;
@@ -322,7 +330,7 @@ static void transport_apply_ex(rte_ctx* ctx, int mode, int single, const double*
     a.mode = mode;
     a.j_single = single;
     a.out = single >= 0 ? nullptr : out;
-    a.fout = single >= 0 ? out : nullptr;
+    a.fout = single >= 0 ? out : fout;
     a.active = active;
     a.rho_prev = rho_prev;
     a.delta = delta;
@@ -371,6 +379,8 @@ static void transport_apply_ex(rte_ctx* ctx, int mode, int single, const double*
   a.ybuf = ctx->ws_c.p;
   a.sync = ctx->ws_sync.p;
   a.active = active;
+  a.fout = fout;
+  a.nv = ctx->nv;
   {
     ProfScope ps(ctx, RTE_PROF_SWEEP, st);
     launch_sweep2d(a, st);
@@ -386,6 +396,13 @@ static void transport_apply_ex(rte_ctx* ctx, int mode, int single, const double*
 void transport_apply(rte_ctx* ctx, int mode, const double* rho, double* out, const int* active,
                      const double* rho_prev, double* delta, unsigned long long* change_bits, cudaStream_t st) {
   transport_apply_ex(ctx, mode, -1, rho, out, active, rho_prev, delta, change_bits, st);
+}
+
+// one kinetic sweep: f (all original directions) and rho* = density(f), with
+// the SI epilogue against rho (transport_system.cpp:420-441)
+void kinetic_fixed_point(rte_ctx* ctx, const double* rho, double* rstar, double* f, const int* active,
+                         double* delta, unsigned long long* bits, cudaStream_t st) {
+  transport_apply_ex(ctx, SRC_MS_RHO | SRC_G | SRC_BC, -1, rho, rstar, active, rho, delta, bits, st, f);
 }
 
 void launch_apply_block(int S, int ncells, int nl, int block, const double* m, const double* x, double* out,
@@ -518,30 +535,9 @@ int rte_sweep_direction(rte_ctx* ctx, int j, const double* rhs, double* f, void*
 int rte_kinetic_sweep(rte_ctx* ctx, const double* rho, double* f, void* stream) {
   return guarded(ctx, [&] {
     DeviceGuard dg(ctx->device);
-    if (ctx->geom == RTE_SLAB1D) {
-      Sweep1DArgs a{};
-      a.S = ctx->S;
-      a.N = ctx->ncells;
-      a.nv = ctx->nv;
-      a.ndof = ctx->ndof;
-      a.width = ctx->width.p;
-      a.vx = ctx->dvx.p;
-      a.w = ctx->dw.p;
-      a.block = ctx->block;
-      a.mt = ctx->mt.p;
-      a.ms = ctx->ms.p;
-      a.g = ctx->g.p;
-      a.g_shared = ctx->g_shared;
-      a.rho = rho;
-      a.inflow_l = ctx->inflow[0];
-      a.inflow_r = ctx->inflow[1];
-      a.mode = SRC_MS_RHO | SRC_G | SRC_BC;
-      a.j_single = -1;
-      a.fout = f;
-      launch_sweep1d(a, as_stream(stream));
-      return;
-    }
-    throw Error(RTE_ERR_UNSUPPORTED, "kinetic_sweep: xy geometry not implemented in this build");
+    ctx->ws_b.alloc((size_t)ctx->S * ctx->ndof);
+    transport_apply_ex(ctx, SRC_MS_RHO | SRC_G | SRC_BC, -1, rho, ctx->ws_b.p, nullptr, nullptr, nullptr, nullptr,
+                       as_stream(stream), f);
   });
 }
 
@@ -585,8 +581,21 @@ int rte_set_affine(rte_ctx* ctx, const rte_affine* aff) {
   });
 }
 
-int rte_apply_term_kinetic(rte_ctx* ctx, int, int, const double*, double*, void*) {
-  return guarded(ctx, [&] { throw Error(RTE_ERR_UNSUPPORTED, "apply_term_kinetic: not implemented in this build"); });
+int rte_apply_term_kinetic(rte_ctx* ctx, int k, int n_cols, const double* u, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    apply_term_kinetic(ctx, k, n_cols, u, out, as_stream(stream));
+  });
+}
+
+int rte_collect_snapshots(rte_ctx* ctx, int window, double eps_train, int max_iters, double* f_iter_dev,
+                          double* f_conv_dev, double* drho_dev, int* converged_host, int* n_iter_host) {
+  return guarded(ctx, [&] {
+    RTE_REQUIRE(window >= 1 && max_iters >= 1, RTE_ERR_INVALID, "collect_snapshots: bad window / max_iters");
+    DeviceGuard dg(ctx->device);
+    collect_snapshots(ctx, window, eps_train, max_iters, f_iter_dev, f_conv_dev, drho_dev, converged_host,
+                      n_iter_host, nullptr);
+  });
 }
 
 int rte_dsa_setup(rte_ctx* ctx, void* stream) {
@@ -781,6 +790,94 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
     }
     if (history) RTE_CUDA(cudaMemcpy(history, hist.p, sizeof(double) * S * cfg.max_iters, cudaMemcpyDeviceToHost));
     if (log) RTE_CUDA(cudaMemcpy(log, lg.p, (size_t)S * cfg.max_iters, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rte_snapshot_columns(rte_ctx* ctx, int window, const double* f_iter, const double* f_conv, const int* n_iter,
+                         const int* conv, int kind, int window_limit, double* out, int* n_cols) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    *n_cols = snapshot_columns(ctx->S, window, (long)ctx->nv * ctx->ndof, f_iter, f_conv, n_iter, conv, kind,
+                               window_limit > 0 ? window_limit : (1 << 30), out, nullptr);
+  });
+}
+
+int rte_pod(int device, long m, int n, const double* F, int rank_max, double* U, double* sigma, void* stream) {
+  return guarded(nullptr, [&] {
+    DeviceGuard dg(device);
+    pod(m, n, F, rank_max, U, sigma, as_stream(stream));
+  });
+}
+
+int rte_truncation_rank(const double* s, int n, double eps_pod) {
+  // pod.cpp:117-139: modes below 1e-14 sigma_1 are exact zeros; smallest l
+  // with partial/total >= 1 - eps.  -1 for a zero matrix.
+  if (n <= 0 || !(s[0] > 0)) return -1;
+  const double guard = 1e-14 * s[0];
+  int kept = 0;
+  double total = 0;
+  for (int k = 0; k < n; ++k) {
+    if (s[k] >= guard) {
+      total += s[k];
+      kept = k + 1;
+    } else {
+      break;
+    }
+  }
+  double partial = 0;
+  for (int l = 0; l < kept; ++l) {
+    partial += s[l];
+    if (partial / total >= 1.0 - eps_pod) return l + 1;
+  }
+  return kept;
+}
+
+int rte_build_rom(rte_ctx* ctx, int r, const double* U, double* u_rho, double* u_iso, double* a_r, double* b_r) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    // kinetic right-hand side b_j = G + g_j^bc (transport_system.cpp:615-624, 142-187)
+    const long nd = ctx->ndof;
+    std::vector<double> g(nd);
+    RTE_CUDA(cudaMemcpy(g.data(), ctx->g.p, sizeof(double) * nd, cudaMemcpyDeviceToHost));
+    std::vector<double> b((size_t)ctx->nv * nd);
+    const double s3 = kSqrt3;
+    for (int j = 0; j < ctx->nv; ++j) {
+      double* bj = b.data() + (size_t)j * nd;
+      std::copy(g.begin(), g.end(), bj);
+      const double vx = ctx->vx[j], vy = ctx->vy[j];
+      if (ctx->geom == RTE_SLAB1D) {
+        const int n = ctx->nx;
+        if (vx > 0 && ctx->inflow[0] != 0) {
+          const double a = vx * ctx->inflow[0] / std::sqrt(ctx->bounds[1] - ctx->bounds[0]);
+          bj[0] += a;
+          bj[1] += -s3 * a;
+        } else if (vx < 0 && ctx->inflow[1] != 0) {
+          const double a = -vx * ctx->inflow[1] / std::sqrt(ctx->bounds[n] - ctx->bounds[n - 1]);
+          bj[2 * (n - 1)] += a;
+          bj[2 * (n - 1) + 1] += s3 * a;
+        }
+        continue;
+      }
+      const int nx = ctx->nx, ny = ctx->ny;
+      const double sx = 1.0 / std::sqrt(ctx->hx), sy = 1.0 / std::sqrt(ctx->hy);
+      if (vx > 0 && ctx->inflow[0] != 0) {
+        const double a = vx * ctx->inflow[0] * sx * std::sqrt(ctx->hy);
+        for (int iy = 0; iy < ny; ++iy) { bj[4L * (nx * iy)] += a; bj[4L * (nx * iy) + 1] += -s3 * a; }
+      }
+      if (vx < 0 && ctx->inflow[1] != 0) {
+        const double a = -vx * ctx->inflow[1] * sx * std::sqrt(ctx->hy);
+        for (int iy = 0; iy < ny; ++iy) { bj[4L * (nx - 1 + nx * iy)] += a; bj[4L * (nx - 1 + nx * iy) + 1] += s3 * a; }
+      }
+      if (vy > 0 && ctx->inflow[2] != 0) {
+        const double a = vy * ctx->inflow[2] * sy * std::sqrt(ctx->hx);
+        for (int ix = 0; ix < nx; ++ix) { bj[4L * ix] += a; bj[4L * ix + 2] += -s3 * a; }
+      }
+      if (vy < 0 && ctx->inflow[3] != 0) {
+        const double a = -vy * ctx->inflow[3] * sy * std::sqrt(ctx->hx);
+        for (int ix = 0; ix < nx; ++ix) { bj[4L * (ix + nx * (ny - 1))] += a; bj[4L * (ix + nx * (ny - 1)) + 2] += s3 * a; }
+      }
+    }
+    build_rom(ctx, r, U, b.data(), u_rho, u_iso, a_r, b_r, nullptr);
   });
 }
 

@@ -1,0 +1,349 @@
+// pod.cu -- K7: offline POD and Galerkin projections on the device.
+//
+// Replaces pod_truncate (pod.cpp:141-304: dgesdd in-core or out-of-core TSQR)
+// and build_reduced_model (reduced_model.cpp:106-199).
+//
+// POD: shifted CholeskyQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa
+// 2020), whose backward error matches Householder QR for condition numbers up
+// to 1/u, so small singular values keep the accuracy the reference's
+// Householder/SVD path gives (a plain Gram eigen-decomposition would square
+// the condition number).  The only O(m) work -- the Gram products
+// F^T F and the right-multiplications F R^{-1}, Q W -- runs on the device
+// with deterministic two-stage reductions; the n x n factors (n <= 128)
+// are handled on the host: Cholesky and a one-sided Jacobi SVD of R (high
+// relative accuracy).
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <vector>
+
+#include "rte_internal.cuh"
+
+namespace rte {
+namespace {
+
+constexpr int TT = 32;        // output tile
+constexpr int RCH = 32;       // rows per smem stage
+constexpr int kRowChunk = 8192;
+
+// partial[chunk][tile] of C = A^T B (A: m x p, B: m x q, column-major, ld = m)
+__global__ void k_gram_partial(long m, int p, int q, const double* __restrict__ A, const double* __restrict__ B,
+                               double* __restrict__ part) {
+  __shared__ double sa[RCH][TT + 1], sb[RCH][TT + 1];
+  const int tiles_q = (q + TT - 1) / TT;
+  const int ti = blockIdx.y / tiles_q, tj = blockIdx.y % tiles_q;
+  const long r0 = (long)blockIdx.x * kRowChunk;
+  const long r1 = min(m, r0 + kRowChunk);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads, 4 outputs each
+  double acc[4] = {0, 0, 0, 0};
+  for (long rb = r0; rb < r1; rb += RCH) {
+    for (int e = threadIdx.x; e < RCH * TT; e += blockDim.x) {
+      const int rr = e % RCH, cc = e / RCH;
+      const long row = rb + rr;
+      const int ca = ti * TT + cc, cb = tj * TT + cc;
+      sa[rr][cc] = (row < r1 && ca < p) ? A[(long)ca * m + row] : 0.0;
+      sb[rr][cc] = (row < r1 && cb < q) ? B[(long)cb * m + row] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < RCH; ++rr) {
+      const double bv = sb[rr][tx];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] = fma(sa[rr][ty * 4 + k], bv, acc[k]);
+    }
+    __syncthreads();
+  }
+  double* o = part + ((long)blockIdx.x * gridDim.y + blockIdx.y) * TT * TT;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) o[(ty * 4 + k) * TT + tx] = acc[k];
+}
+
+__global__ void k_gram_reduce(int nchunks, int p, int q, const double* __restrict__ part, double* __restrict__ C) {
+  const int tiles_q = (q + TT - 1) / TT;
+  const int ntiles = gridDim.x;
+  const int tile = blockIdx.x;
+  const int ti = tile / tiles_q, tj = tile % tiles_q;
+  for (int e = threadIdx.x; e < TT * TT; e += blockDim.x) {
+    double v = 0.0;
+    for (int c = 0; c < nchunks; ++c) v += part[((long)c * ntiles + tile) * TT * TT + e];
+    const int i = ti * TT + e / TT, j = tj * TT + e % TT;
+    if (i < p && j < q) C[(long)j * p + i] = v;  // column-major p x q
+  }
+}
+
+// Y (m x k) = A (m x n) M (n x k), column-major; M in shared memory
+__global__ void k_rmul(long m, int n, int k, const double* __restrict__ A, const double* __restrict__ M,
+                       double* __restrict__ Y) {
+  extern __shared__ double sm[];
+  for (int e = threadIdx.x; e < n * k; e += blockDim.x) sm[e] = M[e];
+  __syncthreads();
+  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= m) return;
+  for (int c0 = 0; c0 < k; c0 += 16) {
+    double acc[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+    for (int l = 0; l < n; ++l) {
+      const double a = A[(long)l * m + row];
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c0 + c < k) acc[c] = fma(a, sm[(long)(c0 + c) * n + l], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c0 + c < k) Y[(long)(c0 + c) * m + row] = acc[c];
+  }
+}
+
+// u_rho / u_iso: out[c][i] = sum_j wj U[c][j][i]
+__global__ void k_block_sum(int r, int nv, long nd, const double* __restrict__ U, const double* __restrict__ w,
+                            double* __restrict__ out) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)r * nd) return;
+  const long c = t / nd, i = t - c * nd;
+  double v = 0.0;
+  for (int j = 0; j < nv; ++j) v += (w ? w[j] : 1.0) * U[(c * nv + j) * nd + i];
+  out[t] = v;
+}
+
+void gram(long m, int p, int q, const double* A, const double* B, double* C_dev, cudaStream_t st) {
+  const int tiles = ((p + TT - 1) / TT) * ((q + TT - 1) / TT);
+  const int nch = (int)((m + kRowChunk - 1) / kRowChunk);
+  DBuf<double> part;
+  part.alloc((size_t)nch * tiles * TT * TT);
+  k_gram_partial<<<dim3(nch, tiles), 256, 0, st>>>(m, p, q, A, B, part.p);
+  k_gram_reduce<<<tiles, 256, 0, st>>>(nch, p, q, part.p, C_dev);
+  RTE_CUDA(cudaGetLastError());
+  RTE_CUDA(cudaStreamSynchronize(st));
+}
+
+std::vector<double> gram_host(long m, int p, int q, const double* A, const double* B, cudaStream_t st) {
+  DBuf<double> C;
+  C.alloc((size_t)p * q);
+  gram(m, p, q, A, B, C.p, st);
+  std::vector<double> h((size_t)p * q);
+  RTE_CUDA(cudaMemcpy(h.data(), C.p, sizeof(double) * p * q, cudaMemcpyDeviceToHost));
+  return h;
+}
+
+void rmul(long m, int n, int k, const double* A, const std::vector<double>& M, double* Y, cudaStream_t st) {
+  DBuf<double> dM;
+  dM.upload(M.data(), M.size());
+  const size_t smem = sizeof(double) * n * k;
+  RTE_REQUIRE(smem <= 200 * 1024, RTE_ERR_UNSUPPORTED, "pod: too many columns");
+  static bool cfg = false;
+  if (!cfg) {
+    RTE_CUDA(cudaFuncSetAttribute(k_rmul, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    cfg = true;
+  }
+  k_rmul<<<(int)((m + 127) / 128), 128, smem, st>>>(m, n, k, A, dM.p, Y);
+  RTE_CUDA(cudaGetLastError());
+  RTE_CUDA(cudaStreamSynchronize(st));
+}
+
+// ---- host dense linear algebra (column-major n x n) ----------------------
+
+// upper Cholesky G = R^T R; false if not positive definite
+bool cholesky_upper(const std::vector<double>& G, int n, std::vector<double>& R) {
+  R.assign((size_t)n * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    double d = G[(size_t)j * n + j];
+    for (int k = 0; k < j; ++k) d -= R[(size_t)j * n + k] * R[(size_t)j * n + k];
+    if (!(d > 0)) return false;
+    const double rjj = std::sqrt(d);
+    R[(size_t)j * n + j] = rjj;
+    for (int i = j + 1; i < n; ++i) {
+      double v = G[(size_t)i * n + j];
+      for (int k = 0; k < j; ++k) v -= R[(size_t)j * n + k] * R[(size_t)i * n + k];
+      R[(size_t)i * n + j] = v / rjj;  // R(j, i) stored column-major at [i*n + j]
+    }
+  }
+  return true;
+}
+
+// inverse of upper triangular R (column-major)
+std::vector<double> inv_upper(const std::vector<double>& R, int n) {
+  std::vector<double> X((size_t)n * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    X[(size_t)j * n + j] = 1.0 / R[(size_t)j * n + j];
+    for (int i = j - 1; i >= 0; --i) {
+      double v = 0.0;
+      for (int k = i + 1; k <= j; ++k) v += R[(size_t)k * n + i] * X[(size_t)j * n + k];
+      X[(size_t)j * n + i] = -v / R[(size_t)i * n + i];
+    }
+  }
+  return X;
+}
+
+std::vector<double> matmul_cm(const std::vector<double>& A, const std::vector<double>& B, int n) {
+  std::vector<double> C((size_t)n * n, 0.0);
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < n; ++k) {
+      const double b = B[(size_t)j * n + k];
+      if (b == 0) continue;
+      for (int i = 0; i < n; ++i) C[(size_t)j * n + i] += A[(size_t)k * n + i] * b;
+    }
+  return C;
+}
+
+// One-sided Jacobi SVD of R (n x n, column-major): R = W diag(s) V^T.
+// Applied to A = R^T: A J has orthogonal columns (norms = s), so the left
+// singular vectors of R are the accumulated rotations J.
+void jacobi_svd_left(const std::vector<double>& R, int n, std::vector<double>& s, std::vector<double>& W) {
+  std::vector<double> A((size_t)n * n), J((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) A[(size_t)j * n + i] = R[(size_t)i * n + j];  // A = R^T
+  for (int i = 0; i < n; ++i) J[(size_t)i * n + i] = 1.0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        double alpha = 0, beta = 0, gamma = 0;
+        for (int i = 0; i < n; ++i) {
+          const double ap = A[(size_t)p * n + i], aq = A[(size_t)q * n + i];
+          alpha += ap * ap;
+          beta += aq * aq;
+          gamma += ap * aq;
+        }
+        if (gamma == 0.0) continue;
+        const double c0 = std::fabs(gamma) / std::sqrt(alpha * beta);
+        off = std::max(off, c0);
+        if (c0 < 1e-16) continue;
+        const double zeta = (beta - alpha) / (2.0 * gamma);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+        for (int i = 0; i < n; ++i) {
+          const double ap = A[(size_t)p * n + i], aq = A[(size_t)q * n + i];
+          A[(size_t)p * n + i] = c * ap - sn * aq;
+          A[(size_t)q * n + i] = sn * ap + c * aq;
+          const double jp = J[(size_t)p * n + i], jq = J[(size_t)q * n + i];
+          J[(size_t)p * n + i] = c * jp - sn * jq;
+          J[(size_t)q * n + i] = sn * jp + c * jq;
+        }
+      }
+    if (off < 1e-15) break;
+  }
+  std::vector<double> nrm(n);
+  for (int j = 0; j < n; ++j) {
+    double v = 0;
+    for (int i = 0; i < n; ++i) v += A[(size_t)j * n + i] * A[(size_t)j * n + i];
+    nrm[j] = std::sqrt(v);
+  }
+  std::vector<int> ord(n);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return nrm[a] > nrm[b]; });
+  s.resize(n);
+  W.assign((size_t)n * n, 0.0);
+  for (int k = 0; k < n; ++k) {
+    s[k] = nrm[ord[k]];
+    for (int i = 0; i < n; ++i) W[(size_t)k * n + i] = J[(size_t)ord[k] * n + i];
+  }
+}
+
+__global__ void k_sub(long n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ o) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) o[t] = a[t] - b[t];
+}
+
+}  // namespace
+
+// Snapshot matrices (PrimarySource / CorrectionSource, snapshots.cpp:316-376):
+// kind 0 = converged f of converged samples; kind 1 = f_conv - f^(l),
+// l <= min(n_iter, window), converged samples only.  Returns column count.
+int snapshot_columns(int S, int window, long kdim, const double* f_iter, const double* f_conv, const int* n_iter,
+                     const int* conv, int kind, int window_limit, double* out, cudaStream_t st) {
+  int col = 0;
+  for (int s = 0; s < S; ++s) {
+    if (!conv[s]) continue;
+    if (kind == 0) {
+      if (out) RTE_CUDA(cudaMemcpyAsync(out + (long)col * kdim, f_conv + (long)s * kdim, sizeof(double) * kdim,
+                                        cudaMemcpyDeviceToDevice, st));
+      ++col;
+    } else {
+      const int w = std::min(std::min(n_iter[s], window), window_limit);
+      for (int l = 1; l <= w; ++l) {
+        if (out)
+          k_sub<<<(int)((kdim + 255) / 256), 256, 0, st>>>(kdim, f_conv + (long)s * kdim,
+                                                           f_iter + ((long)s * window + l - 1) * kdim,
+                                                           out + (long)col * kdim);
+        ++col;
+      }
+    }
+  }
+  RTE_CUDA(cudaGetLastError());
+  RTE_CUDA(cudaStreamSynchronize(st));
+  return col;
+}
+
+// F: m x n column-major on device (m >= n).  sigma (n values) to host; the
+// first rank_max left singular vectors to U (m x rank_max).
+void pod(long m, int n, const double* F, int rank_max, double* U, double* sigma, cudaStream_t st) {
+  RTE_REQUIRE(n >= 1 && n <= 128, RTE_ERR_UNSUPPORTED, "pod: 1..128 snapshot columns supported");
+  RTE_REQUIRE(m >= n, RTE_ERR_UNSUPPORTED, "pod: wide snapshot matrices (rows < columns) not supported");
+  RTE_REQUIRE(rank_max >= 0 && rank_max <= n, RTE_ERR_INVALID, "pod: rank_max out of range");
+  std::vector<double> G = gram_host(m, n, n, F, F, st);
+  double fro2 = 0.0;
+  for (int i = 0; i < n; ++i) fro2 += G[(size_t)i * n + i];
+  RTE_REQUIRE(fro2 > 0, RTE_ERR_INVALID, "pod: snapshot matrix is zero");
+  const double u = 1.1102230246251565e-16;
+  const double shift = 11.0 * ((double)m * n + (double)n * (n + 1)) * u * fro2;
+  DBuf<double> Q1, Q2;
+  Q1.alloc((size_t)m * n);
+  Q2.alloc((size_t)m * n);
+  std::vector<double> Rtot((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) Rtot[(size_t)i * n + i] = 1.0;
+  const double* src = F;
+  DBuf<double>* dst = &Q1;
+  for (int pass = 0; pass < 3; ++pass) {
+    std::vector<double> Gp = pass == 0 ? G : gram_host(m, n, n, src, src, st);
+    if (pass == 0)
+      for (int i = 0; i < n; ++i) Gp[(size_t)i * n + i] += shift;
+    std::vector<double> R;
+    RTE_REQUIRE(cholesky_upper(Gp, n, R), RTE_ERR_RUNTIME, "pod: CholeskyQR breakdown");
+    rmul(m, n, n, src, inv_upper(R, n), dst->p, st);
+    Rtot = matmul_cm(R, Rtot, n);
+    src = dst->p;
+    dst = dst == &Q1 ? &Q2 : &Q1;
+  }
+  std::vector<double> s, W;
+  jacobi_svd_left(Rtot, n, s, W);
+  for (int k = 0; k < n; ++k) sigma[k] = s[k];
+  if (rank_max > 0) {
+    std::vector<double> Wr(W.begin(), W.begin() + (size_t)n * rank_max);
+    rmul(m, n, rank_max, src, Wr, U, st);
+  }
+}
+
+// build_reduced_model: U (kdim x r) on device, sample 0's discretization.
+void build_rom(rte_ctx* ctx, int r, const double* U, const double* b_kin_host, double* u_rho, double* u_iso,
+               double* a_r, double* b_r, cudaStream_t st) {
+  RTE_REQUIRE(ctx->k_terms > 0, RTE_ERR_INVALID, "build_rom: rte_set_affine first");
+  const long nd = ctx->ndof, kdim = (long)ctx->nv * nd;
+  const int K = ctx->k_terms;
+  DBuf<double> w, tmp;
+  w.upload(ctx->w.data(), ctx->nv);
+  tmp.alloc((size_t)r * nd);
+  k_block_sum<<<(int)((r * nd + 255) / 256), 256, 0, st>>>(r, ctx->nv, nd, U, w.p, tmp.p);
+  RTE_CUDA(cudaMemcpy(u_rho, tmp.p, sizeof(double) * r * nd, cudaMemcpyDeviceToHost));
+  k_block_sum<<<(int)((r * nd + 255) / 256), 256, 0, st>>>(r, ctx->nv, nd, U, nullptr, tmp.p);
+  RTE_CUDA(cudaMemcpy(u_iso, tmp.p, sizeof(double) * r * nd, cudaMemcpyDeviceToHost));
+  DBuf<double> bk;
+  bk.upload(b_kin_host, kdim);
+  std::vector<double> br = gram_host(kdim, r, 1, U, bk.p, st);
+  for (int c = 0; c < r; ++c) b_r[c] = br[c];
+  DBuf<double> Y;
+  Y.alloc((size_t)kdim * r);
+  for (int k = 0; k < K; ++k) {
+    apply_term_kinetic(ctx, k, r, U, Y.p, st);
+    std::vector<double> a = gram_host(kdim, r, r, U, Y.p, st);
+    std::copy(a.begin(), a.end(), a_r + (size_t)k * r * r);
+  }
+  std::vector<double> g = gram_host(kdim, r, r, U, U, st);
+  double ortho = 0.0;
+  for (int i = 0; i < r; ++i)
+    for (int j = 0; j < r; ++j) ortho = std::max(ortho, std::fabs(g[(size_t)j * r + i] - (i == j ? 1.0 : 0.0)));
+  RTE_REQUIRE(ortho <= 1e-10, RTE_ERR_RUNTIME,
+              "reduced model: basis columns are not orthonormal (defect " + std::to_string(ortho) + ")");
+}
+
+}  // namespace rte

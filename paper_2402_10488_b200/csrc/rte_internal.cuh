@@ -94,6 +94,7 @@ struct Slot2D {
   double a, b;   // |vx|/hx, |vy|/hy
   double w;      // folded quadrature weight (sum over the slot's directions)
   double bcx, bcy;  // inflow ghost traces (already scaled), see sweep2d.cu
+  int dir0, dir1;   // original direction indices sharing the slot (-1: none)
 };
 
 struct DsaState {
@@ -229,6 +230,8 @@ struct Sweep2DArgs {
   double* ybuf;          // band-boundary traces
   unsigned int* sync;    // progress counters + ticket
   const int* active;
+  double* fout;          // kinetic output [S][nv][ndof] (null: no kinetic store)
+  int nv;
 };
 void launch_sweep2d(const Sweep2DArgs& a, cudaStream_t st);
 
@@ -277,6 +280,18 @@ void rom_setup(rte_ctx* ctx, int which, int* singular_dev, cudaStream_t st);
 void rom_correct(rte_ctx* ctx, const double* ms_delta, double* corr, const int* kind, cudaStream_t st);
 void romig(rte_ctx* ctx, double* rho0, int* status_dev, cudaStream_t st);
 void rom_destroy(RomState* r);
+
+// kinetic operators and training (kinetic.cu)
+void apply_term_kinetic(rte_ctx* ctx, int k, int ncols, const double* u, double* out, cudaStream_t st);
+void collect_snapshots(rte_ctx* ctx, int window, double eps, int max_iters, double* f_iter, double* f_conv,
+                       double* drho_iter, int* conv_h, int* n_iter_h, cudaStream_t st);
+
+// POD / reduced-model projections (pod.cu)
+void pod(long m, int n, const double* F, int rank_max, double* U, double* sigma, cudaStream_t st);
+void build_rom(rte_ctx* ctx, int r, const double* U, const double* b_kin_host, double* u_rho, double* u_iso,
+               double* a_r, double* b_r, cudaStream_t st);
+int snapshot_columns(int S, int window, long kdim, const double* f_iter, const double* f_conv, const int* n_iter,
+                     const int* conv, int kind, int window_limit, double* out, cudaStream_t st);
 
 // transport helpers used by the C-ABI (capi.cu)
 void transport_apply(rte_ctx* ctx, int mode, const double* rho, double* out, const int* active,

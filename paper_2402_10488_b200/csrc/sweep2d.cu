@@ -46,7 +46,8 @@ constexpr int kRC = 40;  // ring slots (columns): >= 31 + 2 * kC
 constexpr int kRP = 162; // ring slot pitch in doubles (5 comps x 32 rows, padded to even)
 
 struct DirConst {
-  double a, b, w, c4b, k1, a2, k2, a12, k6, tb, be, bcx, bcy, pad0, pad1, pad2;
+  double a, b, w, c4b, k1, a2, k2, a12, k6, tb, be, bcx, bcy, pad0;
+  int dir0, dir1, pad1, pad2;
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -197,7 +198,7 @@ __device__ __forceinline__ void convert_chunk(const Sweep2DArgs& a, const Smem& 
   dst[128] = sg;
 }
 
-template <int D>
+template <int D, bool KIN>
 __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const Sweep2DArgs a) {
   extern __shared__ double smraw[];
   constexpr int ndir = kNW * D;
@@ -251,6 +252,8 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
       d.be = kSqrt3 * sl.b;
       d.bcx = (a.mode & SRC_BC) ? sl.bcx : 0.0;
       d.bcy = (a.mode & SRC_BC) ? sl.bcy : 0.0;
+      d.dir0 = sl.dir0;
+      d.dir1 = sl.dir1;
       sm.tab[i] = d;
     }
     const double2* ybelow =
@@ -327,6 +330,22 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
           acc1 = fma(wv, f[1], acc1);
           acc2 = fma(wv, f[2], acc2);
           acc3 = fma(wv, f[3], acc3);
+          if (KIN && ok) {
+            // kinetic store: f of every original direction of this slot
+            const int ix = qx ? nx - 1 - x : x;
+            const long pc = (long)(qy ? ny - 1 - yr : yr) * nx + ix;
+            const double2 v01 = make_double2(f[0], sx * f[1]), v23 = make_double2(sy * f[2], sx * sy * f[3]);
+            if (dc.dir0 >= 0) {
+              double* o = a.fout + ((long)s * a.nv + dc.dir0) * nd + 4 * pc;
+              *reinterpret_cast<double2*>(o) = v01;
+              *reinterpret_cast<double2*>(o + 2) = v23;
+            }
+            if (dc.dir1 >= 0) {
+              double* o = a.fout + ((long)s * a.nv + dc.dir1) * nd + 4 * pc;
+              *reinterpret_cast<double2*>(o) = v01;
+              *reinterpret_cast<double2*>(o + 2) = v23;
+            }
+          }
         }
         if (lane == 31 && ok && band + 1 < nbands) {
 #pragma unroll
@@ -377,20 +396,20 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
 }
 
 template <int D>
-size_t smem_bytes() {
+size_t smem_bytes() {  // NOLINT
   return sizeof(double) * ((size_t)kC * kNW * 4 * 32 + (size_t)kRC * kRP + (size_t)kC * 32 * 10 +
                            (size_t)2 * kC * kNW * D * 2) +
          sizeof(DirConst) * kNW * D;
 }
 
-template <int D>
+template <int D, bool KIN>
 void launch_d(const Sweep2DArgs& a, cudaStream_t st) {
   const size_t smem = smem_bytes<D>();
   static int max_ctas = -1;
   if (max_ctas < 0) {
-    RTE_CUDA(cudaFuncSetAttribute(sweep2d_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RTE_CUDA(cudaFuncSetAttribute(sweep2d_kernel<D, KIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0, dev = 0, sms = 0;
-    RTE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep2d_kernel<D>, kNW * 32, smem));
+    RTE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep2d_kernel<D, KIN>, kNW * 32, smem));
     RTE_CUDA(cudaGetDevice(&dev));
     RTE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     max_ctas = std::max(1, per_sm) * sms;
@@ -398,7 +417,7 @@ void launch_d(const Sweep2DArgs& a, cudaStream_t st) {
   const int nbands = (a.ny + 31) / 32;
   const long total = (long)nbands * a.S * 4 * a.groups;
   const int grid = (int)std::min<long>(total, max_ctas);
-  sweep2d_kernel<D><<<grid, kNW * 32, smem, st>>>(a);
+  sweep2d_kernel<D, KIN><<<grid, kNW * 32, smem, st>>>(a);
   RTE_CUDA(cudaGetLastError());
 }
 
@@ -439,11 +458,20 @@ __global__ void reduce_partials_kernel(int S, long nd, int nparts, const double*
 
 void launch_sweep2d(const Sweep2DArgs& a, cudaStream_t st) {
   const int dpc = a.nq_pad / a.groups / kNW;  // directions per lane
+  if (a.fout) {
+    switch (dpc) {
+      case 1: return launch_d<1, true>(a, st);
+      case 2: return launch_d<2, true>(a, st);
+      case 4: return launch_d<4, true>(a, st);
+      case 8: return launch_d<8, true>(a, st);
+      default: throw Error(RTE_ERR_UNSUPPORTED, "sweep2d: unsupported direction grouping");
+    }
+  }
   switch (dpc) {
-    case 1: return launch_d<1>(a, st);
-    case 2: return launch_d<2>(a, st);
-    case 4: return launch_d<4>(a, st);
-    case 8: return launch_d<8>(a, st);
+    case 1: return launch_d<1, false>(a, st);
+    case 2: return launch_d<2, false>(a, st);
+    case 4: return launch_d<4, false>(a, st);
+    case 8: return launch_d<8, false>(a, st);
     default: throw Error(RTE_ERR_UNSUPPORTED, "sweep2d: unsupported direction grouping");
   }
 }

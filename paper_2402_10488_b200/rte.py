@@ -520,3 +520,100 @@ def sisa_solve(batch: TransportBatch, method: str, config: SolveConfig):
                                "supplied" if (config.initial_guess is not None or method == "ROMIG") else "zero",
                                lg, int(r.switch_iter), bool(r.singular)))
     return rho, out
+
+
+# ---------------------------------------------------------------------------
+# Offline stage on the device: snapshots (snapshots.cpp:118-194), POD
+# (pod.cpp), Galerkin projections (reduced_model.cpp:106-199).
+
+@dataclass
+class Snapshots:
+    window: int
+    f_iter: object        # torch [S, window, kdim]
+    f_conv: object        # torch [S, kdim]
+    drho: object          # torch [S, window, n_dof]
+    converged: np.ndarray
+    n_iter: np.ndarray
+
+    @property
+    def w_mu(self):
+        return np.minimum(self.n_iter, self.window)
+
+
+def collect_snapshots(batch: TransportBatch, window: int = 3, eps_train: float = 1e-11,
+                      max_iters: int = 2000) -> Snapshots:
+    kdim = batch.kinetic_dim()
+    f_iter = batch._out(batch.S, window, kdim)
+    f_iter.zero_()
+    f_conv = batch._out(batch.S, kdim)
+    drho = batch._out(batch.S, window, batch.nd)
+    drho.zero_()
+    conv = (ctypes.c_int * batch.S)()
+    nit = (ctypes.c_int * batch.S)()
+    _torch().cuda.synchronize(batch.device)
+    batch._call(capi.load().rte_collect_snapshots, int(window), float(eps_train), int(max_iters),
+                f_iter.data_ptr(), f_conv.data_ptr(), drho.data_ptr(), conv, nit)
+    return Snapshots(window, f_iter, f_conv, drho, np.array(conv[:], dtype=np.int32),
+                     np.array(nit[:], dtype=np.int32))
+
+
+def snapshot_matrix(batch: TransportBatch, snaps: Snapshots, kind: str, window_limit: int = 0):
+    """'primary' or 'correction' columns as a torch tensor [n_cols, kdim]
+    (i.e. column-major kdim x n_cols)."""
+    L = capi.load()
+    k = 0 if kind == "primary" else 1
+    conv = (ctypes.c_int * batch.S)(*snaps.converged.tolist())
+    nit = (ctypes.c_int * batch.S)(*snaps.n_iter.tolist())
+    n = ctypes.c_int()
+    batch._call(L.rte_snapshot_columns, snaps.window, snaps.f_iter.data_ptr(), snaps.f_conv.data_ptr(), nit, conv,
+                k, int(window_limit), None, ctypes.byref(n))
+    out = batch._out(n.value, batch.kinetic_dim())
+    batch._call(L.rte_snapshot_columns, snaps.window, snaps.f_iter.data_ptr(), snaps.f_conv.data_ptr(), nit, conv,
+                k, int(window_limit), out.data_ptr(), ctypes.byref(n))
+    return out
+
+
+def truncation_rank(singular_values, eps_pod) -> int:
+    s = np.ascontiguousarray(singular_values, dtype=np.float64)
+    r = capi.load().rte_truncation_rank(capi.dptr(s), int(s.size), float(eps_pod))
+    if r < 0:
+        raise ValueError("pod: snapshot matrix is zero")
+    return r
+
+
+def pod(F, rank_max: int, device: int = 0):
+    """POD of F [n_cols, m] (column-major m x n_cols) on the device: returns
+    (U [rank_max, m] torch, all singular values numpy)."""
+    torch = _torch()
+    n, m = F.shape
+    U = torch.empty((rank_max, m), dtype=torch.float64, device=F.device)
+    sig = np.zeros(n)
+    torch.cuda.synchronize(device)
+    capi.check(capi.load().rte_pod(device, m, n, ctypes.c_void_p(F.data_ptr()), int(rank_max),
+                                   ctypes.c_void_p(U.data_ptr()), capi.dptr(sig), None))
+    return U, sig
+
+
+def build_reduced_model(batch: TransportBatch, U, all_singular_values, eps_pod: float, eps_train: float,
+                        kind: str) -> ReducedModel:
+    """build_reduced_model (reduced_model.cpp:106-199) with the projections on
+    the device; U: torch [r, kdim] (column-major basis)."""
+    r = U.shape[0]
+    nd, K = batch.nd, batch.k_terms
+    u_rho = np.zeros(r * nd)
+    u_iso = np.zeros(r * nd)
+    a_r = np.zeros(K * r * r)
+    b_r = np.zeros(r)
+    _torch().cuda.synchronize(batch.device)
+    batch._call(capi.load().rte_build_rom, int(r), ctypes.c_void_p(U.data_ptr()), capi.dptr(u_rho),
+                capi.dptr(u_iso), capi.dptr(a_r), capi.dptr(b_r))
+    sv = np.asarray(all_singular_values, dtype=np.float64)
+    total = float(np.sum(sv))
+    m = ReducedModel(int(batch.mesh.geometry), batch.quad.n(), nd, r, K, kind, eps_pod, eps_train)
+    m.u_rho = u_rho.reshape(r, nd).T.copy()
+    m.u_iso = u_iso.reshape(r, nd).T.copy()
+    m.a_r = [a_r[k * r * r:(k + 1) * r * r].reshape(r, r).T.copy() for k in range(K)]
+    m.b_r = b_r
+    m.singular_values = sv[:r].copy()
+    m.discarded_fraction = float(np.sum(sv[r:])) / total if total > 0 else 0.0
+    return m
