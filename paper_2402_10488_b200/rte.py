@@ -349,6 +349,17 @@ class TransportBatch:
         self._call(capi.load().rte_density_of, f.data_ptr(), out.data_ptr(), self._stream())
         return out
 
+    def apply_term_kinetic(self, k, u):
+        """A_k u (transport_system.cpp:560-596) for kinetic columns u [n, kdim]
+        (term operators are parameter independent)."""
+        u = self._dev(u)
+        if u.dim() == 1:
+            u = u.reshape(1, -1)
+        out = self._out(u.shape[0], self.kinetic_dim())
+        self._call(capi.load().rte_apply_term_kinetic, int(k), int(u.shape[0]), u.data_ptr(), out.data_ptr(),
+                   self._stream())
+        return out
+
     def apply_Ms(self, x):
         x = self._dev(x, (self.S, self.nd))
         out = self._out(self.S, self.nd)
