@@ -90,6 +90,8 @@ def test_pin_cell_offline_and_romsad():
     U, sig = rte.pod(F, r)
     eps_pod = float(np.sum(sig[r:]) / np.sum(sig))
     dm = rte.build_reduced_model(tb, U, sig, eps_pod, 1e-8, "c")
+    om_ = ro.ReducedModel(dm.geometry, dm.n_v, dm.n_dof, dm.rank, dm.k_affine, dm.kind, dm.eps_pod, dm.eps_train,
+                          dm.u_rho, dm.u_iso, dm.a_r, dm.singular_values, dm.discarded_fraction, dm.b_r)
     b = rte.TransportBatch(pin_cell(rte)(nx), pm, quad_p, test)
     rte.load_rom(b, 1, dm)
     eps_r = ro.romsad_tolerance(1e-8, eps_pod)
@@ -97,6 +99,6 @@ def test_pin_cell_offline_and_romsad():
     rho = rho.cpu().numpy()
     for s, mu in enumerate(test):
         o = ro.TransportSystem(make(nx), om, ro.build_dg_space(om), quad_o, mu)
-        o_rho, o_rep = ro.sisa_solve(o, ro.RomsadStrategy(dm, ro.build_dsa(o), 5, eps_r), ro.SolveConfig(eps_sisa=1e-8))
+        o_rho, o_rep = ro.sisa_solve(o, ro.RomsadStrategy(om_, ro.build_dsa(o), 5, eps_r), ro.SolveConfig(eps_sisa=1e-8))
         assert reps[s].iterations == o_rep.iterations and reps[s].correction_log == o_rep.correction_log
         assert rel_l2(rho[s], o_rho) < 1e-8
