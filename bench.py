@@ -101,14 +101,27 @@ def barrier(world):
         dist.barrier()
 
 
-def max_over_ranks(v, world, device):
+def max_over_ranks(v, world, device=None):
+    """Max of a per-rank scalar (device-timed milliseconds) over all ranks."""
     if world == 1:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda:%d" % device)
+    dev = "cuda:%d" % device if device is not None else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def shard_seed(base_seed, rank):
+    """Weak scaling: every rank owns an independent seeded 16-sample batch
+    (samples are independent solves; no data-path collective)."""
+    return base_seed + rank
+
+
+def aggregate_value(updates_per_rank_step, steps, world, ms_max):
+    """Whole-job throughput: units of all ranks / max-over-ranks time."""
+    return updates_per_rank_step * steps * world / (ms_max * 1e-3)
 
 
 # ---------------------------------------------------------------------------
@@ -122,7 +135,7 @@ def run_b200(args, rank, world, device):
     nx, S = args.nx, args.samples
     mesh = rte.Mesh.rect_uniform(0, 1, nx, 0, 1, nx)
     quad = rte.chebyshev_legendre(PHI, VZ)
-    st, ss = configs.c5_coefficients(nx, S, seed=configs.SEEDS["c5"] + rank)
+    st, ss = configs.c5_coefficients(nx, S, seed=shard_seed(configs.SEEDS["c5"], rank))
     px, py = mesh.cell_points()
     g = mesh.project(np.ones(px.size))
     batch = rte.TransportBatch.from_cells(mesh, quad, st, ss, g, device=device)
@@ -162,7 +175,7 @@ def run_b200(args, rank, world, device):
     capi.check(L.rte_profile_read(batch._h, ms_k, n_k), batch._h)
     L.rte_profile_enable(batch._h, 0)
     ms_max = max_over_ranks(ms_total, world, device)
-    value = upd_step * args.steps * world / (ms_max * 1e-3)
+    value = aggregate_value(upd_step, args.steps, world, ms_max)
 
     # end-to-end through the C-ABI with host buffers: create (H2D of the
     # problem), K iterations, D2H of the result.
