@@ -735,15 +735,16 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
           RTE_CUDA(cudaGetLastError());
         }
         if (need_dsa) {
-          ProfScope ps(ctx, RTE_PROF_DSA, st);
+          ProfScope ps(ctx, RTE_PROF_DSA, st, ctx->geom == RTE_XY2D ? 0 : 1);
           dsa_apply(ctx, delta.p, corr.p, sst.kind, 1, st);
+          if (ctx->geom == RTE_XY2D && ctx->prof) ctx->prof_n[RTE_PROF_DSA] += dsa2d_take_launches(ctx);
         }
         if (need_rom) {
           ProfScope ps(ctx, RTE_PROF_ROM, st);
           rom_correct(ctx, delta.p, corr.p, sst.kind, st);
         }
         {
-          ProfScope ps(ctx, RTE_PROF_OTHER, st, 2);
+          ProfScope ps(ctx, RTE_PROF_OTHER, st, 1);
           si_finalize_kernel<<<dim3(fin_bx, S), 256, 0, st>>>(S, nd, sst.kind, rstar.p, corr.p, rho);
           RTE_CUDA(cudaGetLastError());
         }

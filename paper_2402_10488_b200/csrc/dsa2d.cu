@@ -61,6 +61,7 @@ struct Dsa2D {
   int nu = 2;
   int last_iters = 0;
   int nblk = 64;
+  long nlaunch = 0;           // kernel launches issued (for launch accounting)
   const double* sgt = nullptr;
   const double* sgs = nullptr;
 };
@@ -1061,8 +1062,10 @@ static void smooth(Dsa2D* d, int l, const double* b, double* x, const int* act, 
   const int S = d->S;
   const long half = (lv.nc + 1) / 2;
   const int c0 = reverse ? 1 : 0;
+  ++d->nlaunch;
   k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, c0, lv.Dinvf.p, d->sgt, d->sgs, l, x, b,
                                                       act, zero_init ? 1 : 0);
+  ++d->nlaunch;
   k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, 1 - c0, lv.Dinvf.p, d->sgt, d->sgs, l, x,
                                                       b, act, 0);
 }
@@ -1073,6 +1076,7 @@ static void vcycle(Dsa2D* d, int l, const double* b, double* x, const int* act, 
   const bool last = (size_t)l + 1 == d->L.size();
   if (last) {
     if (d->ncoarse > 0) {
+      ++d->nlaunch;
       k_dense_apply<<<S, 256, 0, st>>>(d->ncoarse, d->coarse_inv.p, b, x, act);
       RTE_CUDA(cudaGetLastError());
     } else {
@@ -1082,11 +1086,14 @@ static void vcycle(Dsa2D* d, int l, const double* b, double* x, const int* act, 
     return;
   }
   for (int k = 0; k < d->nu; ++k) smooth(d, l, b, x, act, k == 0, false, st);
+  ++d->nlaunch;
   k_apply<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, lv.Df.p, d->sgt, d->sgs, l, x, b,
                                                           lv.r.p, 1, act);
   Level& lc = d->L[l + 1];
+  ++d->nlaunch;
   k_restrict<<<nblocks((long)S * lc.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, d->P.p, lv.r.p, lc.b.p, act);
   vcycle(d, l + 1, lc.b.p, lc.x.p, act, st);
+  ++d->nlaunch;
   k_prolong_add<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, d->P.p, lc.x.p, x, act);
   for (int k = 0; k < d->nu; ++k) smooth(d, l, b, x, act, false, true, st);
   RTE_CUDA(cudaGetLastError());
@@ -1102,6 +1109,7 @@ static void dots(Dsa2D* d, long n, std::initializer_list<std::pair<const double*
     ++q;
   }
   a.nq = q;
+  ++d->nlaunch;
   k_dots<<<dim3(d->nblk, d->S), 256, 0, st>>>(d->S, n, a, d->part.p, d->act.p);
   RTE_CUDA(cudaGetLastError());
 }
@@ -1114,6 +1122,7 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   const long n = l0.nc * NB;
   const dim3 vgrid(d->nblk, S);
   // b -> l0.b ; x = 0 ; r = b ; rh = r
+  ++d->nlaunch;
   k_pack_rhs<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, rhs, ctx->ms.p, apply_ms, l0.b.p, kind);
   RTE_CUDA(cudaMemsetAsync(d->x.p, 0, sizeof(double) * S * n, st));
   RTE_CUDA(cudaMemsetAsync(d->p.p, 0, sizeof(double) * S * n, st));
@@ -1126,9 +1135,11 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     a.a[0] = l0.b.p;
     a.b[0] = l0.b.p;
     a.nq = 1;
+    ++d->nlaunch;
     k_dots<<<vgrid, 256, 0, st>>>(S, n, a, d->part.p, nullptr);
   }
   std::vector<int> mask_h;
+  ++d->nlaunch;
   k_bicg_init<<<(S + 127) / 128, 128, 0, st>>>(S, d->nblk, d->part.p, d->scal.p, d->act.p, nullptr);
   RTE_CUDA(cudaGetLastError());
   if (kind) {
@@ -1140,20 +1151,26 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   int it = 0;
   for (; it < d->maxit; ++it) {
     dots(d, n, {{d->rh.p, d->r.p}}, st);
+    ++d->nlaunch;
     k_bicg_p<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->r.p, d->p.p, d->v.p, d->act.p);
     vcycle(d, 0, d->p.p, d->ph.p, d->act.p, st);
+    ++d->nlaunch;
     k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, nullptr, d->sgt, d->sgs, 0, d->ph.p,
                                                             nullptr, d->v.p, 0, d->act.p);
     dots(d, n, {{d->rh.p, d->v.p}}, st);
+    ++d->nlaunch;
     k_bicg_s<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->r.p, d->v.p, d->s.p, d->act.p);
     vcycle(d, 0, d->s.p, d->sh.p, d->act.p, st);
+    ++d->nlaunch;
     k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, nullptr, d->sgt, d->sgs, 0, d->sh.p,
                                                             nullptr, d->t.p, 0, d->act.p);
     dots(d, n, {{d->t.p, d->s.p}, {d->t.p, d->t.p}}, st);
+    ++d->nlaunch;
     k_bicg_x<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->x.p, d->ph.p, d->sh.p, d->r.p, d->s.p,
                                     d->t.p, d->act.p);
     dots(d, n, {{d->r.p, d->r.p}}, st);
     RTE_CUDA(cudaMemsetAsync(d->nact.p, 0, sizeof(int), st));
+    ++d->nlaunch;
     k_bicg_check<<<(S + 127) / 128, 128, 0, st>>>(S, d->nblk, d->part.p, d->scal.p, d->act.p, tol2, d->maxit,
                                                   d->nact.p);
     RTE_CUDA(cudaGetLastError());
@@ -1168,12 +1185,21 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   }
   cudaFreeHost(nact_h);
   d->last_iters = it;
+  ++d->nlaunch;
   k_unpack<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, d->x.p, out, kind);
   RTE_CUDA(cudaGetLastError());
   (void)mask_h;
 }
 
 void dsa2d_destroy(void* p) { delete static_cast<Dsa2D*>(p); }
+
+long dsa2d_take_launches(rte_ctx* ctx) {
+  if (!ctx->dsa || !ctx->dsa->impl2d) return 0;
+  auto* d = static_cast<Dsa2D*>(ctx->dsa->impl2d);
+  const long n = d->nlaunch;
+  d->nlaunch = 0;
+  return n;
+}
 
 int dsa2d_last_iters(const rte_ctx* ctx) {
   if (!ctx->dsa || !ctx->dsa->impl2d) return 0;
