@@ -38,7 +38,7 @@ struct Level {
   long nc;
   DBuf<double> D, Dinv;       // [S][nc][144] fp64 (setup only)
   DBuf<float> Df, Dinvf;      // [S][nc][144] fp32 copies used by the V-cycle (preconditioner)
-  DBuf<double> x, b, r;       // [S][nc][12]
+  DBuf<float> x, b, r;        // [S][12][nc] V-cycle vectors (fp32 storage, fp64 arithmetic)
   DBuf<double> nbr;           // [4][144] W, E, S, N face-coupling blocks (constant)
   std::vector<double> nbr_h;
 };
@@ -51,7 +51,7 @@ struct Dsa2D {
   DBuf<double> P;             // [4][16] prolongation blocks E2 per sub-cell position (row-major fine x coarse)
   DBuf<double> Dint;          // [levels][144] constant internal-coupling part of the coarse diagonal
   // BiCGStab
-  DBuf<double> r, rh, p, v, s, t, x, ph, sh;
+  DBuf<double> r, rh, p, v, s, t, x, ph, sh, rhs;
   DBuf<double> scal;          // per sample scalars [S][16]
   DBuf<double> part;          // dot partials [S][kDotBlocks][4]
   DBuf<int> act;              // per-sample active flag
@@ -163,12 +163,13 @@ __device__ __forceinline__ void lift_mv(const double* M, const double* v, double
 
 // Vectors are component-major per sample (SoA): x[s][r][cell], so a warp's
 // loads of one component of consecutive cells coalesce.
-__device__ __forceinline__ void face_mv(int lev, int dir, const double* __restrict__ xs, long nc, long cn, double* y) {
+template <typename T>
+__device__ __forceinline__ void face_mv(int lev, int dir, const T* __restrict__ xs, long nc, long cn, double* y) {
   const int axis = dir >> 1;
   const int j = axis == 0 ? 4 : 8, o = axis == 0 ? 8 : 4;
   double v[NB];
 #pragma unroll
-  for (int r = 0; r < NB; ++r) v[r] = xs[r * nc + cn];
+  for (int r = 0; r < NB; ++r) v[r] = (double)xs[r * nc + cn];
   lift_mv(c_face[lev][dir][0], v, y, axis);
   lift_mv(c_face[lev][dir][1], v + j, y, axis);
   lift_mv(c_face[lev][dir][2], v, y + j, axis);
@@ -385,6 +386,14 @@ __device__ __forceinline__ void blk_mv_accf(const float* __restrict__ M, long st
   }
 }
 
+template <typename A, typename B>
+__global__ void k_cvt(long n, const A* __restrict__ a, B* __restrict__ b, const int* __restrict__ act, long per) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  if (act && !act[t / per]) return;
+  b[t] = (B)a[t];
+}
+
 // [S][nc][144] fp64 -> [S][144][nc] fp32
 __global__ void k_to_f32(int S, long nc, const double* __restrict__ a, float* __restrict__ b) {
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -405,7 +414,8 @@ __device__ __forceinline__ void blk_mv_acc(const double* __restrict__ M, const d
 }
 
 // off-diagonal (face) contributions sum_nbr C_dir x_nbr
-__device__ __forceinline__ void face_terms(int lev, const double* __restrict__ xs, int nx, int ny, int ix, int iy,
+template <typename T>
+__device__ __forceinline__ void face_terms(int lev, const T* __restrict__ xs, int nx, int ny, int ix, int iy,
                                            long c, double* y) {
   const long nc = (long)nx * ny;
   if (ix > 0) face_mv(lev, 0, xs, nc, c - 1, y);
@@ -415,9 +425,10 @@ __device__ __forceinline__ void face_terms(int lev, const double* __restrict__ x
 }
 
 // y = K x (mode 0) or y = b - K x (mode 1)
+template <typename T>
 __global__ void k_apply(int S, int nx, int ny, const float* __restrict__ D, const double* __restrict__ sgt,
                         const double* __restrict__ sgs, int lev,
-                        const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ y, int mode,
+                        const T* __restrict__ x, const T* __restrict__ b, T* __restrict__ y, int mode,
                         const int* __restrict__ act) {
   const long nc = (long)nx * ny;
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -425,33 +436,34 @@ __global__ void k_apply(int S, int nx, int ny, const float* __restrict__ D, cons
   const long s = t / nc, c = t - s * nc;
   if (act && !act[s]) return;
   const int ix = (int)(c % nx), iy = (int)(c / nx);
-  const double* xs = x + s * nc * NB;
+  const T* xs = x + s * nc * NB;
   double acc[NB], xl[NB];
 #pragma unroll
   for (int r = 0; r < NB; ++r) {
     acc[r] = 0.0;
-    xl[r] = xs[r * nc + c];
+    xl[r] = (double)xs[r * nc + c];
   }
   if (D)
     blk_mv_accf(D + s * nc * NB2 + c, nc, xl, acc);
   else
     fine_block_mv(sgt[t], sgt[t] - sgs[t], xl, acc);
   face_terms(lev, xs, nx, ny, ix, iy, c, acc);
-  double* yo = y + s * nc * NB + c;
+  T* yo = y + s * nc * NB + c;
   if (mode == 1) {
-    const double* bi = b + s * nc * NB + c;
+    const T* bi = b + s * nc * NB + c;
 #pragma unroll
-    for (int r = 0; r < NB; ++r) yo[r * nc] = bi[r * nc] - acc[r];
+    for (int r = 0; r < NB; ++r) yo[r * nc] = (T)((double)bi[r * nc] - acc[r]);
   } else {
 #pragma unroll
-    for (int r = 0; r < NB; ++r) yo[r * nc] = acc[r];
+    for (int r = 0; r < NB; ++r) yo[r * nc] = (T)acc[r];
   }
 }
 
 // red-black block Gauss-Seidel half sweep: x_c = Dinv_c (b_c - sum_nbr C x_nbr)
+template <typename T>
 __global__ void k_gs(int S, int nx, int ny, int color, const float* __restrict__ Dinv, const double* __restrict__ sgt,
                      const double* __restrict__ sgs, int lev,
-                     double* __restrict__ x, const double* __restrict__ b, const int* __restrict__ act, int zero_init) {
+                     T* __restrict__ x, const T* __restrict__ b, const int* __restrict__ act, int zero_init) {
   const long nc = (long)nx * ny;
   const long half = (nc + 1) / 2;
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -479,15 +491,15 @@ __global__ void k_gs(int S, int nx, int ny, int color, const float* __restrict__
     const int ix = first + 2 * (int)rem;
     if (ix >= nx) return;
     c = (long)iy * nx + ix;
-    const double* xs = x + s * nc * NB;
+    const T* xs = x + s * nc * NB;
     double acc[NB];
-    const double* bi = b + s * nc * NB + c;
+    const T* bi = b + s * nc * NB + c;
 #pragma unroll
     for (int r = 0; r < NB; ++r) acc[r] = 0.0;
     if (!zero_init) face_terms(lev, xs, nx, ny, ix, iy, c, acc);
     double rr[NB];
 #pragma unroll
-    for (int r = 0; r < NB; ++r) rr[r] = bi[r * nc] - acc[r];
+    for (int r = 0; r < NB; ++r) rr[r] = (double)bi[r * nc] - acc[r];
     double out[NB];
     if (Dinv) {
 #pragma unroll
@@ -497,15 +509,16 @@ __global__ void k_gs(int S, int nx, int ny, int color, const float* __restrict__
       const long fi = s * nc + c;
       fine_block_solve(sgt[fi], sgt[fi] - sgs[fi], rr, out);
     }
-    double* xo = x + s * nc * NB + c;
+    T* xo = x + s * nc * NB + c;
 #pragma unroll
-    for (int r = 0; r < NB; ++r) xo[r * nc] = out[r];
+    for (int r = 0; r < NB; ++r) xo[r * nc] = (T)out[r];
   }
 }
 
 // restriction b_C = sum_pos P_pos^T r_c
-__global__ void k_restrict(int S, int fnx, int fny, const double* __restrict__ P, const double* __restrict__ rf,
-                           double* __restrict__ bc, const int* __restrict__ act) {
+template <typename T>
+__global__ void k_restrict(int S, int fnx, int fny, const double* __restrict__ P, const T* __restrict__ rf,
+                           T* __restrict__ bc, const int* __restrict__ act) {
   const int cnx = fnx / 2, cny = fny / 2;
   const long ncc = (long)cnx * cny;
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -520,23 +533,24 @@ __global__ void k_restrict(int S, int fnx, int fny, const double* __restrict__ P
     for (int px = 0; px < 2; ++px) {
       const long c = (long)(2 * cy + py) * fnx + 2 * cx + px;
       const long nf = (long)fnx * fny;
-      const double* r = rf + s * nf * NB + c;
+      const T* r = rf + s * nf * NB + c;
       const double* E = P + (px + 2 * py) * 16;
       for (int f = 0; f < 3; ++f)
         for (int k = 0; k < 4; ++k) {
           double acc = out[4 * f + k];
-          for (int l = 0; l < 4; ++l) acc = fma(E[4 * l + k], r[(4 * f + l) * nf], acc);
+          for (int l = 0; l < 4; ++l) acc = fma(E[4 * l + k], (double)r[(4 * f + l) * nf], acc);
           out[4 * f + k] = acc;
         }
     }
-  double* o = bc + s * ncc * NB + C;
+  T* o = bc + s * ncc * NB + C;
 #pragma unroll
-  for (int r = 0; r < NB; ++r) o[r * ncc] = out[r];
+  for (int r = 0; r < NB; ++r) o[r * ncc] = (T)out[r];
 }
 
 // x_c += P_pos x_C
-__global__ void k_prolong_add(int S, int fnx, int fny, const double* __restrict__ P, const double* __restrict__ xc,
-                              double* __restrict__ xf, const int* __restrict__ act) {
+template <typename T>
+__global__ void k_prolong_add(int S, int fnx, int fny, const double* __restrict__ P, const T* __restrict__ xc,
+                              T* __restrict__ xf, const int* __restrict__ act) {
   const long nf = (long)fnx * fny;
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long)S * nf) return;
@@ -547,13 +561,13 @@ __global__ void k_prolong_add(int S, int fnx, int fny, const double* __restrict_
   const long C = (long)(iy / 2) * cnx + ix / 2;
   const double* E = P + ((ix & 1) + 2 * (iy & 1)) * 16;
   const long ncc = (long)(fnx / 2) * (fny / 2);
-  const double* xcs = xc + s * ncc * NB + C;
-  double* o = xf + s * nf * NB + c;
+  const T* xcs = xc + s * ncc * NB + C;
+  T* o = xf + s * nf * NB + c;
   for (int f = 0; f < 3; ++f)
     for (int l = 0; l < 4; ++l) {
-      double acc = o[(4 * f + l) * nf];
-      for (int k = 0; k < 4; ++k) acc = fma(E[4 * l + k], xcs[(4 * f + k) * ncc], acc);
-      o[(4 * f + l) * nf] = acc;
+      double acc = (double)o[(4 * f + l) * nf];
+      for (int k = 0; k < 4; ++k) acc = fma(E[4 * l + k], (double)xcs[(4 * f + k) * ncc], acc);
+      o[(4 * f + l) * nf] = (T)acc;
     }
 }
 
@@ -650,18 +664,19 @@ __global__ void k_dense_inverse(int n, double* __restrict__ A, double* __restric
   }
 }
 
-__global__ void k_dense_apply(int n, const double* __restrict__ Ainv, const double* __restrict__ b,
-                              double* __restrict__ x, const int* __restrict__ act) {
+template <typename T>
+__global__ void k_dense_apply(int n, const double* __restrict__ Ainv, const T* __restrict__ b,
+                              T* __restrict__ x, const int* __restrict__ act) {
   const int s = blockIdx.x;
   if (act && !act[s]) return;
   const double* a = Ainv + (long)s * n * n;
-  const double* bs = b + (long)s * n;
+  const T* bs = b + (long)s * n;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int r = wid; r < n; r += nw) {
     double acc = 0.0;
-    for (int c = lane; c < n; c += 32) acc = fma(a[(long)r * n + c], bs[c], acc);
+    for (int c = lane; c < n; c += 32) acc = fma(a[(long)r * n + c], (double)bs[c], acc);
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) x[(long)s * n + r] = acc;
+    if (lane == 0) x[(long)s * n + r] = (T)acc;
   }
 }
 
@@ -826,7 +841,7 @@ inline int nblocks(long n, int bs = 256) { return (int)((n + bs - 1) / bs); }
 
 // ----------------------------------------------------------------------------
 
-static void vcycle(Dsa2D* d, int l, const double* b, double* x, const int* act, cudaStream_t st);
+static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cudaStream_t st);
 
 void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   auto* d = static_cast<Dsa2D*>(ctx->dsa->impl2d);
@@ -1047,7 +1062,7 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   }
   // Krylov workspace
   const size_t nv = (size_t)S * l0.nc * NB;
-  for (DBuf<double>* b : {&d->r, &d->rh, &d->p, &d->v, &d->s, &d->t, &d->x, &d->ph, &d->sh}) b->alloc(nv);
+  for (DBuf<double>* b : {&d->r, &d->rh, &d->p, &d->v, &d->s, &d->t, &d->x, &d->ph, &d->sh, &d->rhs}) b->alloc(nv);
   d->scal.alloc((size_t)S * 16);
   d->nblk = (int)std::min<long>(512, std::max<long>(16, (long)l0.nc * NB / 4096));
   d->part.alloc((size_t)S * d->nblk * 4);
@@ -1056,7 +1071,7 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   RTE_CUDA(cudaStreamSynchronize(st));
 }
 
-static void smooth(Dsa2D* d, int l, const double* b, double* x, const int* act, bool zero_init, bool reverse,
+static void smooth(Dsa2D* d, int l, const float* b, float* x, const int* act, bool zero_init, bool reverse,
                    cudaStream_t st) {
   Level& lv = d->L[l];
   const int S = d->S;
@@ -1070,7 +1085,7 @@ static void smooth(Dsa2D* d, int l, const double* b, double* x, const int* act, 
                                                       b, act, 0);
 }
 
-static void vcycle(Dsa2D* d, int l, const double* b, double* x, const int* act, cudaStream_t st) {
+static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cudaStream_t st) {
   Level& lv = d->L[l];
   const int S = d->S;
   const bool last = (size_t)l + 1 == d->L.size();
@@ -1099,6 +1114,18 @@ static void vcycle(Dsa2D* d, int l, const double* b, double* x, const int* act, 
   RTE_CUDA(cudaGetLastError());
 }
 
+// one V-cycle as the preconditioner: fp64 in -> fp32 V-cycle -> fp64 out
+static void precond(Dsa2D* d, const double* in, double* out, cudaStream_t st) {
+  Level& l0 = d->L[0];
+  const long n = (long)d->S * l0.nc * NB;
+  ++d->nlaunch;
+  k_cvt<double, float><<<nblocks(n), 256, 0, st>>>(n, in, l0.b.p, d->act.p, l0.nc * NB);
+  vcycle(d, 0, l0.b.p, l0.x.p, d->act.p, st);
+  ++d->nlaunch;
+  k_cvt<float, double><<<nblocks(n), 256, 0, st>>>(n, l0.x.p, out, d->act.p, l0.nc * NB);
+  RTE_CUDA(cudaGetLastError());
+}
+
 static void dots(Dsa2D* d, long n, std::initializer_list<std::pair<const double*, const double*>> pairs,
                  cudaStream_t st) {
   DotArgs a{};
@@ -1123,17 +1150,17 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   const dim3 vgrid(d->nblk, S);
   // b -> l0.b ; x = 0 ; r = b ; rh = r
   ++d->nlaunch;
-  k_pack_rhs<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, rhs, ctx->ms.p, apply_ms, l0.b.p, kind);
+  k_pack_rhs<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, rhs, ctx->ms.p, apply_ms, d->rhs.p, kind);
   RTE_CUDA(cudaMemsetAsync(d->x.p, 0, sizeof(double) * S * n, st));
   RTE_CUDA(cudaMemsetAsync(d->p.p, 0, sizeof(double) * S * n, st));
   RTE_CUDA(cudaMemsetAsync(d->v.p, 0, sizeof(double) * S * n, st));
-  RTE_CUDA(cudaMemcpyAsync(d->r.p, l0.b.p, sizeof(double) * S * n, cudaMemcpyDeviceToDevice, st));
-  RTE_CUDA(cudaMemcpyAsync(d->rh.p, l0.b.p, sizeof(double) * S * n, cudaMemcpyDeviceToDevice, st));
+  RTE_CUDA(cudaMemcpyAsync(d->r.p, d->rhs.p, sizeof(double) * S * n, cudaMemcpyDeviceToDevice, st));
+  RTE_CUDA(cudaMemcpyAsync(d->rh.p, d->rhs.p, sizeof(double) * S * n, cudaMemcpyDeviceToDevice, st));
   // initial ||b||^2 with every sample counted (mask applied inside init)
   {
     DotArgs a{};
-    a.a[0] = l0.b.p;
-    a.b[0] = l0.b.p;
+    a.a[0] = d->rhs.p;
+    a.b[0] = d->rhs.p;
     a.nq = 1;
     ++d->nlaunch;
     k_dots<<<vgrid, 256, 0, st>>>(S, n, a, d->part.p, nullptr);
@@ -1153,16 +1180,16 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     dots(d, n, {{d->rh.p, d->r.p}}, st);
     ++d->nlaunch;
     k_bicg_p<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->r.p, d->p.p, d->v.p, d->act.p);
-    vcycle(d, 0, d->p.p, d->ph.p, d->act.p, st);
+    precond(d, d->p.p, d->ph.p, st);
     ++d->nlaunch;
-    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, nullptr, d->sgt, d->sgs, 0, d->ph.p,
+    k_apply<double><<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, nullptr, d->sgt, d->sgs, 0, d->ph.p,
                                                             nullptr, d->v.p, 0, d->act.p);
     dots(d, n, {{d->rh.p, d->v.p}}, st);
     ++d->nlaunch;
     k_bicg_s<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->r.p, d->v.p, d->s.p, d->act.p);
-    vcycle(d, 0, d->s.p, d->sh.p, d->act.p, st);
+    precond(d, d->s.p, d->sh.p, st);
     ++d->nlaunch;
-    k_apply<<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, nullptr, d->sgt, d->sgs, 0, d->sh.p,
+    k_apply<double><<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, nullptr, d->sgt, d->sgs, 0, d->sh.p,
                                                             nullptr, d->t.p, 0, d->act.p);
     dots(d, n, {{d->t.p, d->s.p}, {d->t.p, d->t.p}}, st);
     ++d->nlaunch;
