@@ -20,6 +20,7 @@
 // All per-sample inner products use a two-stage fixed-order reduction, so the
 // solve is deterministic.  Samples converge independently (masked).
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "rte_internal.cuh"
@@ -58,7 +59,8 @@ struct Dsa2D {
   DBuf<int> nact;
   double tol = 1e-12;
   int maxit = 1000;
-  int nu = 2;
+  int nu = 2;          // smoothing steps on the finest level
+  int nu_coarse = 2;   // smoothing steps on coarser levels
   int last_iters = 0;
   int nblk = 64;
   long nlaunch = 0;           // kernel launches issued (for launch accounting)
@@ -826,6 +828,8 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   }
   const int S = ctx->S;
   d->S = S;
+  if (const char* e = std::getenv("RTE_DSA_NU")) d->nu = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("RTE_DSA_NU_COARSE")) d->nu_coarse = std::max(1, std::atoi(e));
   // moments (dsa.cpp:167-192, 223-226)
   double m1x = 0, m2x = 0, m3x = 0, m1y = 0, m2y = 0, m3y = 0, m3yx = 0, m3xy = 0;
   for (int j = 0; j < ctx->nv; ++j) {
@@ -1092,7 +1096,8 @@ static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cu
     }
     return;
   }
-  for (int k = 0; k < d->nu; ++k) smooth(d, l, b, x, act, k == 0, false, st);
+  const int nu = l == 0 ? d->nu : d->nu_coarse;
+  for (int k = 0; k < nu; ++k) smooth(d, l, b, x, act, k == 0, false, st);
   ++d->nlaunch;
   k_apply<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, lv.Df.p, d->sgt, d->sgs, l, x, b,
                                                           lv.r.p, 1, act);
@@ -1102,7 +1107,7 @@ static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cu
   vcycle(d, l + 1, lc.b.p, lc.x.p, act, st);
   ++d->nlaunch;
   k_prolong_add<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, d->P.p, lc.x.p, x, act);
-  for (int k = 0; k < d->nu; ++k) smooth(d, l, b, x, act, false, true, st);
+  for (int k = 0; k < nu; ++k) smooth(d, l, b, x, act, false, true, st);
   RTE_CUDA(cudaGetLastError());
 }
 
