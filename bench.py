@@ -38,6 +38,15 @@ BYTES_PER_UPDATE = 40     # sigma_t + 4 source moments (operand-st
 PHI, VZ = 32, 16          # CL(32,16) -> 256 unique (vx, vy) slots
 
 
+def gs_traffic():
+    """DRAM bytes per fine-level k_gs launch from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "dsa_gs_traffic.json")
+    try:
+        return json.load(open(p)).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -170,8 +179,9 @@ def run_b200(args, rank, world, device):
     barrier(world)
     ck = clocks.stop()
     ms_total = e0.elapsed_time(e1)
-    ms_k = (ctypes.c_double * 5)()
-    n_k = (ctypes.c_long * 5)()
+    NK = len(capi.PROF_KINDS)
+    ms_k = (ctypes.c_double * NK)()
+    n_k = (ctypes.c_long * NK)()
     capi.check(L.rte_profile_read(batch._h, ms_k, n_k), batch._h)
     L.rte_profile_enable(batch._h, 0)
     ms_max = max_over_ranks(ms_total, world, device)
@@ -215,7 +225,14 @@ def run_b200(args, rank, world, device):
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    gpu_launches = int(sum(n_k[k] for k in range(5)))
+    gpu_launches = int(sum(n_k[k] for k in range(5)))  # kind 5 is a subset of kind 2
+    # dominant kernel of the step: the finest-level DSA smoother half-sweep
+    # (k_gs).  Algorithmic bytes per launch (fp32 V-cycle vectors): own-colour
+    # b read + x write (2 x 48 B), other-colour x read (48 B), sigma_t,
+    # sigma_s (16 B) per own-colour cell -> 160 B x S x cells / 2.
+    gs_ms = ms_k[5] / max(n_k[5], 1)
+    gs_bytes = 160.0 * S * nx * nx / 2
+    gs_ach = gs_bytes / (gs_ms * 1e-3) / 1e9 if n_k[5] else None
     line = {
         "metric": "sweep cell*direction*sample updates/s (1 SI%s iteration per step)" % ("-DSA" if dsa_ok else ""),
         "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -227,10 +244,15 @@ def run_b200(args, rank, world, device):
                    else "not in this build (step = sweep + source update only)",
                    "l2": "inputs (%.1f GB per step) exceed the 126 MB L2" % (S * nx * nx * 4 * 8 * 3 / 1e9)},
         "e2e": e2e,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+        "roofline": ({"bound": "hbm", "achieved": gs_ach, "peak": hbm_peak, "unit": "GB/s",
+                      "frac": gs_ach / hbm_peak, "traffic": gs_traffic(),
+                      "kernel": "k_gs<float> (finest-level DSA red-black block Gauss-Seidel half-sweep)",
+                      "per_launch_ms": gs_ms, "bytes_per_launch": gs_bytes,
+                      "share_of_step": ms_k[5] / ms_total, "peak_kind": peak_kind} if gs_ach else None),
+        "sweep_roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "kernel": "sweep2d_kernel", "per_launch_ms": sweep_ms, "bytes_per_update": BYTES_PER_UPDATE,
-                     "peak_kind": peak_kind,
+                     "share_of_step": ms_k[0] / ms_total, "peak_kind": peak_kind,
                      "fp64": {"achieved_tflops": fp64_ach, "peak_tflops": tf.value, "frac": fp64_ach / tf.value,
                               "flop_per_update": FLOP_PER_UPDATE, "peak_kind": "measured DFMA probe"}},
         "kernel_ms": {k: ms_k[i] for i, k in enumerate(capi.PROF_KINDS)},

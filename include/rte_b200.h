@@ -235,7 +235,9 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg, double* rho_dev, rte_si
 /* Per-context kernel timing with CUDA events recorded on the launching stream
  * around every kernel the context issues, by category.  Off by default. */
 enum rte_prof_kind { RTE_PROF_SWEEP = 0, RTE_PROF_REDUCE = 1, RTE_PROF_DSA = 2, RTE_PROF_ROM = 3,
-                     RTE_PROF_OTHER = 4, RTE_PROF_KINDS = 5 };
+                     RTE_PROF_OTHER = 4, RTE_PROF_DSA_SMOOTH0 = 5, RTE_PROF_KINDS = 6 };
+/* RTE_PROF_DSA_SMOOTH0 times the finest-level XY DSA smoother half-sweeps
+ * individually (they are also included in RTE_PROF_DSA). */
 int rte_profile_enable(rte_ctx* ctx, int on);
 /* Synchronizes, returns summed milliseconds and launch counts per kind since
  * the last read, and clears them. */

@@ -16,7 +16,7 @@ RTE_OK, RTE_ERR_INVALID, RTE_ERR_RUNTIME, RTE_ERR_CUDA, RTE_ERR_UNSUPPORTED = 0,
 RTE_SLAB1D, RTE_XY2D = 0, 1
 RTE_SI, RTE_DSA, RTE_ROMSA, RTE_ROMSAD, RTE_ROMIG = 0, 1, 2, 3, 4
 RTE_NORM_ABS, RTE_NORM_REL = 0, 1
-PROF_KINDS = ("sweep", "reduce", "dsa", "rom", "other")
+PROF_KINDS = ("sweep", "reduce", "dsa", "rom", "other", "dsa_smooth0")
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _ip = ctypes.POINTER(ctypes.c_int)

@@ -64,6 +64,7 @@ struct Dsa2D {
   int last_iters = 0;
   int nblk = 64;
   long nlaunch = 0;           // kernel launches issued (for launch accounting)
+  rte_ctx* ctx = nullptr;     // for per-kernel profiling of the fine smoother
   const double* sgt = nullptr;
   const double* sgs = nullptr;
 };
@@ -828,6 +829,7 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   }
   const int S = ctx->S;
   d->S = S;
+  d->ctx = ctx;
   if (const char* e = std::getenv("RTE_DSA_NU")) d->nu = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_NU_COARSE")) d->nu_coarse = std::max(1, std::atoi(e));
   // moments (dsa.cpp:167-192, 223-226)
@@ -1073,6 +1075,7 @@ static void smooth(Dsa2D* d, int l, const float* b, float* x, const int* act, bo
   const int S = d->S;
   const long half = (lv.nc + 1) / 2;
   const int c0 = reverse ? 1 : 0;
+  ProfScope ps(l == 0 ? d->ctx : nullptr, RTE_PROF_DSA_SMOOTH0, st, 2);
   ++d->nlaunch;
   k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, c0, lv.Dinvf.p, d->sgt, d->sgs, l, x, b,
                                                       act, zero_init ? 1 : 0);

@@ -151,8 +151,8 @@ struct rte_ctx {
   bool prof = false;
   struct ProfEv { int kind; cudaEvent_t a, b; };
   std::vector<ProfEv> prof_ev;
-  double prof_ms[RTE_PROF_KINDS] = {0, 0, 0, 0, 0};
-  long prof_n[RTE_PROF_KINDS] = {0, 0, 0, 0, 0};
+  double prof_ms[RTE_PROF_KINDS] = {0, 0, 0, 0, 0, 0};
+  long prof_n[RTE_PROF_KINDS] = {0, 0, 0, 0, 0, 0};
 
   rte::DsaState* dsa = nullptr;
   rte::RomState* rom[2] = {nullptr, nullptr};
