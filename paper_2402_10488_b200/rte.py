@@ -442,6 +442,61 @@ class ReducedModel:
     singular_values: np.ndarray = None
     discarded_fraction: float = 0.0
     b_r: np.ndarray = None
+    basis_seconds: float = 0.0
+    operators_seconds: float = 0.0
+
+    _MAGIC = b"RTEROM1\0"
+
+    def save(self, path: str) -> None:
+        """RTEROM1 writer (reduced_model.cpp:41-64): header, then u_rho, u_iso,
+        a_r[k] column-major, singular values, b_r -- all little-endian."""
+        import struct
+        try:
+            f = open(path, "wb")
+        except OSError as e:
+            raise RuntimeError("reduced model: cannot create " + path) from e
+        with f:
+            f.write(self._MAGIC)
+            f.write(struct.pack("<IIQQIIB", 1, int(self.geometry), int(self.n_v), int(self.n_dof), int(self.rank),
+                                int(self.k_affine), ord(self.kind)))
+            f.write(struct.pack("<5d", self.eps_pod, self.eps_train, self.discarded_fraction, self.basis_seconds,
+                                self.operators_seconds))
+            for a in [self.u_rho, self.u_iso] + list(self.a_r):
+                f.write(np.asarray(a, dtype=np.float64).tobytes(order="F"))
+            f.write(np.asarray(self.singular_values, dtype=np.float64).tobytes())
+            f.write(np.asarray(self.b_r, dtype=np.float64).tobytes())
+
+    @staticmethod
+    def load(path: str) -> "ReducedModel":
+        """RTEROM1 reader (reduced_model.cpp:66-104), same error messages."""
+        import struct
+        try:
+            f = open(path, "rb")
+        except OSError as e:
+            raise RuntimeError("reduced model: cannot open " + path) from e
+        with f:
+            def raw(n):
+                b = f.read(n)
+                if len(b) != n:
+                    raise RuntimeError("reduced model: truncated file")
+                return b
+            if raw(8) != ReducedModel._MAGIC:
+                raise RuntimeError("reduced model: " + path + " has wrong magic")
+            if struct.unpack("<I", raw(4))[0] != 1:
+                raise RuntimeError("reduced model: unsupported version in " + path)
+            geom, nv, nd, r, k, kind = struct.unpack("<IQQIIB", raw(29))
+            eps_pod, eps_train, disc, bs, os_ = struct.unpack("<5d", raw(40))
+
+            def mat(rows, cols):
+                return np.frombuffer(raw(8 * rows * cols), dtype=np.float64).reshape((rows, cols), order="F").copy()
+            m = ReducedModel(geom, nv, nd, r, k, chr(kind), eps_pod, eps_train)
+            m.discarded_fraction, m.basis_seconds, m.operators_seconds = disc, bs, os_
+            m.u_rho = mat(nd, r)
+            m.u_iso = mat(nd, r)
+            m.a_r = [mat(r, r) for _ in range(k)]
+            m.singular_values = np.frombuffer(raw(8 * r), dtype=np.float64).copy()
+            m.b_r = np.frombuffer(raw(8 * r), dtype=np.float64).copy()
+        return m
 
 
 def load_rom(batch: TransportBatch, which: int, model) -> None:
