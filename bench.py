@@ -227,11 +227,15 @@ def run_b200(args, rank, world, device):
             traffic = None
     gpu_launches = int(sum(n_k[k] for k in range(5)))  # kind 5 is a subset of kind 2
     # dominant kernel of the step: the finest-level DSA smoother half-sweep
-    # (k_gs).  Algorithmic bytes per launch (fp32 V-cycle vectors): own-colour
-    # b read + x write (2 x 48 B), other-colour x read (48 B), sigma_t,
-    # sigma_s (16 B) per own-colour cell -> 160 B x S x cells / 2.
+    # (k_gs_rb<true,*>).  Algorithmic bytes per own-colour cell (fp32 V-cycle
+    # vectors, red-black layout): b read + x write (2 x 48 B), other-colour x
+    # read (48 B), (sigma_t, sigma_a) (8 B) = 152 B; per V-cycle of 4 nu
+    # half-sweeps one starts from x = 0 (104 B), one also reads x_old and
+    # writes delta (248 B), one also reads the coarse correction (176 B).
+    nu = int(os.environ.get("RTE_DSA_NU", "3"))
+    gs_cell = (104 + 248 + 176 + (4 * nu - 3) * 152) / (4 * nu)
     gs_ms = ms_k[5] / max(n_k[5], 1)
-    gs_bytes = 160.0 * S * nx * nx / 2
+    gs_bytes = gs_cell * S * nx * nx / 2
     gs_ach = gs_bytes / (gs_ms * 1e-3) / 1e9 if n_k[5] else None
     line = {
         "metric": "sweep cell*direction*sample updates/s (1 SI%s iteration per step)" % ("-DSA" if dsa_ok else ""),

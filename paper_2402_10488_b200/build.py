@@ -11,8 +11,11 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "librte_b200.so")
+# Development variants: RTE_BUILD_DEFINES="-DNAME ..." builds into
+# RTE_BUILD_OUT (a separate library path, with its own object directory).
+DEFINES = os.environ.get("RTE_BUILD_DEFINES", "").split()
+LIB = os.environ.get("RTE_BUILD_OUT") or os.path.join(HERE, "librte_b200.so")
+BUILD = os.path.join(HERE, "_build") if not os.environ.get("RTE_BUILD_OUT") else LIB + ".objs"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
@@ -33,7 +36,7 @@ def _compile(src, force):
             os.path.join(os.path.dirname(HERE), "include", "rte_b200.h")]
     if not force and not _stale(obj, deps):
         return obj, ""
-    cmd = [NVCC] + ARCH + FLAGS + ["-c", path, "-o", obj]
+    cmd = [NVCC] + ARCH + FLAGS + DEFINES + ["-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed for %s:\n%s%s" % (src, r.stdout, r.stderr))

@@ -13,14 +13,25 @@
 //     embedding of coarse bilinear modes into the four fine cells and the
 //     coarse operator is the Galerkin product P^T K P (coarse face blocks
 //     stay constant, coarse diagonal blocks are formed on the device);
-//   - smoother: red-black block Gauss-Seidel with the stored inverse
-//     diagonal blocks (same-colour cells do not couple, so a colour sweep is
-//     one parallel kernel);
-//   - coarsest level (<= 64 cells): explicit dense inverse per sample.
+//   - smoother: red-black block Gauss-Seidel (same-colour cells do not
+//     couple, so a colour half-sweep is one parallel kernel); the fine cell
+//     solve is closed form in (sigma_t, sigma_a), coarse cells use a stored
+//     Schur factorisation (T1^-1, T2^-1, S^-1: 48 floats instead of 144);
+//   - coarsest level (<= 16 cells): explicit dense inverse per sample.
+// HBM layout of the V-cycle (fp32 storage, fp64 arithmetic): every level
+// stores its vectors component-major with the cells of each row split by
+// colour (colour-0 cells of the row first, then colour-1), so a colour
+// half-sweep streams contiguous own-colour data instead of half of every
+// sector.  The restricted residual is formed from the last pre-smoothing
+// half-sweep's update delta (r = -sum_nbr C delta on colour 0, 0 on colour 1),
+// and the prolongation is folded into the first post-smoothing half-sweep, so
+// no level ever runs a separate residual or prolongation pass.
 // All per-sample inner products use a two-stage fixed-order reduction, so the
 // solve is deterministic.  Samples converge independently (masked).
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
+#include <cstring>
 #include <vector>
 
 #include "rte_internal.cuh"
@@ -33,13 +44,18 @@ constexpr int NB = 12;  // unknowns per cell
 constexpr int NB2 = NB * NB;
 constexpr int kMaxCoarseCells = 16;
 constexpr int kMaxLevels = 16;
+#ifdef RTE_DSA_FAC64
+using FacT = double;
+#else
+using FacT = float;  // coarse Schur factors (V-cycle preconditioner storage)
+#endif
 
 struct Level {
   int nx, ny;
   long nc;
-  DBuf<double> D, Dinv;       // [S][nc][144] fp64 (setup only)
-  DBuf<float> Df, Dinvf;      // [S][nc][144] fp32 copies used by the V-cycle (preconditioner)
-  DBuf<float> x, b, r;        // [S][12][nc] V-cycle vectors (fp32 storage, fp64 arithmetic)
+  DBuf<double> D;             // [S][nc][144] fp64 natural cell order (setup only)
+  DBuf<FacT> fac;             // [S][48][nc] coarse cell factors T1^-1, T2^-1, S^-1 (red-black order)
+  DBuf<float> x, b, r;        // [S][12][nc] V-cycle vectors (red-black order); r holds the update delta
   DBuf<double> nbr;           // [4][144] W, E, S, N face-coupling blocks (constant)
   std::vector<double> nbr_h;
 };
@@ -51,10 +67,12 @@ struct Dsa2D {
   int ncoarse = 0;            // unknowns of the coarsest level if dense (0: smoothing only)
   DBuf<double> P;             // [4][16] prolongation blocks E2 per sub-cell position (row-major fine x coarse)
   DBuf<double> Dint;          // [levels][144] constant internal-coupling part of the coarse diagonal
-  // BiCGStab
-  DBuf<double> r, rh, p, v, s, t, x, ph, sh, rhs;
+  // BiCGStab (fp64, natural order [S][12][nc]); the shadow residual is the rhs
+  DBuf<double> r, p, v, s, t, x, rhs;
+  DBuf<float> xa, xb;         // preconditioned directions M^-1 p, M^-1 s (fp32, red-black order)
+  DBuf<float2> sig;           // fine (sigma_t, sigma_a) in red-black order for the V-cycle
   DBuf<double> scal;          // per sample scalars [S][16]
-  DBuf<double> part;          // dot partials [S][kDotBlocks][4]
+  DBuf<double> part, part2;   // dot partials [S][nblk][4] (two sets: producer / consumer overlap)
   DBuf<int> act;              // per-sample active flag
   DBuf<int> nact;
   double tol = 1e-12;
@@ -68,8 +86,6 @@ struct Dsa2D {
   const double* sgt = nullptr;
   const double* sgs = nullptr;
 };
-
-constexpr int kDotBlocks = 64;
 
 // ----------------------------------------------------------------------------
 // host-side constant blocks
@@ -166,18 +182,22 @@ __device__ __forceinline__ void lift_mv(const double* M, const double* v, double
 
 // Vectors are component-major per sample (SoA): x[s][r][cell], so a warp's
 // loads of one component of consecutive cells coalesce.
-template <typename T>
-__device__ __forceinline__ void face_mv(int lev, int dir, const T* __restrict__ xs, long nc, long cn, double* y) {
+__device__ __forceinline__ void face_lift(int lev, int dir, const double* v, double* y) {
   const int axis = dir >> 1;
   const int j = axis == 0 ? 4 : 8, o = axis == 0 ? 8 : 4;
-  double v[NB];
-#pragma unroll
-  for (int r = 0; r < NB; ++r) v[r] = (double)xs[r * nc + cn];
   lift_mv(c_face[lev][dir][0], v, y, axis);
   lift_mv(c_face[lev][dir][1], v + j, y, axis);
   lift_mv(c_face[lev][dir][2], v, y + j, axis);
   lift_mv(c_face[lev][dir][3], v + j, y + j, axis);
   lift_mv(c_face[lev][dir][4], v + o, y + o, axis);
+}
+
+template <typename T>
+__device__ __forceinline__ void face_mv(int lev, int dir, const T* __restrict__ xs, long nc, long cn, double* y) {
+  double v[NB];
+#pragma unroll
+  for (int r = 0; r < NB; ++r) v[r] = (double)xs[r * nc + cn];
+  face_lift(lev, dir, v, y);
 }
 
 // Fine-level diagonal block D_c = Dconst + diag(sigma_a I4, 3 m2x sigma_t I4,
@@ -252,52 +272,6 @@ __global__ void k_fine_diag(int S, long nc, const double* __restrict__ st, const
   }
 }
 
-// 12x12 inverse, Gauss-Jordan with partial pivoting (thread per block).
-__global__ void k_inv12(long n, const double* __restrict__ D, double* __restrict__ Dinv) {
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  double a[NB][NB], iv[NB][NB];
-  for (int r = 0; r < NB; ++r)
-    for (int c = 0; c < NB; ++c) {
-      a[r][c] = D[t * NB2 + r * NB + c];
-      iv[r][c] = r == c ? 1.0 : 0.0;
-    }
-  for (int k = 0; k < NB; ++k) {
-    int p = k;
-    double best = fabs(a[k][k]);
-    for (int r = k + 1; r < NB; ++r)
-      if (fabs(a[r][k]) > best) {
-        best = fabs(a[r][k]);
-        p = r;
-      }
-    if (p != k)
-      for (int c = 0; c < NB; ++c) {
-        double x = a[k][c];
-        a[k][c] = a[p][c];
-        a[p][c] = x;
-        x = iv[k][c];
-        iv[k][c] = iv[p][c];
-        iv[p][c] = x;
-      }
-    const double id = 1.0 / a[k][k];
-    for (int c = 0; c < NB; ++c) {
-      a[k][c] *= id;
-      iv[k][c] *= id;
-    }
-    for (int r = 0; r < NB; ++r)
-      if (r != k) {
-        const double f = a[r][k];
-        if (f != 0.0)
-          for (int c = 0; c < NB; ++c) {
-            a[r][c] -= f * a[k][c];
-            iv[r][c] -= f * iv[k][c];
-          }
-      }
-  }
-  for (int r = 0; r < NB; ++r)
-    for (int c = 0; c < NB; ++c) Dinv[t * NB2 + r * NB + c] = iv[r][c];
-}
-
 // Coarse diagonal blocks: D_C = sum_pos P_pos^T D_c P_pos + Dint (Galerkin).
 __global__ void k_galerkin_diag(int S, int fnx, int fny, const double* __restrict__ Df, const double* __restrict__ sgt,
                                 const double* __restrict__ sgs, const double* __restrict__ P,
@@ -350,206 +324,361 @@ __global__ void k_galerkin_diag(int S, int fnx, int fny, const double* __restric
   for (int e = 0; e < NB2; ++e) Dc[t * NB2 + e] = out[e];
 }
 
-// Coarse-level blocks are stored element-major in fp32: M[s][e][cell]
-// (e = r * 12 + c), so a warp's loads of one element coalesce.  `M` points at
-// (sample s, element 0, cell c); `stride` = cells per sample of the level.
-__device__ __forceinline__ void blk_mv_accf(const float* __restrict__ M, long stride, const double* __restrict__ x,
-                                            double* y) {
-#pragma unroll
-  for (int r = 0; r < NB; ++r) {
-    double acc = y[r];
-#pragma unroll
-    for (int c = 0; c < NB; ++c) acc = fma((double)M[(r * NB + c) * stride], x[c], acc);
-    y[r] = acc;
-  }
+// ---- red-black storage order ------------------------------------------------
+// Cells of colour (ix + iy) & 1 == 0 come first in every row, then colour 1.
+__host__ __device__ __forceinline__ int rb_cnt0(int nx, int iy) { return (nx + 1 - (iy & 1)) >> 1; }
+__host__ __device__ __forceinline__ long rbidx(int nx, int ix, int iy) {
+  return (long)iy * nx + (((ix + iy) & 1) ? rb_cnt0(nx, iy) : 0) + (ix >> 1);
 }
 
-template <typename A, typename B>
-__global__ void k_cvt(long n, const A* __restrict__ a, B* __restrict__ b, const int* __restrict__ act, long per) {
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  if (act && !act[t / per]) return;
-  b[t] = (B)a[t];
-}
+__constant__ double c_P[4][16];               // prolongation E2 per sub-cell position: [4 * fine + coarse]
+__constant__ double c_cpl[kMaxLevels][4][16]; // per level: B1 (rho<-Jx), B2 (rho<-Jy), C1 (Jx<-rho), C2 (Jy<-rho)
 
-// [S][nc][144] fp64 -> [S][144][nc] fp32
-__global__ void k_to_f32(int S, long nc, const double* __restrict__ a, float* __restrict__ b) {
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long)S * nc * NB2) return;
-  const long s = t / (nc * NB2), rem = t - s * nc * NB2;
-  const long e = rem / nc, c = rem - e * nc;
-  b[t] = (float)a[(s * nc + c) * NB2 + e];
-}
-
-__device__ __forceinline__ void blk_mv_acc(const double* __restrict__ M, const double* __restrict__ x, double* y) {
-#pragma unroll
-  for (int r = 0; r < NB; ++r) {
-    double acc = y[r];
-#pragma unroll
-    for (int c = 0; c < NB; ++c) acc = fma(M[r * NB + c], x[c], acc);
-    y[r] = acc;
-  }
-}
-
-// off-diagonal (face) contributions sum_nbr C_dir x_nbr
+// off-diagonal (face) contributions sum_nbr C_dir x_nbr, red-black storage
 template <typename T>
-__device__ __forceinline__ void face_terms(int lev, const T* __restrict__ xs, int nx, int ny, int ix, int iy,
-                                           long c, double* y) {
+__device__ __forceinline__ void face_terms_rb(int lev, const T* __restrict__ xs, int nx, int ny, int ix, int iy,
+                                              double* y) {
   const long nc = (long)nx * ny;
-  if (ix > 0) face_mv(lev, 0, xs, nc, c - 1, y);
-  if (ix < nx - 1) face_mv(lev, 1, xs, nc, c + 1, y);
-  if (iy > 0) face_mv(lev, 2, xs, nc, c - nx, y);
-  if (iy < ny - 1) face_mv(lev, 3, xs, nc, c + nx, y);
+  if (ix > 0) face_mv(lev, 0, xs, nc, rbidx(nx, ix - 1, iy), y);
+  if (ix < nx - 1) face_mv(lev, 1, xs, nc, rbidx(nx, ix + 1, iy), y);
+  if (iy > 0) face_mv(lev, 2, xs, nc, rbidx(nx, ix, iy - 1), y);
+  if (iy < ny - 1) face_mv(lev, 3, xs, nc, rbidx(nx, ix, iy + 1), y);
 }
 
-// y = K x (mode 0) or y = b - K x (mode 1)
-template <typename T>
-__global__ void k_apply(int S, int nx, int ny, const float* __restrict__ D, const double* __restrict__ sgt,
-                        const double* __restrict__ sgs, int lev,
-                        const T* __restrict__ x, const T* __restrict__ b, T* __restrict__ y, int mode,
-                        const int* __restrict__ act) {
+// face term of neighbour (jx, jy) whose value is x_f + (P x_C): the coarse-grid
+// correction prolonged on the fly (the corrected fine vector is never stored)
+__device__ __forceinline__ void face_mv_prolong(int lev, int dir, const float* __restrict__ xs, long nc, int nx,
+                                                int jx, int jy, const float* __restrict__ xcs, long ncc, int cnx,
+                                                double* y) {
+  const long cn = rbidx(nx, jx, jy);
+  const long C = rbidx(cnx, jx >> 1, jy >> 1);
+  const double* E = c_P[(jx & 1) + 2 * (jy & 1)];
+  double v[NB];
+#pragma unroll
+  for (int f = 0; f < 3; ++f) {
+    double xc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) xc[k] = (double)xcs[(4 * f + k) * ncc + C];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      double acc = (double)xs[(4 * f + l) * nc + cn];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc = fma(E[4 * l + k], xc[k], acc);
+      v[4 * f + l] = acc;
+    }
+  }
+  face_lift(lev, dir, v, y);
+}
+
+// x = D_C^{-1} r for a coarse cell from its Schur factors (f: element stride nc)
+//   D_C = [[A, B1, B2], [C1, T1, 0], [C2, 0, T2]],  S = A - B1 T1^-1 C1 - B2 T2^-1 C2
+__device__ __forceinline__ void coarse_block_solve(int lev, const FacT* __restrict__ f, long nc, const double* r,
+                                                   double* x) {
+  FacT t1[16], t2[16], si[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    t1[e] = f[e * nc];
+    t2[e] = f[(16 + e) * nc];
+    si[e] = f[(32 + e) * nc];
+  }
+  const double* B1 = c_cpl[lev][0];
+  const double* B2 = c_cpl[lev][1];
+  const double* C1 = c_cpl[lev][2];
+  const double* C2 = c_cpl[lev][3];
+  double yx[4], yy[4], z[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double ax = 0.0, ay = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      ax = fma((double)t1[4 * i + k], r[4 + k], ax);
+      ay = fma((double)t2[4 * i + k], r[8 + k], ay);
+    }
+    yx[i] = ax;
+    yy[i] = ay;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double a = r[i];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a -= B1[4 * i + k] * yx[k] + B2[4 * i + k] * yy[k];
+    z[i] = a;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a = fma((double)si[4 * i + k], z[k], a);
+    x[i] = a;
+  }
+  double wx[4], wy[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double a = r[4 + i], b = r[8 + i];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a -= C1[4 * i + k] * x[k];
+      b -= C2[4 * i + k] * x[k];
+    }
+    wx[i] = a;
+    wy[i] = b;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a = fma((double)t1[4 * i + k], wx[k], a);
+      b = fma((double)t2[4 * i + k], wy[k], b);
+    }
+    x[4 + i] = a;
+    x[8 + i] = b;
+  }
+}
+
+// 4x4 inverse, Gauss-Jordan with partial pivoting (setup only)
+__device__ __forceinline__ void inv4(const double* a_in, double* iv) {
+  double a[16];
+  for (int e = 0; e < 16; ++e) {
+    a[e] = a_in[e];
+    iv[e] = (e / 4 == e % 4) ? 1.0 : 0.0;
+  }
+  for (int k = 0; k < 4; ++k) {
+    int p = k;
+    for (int r = k + 1; r < 4; ++r)
+      if (fabs(a[4 * r + k]) > fabs(a[4 * p + k])) p = r;
+    if (p != k)
+      for (int c = 0; c < 4; ++c) {
+        double t = a[4 * k + c];
+        a[4 * k + c] = a[4 * p + c];
+        a[4 * p + c] = t;
+        t = iv[4 * k + c];
+        iv[4 * k + c] = iv[4 * p + c];
+        iv[4 * p + c] = t;
+      }
+    const double id = 1.0 / a[4 * k + k];
+    for (int c = 0; c < 4; ++c) {
+      a[4 * k + c] *= id;
+      iv[4 * k + c] *= id;
+    }
+    for (int r = 0; r < 4; ++r)
+      if (r != k) {
+        const double f = a[4 * r + k];
+        for (int c = 0; c < 4; ++c) {
+          a[4 * r + c] -= f * a[4 * k + c];
+          iv[4 * r + c] -= f * iv[4 * k + c];
+        }
+      }
+  }
+}
+
+// Coarse cell factors from the fp64 Galerkin block (natural order) into the
+// fp32 red-black factor array; also checks that the field-coupling blocks are
+// the level constants of c_cpl and that Jx-Jy blocks vanish (max relative
+// deviation into *err as ordered double bits).
+__global__ void k_coarse_factor(int S, int nx, int ny, int lev, const double* __restrict__ D,
+                                FacT* __restrict__ fac, unsigned long long* __restrict__ err) {
   const long nc = (long)nx * ny;
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long)S * nc) return;
   const long s = t / nc, c = t - s * nc;
-  if (act && !act[s]) return;
-  const int ix = (int)(c % nx), iy = (int)(c / nx);
-  const T* xs = x + s * nc * NB;
-  double acc[NB], xl[NB];
-#pragma unroll
-  for (int r = 0; r < NB; ++r) {
-    acc[r] = 0.0;
-    xl[r] = (double)xs[r * nc + c];
+  const double* d = D + t * NB2;
+  auto blk = [&](int f1, int f2, double* o) {
+    for (int i = 0; i < 4; ++i)
+      for (int k = 0; k < 4; ++k) o[4 * i + k] = d[(4 * f1 + i) * NB + 4 * f2 + k];
+  };
+  double A[16], T1[16], T2[16], B1[16], B2[16], C1[16], C2[16], X1[16], X2[16];
+  blk(0, 0, A); blk(1, 1, T1); blk(2, 2, T2); blk(0, 1, B1); blk(0, 2, B2); blk(1, 0, C1); blk(2, 0, C2);
+  blk(1, 2, X1); blk(2, 1, X2);
+  double mag = 0.0, dev = 0.0;
+  for (int e = 0; e < NB2; ++e) mag = fmax(mag, fabs(d[e]));
+  for (int e = 0; e < 16; ++e) {
+    dev = fmax(dev, fabs(B1[e] - c_cpl[lev][0][e]));
+    dev = fmax(dev, fabs(B2[e] - c_cpl[lev][1][e]));
+    dev = fmax(dev, fabs(C1[e] - c_cpl[lev][2][e]));
+    dev = fmax(dev, fabs(C2[e] - c_cpl[lev][3][e]));
+    dev = fmax(dev, fabs(X1[e]));
+    dev = fmax(dev, fabs(X2[e]));
   }
-  if (D)
-    blk_mv_accf(D + s * nc * NB2 + c, nc, xl, acc);
-  else
-    fine_block_mv(sgt[t], sgt[t] - sgs[t], xl, acc);
-  face_terms(lev, xs, nx, ny, ix, iy, c, acc);
-  T* yo = y + s * nc * NB + c;
-  if (mode == 1) {
-    const T* bi = b + s * nc * NB + c;
+  const double rel = mag > 0.0 ? dev / mag : 0.0;
+  atomicMax(err, (unsigned long long)__double_as_longlong(rel));
+  double T1i[16], T2i[16], Sm[16], Si[16], P1[16], P2[16];
+  inv4(T1, T1i);
+  inv4(T2, T2i);
+  // P = T^-1 C, then S = A - B1 P1 - B2 P2
 #pragma unroll
-    for (int r = 0; r < NB; ++r) yo[r * nc] = (T)((double)bi[r * nc] - acc[r]);
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double p1 = 0.0, p2 = 0.0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        p1 += T1i[4 * i + m] * C1[4 * m + k];
+        p2 += T2i[4 * i + m] * C2[4 * m + k];
+      }
+      P1[4 * i + k] = p1;
+      P2[4 * i + k] = p2;
+    }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double a = A[4 * i + k];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) a -= B1[4 * i + m] * P1[4 * m + k] + B2[4 * i + m] * P2[4 * m + k];
+      Sm[4 * i + k] = a;
+    }
+  inv4(Sm, Si);
+  const long o = rbidx(nx, (int)(c % nx), (int)(c / nx));
+  FacT* fo = fac + s * nc * 48 + o;
+  for (int e = 0; e < 16; ++e) {
+    fo[e * nc] = (FacT)T1i[e];
+    fo[(16 + e) * nc] = (FacT)T2i[e];
+    fo[(32 + e) * nc] = (FacT)Si[e];
+  }
+}
+
+// debug: max_j |D_C^{-1} D_C e_j - e_j| over cells via the stored factors
+__global__ void k_check_factor(int S, int nx, int ny, int lev, const double* __restrict__ D,
+                               const FacT* __restrict__ fac, unsigned long long* __restrict__ err) {
+  const long nc = (long)nx * ny;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)S * nc) return;
+  const long s = t / nc, c = t - s * nc;
+  const long o = rbidx(nx, (int)(c % nx), (int)(c / nx));
+  double e = 0.0;
+  for (int j = 0; j < NB; ++j) {
+    double r[NB], x[NB];
+    for (int i = 0; i < NB; ++i) r[i] = D[t * NB2 + i * NB + j];
+    coarse_block_solve(lev, fac + s * nc * 48 + o, nc, r, x);
+    for (int i = 0; i < NB; ++i) e = fmax(e, fabs(x[i] - (i == j ? 1.0 : 0.0)));
+  }
+  atomicMax(err, (unsigned long long)__double_as_longlong(e));
+}
+
+// fine (sigma_t, sigma_a) in red-black order, fp32 (V-cycle only)
+__global__ void k_sig_rb(int S, int nx, int ny, const double* __restrict__ st, const double* __restrict__ ss,
+                         float2* __restrict__ out) {
+  const long nc = (long)nx * ny;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)S * nc) return;
+  const long s = t / nc, c = t - s * nc;
+  out[s * nc + rbidx(nx, (int)(c % nx), (int)(c / nx))] = make_float2((float)st[t], (float)(st[t] - ss[t]));
+}
+
+// One colour half-sweep of block Gauss-Seidel on a level (red-black storage):
+//   x_c = D_c^{-1} (b_c - sum_nbr C x_nbr)   for every cell of colour `color`.
+struct GsArgs {
+  int S, nx, ny, lev, color;
+  float* x;
+  const float* b;
+  const float2* sig;    // finest level: (sigma_t, sigma_a), else null
+  const FacT* fac;      // coarse level: Schur factors, else null
+  const int* act;
+  int zero_nbr;         // x == 0 on entry (first half-sweep of a cycle): skip the face terms
+  float* delta;         // if set: delta = x_new - x_old on own cells (residual bookkeeping)
+  int old_zero;         // x_old == 0 for delta
+  const float* xc;      // if set: neighbours carry the prolonged coarse correction P x_C
+};
+
+template <bool FINE, bool PROLONG>
+__global__ void __launch_bounds__(128) k_gs_rb(GsArgs a) {
+  const int h = (a.nx + 1) >> 1;
+  const long per = (long)a.ny * h;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)a.S * per) return;
+  const int s = (int)(t / per);
+  const long rem = t - s * per;
+  const int iy = (int)(rem / h), k = (int)(rem - (long)iy * h);
+  if (a.act && !a.act[s]) return;
+  const int c0 = rb_cnt0(a.nx, iy);
+  if (k >= (a.color ? a.nx - c0 : c0)) return;
+  const int ix = 2 * k + ((a.color + iy) & 1);
+  const long nc = (long)a.nx * a.ny;
+  const long own = (long)iy * a.nx + (a.color ? c0 : 0) + k;
+  const float* xs = a.x + s * nc * NB;
+  double acc[NB];
+#pragma unroll
+  for (int r = 0; r < NB; ++r) acc[r] = 0.0;
+  if (!a.zero_nbr) {
+    if (PROLONG) {
+      const int cnx = a.nx >> 1;
+      const long ncc = (long)cnx * (a.ny >> 1);
+      const float* xcs = a.xc + s * ncc * NB;
+      if (ix > 0) face_mv_prolong(a.lev, 0, xs, nc, a.nx, ix - 1, iy, xcs, ncc, cnx, acc);
+      if (ix < a.nx - 1) face_mv_prolong(a.lev, 1, xs, nc, a.nx, ix + 1, iy, xcs, ncc, cnx, acc);
+      if (iy > 0) face_mv_prolong(a.lev, 2, xs, nc, a.nx, ix, iy - 1, xcs, ncc, cnx, acc);
+      if (iy < a.ny - 1) face_mv_prolong(a.lev, 3, xs, nc, a.nx, ix, iy + 1, xcs, ncc, cnx, acc);
+    } else {
+      face_terms_rb(a.lev, xs, a.nx, a.ny, ix, iy, acc);
+    }
+  }
+  const float* bi = a.b + s * nc * NB + own;
+  double rr[NB];
+#pragma unroll
+  for (int r = 0; r < NB; ++r) rr[r] = (double)bi[r * nc] - acc[r];
+  double out[NB];
+  if (FINE) {
+    const float2 sg = a.sig[s * nc + own];
+    fine_block_solve((double)sg.x, (double)sg.y, rr, out);
+  } else {
+    coarse_block_solve(a.lev, a.fac + s * nc * 48 + own, nc, rr, out);
+  }
+  float* xo = a.x + s * nc * NB + own;
+  if (a.delta) {
+    float* dl = a.delta + s * nc * NB + own;
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      const float xn = (float)out[r];
+      dl[r * nc] = a.old_zero ? xn : (float)((double)xn - (double)xo[r * nc]);
+      xo[r * nc] = xn;
+    }
   } else {
 #pragma unroll
-    for (int r = 0; r < NB; ++r) yo[r * nc] = (T)acc[r];
+    for (int r = 0; r < NB; ++r) xo[r * nc] = (float)out[r];
   }
 }
 
-// red-black block Gauss-Seidel half sweep: x_c = Dinv_c (b_c - sum_nbr C x_nbr)
-template <typename T>
-__global__ void k_gs(int S, int nx, int ny, int color, const float* __restrict__ Dinv, const double* __restrict__ sgt,
-                     const double* __restrict__ sgs, int lev,
-                     T* __restrict__ x, const T* __restrict__ b, const int* __restrict__ act, int zero_init) {
-  const long nc = (long)nx * ny;
-  const long half = (nc + 1) / 2;
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long)S * half) return;
-  const long s = t / half, k = t - s * half;
-  if (act && !act[s]) return;
-  long c;
-  // exact mapping: enumerate colour cells row by row
-  {
-    const int per_even_row = (nx + 1 - color) / 2;  // cells with (ix + iy)%2==color for iy even
-    const int per_odd_row = (nx + color) / 2;
-    const long pair = per_even_row + per_odd_row;
-    const long iy2 = k / pair;
-    long rem = k - iy2 * pair;
-    int iy = (int)(2 * iy2);
-    int first;
-    if (rem < per_even_row) {
-      first = color;  // even row: ix parity == color
-    } else {
-      rem -= per_even_row;
-      iy += 1;
-      first = 1 - color;
-    }
-    if (iy >= ny) return;
-    const int ix = first + 2 * (int)rem;
-    if (ix >= nx) return;
-    c = (long)iy * nx + ix;
-    const T* xs = x + s * nc * NB;
-    double acc[NB];
-    const T* bi = b + s * nc * NB + c;
-#pragma unroll
-    for (int r = 0; r < NB; ++r) acc[r] = 0.0;
-    if (!zero_init) face_terms(lev, xs, nx, ny, ix, iy, c, acc);
-    double rr[NB];
-#pragma unroll
-    for (int r = 0; r < NB; ++r) rr[r] = (double)bi[r * nc] - acc[r];
-    double out[NB];
-    if (Dinv) {
-#pragma unroll
-      for (int r = 0; r < NB; ++r) out[r] = 0.0;
-      blk_mv_accf(Dinv + s * nc * NB2 + c, nc, rr, out);
-    } else {
-      const long fi = s * nc + c;
-      fine_block_solve(sgt[fi], sgt[fi] - sgs[fi], rr, out);
-    }
-    T* xo = x + s * nc * NB + c;
-#pragma unroll
-    for (int r = 0; r < NB; ++r) xo[r * nc] = (T)out[r];
-  }
-}
-
-// restriction b_C = sum_pos P_pos^T r_c
-template <typename T>
-__global__ void k_restrict(int S, int fnx, int fny, const double* __restrict__ P, const T* __restrict__ rf,
-                           T* __restrict__ bc, const int* __restrict__ act) {
+// Restriction of the residual after a pre-smoothing cycle that ended with a
+// colour-1 half-sweep: colour-1 residuals vanish, colour-0 residuals are
+// r_f = -sum_nbr C delta_nbr (delta = last colour-1 update).
+//   b_C = sum_{f in colour-0 children} E_f^T r_f
+__global__ void k_restrict_delta(int S, int fnx, int fny, int lev, const float* __restrict__ delta,
+                                 float* __restrict__ bc, const int* __restrict__ act) {
   const int cnx = fnx / 2, cny = fny / 2;
-  const long ncc = (long)cnx * cny;
+  const long ncc = (long)cnx * cny, nf = (long)fnx * fny;
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long)S * ncc) return;
   const long s = t / ncc, C = t - s * ncc;
   if (act && !act[s]) return;
   const int cx = (int)(C % cnx), cy = (int)(C / cnx);
+  const float* ds = delta + s * nf * NB;
   double out[NB];
 #pragma unroll
   for (int r = 0; r < NB; ++r) out[r] = 0.0;
-  for (int py = 0; py < 2; ++py)
-    for (int px = 0; px < 2; ++px) {
-      const long c = (long)(2 * cy + py) * fnx + 2 * cx + px;
-      const long nf = (long)fnx * fny;
-      const T* r = rf + s * nf * NB + c;
-      const double* E = P + (px + 2 * py) * 16;
-      for (int f = 0; f < 3; ++f)
-        for (int k = 0; k < 4; ++k) {
-          double acc = out[4 * f + k];
-          for (int l = 0; l < 4; ++l) acc = fma(E[4 * l + k], (double)r[(4 * f + l) * nf], acc);
-          out[4 * f + k] = acc;
-        }
-    }
-  T* o = bc + s * ncc * NB + C;
 #pragma unroll
-  for (int r = 0; r < NB; ++r) o[r * ncc] = (T)out[r];
+  for (int q = 0; q < 2; ++q) {  // colour-0 children (0,0) and (1,1)
+    double y[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) y[r] = 0.0;
+    face_terms_rb(lev, ds, fnx, fny, 2 * cx + q, 2 * cy + q, y);
+    const double* E = c_P[q ? 3 : 0];
+#pragma unroll
+    for (int f = 0; f < 3; ++f)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double acc = out[4 * f + k];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) acc = fma(-E[4 * l + k], y[4 * f + l], acc);
+        out[4 * f + k] = acc;
+      }
+  }
+  float* o = bc + s * ncc * NB + rbidx(cnx, cx, cy);
+#pragma unroll
+  for (int r = 0; r < NB; ++r) o[r * ncc] = (float)out[r];
 }
 
-// x_c += P_pos x_C
-template <typename T>
-__global__ void k_prolong_add(int S, int fnx, int fny, const double* __restrict__ P, const T* __restrict__ xc,
-                              T* __restrict__ xf, const int* __restrict__ act) {
-  const long nf = (long)fnx * fny;
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long)S * nf) return;
-  const long s = t / nf, c = t - s * nf;
-  if (act && !act[s]) return;
-  const int ix = (int)(c % fnx), iy = (int)(c / fnx);
-  const int cnx = fnx / 2;
-  const long C = (long)(iy / 2) * cnx + ix / 2;
-  const double* E = P + ((ix & 1) + 2 * (iy & 1)) * 16;
-  const long ncc = (long)(fnx / 2) * (fny / 2);
-  const T* xcs = xc + s * ncc * NB + C;
-  T* o = xf + s * nf * NB + c;
-  for (int f = 0; f < 3; ++f)
-    for (int l = 0; l < 4; ++l) {
-      double acc = (double)o[(4 * f + l) * nf];
-      for (int k = 0; k < 4; ++k) acc = fma(E[4 * l + k], (double)xcs[(4 * f + k) * ncc], acc);
-      o[(4 * f + l) * nf] = (T)acc;
-    }
-}
-
-// dense coarsest operator [S][n][n] (n = 12 nc)
+// dense coarsest operator [S][n][n] (n = 12 nc), unknown index r * nc + rb(cell)
 __global__ void k_dense_coarse(int S, int nx, int ny, const double* __restrict__ D, const double* __restrict__ nbr,
                                double* __restrict__ A) {
   const long nc = (long)nx * ny, n = nc * NB;
@@ -558,16 +687,15 @@ __global__ void k_dense_coarse(int S, int nx, int ny, const double* __restrict__
   const long s = t / nc, c = t - s * nc;
   const int ix = (int)(c % nx), iy = (int)(c / nx);
   double* As = A + s * n * n;
-  // SoA ordering of the coarsest vector: index(cell, r) = r * nc + cell
-  auto col = [&](long cell, int q) { return (long)q * nc + cell; };
+  auto col = [&](int jx, int jy, int q) { return (long)q * nc + rbidx(nx, jx, jy); };
   for (int r = 0; r < NB; ++r) {
-    double* row = As + col(c, r) * n;
+    double* row = As + col(ix, iy, r) * n;
     for (long j = 0; j < n; ++j) row[j] = 0.0;
-    for (int q = 0; q < NB; ++q) row[col(c, q)] = D[t * NB2 + r * NB + q];
-    if (ix > 0) for (int q = 0; q < NB; ++q) row[col(c - 1, q)] = nbr[0 * NB2 + r * NB + q];
-    if (ix < nx - 1) for (int q = 0; q < NB; ++q) row[col(c + 1, q)] = nbr[1 * NB2 + r * NB + q];
-    if (iy > 0) for (int q = 0; q < NB; ++q) row[col(c - nx, q)] = nbr[2 * NB2 + r * NB + q];
-    if (iy < ny - 1) for (int q = 0; q < NB; ++q) row[col(c + nx, q)] = nbr[3 * NB2 + r * NB + q];
+    for (int q = 0; q < NB; ++q) row[col(ix, iy, q)] = D[t * NB2 + r * NB + q];
+    if (ix > 0) for (int q = 0; q < NB; ++q) row[col(ix - 1, iy, q)] = nbr[0 * NB2 + r * NB + q];
+    if (ix < nx - 1) for (int q = 0; q < NB; ++q) row[col(ix + 1, iy, q)] = nbr[1 * NB2 + r * NB + q];
+    if (iy > 0) for (int q = 0; q < NB; ++q) row[col(ix, iy - 1, q)] = nbr[2 * NB2 + r * NB + q];
+    if (iy < ny - 1) for (int q = 0; q < NB; ++q) row[col(ix, iy + 1, q)] = nbr[3 * NB2 + r * NB + q];
   }
 }
 
@@ -659,12 +787,51 @@ __global__ void k_dense_apply(int n, const double* __restrict__ Ainv, const T* _
 }
 
 // ---- BiCGStab helpers -------------------------------------------------------
-// per-sample partial dots of up to 4 pairs: part[s][blk][q] = sum a_q . b_q
+// Vectors are fp64, natural order [S][12][nc]; one grid row (blockIdx.y) per
+// sample, nblk blocks per sample, grid-stride inside the sample.  Dot
+// products are fused into the kernels that produce their operands: each block
+// writes its fixed-order partial sums part[s][blk][q], and the consuming
+// kernel reduces the nblk partials in a fixed order (warp 0, lane-strided,
+// then a shuffle tree), so the solve is bitwise deterministic.
 struct DotArgs {
   const double* a[4];
   const double* b[4];
   int nq;
 };
+
+constexpr int kBT = 256;  // threads per block of the vector kernels
+
+// per-sample reduction of the partials of this sample into out[0..nq) (all threads)
+__device__ __forceinline__ void reduce_parts(const double* __restrict__ part, int s, int nblk, int nq, double* out) {
+  __shared__ double sh[4];
+  if (threadIdx.x < 32) {
+    for (int q = 0; q < nq; ++q) {
+      double v = 0.0;
+      for (int b = threadIdx.x; b < nblk; b += 32) v += part[((long)s * nblk + b) * 4 + q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (threadIdx.x == 0) sh[q] = v;
+    }
+  }
+  __syncthreads();
+  for (int q = 0; q < nq; ++q) out[q] = sh[q];
+}
+
+// block-level fixed-order sum of up to 2 per-thread values -> part[s][blk][0..nq)
+__device__ __forceinline__ void block_parts(double a0, double a1, int nq, double* __restrict__ part, int s) {
+  __shared__ double red[2][kBT];
+  red[0][threadIdx.x] = a0;
+  red[1][threadIdx.x] = a1;
+  __syncthreads();
+  for (int o = kBT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + o];
+      red[1][threadIdx.x] += red[1][threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < nq) part[((long)s * gridDim.x + blockIdx.x) * 4 + threadIdx.x] = red[threadIdx.x][0];
+}
 
 __global__ void k_dots(int S, long n, DotArgs d, double* __restrict__ part, const int* __restrict__ act) {
   const int s = blockIdx.y;
@@ -676,107 +843,156 @@ __global__ void k_dots(int S, long n, DotArgs d, double* __restrict__ part, cons
     for (int q = 0; q < 4; ++q)
       if (q < d.nq) acc[q] = fma(d.a[q][g], d.b[q][g], acc[q]);
   }
-  __shared__ double red[4][256];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = acc[q];
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x < 4) part[((long)s * gridDim.x + blockIdx.x) * 4 + threadIdx.x] = red[threadIdx.x][0];
+  block_parts(acc[0], acc[1], d.nq < 2 ? d.nq : 2, part, s);
 }
 
-// scalar state per sample (scal[s*16 + k]):
-// 0 rho_old, 1 alpha, 2 omega, 3 rho, 4 bnorm2, 5 rnorm2, 6 iters, 7 converged
-enum { SC_RHO_OLD = 0, SC_ALPHA, SC_OMEGA, SC_RHO, SC_BNORM2, SC_RNORM2, SC_ITERS, SC_CONV, SC_RHV, SC_TS, SC_TT };
+// scalar state per sample (scal[s*16 + k])
+enum { SC_RHO_OLD = 0, SC_ALPHA, SC_OMEGA, SC_RHO, SC_BNORM2, SC_RNORM2, SC_ITERS, SC_CONV, SC_RHV, SC_TS, SC_TT,
+       SC_RHO_NEW };
 
-__device__ double sum_parts(const double* part, int s, int nblk, int q) {
-  double v = 0.0;
-  for (int b = 0; b < nblk; ++b) v += part[((long)s * nblk + b) * 4 + q];
-  return v;
+// natural SoA element i of a sample -> red-black position (32-bit index math)
+__device__ __forceinline__ unsigned nat2rb(unsigned i, unsigned nc, unsigned nx) {
+  const unsigned q = i / nc, c = i - q * nc;
+  const unsigned iy = c / nx, ix = c - iy * nx;
+  return q * nc + (unsigned)rbidx((int)nx, (int)ix, (int)iy);
 }
 
-// stage kernels operate on one sample per thread (S threads)
 __global__ void k_bicg_init(int S, int nblk, const double* part, double* scal, int* act, const int* mask) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S) return;
   double* sc = scal + s * 16;
-  const double bn = sum_parts(part, s, nblk, 0);
+  double bn = 0.0;
+  for (int b = 0; b < nblk; ++b) bn += part[((long)s * nblk + b) * 4];
   sc[SC_RHO_OLD] = 1.0;
   sc[SC_ALPHA] = 1.0;
   sc[SC_OMEGA] = 1.0;
   sc[SC_BNORM2] = bn;
   sc[SC_RNORM2] = bn;
+  sc[SC_RHO_NEW] = bn;  // (rh, r) with rh = r = b
   sc[SC_ITERS] = 0;
   sc[SC_CONV] = 0;
   act[s] = (mask ? mask[s] : 1) && bn > 0.0;
   if (!(bn > 0.0)) sc[SC_CONV] = 1;
 }
 
-// rho = (rh, r); beta = (rho/rho_old)(alpha/omega); p = r + beta (p - omega v)
-__global__ void k_bicg_p(int S, long n, int nblk, const double* part, double* scal, const double* r, double* p,
-                         const double* v, const int* act) {
+// beta = (rho/rho_old)(alpha/omega); p = r + beta (p - omega v); b0 = fp32 rb(p)
+__global__ void __launch_bounds__(kBT) k_bicg_p(int S, unsigned n, unsigned nc, unsigned nx, double* scal,
+                                                const double* r, double* p, const double* v, float* b0,
+                                                const int* act) {
   const int s = blockIdx.y;
   if (!act[s]) return;
   double* sc = scal + s * 16;
-  const double rho = sum_parts(part, s, nblk, 0);
+  const double rho = sc[SC_RHO_NEW];
   const double beta = (rho / sc[SC_RHO_OLD]) * (sc[SC_ALPHA] / sc[SC_OMEGA]);
   const double om = sc[SC_OMEGA];
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-    const long g = (long)s * n + i;
-    p[g] = r[g] + beta * (p[g] - om * v[g]);
+  const long base = (long)s * n;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double pv = r[base + i] + beta * (p[base + i] - om * v[base + i]);
+    p[base + i] = pv;
+    b0[base + nat2rb(i, nc, nx)] = (float)pv;
   }
-  __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    // deferred: rho_old updated by k_bicg_s after alpha is known
-    sc[SC_RHO] = rho;
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_RHO] = rho;
 }
 
-// alpha = rho / (rh, v); s = r - alpha v
-__global__ void k_bicg_s(int S, long n, int nblk, const double* part, double* scal, const double* r, const double* v,
-                         double* sv, const int* act) {
+// out = K x (x: fp32 red-black preconditioned vector, exact in fp64), with the
+// fused partial dots: mode 0 q0 = (d0, out); mode 1 q0 = (out, d0), q1 = (out, out)
+template <int mode>
+__global__ void __launch_bounds__(kBT, 2) k_apply_dot(int S, int nx, int ny, const double* __restrict__ sgt,
+                                                      const double* __restrict__ sgs, const float* __restrict__ xin,
+                                                      double* __restrict__ out, const double* __restrict__ d0,
+                                                      double* __restrict__ part, const int* __restrict__ act) {
+  const int s = blockIdx.y;
+  if (!act[s]) return;
+  const long nc = (long)nx * ny;
+  const float* xs = xin + s * nc * NB;
+  double a0 = 0.0, a1 = 0.0;
+  for (long c = (long)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (long)gridDim.x * blockDim.x) {
+    const int iy = (int)(c / nx), ix = (int)(c - (long)iy * nx);
+    const long own = rbidx(nx, ix, iy);
+    double acc[NB], xl[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      acc[r] = 0.0;
+      xl[r] = (double)xs[r * nc + own];
+    }
+    const long fi = (long)s * nc + c;
+    fine_block_mv(sgt[fi], sgt[fi] - sgs[fi], xl, acc);
+    face_terms_rb(0, xs, nx, ny, ix, iy, acc);
+    double* yo = out + (long)s * nc * NB + c;
+    const double* dd = d0 + (long)s * nc * NB + c;
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      yo[r * nc] = acc[r];
+      const double dv = dd[r * nc];
+      if (mode == 0) {
+        a0 = fma(dv, acc[r], a0);
+      } else {
+        a0 = fma(acc[r], dv, a0);
+        a1 = fma(acc[r], acc[r], a1);
+      }
+    }
+  }
+  block_parts(a0, a1, mode == 0 ? 1 : 2, part, s);
+}
+
+// alpha = rho / (rh, v); s = r - alpha v; b0 = fp32 rb(s)
+__global__ void __launch_bounds__(kBT) k_bicg_s(int S, unsigned n, unsigned nc, unsigned nx, int nblk,
+                                                const double* part, double* scal, const double* r, const double* v,
+                                                double* sv, float* b0, const int* act) {
   const int s = blockIdx.y;
   if (!act[s]) return;
   double* sc = scal + s * 16;
-  const double rhv = sum_parts(part, s, nblk, 0);
+  double rhv;
+  reduce_parts(part, s, nblk, 1, &rhv);
   const double alpha = sc[SC_RHO] / rhv;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-    const long g = (long)s * n + i;
-    sv[g] = r[g] - alpha * v[g];
+  const long base = (long)s * n;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double x = r[base + i] - alpha * v[base + i];
+    sv[base + i] = x;
+    b0[base + nat2rb(i, nc, nx)] = (float)x;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_RHV] = alpha;
 }
 
-// omega = (t,s)/(t,t); x += alpha ph + omega sh; r = s - omega t
-__global__ void k_bicg_x(int S, long n, int nblk, const double* part, double* scal, double* x, const double* ph,
-                         const double* sh, double* r, const double* sv, const double* t, const int* act) {
+// omega = (t,s)/(t,t); x += alpha ph + omega sh; r = s - omega t;
+// fused partials q0 = (r, r), q1 = (rh, r)
+__global__ void __launch_bounds__(kBT) k_bicg_x(int S, unsigned n, unsigned nc, unsigned nx, int nblk,
+                                                const double* part, double* scal, double* x, const float* ph,
+                                                const float* sh, double* r, const double* sv, const double* t,
+                                                const double* rh, double* part2, const int* act) {
   const int s = blockIdx.y;
   if (!act[s]) return;
   double* sc = scal + s * 16;
-  const double ts = sum_parts(part, s, nblk, 0), tt = sum_parts(part, s, nblk, 1);
+  double q[2];
+  reduce_parts(part, s, nblk, 2, q);
   const double alpha = sc[SC_RHV];
-  const double omega = tt > 0.0 ? ts / tt : 0.0;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-    const long g = (long)s * n + i;
-    x[g] += alpha * ph[g] + omega * sh[g];
-    r[g] = sv[g] - omega * t[g];
+  const double omega = q[1] > 0.0 ? q[0] / q[1] : 0.0;
+  const long base = (long)s * n;
+  double a0 = 0.0, a1 = 0.0;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned k = nat2rb(i, nc, nx);
+    x[base + i] += alpha * (double)ph[base + k] + omega * (double)sh[base + k];
+    const double rv = sv[base + i] - omega * t[base + i];
+    r[base + i] = rv;
+    a0 = fma(rv, rv, a0);
+    a1 = fma(rh[base + i], rv, a1);
   }
+  block_parts(a0, a1, 2, part2, s);
   if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_TS] = omega;
 }
 
-// scalar bookkeeping + convergence: rnorm2 = (r, r)
+// scalar bookkeeping + convergence: rnorm2 = (r, r), next rho = (rh, r)
 __global__ void k_bicg_check(int S, int nblk, const double* part, double* scal, int* act, double tol2, int maxit,
                              int* nact) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= S) return;
+  const int s = blockIdx.x;
   if (!act[s]) return;
   double* sc = scal + s * 16;
-  const double rn = sum_parts(part, s, nblk, 0);
+  double q[2];
+  reduce_parts(part, s, nblk, 2, q);
+  if (threadIdx.x != 0) return;
+  const double rn = q[0];
   sc[SC_RNORM2] = rn;
+  sc[SC_RHO_NEW] = q[1];
   sc[SC_RHO_OLD] = sc[SC_RHO];
   sc[SC_ALPHA] = sc[SC_RHV];
   sc[SC_OMEGA] = sc[SC_TS];
@@ -818,8 +1034,6 @@ inline int nblocks(long n, int bs = 256) { return (int)((n + bs - 1) / bs); }
 }  // namespace
 
 // ----------------------------------------------------------------------------
-
-static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cudaStream_t st);
 
 void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   auto* d = static_cast<Dsa2D*>(ctx->dsa->impl2d);
@@ -925,8 +1139,14 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
         for (int c = 0; c < 4; ++c) Ph[(px + 2 * py) * 16 + 4 * r + c] = P12[px + 2 * py][(size_t)r * NB + c];
     }
   d->P.upload(Ph.data(), Ph.size());
+  RTE_CUDA(cudaMemcpyToSymbol(c_P, Ph.data(), sizeof(double) * 64));
 
-  // levels
+  // levels; Kc tracks the cell-independent part of each level's diagonal
+  // block (the sigma-dependent part only touches the rho-rho, Jx-Jx and
+  // Jy-Jy field blocks), whose field-coupling blocks B1, B2, C1, C2 the
+  // coarse smoother takes from constant memory
+  std::vector<double> cpl((size_t)kMaxLevels * 4 * 16, 0.0);
+  Mat Kc = Dc;
   d->L.clear();
   d->L.reserve(16);
   int nx = ctx->nx, ny = ctx->ny;
@@ -940,11 +1160,19 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
     lv.nbr_h.resize(4 * NB2);
     for (int k = 0; k < 4; ++k) std::copy(nbr[k].begin(), nbr[k].end(), lv.nbr_h.begin() + k * NB2);
     lv.nbr.upload(lv.nbr_h.data(), lv.nbr_h.size());
-    if (!d->L.empty() && &lv != &d->L.front()) {
+    const size_t li = d->L.size() - 1;
+    if (li > 0) {
       lv.D.alloc((size_t)S * lv.nc * NB2);
-      lv.Dinv.alloc((size_t)S * lv.nc * NB2);
+      lv.fac.alloc((size_t)S * lv.nc * 48);
+      lv.x.alloc((size_t)S * lv.nc * NB);
     }
-    lv.x.alloc((size_t)S * lv.nc * NB);
+    if (li < (size_t)kMaxLevels) {
+      const int fb[4][2] = {{0, 1}, {0, 2}, {1, 0}, {2, 0}};
+      for (int m = 0; m < 4; ++m)
+        for (int i = 0; i < 4; ++i)
+          for (int k = 0; k < 4; ++k)
+            cpl[(li * 4 + m) * 16 + 4 * i + k] = Kc[(size_t)(4 * fb[m][0] + i) * NB + 4 * fb[m][1] + k];
+    }
     lv.b.alloc((size_t)S * lv.nc * NB);
     lv.r.alloc((size_t)S * lv.nc * NB);
     const bool can = nx % 2 == 0 && ny % 2 == 0 && lv.nc > kMaxCoarseCells;
@@ -974,12 +1202,18 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
     add(Din, galerkin(nbr[2], P01, P00));  // (x,1)->(x,0) south
     add(Din, galerkin(nbr[2], P11, P10));
     dint_all.insert(dint_all.end(), Din.begin(), Din.end());
+    {
+      Mat Kn = Din;
+      for (int q = 0; q < 4; ++q) add(Kn, galerkin(Kc, P12[q], P12[q]));
+      Kc = Kn;
+    }
     nbr = {W, E, Sb, Nb};
     nx /= 2;
     ny /= 2;
   }
   d->Dint.upload(dint_all.data(), dint_all.size());
   RTE_REQUIRE(d->L.size() <= (size_t)kMaxLevels, RTE_ERR_UNSUPPORTED, "dsa: too many multigrid levels");
+  RTE_CUDA(cudaMemcpyToSymbol(c_cpl, cpl.data(), sizeof(double) * cpl.size()));
   {
     std::vector<double> cf((size_t)kMaxLevels * 4 * 5 * 4, 0.0);
     for (size_t l = 0; l < d->L.size(); ++l)
@@ -1011,15 +1245,19 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
       }
     RTE_CUDA(cudaMemcpyToSymbol(c_face, cf.data(), sizeof(double) * cf.size()));
   }
-  // coarse diagonal blocks (Galerkin) and their inverses; level 0 is matrix-free
+  // coarse diagonal blocks (Galerkin, fp64, natural order) -> Schur factors
+  // (fp32, red-black order); level 0 is matrix-free
   const Level& l0 = d->L[0];
+  DBuf<unsigned long long> ferr;
+  ferr.alloc(1);
+  RTE_CUDA(cudaMemsetAsync(ferr.p, 0, sizeof(unsigned long long), st));
   for (size_t l = 1; l < d->L.size(); ++l) {
     Level& lv = d->L[l];
     const Level& f = d->L[l - 1];
     k_galerkin_diag<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, f.nx, f.ny, l == 1 ? nullptr : f.D.p, d->sgt,
                                                                    d->sgs, d->P.p, d->Dint.p + (l - 1) * NB2, lv.D.p);
     RTE_CUDA(cudaGetLastError());
-    k_inv12<<<nblocks((long)S * lv.nc, 64), 64, 0, st>>>((long)S * lv.nc, lv.D.p, lv.Dinv.p);
+    k_coarse_factor<<<nblocks((long)S * lv.nc, 64), 64, 0, st>>>(S, lv.nx, lv.ny, (int)l, lv.D.p, lv.fac.p, ferr.p);
     RTE_CUDA(cudaGetLastError());
   }
   if (d->L.size() == 1 && l0.nc <= kMaxCoarseCells) {
@@ -1042,48 +1280,69 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
     RTE_CUDA(cudaGetLastError());
     RTE_CUDA(cudaStreamSynchronize(st));
   }
-  // fp32 copies of the coarse blocks for the V-cycle (the V-cycle is only a
-  // preconditioner: the outer BiCGStab residuals stay fp64), fp64 released
-  for (size_t l = 1; l < d->L.size(); ++l) {
-    Level& lv = d->L[l];
-    const long nb = (long)S * lv.nc * NB2;
-    lv.Df.alloc(nb);
-    lv.Dinvf.alloc(nb);
-    k_to_f32<<<nblocks(nb), 256, 0, st>>>(S, lv.nc, lv.D.p, lv.Df.p);
-    k_to_f32<<<nblocks(nb), 256, 0, st>>>(S, lv.nc, lv.Dinv.p, lv.Dinvf.p);
-    RTE_CUDA(cudaGetLastError());
+  {
+    unsigned long long eb = 0;
+    RTE_CUDA(cudaMemcpyAsync(&eb, ferr.p, sizeof(eb), cudaMemcpyDeviceToHost, st));
+    RTE_CUDA(cudaStreamSynchronize(st));
+    double e;
+    std::memcpy(&e, &eb, sizeof(e));
+    RTE_REQUIRE(e <= 1e-12, RTE_ERR_RUNTIME, "dsa: coarse diagonal blocks lost their field-coupling structure");
   }
-  RTE_CUDA(cudaStreamSynchronize(st));
-  for (size_t l = 1; l < d->L.size(); ++l) {
-    d->L[l].D.release();
-    d->L[l].Dinv.release();
+  {
+    // verify the stored factors against the fp64 blocks: max |D^-1 D - I|
+    // (fp32 factors: ~1e-7 for well-conditioned blocks)
+    for (size_t l = 1; l < d->L.size(); ++l) {
+      Level& lv = d->L[l];
+      RTE_CUDA(cudaMemsetAsync(ferr.p, 0, sizeof(unsigned long long), st));
+      k_check_factor<<<nblocks((long)S * lv.nc, 64), 64, 0, st>>>(S, lv.nx, lv.ny, (int)l, lv.D.p, lv.fac.p, ferr.p);
+      unsigned long long eb = 0;
+      RTE_CUDA(cudaMemcpyAsync(&eb, ferr.p, sizeof(eb), cudaMemcpyDeviceToHost, st));
+      RTE_CUDA(cudaStreamSynchronize(st));
+      double e;
+      std::memcpy(&e, &eb, sizeof(e));
+      if (std::getenv("RTE_DSA_TRACE"))
+        std::fprintf(stderr, "[dsa2d] level %zu (%dx%d): factor check max|D^-1 D - I| = %.3e\n", l, lv.nx, lv.ny, e);
+      RTE_REQUIRE(e <= 1e-3, RTE_ERR_RUNTIME, "dsa: coarse cell factorisation check failed");
+    }
   }
+  for (size_t l = 0; l < d->L.size(); ++l) d->L[l].D.release();
+  // fine-level coefficients for the V-cycle (fp32, red-black order)
+  d->sig.alloc((size_t)S * l0.nc);
+  k_sig_rb<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->sig.p);
+  RTE_CUDA(cudaGetLastError());
   // Krylov workspace
   const size_t nv = (size_t)S * l0.nc * NB;
-  for (DBuf<double>* b : {&d->r, &d->rh, &d->p, &d->v, &d->s, &d->t, &d->x, &d->ph, &d->sh, &d->rhs}) b->alloc(nv);
+  RTE_REQUIRE(l0.nc * NB < (1L << 31), RTE_ERR_UNSUPPORTED, "dsa: more than 2^31 unknowns per sample");
+  for (DBuf<double>* b : {&d->r, &d->p, &d->v, &d->s, &d->t, &d->x, &d->rhs}) b->alloc(nv);
+  d->xa.alloc(nv);
+  d->xb.alloc(nv);
   d->scal.alloc((size_t)S * 16);
   d->nblk = (int)std::min<long>(512, std::max<long>(16, (long)l0.nc * NB / 4096));
   d->part.alloc((size_t)S * d->nblk * 4);
+  d->part2.alloc((size_t)S * d->nblk * 4);
   d->act.alloc(S);
   d->nact.alloc(1);
   RTE_CUDA(cudaStreamSynchronize(st));
 }
 
-static void smooth(Dsa2D* d, int l, const float* b, float* x, const int* act, bool zero_init, bool reverse,
-                   cudaStream_t st) {
+// one colour half-sweep on level l
+static void gs(Dsa2D* d, int l, int color, const float* b, float* x, const int* act, bool zero_nbr, float* delta,
+               bool old_zero, const float* xc, cudaStream_t st) {
   Level& lv = d->L[l];
-  const int S = d->S;
-  const long half = (lv.nc + 1) / 2;
-  const int c0 = reverse ? 1 : 0;
-  ProfScope ps(l == 0 ? d->ctx : nullptr, RTE_PROF_DSA_SMOOTH0, st, 2);
+  GsArgs a{d->S, lv.nx, lv.ny, l, color, x, b, l == 0 ? d->sig.p : nullptr, l == 0 ? nullptr : lv.fac.p,
+           act, zero_nbr ? 1 : 0, delta, old_zero ? 1 : 0, xc};
+  const long n = (long)d->S * lv.ny * ((lv.nx + 1) / 2);
+  ProfScope ps(l == 0 ? d->ctx : nullptr, RTE_PROF_DSA_SMOOTH0, st, 1);
   ++d->nlaunch;
-  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, c0, lv.Dinvf.p, d->sgt, d->sgs, l, x, b,
-                                                      act, zero_init ? 1 : 0);
-  ++d->nlaunch;
-  k_gs<<<nblocks((long)S * half, 128), 128, 0, st>>>(S, lv.nx, lv.ny, 1 - c0, lv.Dinvf.p, d->sgt, d->sgs, l, x,
-                                                      b, act, 0);
+  const int g = nblocks(n, 128);
+  if (l == 0)
+    xc ? k_gs_rb<true, true><<<g, 128, 0, st>>>(a) : k_gs_rb<true, false><<<g, 128, 0, st>>>(a);
+  else
+    xc ? k_gs_rb<false, true><<<g, 128, 0, st>>>(a) : k_gs_rb<false, false><<<g, 128, 0, st>>>(a);
 }
 
+// V-cycle on level l: b, x in the level's red-black layout; x need not be
+// initialised (the first half-sweep treats it as zero)
 static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cudaStream_t st) {
   Level& lv = d->L[l];
   const int S = d->S;
@@ -1094,50 +1353,32 @@ static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cu
       k_dense_apply<<<S, 256, 0, st>>>(d->ncoarse, d->coarse_inv.p, b, x, act);
       RTE_CUDA(cudaGetLastError());
     } else {
-      smooth(d, l, b, x, act, true, false, st);
-      for (int k = 1; k < 20; ++k) smooth(d, l, b, x, act, false, k % 2 == 1, st);
+      for (int k = 0; k < 20; ++k) {
+        gs(d, l, 0, b, x, act, k == 0, nullptr, false, nullptr, st);
+        gs(d, l, 1, b, x, act, false, nullptr, false, nullptr, st);
+      }
     }
     return;
   }
   const int nu = l == 0 ? d->nu : d->nu_coarse;
-  for (int k = 0; k < nu; ++k) smooth(d, l, b, x, act, k == 0, false, st);
-  ++d->nlaunch;
-  k_apply<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, lv.Df.p, d->sgt, d->sgs, l, x, b,
-                                                          lv.r.p, 1, act);
+  // pre-smoothing: colour 0 then colour 1; the last colour-1 update is kept
+  // as delta so the residual is -C delta on colour 0 and 0 on colour 1
+  for (int k = 0; k < nu; ++k) {
+    gs(d, l, 0, b, x, act, k == 0, nullptr, false, nullptr, st);
+    gs(d, l, 1, b, x, act, false, k == nu - 1 ? lv.r.p : nullptr, k == 0, nullptr, st);
+  }
   Level& lc = d->L[l + 1];
   ++d->nlaunch;
-  k_restrict<<<nblocks((long)S * lc.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, d->P.p, lv.r.p, lc.b.p, act);
+  k_restrict_delta<<<nblocks((long)S * lc.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, l, lv.r.p, lc.b.p, act);
+  RTE_CUDA(cudaGetLastError());
   vcycle(d, l + 1, lc.b.p, lc.x.p, act, st);
-  ++d->nlaunch;
-  k_prolong_add<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, d->P.p, lc.x.p, x, act);
-  for (int k = 0; k < nu; ++k) smooth(d, l, b, x, act, false, true, st);
-  RTE_CUDA(cudaGetLastError());
-}
-
-// one V-cycle as the preconditioner: fp64 in -> fp32 V-cycle -> fp64 out
-static void precond(Dsa2D* d, const double* in, double* out, cudaStream_t st) {
-  Level& l0 = d->L[0];
-  const long n = (long)d->S * l0.nc * NB;
-  ++d->nlaunch;
-  k_cvt<double, float><<<nblocks(n), 256, 0, st>>>(n, in, l0.b.p, d->act.p, l0.nc * NB);
-  vcycle(d, 0, l0.b.p, l0.x.p, d->act.p, st);
-  ++d->nlaunch;
-  k_cvt<float, double><<<nblocks(n), 256, 0, st>>>(n, l0.x.p, out, d->act.p, l0.nc * NB);
-  RTE_CUDA(cudaGetLastError());
-}
-
-static void dots(Dsa2D* d, long n, std::initializer_list<std::pair<const double*, const double*>> pairs,
-                 cudaStream_t st) {
-  DotArgs a{};
-  int q = 0;
-  for (auto& pr : pairs) {
-    a.a[q] = pr.first;
-    a.b[q] = pr.second;
-    ++q;
+  // post-smoothing: colour 1 then colour 0; the first colour-1 half-sweep sees
+  // its colour-0 neighbours with the coarse correction prolonged on the fly,
+  // and the colour-0 half-sweep that follows overwrites them
+  for (int k = 0; k < nu; ++k) {
+    gs(d, l, 1, b, x, act, false, nullptr, false, k == 0 ? lc.x.p : nullptr, st);
+    gs(d, l, 0, b, x, act, false, nullptr, false, nullptr, st);
   }
-  a.nq = q;
-  ++d->nlaunch;
-  k_dots<<<dim3(d->nblk, d->S), 256, 0, st>>>(d->S, n, a, d->part.p, d->act.p);
   RTE_CUDA(cudaGetLastError());
 }
 
@@ -1147,60 +1388,60 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   const int S = d->S;
   Level& l0 = d->L[0];
   const long n = l0.nc * NB;
+  const unsigned un = (unsigned)n, unc = (unsigned)l0.nc, unx = (unsigned)l0.nx;
   const dim3 vgrid(d->nblk, S);
-  // b -> l0.b ; x = 0 ; r = b ; rh = r
+  // b -> rhs (also the shadow residual) ; x = p = v = 0 ; r = b
   ++d->nlaunch;
   k_pack_rhs<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, rhs, ctx->ms.p, apply_ms, d->rhs.p, kind);
   RTE_CUDA(cudaMemsetAsync(d->x.p, 0, sizeof(double) * S * n, st));
   RTE_CUDA(cudaMemsetAsync(d->p.p, 0, sizeof(double) * S * n, st));
   RTE_CUDA(cudaMemsetAsync(d->v.p, 0, sizeof(double) * S * n, st));
   RTE_CUDA(cudaMemcpyAsync(d->r.p, d->rhs.p, sizeof(double) * S * n, cudaMemcpyDeviceToDevice, st));
-  RTE_CUDA(cudaMemcpyAsync(d->rh.p, d->rhs.p, sizeof(double) * S * n, cudaMemcpyDeviceToDevice, st));
-  // initial ||b||^2 with every sample counted (mask applied inside init)
   {
     DotArgs a{};
     a.a[0] = d->rhs.p;
     a.b[0] = d->rhs.p;
     a.nq = 1;
     ++d->nlaunch;
-    k_dots<<<vgrid, 256, 0, st>>>(S, n, a, d->part.p, nullptr);
+    k_dots<<<vgrid, kBT, 0, st>>>(S, n, a, d->part.p, nullptr);
   }
-  std::vector<int> mask_h;
   ++d->nlaunch;
   k_bicg_init<<<(S + 127) / 128, 128, 0, st>>>(S, d->nblk, d->part.p, d->scal.p, d->act.p, nullptr);
   RTE_CUDA(cudaGetLastError());
-  if (kind) {
-    // samples not selected for DSA: b was packed as zero -> inactive after init
-  }
   const double tol2 = d->tol * d->tol;
   int* nact_h = nullptr;
   RTE_CUDA(cudaMallocHost(&nact_h, sizeof(int)));
   int it = 0;
+  float* b0 = l0.b.p;
+  static const bool trace = std::getenv("RTE_DSA_TRACE") != nullptr;
   for (; it < d->maxit; ++it) {
-    dots(d, n, {{d->rh.p, d->r.p}}, st);
     ++d->nlaunch;
-    k_bicg_p<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->r.p, d->p.p, d->v.p, d->act.p);
-    precond(d, d->p.p, d->ph.p, st);
+    k_bicg_p<<<vgrid, kBT, 0, st>>>(S, un, unc, unx, d->scal.p, d->r.p, d->p.p, d->v.p, b0, d->act.p);
+    vcycle(d, 0, b0, d->xa.p, d->act.p, st);
     ++d->nlaunch;
-    k_apply<double><<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, nullptr, d->sgt, d->sgs, 0, d->ph.p,
-                                                            nullptr, d->v.p, 0, d->act.p);
-    dots(d, n, {{d->rh.p, d->v.p}}, st);
+    k_apply_dot<0><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xa.p, d->v.p, d->rhs.p, d->part.p,
+                                          d->act.p);
     ++d->nlaunch;
-    k_bicg_s<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->r.p, d->v.p, d->s.p, d->act.p);
-    precond(d, d->s.p, d->sh.p, st);
+    k_bicg_s<<<vgrid, kBT, 0, st>>>(S, un, unc, unx, d->nblk, d->part.p, d->scal.p, d->r.p, d->v.p, d->s.p, b0,
+                                    d->act.p);
+    vcycle(d, 0, b0, d->xb.p, d->act.p, st);
     ++d->nlaunch;
-    k_apply<double><<<nblocks((long)S * l0.nc, 128), 128, 0, st>>>(S, l0.nx, l0.ny, nullptr, d->sgt, d->sgs, 0, d->sh.p,
-                                                            nullptr, d->t.p, 0, d->act.p);
-    dots(d, n, {{d->t.p, d->s.p}, {d->t.p, d->t.p}}, st);
+    k_apply_dot<1><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xb.p, d->t.p, d->s.p, d->part.p,
+                                          d->act.p);
     ++d->nlaunch;
-    k_bicg_x<<<vgrid, 256, 0, st>>>(S, n, d->nblk, d->part.p, d->scal.p, d->x.p, d->ph.p, d->sh.p, d->r.p, d->s.p,
-                                    d->t.p, d->act.p);
-    dots(d, n, {{d->r.p, d->r.p}}, st);
+    k_bicg_x<<<vgrid, kBT, 0, st>>>(S, un, unc, unx, d->nblk, d->part.p, d->scal.p, d->x.p, d->xa.p, d->xb.p,
+                                    d->r.p, d->s.p, d->t.p, d->rhs.p, d->part2.p, d->act.p);
     RTE_CUDA(cudaMemsetAsync(d->nact.p, 0, sizeof(int), st));
     ++d->nlaunch;
-    k_bicg_check<<<(S + 127) / 128, 128, 0, st>>>(S, d->nblk, d->part.p, d->scal.p, d->act.p, tol2, d->maxit,
-                                                  d->nact.p);
+    k_bicg_check<<<S, 32, 0, st>>>(S, d->nblk, d->part2.p, d->scal.p, d->act.p, tol2, d->maxit, d->nact.p);
     RTE_CUDA(cudaGetLastError());
+    if (trace) {
+      double sc[16];
+      RTE_CUDA(cudaMemcpyAsync(sc, d->scal.p, sizeof(sc), cudaMemcpyDeviceToHost, st));
+      RTE_CUDA(cudaStreamSynchronize(st));
+      std::fprintf(stderr, "[dsa2d] it %d rel residual %.3e alpha %.3e omega %.3e\n", it,
+                   std::sqrt(sc[SC_RNORM2] / sc[SC_BNORM2]), sc[SC_ALPHA], sc[SC_OMEGA]);
+    }
     if ((it & 3) == 3) {
       RTE_CUDA(cudaMemcpyAsync(nact_h, d->nact.p, sizeof(int), cudaMemcpyDeviceToHost, st));
       RTE_CUDA(cudaStreamSynchronize(st));
@@ -1215,7 +1456,6 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   ++d->nlaunch;
   k_unpack<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, d->x.p, out, kind);
   RTE_CUDA(cudaGetLastError());
-  (void)mask_h;
 }
 
 void dsa2d_destroy(void* p) { delete static_cast<Dsa2D*>(p); }
