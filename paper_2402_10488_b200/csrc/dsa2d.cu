@@ -160,20 +160,44 @@ __constant__ double c_m2x3, c_m2y3;
 // faces (j = Jx, o = Jy) and the mirrored pattern for y faces, at all levels
 // (Galerkin preserves it since sum_s E_s^T E_s = I).  5 matrices of 2x2.
 __constant__ double c_face[kMaxLevels][4][5][4];
+// fp32 mirrors for the V-cycle arithmetic (VR = float)
+__constant__ float c_dconst_f[NB2];
+__constant__ float c_m2_f[2];
+__constant__ float c_face_f[kMaxLevels][4][5][4];
 
-__device__ __forceinline__ void lift_mv(const double* M, const double* v, double* y, int axis) {
+#ifdef RTE_DSA_VCYCLE_FP64
+using VR = double;  // V-cycle arithmetic type
+#else
+using VR = float;
+#endif
+
+template <typename R> __device__ __forceinline__ const R* face_c(int lev, int dir, int m);
+template <> __device__ __forceinline__ const double* face_c<double>(int lev, int dir, int m) { return c_face[lev][dir][m]; }
+template <> __device__ __forceinline__ const float* face_c<float>(int lev, int dir, int m) { return c_face_f[lev][dir][m]; }
+template <typename R> __device__ __forceinline__ R dconst(int i);
+template <> __device__ __forceinline__ double dconst<double>(int i) { return c_dconst[i]; }
+template <> __device__ __forceinline__ float dconst<float>(int i) { return c_dconst_f[i]; }
+template <typename R> __device__ __forceinline__ R m2x3();
+template <typename R> __device__ __forceinline__ R m2y3();
+template <> __device__ __forceinline__ double m2x3<double>() { return c_m2x3; }
+template <> __device__ __forceinline__ double m2y3<double>() { return c_m2y3; }
+template <> __device__ __forceinline__ float m2x3<float>() { return c_m2_f[0]; }
+template <> __device__ __forceinline__ float m2y3<float>() { return c_m2_f[1]; }
+
+template <typename R>
+__device__ __forceinline__ void lift_mv(const R* M, const R* v, R* y, int axis) {
   // y += L_axis(M) v on one 4-mode field
   if (axis == 0) {
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
-      const double v0 = v[2 * b], v1 = v[2 * b + 1];
+      const R v0 = v[2 * b], v1 = v[2 * b + 1];
       y[2 * b] = fma(M[0], v0, fma(M[1], v1, y[2 * b]));
       y[2 * b + 1] = fma(M[2], v0, fma(M[3], v1, y[2 * b + 1]));
     }
   } else {
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
-      const double v0 = v[a], v1 = v[a + 2];
+      const R v0 = v[a], v1 = v[a + 2];
       y[a] = fma(M[0], v0, fma(M[1], v1, y[a]));
       y[a + 2] = fma(M[2], v0, fma(M[3], v1, y[a + 2]));
     }
@@ -182,21 +206,22 @@ __device__ __forceinline__ void lift_mv(const double* M, const double* v, double
 
 // Vectors are component-major per sample (SoA): x[s][r][cell], so a warp's
 // loads of one component of consecutive cells coalesce.
-__device__ __forceinline__ void face_lift(int lev, int dir, const double* v, double* y) {
+template <typename R>
+__device__ __forceinline__ void face_lift(int lev, int dir, const R* v, R* y) {
   const int axis = dir >> 1;
   const int j = axis == 0 ? 4 : 8, o = axis == 0 ? 8 : 4;
-  lift_mv(c_face[lev][dir][0], v, y, axis);
-  lift_mv(c_face[lev][dir][1], v + j, y, axis);
-  lift_mv(c_face[lev][dir][2], v, y + j, axis);
-  lift_mv(c_face[lev][dir][3], v + j, y + j, axis);
-  lift_mv(c_face[lev][dir][4], v + o, y + o, axis);
+  lift_mv(face_c<R>(lev, dir, 0), v, y, axis);
+  lift_mv(face_c<R>(lev, dir, 1), v + j, y, axis);
+  lift_mv(face_c<R>(lev, dir, 2), v, y + j, axis);
+  lift_mv(face_c<R>(lev, dir, 3), v + j, y + j, axis);
+  lift_mv(face_c<R>(lev, dir, 4), v + o, y + o, axis);
 }
 
-template <typename T>
-__device__ __forceinline__ void face_mv(int lev, int dir, const T* __restrict__ xs, long nc, long cn, double* y) {
-  double v[NB];
+template <typename R, typename T>
+__device__ __forceinline__ void face_mv(int lev, int dir, const T* __restrict__ xs, long nc, long cn, R* y) {
+  R v[NB];
 #pragma unroll
-  for (int r = 0; r < NB; ++r) v[r] = (double)xs[r * nc + cn];
+  for (int r = 0; r < NB; ++r) v[r] = (R)xs[r * nc + cn];
   face_lift(lev, dir, v, y);
 }
 
@@ -231,30 +256,31 @@ __device__ __forceinline__ void fine_block_mv(double sgt, double sga, const doub
 // partner, so the Schur complement S = A - B1 T1^{-1} C1 - B2 T2^{-1} C2 is
 // diagonal: ~40 flops per cell (verified against the generic 12x12 inverse
 // at setup, see check_fine_structure).
-__device__ __forceinline__ void fine_block_solve(double sgt, double sga, const double* r, double* x) {
-  const double ax = c_m2x3 * sgt, ay = c_m2y3 * sgt;
+template <typename R>
+__device__ __forceinline__ void fine_block_solve(R sgt, R sga, const R* r, R* x) {
+  const R ax = m2x3<R>() * sgt, ay = m2y3<R>() * sgt;
   // partners: x-lift pairs (0,1),(2,3) ; y-lift pairs (0,2),(1,3)
   const int px[4] = {1, 0, 3, 2}, py[4] = {2, 3, 0, 1};
-  double it1[4], it2[4];
+  R it1[4], it2[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    it1[k] = 1.0 / (c_dconst[(4 + k) * NB + 4 + k] + ax);
-    it2[k] = 1.0 / (c_dconst[(8 + k) * NB + 8 + k] + ay);
+    it1[k] = R(1) / (dconst<R>((4 + k) * NB + 4 + k) + ax);
+    it2[k] = R(1) / (dconst<R>((8 + k) * NB + 8 + k) + ay);
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int kx = px[i], ky = py[i];
-    const double bx = c_dconst[i * NB + 4 + kx], cx = c_dconst[(4 + kx) * NB + i];
-    const double by = c_dconst[i * NB + 8 + ky], cy = c_dconst[(8 + ky) * NB + i];
-    const double sii = c_dconst[i * NB + i] + sga - bx * it1[kx] * cx - by * it2[ky] * cy;
-    const double rhs = r[i] - bx * it1[kx] * r[4 + kx] - by * it2[ky] * r[8 + ky];
+    const R bx = dconst<R>(i * NB + 4 + kx), cx = dconst<R>((4 + kx) * NB + i);
+    const R by = dconst<R>(i * NB + 8 + ky), cy = dconst<R>((8 + ky) * NB + i);
+    const R sii = dconst<R>(i * NB + i) + sga - bx * it1[kx] * cx - by * it2[ky] * cy;
+    const R rhs = r[i] - bx * it1[kx] * r[4 + kx] - by * it2[ky] * r[8 + ky];
     x[i] = rhs / sii;
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int ix = px[k], iy = py[k];
-    x[4 + k] = (r[4 + k] - c_dconst[(4 + k) * NB + ix] * x[ix]) * it1[k];
-    x[8 + k] = (r[8 + k] - c_dconst[(8 + k) * NB + iy] * x[iy]) * it2[k];
+    x[4 + k] = (r[4 + k] - dconst<R>((4 + k) * NB + ix) * x[ix]) * it1[k];
+    x[8 + k] = (r[8 + k] - dconst<R>((8 + k) * NB + iy) * x[iy]) * it2[k];
   }
 }
 
@@ -333,11 +359,19 @@ __host__ __device__ __forceinline__ long rbidx(int nx, int ix, int iy) {
 
 __constant__ double c_P[4][16];               // prolongation E2 per sub-cell position: [4 * fine + coarse]
 __constant__ double c_cpl[kMaxLevels][4][16]; // per level: B1 (rho<-Jx), B2 (rho<-Jy), C1 (Jx<-rho), C2 (Jy<-rho)
+__constant__ float c_P_f[4][16];
+__constant__ float c_cpl_f[kMaxLevels][4][16];
+template <typename R> __device__ __forceinline__ const R* Pc(int pos);
+template <> __device__ __forceinline__ const double* Pc<double>(int pos) { return c_P[pos]; }
+template <> __device__ __forceinline__ const float* Pc<float>(int pos) { return c_P_f[pos]; }
+template <typename R> __device__ __forceinline__ const R* cplc(int lev, int m);
+template <> __device__ __forceinline__ const double* cplc<double>(int lev, int m) { return c_cpl[lev][m]; }
+template <> __device__ __forceinline__ const float* cplc<float>(int lev, int m) { return c_cpl_f[lev][m]; }
 
 // off-diagonal (face) contributions sum_nbr C_dir x_nbr, red-black storage
-template <typename T>
+template <typename R, typename T>
 __device__ __forceinline__ void face_terms_rb(int lev, const T* __restrict__ xs, int nx, int ny, int ix, int iy,
-                                              double* y) {
+                                              R* y) {
   const long nc = (long)nx * ny;
   if (ix > 0) face_mv(lev, 0, xs, nc, rbidx(nx, ix - 1, iy), y);
   if (ix < nx - 1) face_mv(lev, 1, xs, nc, rbidx(nx, ix + 1, iy), y);
@@ -347,21 +381,22 @@ __device__ __forceinline__ void face_terms_rb(int lev, const T* __restrict__ xs,
 
 // face term of neighbour (jx, jy) whose value is x_f + (P x_C): the coarse-grid
 // correction prolonged on the fly (the corrected fine vector is never stored)
+template <typename R>
 __device__ __forceinline__ void face_mv_prolong(int lev, int dir, const float* __restrict__ xs, long nc, int nx,
                                                 int jx, int jy, const float* __restrict__ xcs, long ncc, int cnx,
-                                                double* y) {
+                                                R* y) {
   const long cn = rbidx(nx, jx, jy);
   const long C = rbidx(cnx, jx >> 1, jy >> 1);
-  const double* E = c_P[(jx & 1) + 2 * (jy & 1)];
-  double v[NB];
+  const R* E = Pc<R>((jx & 1) + 2 * (jy & 1));
+  R v[NB];
 #pragma unroll
   for (int f = 0; f < 3; ++f) {
-    double xc[4];
+    R xc[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) xc[k] = (double)xcs[(4 * f + k) * ncc + C];
+    for (int k = 0; k < 4; ++k) xc[k] = (R)xcs[(4 * f + k) * ncc + C];
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
-      double acc = (double)xs[(4 * f + l) * nc + cn];
+      R acc = (R)xs[(4 * f + l) * nc + cn];
 #pragma unroll
       for (int k = 0; k < 4; ++k) acc = fma(E[4 * l + k], xc[k], acc);
       v[4 * f + l] = acc;
@@ -372,8 +407,8 @@ __device__ __forceinline__ void face_mv_prolong(int lev, int dir, const float* _
 
 // x = D_C^{-1} r for a coarse cell from its Schur factors (f: element stride nc)
 //   D_C = [[A, B1, B2], [C1, T1, 0], [C2, 0, T2]],  S = A - B1 T1^-1 C1 - B2 T2^-1 C2
-__device__ __forceinline__ void coarse_block_solve(int lev, const FacT* __restrict__ f, long nc, const double* r,
-                                                   double* x) {
+template <typename R>
+__device__ __forceinline__ void coarse_block_solve(int lev, const FacT* __restrict__ f, long nc, const R* r, R* x) {
   FacT t1[16], t2[16], si[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
@@ -381,40 +416,40 @@ __device__ __forceinline__ void coarse_block_solve(int lev, const FacT* __restri
     t2[e] = f[(16 + e) * nc];
     si[e] = f[(32 + e) * nc];
   }
-  const double* B1 = c_cpl[lev][0];
-  const double* B2 = c_cpl[lev][1];
-  const double* C1 = c_cpl[lev][2];
-  const double* C2 = c_cpl[lev][3];
-  double yx[4], yy[4], z[4];
+  const R* B1 = cplc<R>(lev, 0);
+  const R* B2 = cplc<R>(lev, 1);
+  const R* C1 = cplc<R>(lev, 2);
+  const R* C2 = cplc<R>(lev, 3);
+  R yx[4], yy[4], z[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    double ax = 0.0, ay = 0.0;
+    R ax = 0, ay = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      ax = fma((double)t1[4 * i + k], r[4 + k], ax);
-      ay = fma((double)t2[4 * i + k], r[8 + k], ay);
+      ax = fma((R)t1[4 * i + k], r[4 + k], ax);
+      ay = fma((R)t2[4 * i + k], r[8 + k], ay);
     }
     yx[i] = ax;
     yy[i] = ay;
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    double a = r[i];
+    R a = r[i];
 #pragma unroll
     for (int k = 0; k < 4; ++k) a -= B1[4 * i + k] * yx[k] + B2[4 * i + k] * yy[k];
     z[i] = a;
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    double a = 0.0;
+    R a = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) a = fma((double)si[4 * i + k], z[k], a);
+    for (int k = 0; k < 4; ++k) a = fma((R)si[4 * i + k], z[k], a);
     x[i] = a;
   }
-  double wx[4], wy[4];
+  R wx[4], wy[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    double a = r[4 + i], b = r[8 + i];
+    R a = r[4 + i], b = r[8 + i];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       a -= C1[4 * i + k] * x[k];
@@ -425,11 +460,11 @@ __device__ __forceinline__ void coarse_block_solve(int lev, const FacT* __restri
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    double a = 0.0, b = 0.0;
+    R a = 0, b = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      a = fma((double)t1[4 * i + k], wx[k], a);
-      b = fma((double)t2[4 * i + k], wy[k], b);
+      a = fma((R)t1[4 * i + k], wx[k], a);
+      b = fma((R)t2[4 * i + k], wy[k], b);
     }
     x[4 + i] = a;
     x[8 + i] = b;
@@ -597,9 +632,9 @@ __global__ void __launch_bounds__(128) k_gs_rb(GsArgs a) {
   const long nc = (long)a.nx * a.ny;
   const long own = (long)iy * a.nx + (a.color ? c0 : 0) + k;
   const float* xs = a.x + s * nc * NB;
-  double acc[NB];
+  VR acc[NB];
 #pragma unroll
-  for (int r = 0; r < NB; ++r) acc[r] = 0.0;
+  for (int r = 0; r < NB; ++r) acc[r] = 0;
   if (!a.zero_nbr) {
     if (PROLONG) {
       const int cnx = a.nx >> 1;
@@ -614,13 +649,13 @@ __global__ void __launch_bounds__(128) k_gs_rb(GsArgs a) {
     }
   }
   const float* bi = a.b + s * nc * NB + own;
-  double rr[NB];
+  VR rr[NB];
 #pragma unroll
-  for (int r = 0; r < NB; ++r) rr[r] = (double)bi[r * nc] - acc[r];
-  double out[NB];
+  for (int r = 0; r < NB; ++r) rr[r] = (VR)bi[r * nc] - acc[r];
+  VR out[NB];
   if (FINE) {
     const float2 sg = a.sig[s * nc + own];
-    fine_block_solve((double)sg.x, (double)sg.y, rr, out);
+    fine_block_solve<VR>((VR)sg.x, (VR)sg.y, rr, out);
   } else {
     coarse_block_solve(a.lev, a.fac + s * nc * 48 + own, nc, rr, out);
   }
@@ -630,7 +665,7 @@ __global__ void __launch_bounds__(128) k_gs_rb(GsArgs a) {
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       const float xn = (float)out[r];
-      dl[r * nc] = a.old_zero ? xn : (float)((double)xn - (double)xo[r * nc]);
+      dl[r * nc] = a.old_zero ? xn : xn - xo[r * nc];
       xo[r * nc] = xn;
     }
   } else {
@@ -653,21 +688,21 @@ __global__ void k_restrict_delta(int S, int fnx, int fny, int lev, const float* 
   if (act && !act[s]) return;
   const int cx = (int)(C % cnx), cy = (int)(C / cnx);
   const float* ds = delta + s * nf * NB;
-  double out[NB];
+  VR out[NB];
 #pragma unroll
-  for (int r = 0; r < NB; ++r) out[r] = 0.0;
+  for (int r = 0; r < NB; ++r) out[r] = 0;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {  // colour-0 children (0,0) and (1,1)
-    double y[NB];
+    VR y[NB];
 #pragma unroll
-    for (int r = 0; r < NB; ++r) y[r] = 0.0;
+    for (int r = 0; r < NB; ++r) y[r] = 0;
     face_terms_rb(lev, ds, fnx, fny, 2 * cx + q, 2 * cy + q, y);
-    const double* E = c_P[q ? 3 : 0];
+    const VR* E = Pc<VR>(q ? 3 : 0);
 #pragma unroll
     for (int f = 0; f < 3; ++f)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        double acc = out[4 * f + k];
+        VR acc = out[4 * f + k];
 #pragma unroll
         for (int l = 0; l < 4; ++l) acc = fma(-E[4 * l + k], y[4 * f + l], acc);
         out[4 * f + k] = acc;
@@ -1126,6 +1161,12 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   const double m2x3 = 3 * m2x, m2y3 = 3 * m2y;
   RTE_CUDA(cudaMemcpyToSymbol(c_m2x3, &m2x3, sizeof(double)));
   RTE_CUDA(cudaMemcpyToSymbol(c_m2y3, &m2y3, sizeof(double)));
+  {
+    std::vector<float> f(Dc.begin(), Dc.end());
+    RTE_CUDA(cudaMemcpyToSymbol(c_dconst_f, f.data(), sizeof(float) * NB2));
+    const float m2f[2] = {(float)m2x3, (float)m2y3};
+    RTE_CUDA(cudaMemcpyToSymbol(c_m2_f, m2f, sizeof(m2f)));
+  }
   d->sgt = ctx->mt.p;
   d->sgs = ctx->ms.p;
 
@@ -1140,6 +1181,10 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
     }
   d->P.upload(Ph.data(), Ph.size());
   RTE_CUDA(cudaMemcpyToSymbol(c_P, Ph.data(), sizeof(double) * 64));
+  {
+    std::vector<float> f(Ph.begin(), Ph.end());
+    RTE_CUDA(cudaMemcpyToSymbol(c_P_f, f.data(), sizeof(float) * 64));
+  }
 
   // levels; Kc tracks the cell-independent part of each level's diagonal
   // block (the sigma-dependent part only touches the rho-rho, Jx-Jx and
@@ -1215,6 +1260,10 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   RTE_REQUIRE(d->L.size() <= (size_t)kMaxLevels, RTE_ERR_UNSUPPORTED, "dsa: too many multigrid levels");
   RTE_CUDA(cudaMemcpyToSymbol(c_cpl, cpl.data(), sizeof(double) * cpl.size()));
   {
+    std::vector<float> f(cpl.begin(), cpl.end());
+    RTE_CUDA(cudaMemcpyToSymbol(c_cpl_f, f.data(), sizeof(float) * f.size()));
+  }
+  {
     std::vector<double> cf((size_t)kMaxLevels * 4 * 5 * 4, 0.0);
     for (size_t l = 0; l < d->L.size(); ++l)
       for (int dir = 0; dir < 4; ++dir) {
@@ -1244,6 +1293,8 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
         RTE_REQUIRE(err <= 1e-12 * mag, RTE_ERR_RUNTIME, "dsa: face coupling lost its lifted structure");
       }
     RTE_CUDA(cudaMemcpyToSymbol(c_face, cf.data(), sizeof(double) * cf.size()));
+    std::vector<float> f(cf.begin(), cf.end());
+    RTE_CUDA(cudaMemcpyToSymbol(c_face_f, f.data(), sizeof(float) * f.size()));
   }
   // coarse diagonal blocks (Galerkin, fp64, natural order) -> Schur factors
   // (fp32, red-black order); level 0 is matrix-free
