@@ -153,6 +153,20 @@ Mat galerkin(const Mat& A, const Mat& Pl, const Mat& Pr) {
 // ----------------------------------------------------------------------------
 // device kernels
 
+// ---- red-black storage order ------------------------------------------------
+// Cells of colour (ix + iy) & 1 == 0 come first in every row, then colour 1.
+__host__ __device__ __forceinline__ int rb_cnt0(int nx, int iy) { return (nx + 1 - (iy & 1)) >> 1; }
+__host__ __device__ __forceinline__ long rbidx(int nx, int ix, int iy) {
+  return (long)iy * nx + (((ix + iy) & 1) ? rb_cnt0(nx, iy) : 0) + (ix >> 1);
+}
+// V-cycle vectors and coarse factors are blocked by 32 cells (AoSoA): the
+// `w` values of cells 32j..32j+31 are stored as [j][w][32], so a warp's
+// loads of one value of consecutive cells coalesce and all values of one
+// cell sit at constant offsets (one address per cell instead of one per value).
+__host__ __device__ __forceinline__ long vblk(long k, int w) { return (k >> 5) * (32L * w) + (k & 31); }
+__host__ __device__ __forceinline__ long vstride(long nc, int w) { return ((nc + 31) >> 5) * (32L * w); }
+
+
 __constant__ double c_dconst[NB2];
 __constant__ double c_m2x3, c_m2y3;
 // Face couplings per level and direction (W, E, S, N): every face block is
@@ -221,7 +235,9 @@ template <typename R, typename T>
 __device__ __forceinline__ void face_mv(int lev, int dir, const T* __restrict__ xs, long nc, long cn, R* y) {
   R v[NB];
 #pragma unroll
-  for (int r = 0; r < NB; ++r) v[r] = (R)xs[r * nc + cn];
+  const T* p = xs + vblk(cn, NB);
+#pragma unroll
+  for (int r = 0; r < NB; ++r) v[r] = (R)p[r * 32];
   face_lift(lev, dir, v, y);
 }
 
@@ -256,6 +272,11 @@ __device__ __forceinline__ void fine_block_mv(double sgt, double sga, const doub
 // partner, so the Schur complement S = A - B1 T1^{-1} C1 - B2 T2^{-1} C2 is
 // diagonal: ~40 flops per cell (verified against the generic 12x12 inverse
 // at setup, see check_fine_structure).
+// reciprocal in the V-cycle arithmetic: exact for fp64, MUFU approximation
+// (~1 ulp) for the fp32 preconditioner
+__device__ __forceinline__ double vrcp(double v) { return 1.0 / v; }
+__device__ __forceinline__ float vrcp(float v) { return __fdividef(1.0f, v); }
+
 template <typename R>
 __device__ __forceinline__ void fine_block_solve(R sgt, R sga, const R* r, R* x) {
   const R ax = m2x3<R>() * sgt, ay = m2y3<R>() * sgt;
@@ -264,8 +285,8 @@ __device__ __forceinline__ void fine_block_solve(R sgt, R sga, const R* r, R* x)
   R it1[4], it2[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    it1[k] = R(1) / (dconst<R>((4 + k) * NB + 4 + k) + ax);
-    it2[k] = R(1) / (dconst<R>((8 + k) * NB + 8 + k) + ay);
+    it1[k] = vrcp(dconst<R>((4 + k) * NB + 4 + k) + ax);
+    it2[k] = vrcp(dconst<R>((8 + k) * NB + 8 + k) + ay);
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -274,7 +295,7 @@ __device__ __forceinline__ void fine_block_solve(R sgt, R sga, const R* r, R* x)
     const R by = dconst<R>(i * NB + 8 + ky), cy = dconst<R>((8 + ky) * NB + i);
     const R sii = dconst<R>(i * NB + i) + sga - bx * it1[kx] * cx - by * it2[ky] * cy;
     const R rhs = r[i] - bx * it1[kx] * r[4 + kx] - by * it2[ky] * r[8 + ky];
-    x[i] = rhs / sii;
+    x[i] = rhs * vrcp(sii);
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -350,13 +371,6 @@ __global__ void k_galerkin_diag(int S, int fnx, int fny, const double* __restric
   for (int e = 0; e < NB2; ++e) Dc[t * NB2 + e] = out[e];
 }
 
-// ---- red-black storage order ------------------------------------------------
-// Cells of colour (ix + iy) & 1 == 0 come first in every row, then colour 1.
-__host__ __device__ __forceinline__ int rb_cnt0(int nx, int iy) { return (nx + 1 - (iy & 1)) >> 1; }
-__host__ __device__ __forceinline__ long rbidx(int nx, int ix, int iy) {
-  return (long)iy * nx + (((ix + iy) & 1) ? rb_cnt0(nx, iy) : 0) + (ix >> 1);
-}
-
 __constant__ double c_P[4][16];               // prolongation E2 per sub-cell position: [4 * fine + coarse]
 __constant__ double c_cpl[kMaxLevels][4][16]; // per level: B1 (rho<-Jx), B2 (rho<-Jy), C1 (Jx<-rho), C2 (Jy<-rho)
 __constant__ float c_P_f[4][16];
@@ -385,18 +399,18 @@ template <typename R>
 __device__ __forceinline__ void face_mv_prolong(int lev, int dir, const float* __restrict__ xs, long nc, int nx,
                                                 int jx, int jy, const float* __restrict__ xcs, long ncc, int cnx,
                                                 R* y) {
-  const long cn = rbidx(nx, jx, jy);
-  const long C = rbidx(cnx, jx >> 1, jy >> 1);
+  const float* pf = xs + vblk(rbidx(nx, jx, jy), NB);
+  const float* pc = xcs + vblk(rbidx(cnx, jx >> 1, jy >> 1), NB);
   const R* E = Pc<R>((jx & 1) + 2 * (jy & 1));
   R v[NB];
 #pragma unroll
   for (int f = 0; f < 3; ++f) {
     R xc[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) xc[k] = (R)xcs[(4 * f + k) * ncc + C];
+    for (int k = 0; k < 4; ++k) xc[k] = (R)pc[(4 * f + k) * 32];
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
-      R acc = (R)xs[(4 * f + l) * nc + cn];
+      R acc = (R)pf[(4 * f + l) * 32];
 #pragma unroll
       for (int k = 0; k < 4; ++k) acc = fma(E[4 * l + k], xc[k], acc);
       v[4 * f + l] = acc;
@@ -412,9 +426,9 @@ __device__ __forceinline__ void coarse_block_solve(int lev, const FacT* __restri
   FacT t1[16], t2[16], si[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
-    t1[e] = f[e * nc];
-    t2[e] = f[(16 + e) * nc];
-    si[e] = f[(32 + e) * nc];
+    t1[e] = f[e * 32];
+    t2[e] = f[(16 + e) * 32];
+    si[e] = f[(32 + e) * 32];
   }
   const R* B1 = cplc<R>(lev, 0);
   const R* B2 = cplc<R>(lev, 1);
@@ -565,11 +579,11 @@ __global__ void k_coarse_factor(int S, int nx, int ny, int lev, const double* __
     }
   inv4(Sm, Si);
   const long o = rbidx(nx, (int)(c % nx), (int)(c / nx));
-  FacT* fo = fac + s * nc * 48 + o;
+  FacT* fo = fac + s * vstride(nc, 48) + vblk(o, 48);
   for (int e = 0; e < 16; ++e) {
-    fo[e * nc] = (FacT)T1i[e];
-    fo[(16 + e) * nc] = (FacT)T2i[e];
-    fo[(32 + e) * nc] = (FacT)Si[e];
+    fo[e * 32] = (FacT)T1i[e];
+    fo[(16 + e) * 32] = (FacT)T2i[e];
+    fo[(32 + e) * 32] = (FacT)Si[e];
   }
 }
 
@@ -585,7 +599,7 @@ __global__ void k_check_factor(int S, int nx, int ny, int lev, const double* __r
   for (int j = 0; j < NB; ++j) {
     double r[NB], x[NB];
     for (int i = 0; i < NB; ++i) r[i] = D[t * NB2 + i * NB + j];
-    coarse_block_solve(lev, fac + s * nc * 48 + o, nc, r, x);
+    coarse_block_solve(lev, fac + s * vstride(nc, 48) + vblk(o, 48), nc, r, x);
     for (int i = 0; i < NB; ++i) e = fmax(e, fabs(x[i] - (i == j ? 1.0 : 0.0)));
   }
   atomicMax(err, (unsigned long long)__double_as_longlong(e));
@@ -631,7 +645,7 @@ __global__ void __launch_bounds__(128) k_gs_rb(GsArgs a) {
   const int ix = 2 * k + ((a.color + iy) & 1);
   const long nc = (long)a.nx * a.ny;
   const long own = (long)iy * a.nx + (a.color ? c0 : 0) + k;
-  const float* xs = a.x + s * nc * NB;
+  const float* xs = a.x + s * vstride(nc, NB);
   VR acc[NB];
 #pragma unroll
   for (int r = 0; r < NB; ++r) acc[r] = 0;
@@ -639,7 +653,7 @@ __global__ void __launch_bounds__(128) k_gs_rb(GsArgs a) {
     if (PROLONG) {
       const int cnx = a.nx >> 1;
       const long ncc = (long)cnx * (a.ny >> 1);
-      const float* xcs = a.xc + s * ncc * NB;
+      const float* xcs = a.xc + s * vstride(ncc, NB);
       if (ix > 0) face_mv_prolong(a.lev, 0, xs, nc, a.nx, ix - 1, iy, xcs, ncc, cnx, acc);
       if (ix < a.nx - 1) face_mv_prolong(a.lev, 1, xs, nc, a.nx, ix + 1, iy, xcs, ncc, cnx, acc);
       if (iy > 0) face_mv_prolong(a.lev, 2, xs, nc, a.nx, ix, iy - 1, xcs, ncc, cnx, acc);
@@ -648,29 +662,30 @@ __global__ void __launch_bounds__(128) k_gs_rb(GsArgs a) {
       face_terms_rb(a.lev, xs, a.nx, a.ny, ix, iy, acc);
     }
   }
-  const float* bi = a.b + s * nc * NB + own;
+  const long vo = s * vstride(nc, NB) + vblk(own, NB);
+  const float* bi = a.b + vo;
   VR rr[NB];
 #pragma unroll
-  for (int r = 0; r < NB; ++r) rr[r] = (VR)bi[r * nc] - acc[r];
+  for (int r = 0; r < NB; ++r) rr[r] = (VR)bi[r * 32] - acc[r];
   VR out[NB];
   if (FINE) {
     const float2 sg = a.sig[s * nc + own];
     fine_block_solve<VR>((VR)sg.x, (VR)sg.y, rr, out);
   } else {
-    coarse_block_solve(a.lev, a.fac + s * nc * 48 + own, nc, rr, out);
+    coarse_block_solve(a.lev, a.fac + s * vstride(nc, 48) + vblk(own, 48), nc, rr, out);
   }
-  float* xo = a.x + s * nc * NB + own;
+  float* xo = a.x + vo;
   if (a.delta) {
-    float* dl = a.delta + s * nc * NB + own;
+    float* dl = a.delta + vo;
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       const float xn = (float)out[r];
-      dl[r * nc] = a.old_zero ? xn : xn - xo[r * nc];
-      xo[r * nc] = xn;
+      dl[r * 32] = a.old_zero ? xn : xn - xo[r * 32];
+      xo[r * 32] = xn;
     }
   } else {
 #pragma unroll
-    for (int r = 0; r < NB; ++r) xo[r * nc] = (float)out[r];
+    for (int r = 0; r < NB; ++r) xo[r * 32] = (float)out[r];
   }
 }
 
@@ -687,7 +702,7 @@ __global__ void k_restrict_delta(int S, int fnx, int fny, int lev, const float* 
   const long s = t / ncc, C = t - s * ncc;
   if (act && !act[s]) return;
   const int cx = (int)(C % cnx), cy = (int)(C / cnx);
-  const float* ds = delta + s * nf * NB;
+  const float* ds = delta + s * vstride(nf, NB);
   VR out[NB];
 #pragma unroll
   for (int r = 0; r < NB; ++r) out[r] = 0;
@@ -708,9 +723,9 @@ __global__ void k_restrict_delta(int S, int fnx, int fny, int lev, const float* 
         out[4 * f + k] = acc;
       }
   }
-  float* o = bc + s * ncc * NB + rbidx(cnx, cx, cy);
+  float* o = bc + s * vstride(ncc, NB) + vblk(rbidx(cnx, cx, cy), NB);
 #pragma unroll
-  for (int r = 0; r < NB; ++r) o[r * ncc] = (float)out[r];
+  for (int r = 0; r < NB; ++r) o[r * 32] = (float)out[r];
 }
 
 // dense coarsest operator [S][n][n] (n = 12 nc), unknown index r * nc + rb(cell)
@@ -806,18 +821,21 @@ __global__ void k_dense_inverse(int n, double* __restrict__ A, double* __restric
 }
 
 template <typename T>
-__global__ void k_dense_apply(int n, const double* __restrict__ Ainv, const T* __restrict__ b,
+__global__ void k_dense_apply(int n, int nc, const double* __restrict__ Ainv, const T* __restrict__ b,
                               T* __restrict__ x, const int* __restrict__ act) {
+  // dense unknown e = q * nc + k  <->  blocked vector position vblk(k, NB) + 32 q
   const int s = blockIdx.x;
   if (act && !act[s]) return;
   const double* a = Ainv + (long)s * n * n;
-  const T* bs = b + (long)s * n;
+  const long vs = vstride(nc, NB);
+  const T* bs = b + (long)s * vs;
+  auto pos = [&](int e) { return vblk(e % nc, NB) + 32 * (e / nc); };
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int r = wid; r < n; r += nw) {
     double acc = 0.0;
-    for (int c = lane; c < n; c += 32) acc = fma(a[(long)r * n + c], (double)bs[c], acc);
+    for (int c = lane; c < n; c += 32) acc = fma(a[(long)r * n + c], (double)bs[pos(c)], acc);
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) x[(long)s * n + r] = (T)acc;
+    if (lane == 0) x[(long)s * vs + pos(r)] = (T)acc;
   }
 }
 
@@ -889,7 +907,8 @@ enum { SC_RHO_OLD = 0, SC_ALPHA, SC_OMEGA, SC_RHO, SC_BNORM2, SC_RNORM2, SC_ITER
 __device__ __forceinline__ unsigned nat2rb(unsigned i, unsigned nc, unsigned nx) {
   const unsigned q = i / nc, c = i - q * nc;
   const unsigned iy = c / nx, ix = c - iy * nx;
-  return q * nc + (unsigned)rbidx((int)nx, (int)ix, (int)iy);
+  const unsigned k = (unsigned)rbidx((int)nx, (int)ix, (int)iy);
+  return (k >> 5) * (32u * NB) + q * 32u + (k & 31u);
 }
 
 __global__ void k_bicg_init(int S, int nblk, const double* part, double* scal, int* act, const int* mask) {
@@ -921,10 +940,11 @@ __global__ void __launch_bounds__(kBT) k_bicg_p(int S, unsigned n, unsigned nc, 
   const double beta = (rho / sc[SC_RHO_OLD]) * (sc[SC_ALPHA] / sc[SC_OMEGA]);
   const double om = sc[SC_OMEGA];
   const long base = (long)s * n;
+  const long vbase = (long)s * vstride(nc, NB);
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double pv = r[base + i] + beta * (p[base + i] - om * v[base + i]);
     p[base + i] = pv;
-    b0[base + nat2rb(i, nc, nx)] = (float)pv;
+    b0[vbase + nat2rb(i, nc, nx)] = (float)pv;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_RHO] = rho;
 }
@@ -939,7 +959,7 @@ __global__ void __launch_bounds__(kBT, 2) k_apply_dot(int S, int nx, int ny, con
   const int s = blockIdx.y;
   if (!act[s]) return;
   const long nc = (long)nx * ny;
-  const float* xs = xin + s * nc * NB;
+  const float* xs = xin + s * vstride(nc, NB);
   double a0 = 0.0, a1 = 0.0;
   for (long c = (long)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (long)gridDim.x * blockDim.x) {
     const int iy = (int)(c / nx), ix = (int)(c - (long)iy * nx);
@@ -948,7 +968,7 @@ __global__ void __launch_bounds__(kBT, 2) k_apply_dot(int S, int nx, int ny, con
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       acc[r] = 0.0;
-      xl[r] = (double)xs[r * nc + own];
+      xl[r] = (double)xs[vblk(own, NB) + r * 32];
     }
     const long fi = (long)s * nc + c;
     fine_block_mv(sgt[fi], sgt[fi] - sgs[fi], xl, acc);
@@ -981,10 +1001,11 @@ __global__ void __launch_bounds__(kBT) k_bicg_s(int S, unsigned n, unsigned nc, 
   reduce_parts(part, s, nblk, 1, &rhv);
   const double alpha = sc[SC_RHO] / rhv;
   const long base = (long)s * n;
+  const long vbase = (long)s * vstride(nc, NB);
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double x = r[base + i] - alpha * v[base + i];
     sv[base + i] = x;
-    b0[base + nat2rb(i, nc, nx)] = (float)x;
+    b0[vbase + nat2rb(i, nc, nx)] = (float)x;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_RHV] = alpha;
 }
@@ -1003,10 +1024,11 @@ __global__ void __launch_bounds__(kBT) k_bicg_x(int S, unsigned n, unsigned nc, 
   const double alpha = sc[SC_RHV];
   const double omega = q[1] > 0.0 ? q[0] / q[1] : 0.0;
   const long base = (long)s * n;
+  const long vbase = (long)s * vstride(nc, NB);
   double a0 = 0.0, a1 = 0.0;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const unsigned k = nat2rb(i, nc, nx);
-    x[base + i] += alpha * (double)ph[base + k] + omega * (double)sh[base + k];
+    x[base + i] += alpha * (double)ph[vbase + k] + omega * (double)sh[vbase + k];
     const double rv = sv[base + i] - omega * t[base + i];
     r[base + i] = rv;
     a0 = fma(rv, rv, a0);
@@ -1208,8 +1230,8 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
     const size_t li = d->L.size() - 1;
     if (li > 0) {
       lv.D.alloc((size_t)S * lv.nc * NB2);
-      lv.fac.alloc((size_t)S * lv.nc * 48);
-      lv.x.alloc((size_t)S * lv.nc * NB);
+      lv.fac.alloc((size_t)S * vstride(lv.nc, 48));
+      lv.x.alloc((size_t)S * vstride(lv.nc, NB));
     }
     if (li < (size_t)kMaxLevels) {
       const int fb[4][2] = {{0, 1}, {0, 2}, {1, 0}, {2, 0}};
@@ -1218,8 +1240,8 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
           for (int k = 0; k < 4; ++k)
             cpl[(li * 4 + m) * 16 + 4 * i + k] = Kc[(size_t)(4 * fb[m][0] + i) * NB + 4 * fb[m][1] + k];
     }
-    lv.b.alloc((size_t)S * lv.nc * NB);
-    lv.r.alloc((size_t)S * lv.nc * NB);
+    lv.b.alloc((size_t)S * vstride(lv.nc, NB));
+    lv.r.alloc((size_t)S * vstride(lv.nc, NB));
     const bool can = nx % 2 == 0 && ny % 2 == 0 && lv.nc > kMaxCoarseCells;
     if (!can) break;
     // coarse constants: face blocks and internal coupling of the coarse diagonal
@@ -1365,8 +1387,8 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   const size_t nv = (size_t)S * l0.nc * NB;
   RTE_REQUIRE(l0.nc * NB < (1L << 31), RTE_ERR_UNSUPPORTED, "dsa: more than 2^31 unknowns per sample");
   for (DBuf<double>* b : {&d->r, &d->p, &d->v, &d->s, &d->t, &d->x, &d->rhs}) b->alloc(nv);
-  d->xa.alloc(nv);
-  d->xb.alloc(nv);
+  d->xa.alloc((size_t)S * vstride(l0.nc, NB));
+  d->xb.alloc((size_t)S * vstride(l0.nc, NB));
   d->scal.alloc((size_t)S * 16);
   d->nblk = (int)std::min<long>(512, std::max<long>(16, (long)l0.nc * NB / 4096));
   d->part.alloc((size_t)S * d->nblk * 4);
@@ -1401,7 +1423,7 @@ static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cu
   if (last) {
     if (d->ncoarse > 0) {
       ++d->nlaunch;
-      k_dense_apply<<<S, 256, 0, st>>>(d->ncoarse, d->coarse_inv.p, b, x, act);
+      k_dense_apply<<<S, 256, 0, st>>>(d->ncoarse, (int)lv.nc, d->coarse_inv.p, b, x, act);
       RTE_CUDA(cudaGetLastError());
     } else {
       for (int k = 0; k < 20; ++k) {
