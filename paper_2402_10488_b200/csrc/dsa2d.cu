@@ -963,16 +963,19 @@ __global__ void __launch_bounds__(kBT, 2) k_apply_dot(int S, int nx, int ny, con
   double a0 = 0.0, a1 = 0.0;
   for (long c = (long)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (long)gridDim.x * blockDim.x) {
     const int iy = (int)(c / nx), ix = (int)(c - (long)iy * nx);
-    const long own = rbidx(nx, ix, iy);
-    double acc[NB], xl[NB];
+    double acc[NB];
 #pragma unroll
-    for (int r = 0; r < NB; ++r) {
-      acc[r] = 0.0;
-      xl[r] = (double)xs[vblk(own, NB) + r * 32];
-    }
-    const long fi = (long)s * nc + c;
-    fine_block_mv(sgt[fi], sgt[fi] - sgs[fi], xl, acc);
+    for (int r = 0; r < NB; ++r) acc[r] = 0.0;
+    // face terms first, then the cell block (keeps fewer values live)
     face_terms_rb(0, xs, nx, ny, ix, iy, acc);
+    {
+      const float* xp = xs + vblk(rbidx(nx, ix, iy), NB);
+      double xl[NB];
+#pragma unroll
+      for (int r = 0; r < NB; ++r) xl[r] = (double)xp[r * 32];
+      const long fi = (long)s * nc + c;
+      fine_block_mv(sgt[fi], sgt[fi] - sgs[fi], xl, acc);
+    }
     double* yo = out + (long)s * nc * NB + c;
     const double* dd = d0 + (long)s * nc * NB + c;
 #pragma unroll

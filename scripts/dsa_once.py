@@ -18,8 +18,12 @@ b = rte.TransportBatch.from_cells(mesh, quad, st, ss, g)
 d = rte.DsaOperator(b)
 d.set_tolerance(tol, 2000)
 rhs = torch.rand(S, b.n_dof(), dtype=torch.float64, device="cuda")
-for k in range(2):
+ts = []
+for k in range(int(os.environ.get("REPS", "3"))):
     torch.cuda.synchronize(); t0 = time.time()
     x = d.solve_density(rhs)
     torch.cuda.synchronize()
-    print("solve %.3f s, krylov iterations %d" % (time.time() - t0, d.last_iterations()), flush=True)
+    ts.append(time.time() - t0)
+print("solve %.3f s (min of %s), krylov iterations %d, %.2f ms/iteration"
+      % (min(ts), " ".join("%.3f" % t for t in ts), d.last_iterations(), 1e3 * min(ts) / d.last_iterations()),
+      flush=True)
