@@ -250,7 +250,7 @@ def run_b200(args, rank, world, device):
         "e2e": e2e,
         "roofline": ({"bound": "hbm", "achieved": gs_ach, "peak": hbm_peak, "unit": "GB/s",
                       "frac": gs_ach / hbm_peak, "traffic": gs_traffic(),
-                      "kernel": "k_gs<float> (finest-level DSA red-black block Gauss-Seidel half-sweep)",
+                      "kernel": "k_gs_rb<true,*> (finest-level DSA red-black block Gauss-Seidel colour half-sweep, fp32, blocked red-black layout)",
                       "per_launch_ms": gs_ms, "bytes_per_launch": gs_bytes,
                       "share_of_step": ms_k[5] / ms_total, "peak_kind": peak_kind} if gs_ach else None),
         "sweep_roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
