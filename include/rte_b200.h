@@ -231,6 +231,35 @@ int rte_romig(rte_ctx* ctx, double* rho0_dev, int* status_host, void* stream);
 int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg, double* rho_dev, rte_si_report* reports_host,
                  double* history_host, char* log_host);
 
+/* ---- (P)GMRES (gmres.cpp:15-124) ------------------------------------------ */
+enum rte_gmres_guess { RTE_GUESS_ZERO = 0, RTE_GUESS_SUPPLIED = 1, RTE_GUESS_ROMIG = 2 };
+
+typedef struct rte_gmres_config {
+  int preconditioned;  /* 1: P = I + C Ms with the consistent DSA operator (PGMRES); 0: GMRES */
+  int restart;         /* SolveConfig::gmres_restart (reference default 25) */
+  double rel_tol;      /* SolveConfig::gmres_rel_tol: preconditioned relative residual (1e-11) */
+  int max_iters;       /* SolveConfig::max_iters: cap on inner iterations */
+  int guess;           /* rte_gmres_guess; RTE_GUESS_ROMIG = PGMRES-ROMIG (runner.cpp:202-205),
+                          needs the primary model (rte_rom_load which = 0) */
+} rte_gmres_config;
+
+typedef struct rte_gmres_report {
+  int converged;
+  int iterations;      /* inner iterations (SolveReport::iterations) */
+  long n_sweep;        /* reference accounting: 1 (bbar) + 1 per cycle start + 1 per inner step */
+  int cycles;          /* restart cycles started */
+  double final_residual; /* converged: ||A rho - bbar||_inf of the verifying cycle start;
+                            else ||rho - L rho - bbar||_inf */
+  int history_len;     /* SolveReport::change_history size (entries beyond history_cap dropped) */
+} rte_gmres_report;
+
+/* Batched gmres_solve for every sample: rho_dev [S][n_dof] holds the guess on
+ * entry (RTE_GUESS_SUPPLIED) and the solution on exit; reports_host[S];
+ * history_host [S][history_cap] (may be NULL).  Synchronizes once per step
+ * (one transport sweep + one DSA solve for every unfinished sample). */
+int rte_gmres_solve(rte_ctx* ctx, const rte_gmres_config* cfg, double* rho_dev, rte_gmres_report* reports_host,
+                    double* history_host, int history_cap);
+
 /* ---- measurement ---------------------------------------------------------- */
 /* Per-context kernel timing with CUDA events recorded on the launching stream
  * around every kernel the context issues, by category.  Off by default. */

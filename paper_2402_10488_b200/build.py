@@ -19,7 +19,7 @@ BUILD = os.path.join(HERE, "_build") if not os.environ.get("RTE_BUILD_OUT") else
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
-SOURCES = ["capi.cu", "sweep1d.cu", "sweep2d.cu", "dsa1d.cu", "dsa2d.cu", "rom.cu", "kinetic.cu", "pod.cu", "setup.cpp"]
+SOURCES = ["capi.cu", "sweep1d.cu", "sweep2d.cu", "dsa1d.cu", "dsa2d.cu", "rom.cu", "kinetic.cu", "pod.cu", "gmres.cu", "setup.cpp"]
 
 
 def _stale(obj, deps):

@@ -16,6 +16,7 @@ RTE_OK, RTE_ERR_INVALID, RTE_ERR_RUNTIME, RTE_ERR_CUDA, RTE_ERR_UNSUPPORTED = 0,
 RTE_SLAB1D, RTE_XY2D = 0, 1
 RTE_SI, RTE_DSA, RTE_ROMSA, RTE_ROMSAD, RTE_ROMIG = 0, 1, 2, 3, 4
 RTE_NORM_ABS, RTE_NORM_REL = 0, 1
+RTE_GUESS_ZERO, RTE_GUESS_SUPPLIED, RTE_GUESS_ROMIG = 0, 1, 2
 PROF_KINDS = ("sweep", "reduce", "dsa", "rom", "other", "dsa_smooth0")
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -54,6 +55,16 @@ class SiReport(ctypes.Structure):
 
 
 # (name, restype, argtypes) for every symbol include/rte_b200.h declares.
+class GmresConfig(ctypes.Structure):
+    _fields_ = [("preconditioned", ctypes.c_int), ("restart", ctypes.c_int), ("rel_tol", ctypes.c_double),
+                ("max_iters", ctypes.c_int), ("guess", ctypes.c_int)]
+
+
+class GmresReport(ctypes.Structure):
+    _fields_ = [("converged", ctypes.c_int), ("iterations", ctypes.c_int), ("n_sweep", ctypes.c_long),
+                ("cycles", ctypes.c_int), ("final_residual", ctypes.c_double), ("history_len", ctypes.c_int)]
+
+
 SIGNATURES = [
     ("rte_create", ctypes.c_int, [ctypes.POINTER(Problem), ctypes.c_int, ctypes.POINTER(_vp)]),
     ("rte_destroy", None, [_vp]),
@@ -88,6 +99,8 @@ SIGNATURES = [
     ("rte_romig", ctypes.c_int, [_vp, _vp, _ip, _vp]),
     ("rte_si_solve", ctypes.c_int, [_vp, ctypes.POINTER(SiConfig), _vp, ctypes.POINTER(SiReport), _dp,
                                     ctypes.c_char_p]),
+    ("rte_gmres_solve", ctypes.c_int, [_vp, ctypes.POINTER(GmresConfig), _vp, ctypes.POINTER(GmresReport), _dp,
+                                       ctypes.c_int]),
     ("rte_profile_enable", ctypes.c_int, [_vp, ctypes.c_int]),
     ("rte_profile_read", ctypes.c_int, [_vp, _dp, ctypes.POINTER(ctypes.c_long)]),
     ("rte_probe_dfma", ctypes.c_int, [ctypes.c_int, _dp]),

@@ -649,6 +649,15 @@ int rte_romig(rte_ctx* ctx, double* rho0, int* status_host, void* stream) {
   });
 }
 
+int rte_gmres_solve(rte_ctx* ctx, const rte_gmres_config* cfg, double* rho, rte_gmres_report* reports,
+                    double* history, int history_cap) {
+  return guarded(ctx, [&] {
+    RTE_REQUIRE(cfg && rho, RTE_ERR_INVALID, "gmres: null argument");
+    DeviceGuard dg(ctx->device);
+    gmres_solve(ctx, *cfg, rho, reports, history, history_cap, nullptr);
+  });
+}
+
 int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_report* reports, double* history,
                  char* log) {
   return guarded(ctx, [&] {

@@ -294,6 +294,10 @@ void build_rom(rte_ctx* ctx, int r, const double* U, const double* b_kin_host, d
 int snapshot_columns(int S, int window, long kdim, const double* f_iter, const double* f_conv, const int* n_iter,
                      const int* conv, int kind, int window_limit, double* out, cudaStream_t st);
 
+// (P)GMRES (gmres.cu)
+void gmres_solve(rte_ctx* ctx, const rte_gmres_config& cfg, double* rho, rte_gmres_report* reports, double* history,
+                 int history_cap, cudaStream_t st);
+
 // transport helpers used by the C-ABI (capi.cu)
 void transport_apply(rte_ctx* ctx, int mode, const double* rho, double* out, const int* active,
                      const double* rho_prev, double* delta, unsigned long long* change_bits, cudaStream_t st);

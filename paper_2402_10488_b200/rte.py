@@ -534,6 +534,8 @@ class SolveConfig:
     initial_guess: Optional[object] = None
     compute_residual: bool = True
     check_every: int = 4
+    gmres_restart: int = 25       # solvers.hpp:16
+    gmres_rel_tol: float = 1e-11  # solvers.hpp:17
 
 
 @dataclass
@@ -585,6 +587,42 @@ def sisa_solve(batch: TransportBatch, method: str, config: SolveConfig):
                                float(r.final_residual), label,
                                "supplied" if (config.initial_guess is not None or method == "ROMIG") else "zero",
                                lg, int(r.switch_iter), bool(r.singular)))
+    return rho, out
+
+
+def gmres_solve(batch: TransportBatch, preconditioner, config: SolveConfig, romig_guess: bool = False):
+    """Batched gmres_solve (gmres.cpp:15-124): restarted GMRES on (I - L) rho =
+    bbar, left-preconditioned with P = I + C Ms when ``preconditioner`` is a
+    DsaOperator (PGMRES) or None (GMRES).  ``romig_guess`` = PGMRES-ROMIG
+    (runner.cpp:202-205: the primary model's romig guess).  Returns
+    (rho [S, n_dof], reports)."""
+    L = capi.load()
+    if romig_guess:
+        guess = capi.RTE_GUESS_ROMIG
+    elif config.initial_guess is not None:
+        guess = capi.RTE_GUESS_SUPPLIED
+    else:
+        guess = capi.RTE_GUESS_ZERO
+    cfg = capi.GmresConfig(1 if preconditioner is not None else 0, int(config.gmres_restart),
+                           float(config.gmres_rel_tol), int(config.max_iters), guess)
+    if guess == capi.RTE_GUESS_SUPPLIED:
+        rho = batch._dev(config.initial_guess, (batch.S, batch.nd)).clone()
+    else:
+        rho = batch._out(batch.S, batch.nd)
+    S = batch.S
+    cap = 2 * int(config.max_iters) + 2
+    reps = (capi.GmresReport * S)()
+    hist = np.zeros(S * cap)
+    _torch().cuda.synchronize(batch.device)
+    capi.check(L.rte_gmres_solve(batch._h, ctypes.byref(cfg), ctypes.c_void_p(rho.data_ptr()), reps,
+                                 capi.dptr(hist), cap), batch._h)
+    out = []
+    for s in range(S):
+        r = reps[s]
+        n = min(int(r.history_len), cap)
+        out.append(SolveReport(bool(r.converged), int(r.n_sweep), int(r.iterations), list(hist[s * cap:s * cap + n]),
+                               float(r.final_residual), "PGMRES" if preconditioner is not None else "GMRES",
+                               "zero" if guess == capi.RTE_GUESS_ZERO else "supplied", "", -1, False))
     return rho, out
 
 
