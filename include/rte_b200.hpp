@@ -147,6 +147,8 @@ struct SolveConfig {  // solvers.hpp:13-19 (+ batch options)
   double eps_romsad = 0.0;
   int fixed_iters = 0;
   const std::vector<double>* initial_guess = nullptr;  // S * n_dof, host
+  int gmres_restart = 25;        // solvers.hpp:16
+  double gmres_rel_tol = 1e-11;  // solvers.hpp:17
 };
 
 struct SolveReport {  // solvers.hpp:21-33 (per sample)
@@ -183,6 +185,35 @@ inline std::pair<std::vector<double>, std::vector<SolveReport>> sisa_solve(Trans
     r.switch_iter = reps[s].switch_iter;
     for (int l = 0; l < r.iterations; ++l)
       if (log[(size_t)s * mi + l]) r.correction_log.push_back(log[(size_t)s * mi + l]);
+  }
+  return {rho.to_host(), out};
+}
+
+// gmres_solve (solvers.hpp:80-82, gmres.cpp:15-124) for all samples:
+// preconditioned = PGMRES with the context's DSA operator; romig_guess =
+// PGMRES-ROMIG (runner.cpp:202-205).  Returns rho [S * n_dof].
+inline std::pair<std::vector<double>, std::vector<SolveReport>> gmres_solve(TransportBatch& b, bool preconditioned,
+                                                                            const SolveConfig& c,
+                                                                            bool romig_guess = false) {
+  const int S = b.n_samples();
+  const long nd = b.n_dof();
+  DeviceVector rho((long)S * nd);
+  if (c.initial_guess) rho.from_host(*c.initial_guess);
+  rte_gmres_config cfg{preconditioned ? 1 : 0, c.gmres_restart, c.gmres_rel_tol, c.max_iters,
+                       romig_guess ? RTE_GUESS_ROMIG : (c.initial_guess ? RTE_GUESS_SUPPLIED : RTE_GUESS_ZERO)};
+  const int cap = 2 * c.max_iters + 2;
+  std::vector<rte_gmres_report> reps(S);
+  std::vector<double> hist((size_t)S * cap);
+  check(rte_gmres_solve(b.handle(), &cfg, rho.data(), reps.data(), hist.data(), cap), b.handle());
+  std::vector<SolveReport> out(S);
+  for (int s = 0; s < S; ++s) {
+    SolveReport& r = out[s];
+    r.converged = reps[s].converged != 0;
+    r.n_sweep = reps[s].n_sweep;
+    r.iterations = reps[s].iterations;
+    const int n = std::min(reps[s].history_len, cap);
+    r.change_history.assign(hist.begin() + (long)s * cap, hist.begin() + (long)s * cap + n);
+    r.final_residual = reps[s].final_residual;
   }
   return {rho.to_host(), out};
 }

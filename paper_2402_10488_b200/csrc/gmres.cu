@@ -14,6 +14,8 @@
 // rotations, back-substitution) follows in small kernels.  Samples that
 // finish are masked.  Reductions are two-stage and fixed-order.
 #include <cmath>
+#include <cstdlib>
+#include <string>
 #include <cstring>
 #include <vector>
 
@@ -359,25 +361,40 @@ void gmres_solve(rte_ctx* ctx, const rte_gmres_config& cfg, double* rho, rte_gmr
   k_gm_init<<<(S + 127) / 128, 128, 0, st>>>(a, part0.p);
   RTE_CUDA(cudaGetLastError());
 
+  static const bool dbg = std::getenv("RTE_GMRES_DEBUG") != nullptr;
+  auto chk = [&](const char* what) {
+    if (!dbg) return;
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) throw Error(RTE_ERR_CUDA, std::string("gmres debug: after ") + what + ": " +
+                                                        cudaGetErrorString(e));
+  };
+  chk("init");
   int* nact_h = nullptr;
   RTE_CUDA(cudaMallocHost(&nact_h, sizeof(int)));
   try {
     for (;;) {
       k_gm_stage<<<vg, kT, 0, st>>>(a, rho, U.p, act.p, kind.p);
       RTE_CUDA(cudaGetLastError());
+      chk("stage");
       transport_apply(ctx, SRC_MS_RHO, U.p, LU.p, act.p, nullptr, nullptr, nullptr, st);
+      chk("sweep");
       RTE_CUDA(cudaMemsetAsync(zmax.p, 0, sizeof(unsigned long long) * S, st));
       k_gm_z<<<vg, kT, 0, st>>>(a, U.p, LU.p, bbar.p, Z.p, zmax.p);
+      chk("z");
       if (pre) dsa_apply(ctx, Z.p, C.p, kind.p, 1, st);
+      chk("dsa");
       // MGS passes; pass i reads the partials of pass i-1
       double* parts[2] = {part0.p, part1.p};
       for (int i = 0; i <= m + 1; ++i)
         k_gm_pass<<<vg, kT, 0, st>>>(a, i, Z.p, pre ? C.p : nullptr, W.p, parts[(i + 1) & 1], parts[i & 1]);
       RTE_CUDA(cudaGetLastError());
+      chk("mgs");
       RTE_CUDA(cudaMemsetAsync(nact.p, 0, sizeof(int), st));
       k_gm_scalar<<<(S + 127) / 128, 128, 0, st>>>(a, part0.p, part1.p, zmax.p, nact.p);
+      chk("scalar");
       k_gm_vec<<<vg, kT, 0, st>>>(a, W.p, rho);
       RTE_CUDA(cudaGetLastError());
+      chk("vec");
       RTE_CUDA(cudaMemcpyAsync(nact_h, nact.p, sizeof(int), cudaMemcpyDeviceToHost, st));
       RTE_CUDA(cudaStreamSynchronize(st));
       if (*nact_h == 0) break;

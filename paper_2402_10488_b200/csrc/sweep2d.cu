@@ -142,15 +142,21 @@ __device__ __forceinline__ void issue_chunk_loads(const Sweep2DArgs& a, const Sm
       const int iy = qy ? ny - 1 - row : row;
       const long pc = (long)iy * nx + ix;
       double* dst = sm.stage + cell * 10;
+      // rho / G are only staged when the mode reads them (the rhs assembly
+      // passes no per-sample rho; apply_L skips the G stream)
       if (part == 0) {
-        const double* src = a.rho + (long)s * nd + 4 * pc;
-        cp_async16(dst, src);
-        cp_async16(dst + 2, src + 2);
+        if (a.mode & (SRC_MS_RHO | SRC_RAW)) {
+          const double* src = a.rho + (long)s * nd + 4 * pc;
+          cp_async16(dst, src);
+          cp_async16(dst + 2, src + 2);
+        }
         cp_async8(dst + 8, a.sig_t + (long)s * ncell + pc);
       } else {
-        const double* src = a.g + (a.g_shared ? 0 : (long)s * nd) + 4 * pc;
-        cp_async16(dst + 4, src);
-        cp_async16(dst + 6, src + 2);
+        if (a.mode & SRC_G) {
+          const double* src = a.g + (a.g_shared ? 0 : (long)s * nd) + 4 * pc;
+          cp_async16(dst + 4, src);
+          cp_async16(dst + 6, src + 2);
+        }
         cp_async8(dst + 9, a.sig_s + (long)s * ncell + pc);
       }
     }

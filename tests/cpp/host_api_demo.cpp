@@ -49,6 +49,14 @@ int main(int argc, char** argv) {
   std::printf("{\"converged\": %d, \"iterations\": %d, \"n_sweep\": %ld, \"log\": \"%s\", \"rho\": [", r.converged,
               r.iterations, r.n_sweep, r.correction_log.c_str());
   for (size_t i = 0; i < res.first.size(); ++i) std::printf(i ? ", %.17g" : "%.17g", res.first[i]);
+  // PGMRES on the same system (gmres.cpp:15-124)
+  rte_b200::SolveConfig gcfg;
+  gcfg.gmres_rel_tol = 1e-11;
+  auto gres = rte_b200::gmres_solve(batch, true, gcfg);
+  const auto& gr = gres.second[0];
+  std::printf("], \"pgmres_converged\": %d, \"pgmres_iterations\": %d, \"pgmres_n_sweep\": %ld, \"pgmres_rho\": [",
+              gr.converged, gr.iterations, gr.n_sweep);
+  for (size_t i = 0; i < gres.first.size(); ++i) std::printf(i ? ", %.17g" : "%.17g", gres.first[i]);
   std::printf("]}\n");
-  return r.converged ? 0 : 1;
+  return r.converged && gr.converged ? 0 : 1;
 }

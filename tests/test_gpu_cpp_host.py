@@ -41,3 +41,7 @@ def test_cpp_host_api_c1_parity():
     assert r["converged"] == 1 and r["iterations"] == rep.iterations and r["n_sweep"] == rep.n_sweep
     assert r["log"] == rep.correction_log
     assert rel_l2(np.array(r["rho"]), rho) < 1e-8
+    grho, grep_ = ro.gmres_solve(sys_, ro.build_dsa(sys_), ro.SolveConfig(gmres_rel_tol=1e-11))
+    assert r["pgmres_converged"] == 1 and r["pgmres_iterations"] == grep_.iterations
+    assert r["pgmres_n_sweep"] == grep_.n_sweep
+    assert rel_l2(np.array(r["pgmres_rho"]), grho) < 1e-8
