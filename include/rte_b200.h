@@ -98,8 +98,22 @@ enum rte_method {
   RTE_DSA = 1,    /* DsaStrategy (solvers.hpp:54-65) */
   RTE_ROMSA = 2,  /* RomsaStrategy (strategies.hpp:25-46) on the correction model */
   RTE_ROMSAD = 3, /* RomsadStrategy (strategies.hpp:48-67) */
-  RTE_ROMIG = 4   /* romig initial guess (strategies.cpp:8-28) + DSA */
+  RTE_ROMIG = 4,  /* romig initial guess (strategies.cpp:8-28) + DSA */
+  RTE_CUSTOM = 5  /* caller-supplied CorrectionStrategy (solvers.hpp:38-51) via rte_si_config.correct */
 };
+
+/* The CorrectionStrategy plugin point (solvers.hpp:38-51) for RTE_CUSTOM:
+ * called once per SI iteration l (1-based) after the stop test, on the
+ * solve's stream, with active_host[s] = 1 for every sample that needs a
+ * correction this iteration.  delta_dev = rho* - rho [S][n_dof] (device);
+ * the callback writes corr_dev[s] for active samples (device, stream-ordered
+ * before it returns) and kind_host[s] = the strategy's last_kind() letter
+ * ('D', 'R', 'S', ...) or 0 for "no correction" (rho = rho*).  The next
+ * iterate is rho = rho* + corr (sisa.cpp:128-130).  Nonzero return aborts the
+ * solve with RTE_ERR_RUNTIME.  strategy.setup(system) is the caller's job
+ * before rte_si_solve. */
+typedef int (*rte_correction_fn)(void* user, int l, int n_samples, long n_dof, const int* active_host,
+                                 const double* delta_dev, double* corr_dev, char* kind_host, void* stream);
 
 enum rte_norm { RTE_NORM_ABS = 0, RTE_NORM_REL = 1 };
 
@@ -115,6 +129,8 @@ typedef struct rte_si_config {
   int use_guess;       /* 1: rho_dev holds the initial guess on entry */
   int compute_residual;/* 1: final ||rho - L rho - bbar||_inf (one extra sweep) */
   int check_every;     /* host polls the active count every k iterations (0 = 4) */
+  rte_correction_fn correct; /* RTE_CUSTOM only */
+  void* correct_user;        /* passed through to correct */
 } rte_si_config;
 
 typedef struct rte_si_report {

@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("RTE_B200_LIB", os.path.join(HERE, "librte_b200.so"))
 
 RTE_OK, RTE_ERR_INVALID, RTE_ERR_RUNTIME, RTE_ERR_CUDA, RTE_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 RTE_SLAB1D, RTE_XY2D = 0, 1
-RTE_SI, RTE_DSA, RTE_ROMSA, RTE_ROMSAD, RTE_ROMIG = 0, 1, 2, 3, 4
+RTE_SI, RTE_DSA, RTE_ROMSA, RTE_ROMSAD, RTE_ROMIG, RTE_CUSTOM = 0, 1, 2, 3, 4, 5
 RTE_NORM_ABS, RTE_NORM_REL = 0, 1
 RTE_GUESS_ZERO, RTE_GUESS_SUPPLIED, RTE_GUESS_ROMIG = 0, 1, 2
 PROF_KINDS = ("sweep", "reduce", "dsa", "rom", "other", "dsa_smooth0")
@@ -41,11 +41,17 @@ class Rom(ctypes.Structure):
                 ("b_r", _dp), ("eps_pod", ctypes.c_double), ("eps_train", ctypes.c_double)]
 
 
+# rte_correction_fn (the CorrectionStrategy plugin point, solvers.hpp:38-51)
+CORRECTION_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_long,
+                                 ctypes.POINTER(ctypes.c_int), ctypes.c_void_p, ctypes.c_void_p,
+                                 ctypes.POINTER(ctypes.c_char), ctypes.c_void_p)
+
+
 class SiConfig(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int), ("eps", ctypes.c_double), ("norm", ctypes.c_int),
                 ("max_iters", ctypes.c_int), ("fixed_iters", ctypes.c_int), ("theta", ctypes.c_int),
                 ("eps_romsad", ctypes.c_double), ("use_guess", ctypes.c_int), ("compute_residual", ctypes.c_int),
-                ("check_every", ctypes.c_int)]
+                ("check_every", ctypes.c_int), ("correct", CORRECTION_FN), ("correct_user", ctypes.c_void_p)]
 
 
 class SiReport(ctypes.Structure):

@@ -130,6 +130,9 @@ __global__ void si_decide_kernel(int S, SiState st, int l, rte_si_config cfg) {
       kind = st.singular[s] ? KIND_SINGULAR : KIND_ROMSA;
       lg = st.singular[s] ? 'S' : 'R';
       break;
+    case RTE_CUSTOM:  // the caller's strategy decides; the log letter comes back from the callback
+      kind = KIND_CUSTOM;
+      break;
     case RTE_ROMSAD:  // strategies.cpp:67-76 (monotone switch)
       if (!st.switched[s] && l <= cfg.theta && ch >= cfg.eps_romsad) {
         kind = KIND_ROMSA;
@@ -151,12 +154,25 @@ __global__ void si_decide_kernel(int S, SiState st, int l, rte_si_config cfg) {
     atomicAdd(st.n_active, 1);
 }
 
+// RTE_CUSTOM: record the callback's kind letters; 0 = no correction
+__global__ void si_custom_kinds_kernel(int S, SiState st, int l, int max_iters, const char* kinds) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S || st.kind[s] != KIND_CUSTOM) return;
+  const char c = kinds[s];
+  if (c == 0) {
+    st.kind[s] = KIND_ACCEPT;
+    return;
+  }
+  st.log[(long)s * max_iters + l - 1] = c;
+  if (c == 'D' && st.switch_iter[s] < 0) st.switch_iter[s] = l;
+}
+
 __global__ void si_finalize_kernel(int S, long nd, const int* __restrict__ kind, const double* __restrict__ rho_star,
                                    const double* __restrict__ corr, double* __restrict__ rho) {
   const int s = blockIdx.y;
   const int k = kind[s];
   if (k == KIND_IDLE) return;
-  const bool add = (k == KIND_DSA || k == KIND_ROMSA);
+  const bool add = (k == KIND_DSA || k == KIND_ROMSA || k == KIND_CUSTOM);
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += (long)gridDim.x * blockDim.x) {
     const long t = (long)s * nd + i;
     rho[t] = add ? rho_star[t] + corr[t] : rho_star[t];
@@ -729,6 +745,11 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
     rstar.alloc((size_t)S * nd);
     delta.alloc((size_t)S * nd);
     corr.alloc((size_t)S * nd);
+    RTE_REQUIRE(cfg.method != RTE_CUSTOM || cfg.correct, RTE_ERR_INVALID, "si_solve: RTE_CUSTOM needs a callback");
+    std::vector<int> kinds_h(S), active_h(S);
+    std::vector<char> letters_h(S);
+    DBuf<char> letters_d;
+    letters_d.alloc(S);
     int* n_active_host = nullptr;
     RTE_CUDA(cudaMallocHost(&n_active_host, sizeof(int)));
     const int fin_bx = (int)std::min<long>((nd + 255) / 256, std::max(1, 8192 / S));
@@ -751,6 +772,23 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
         if (need_rom) {
           ProfScope ps(ctx, RTE_PROF_ROM, st);
           rom_correct(ctx, delta.p, corr.p, sst.kind, st);
+        }
+        if (cfg.method == RTE_CUSTOM) {
+          // host round trip: which samples need a correction, then the callback
+          RTE_CUDA(cudaMemcpyAsync(kinds_h.data(), sst.kind, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
+          RTE_CUDA(cudaStreamSynchronize(st));
+          for (int s = 0; s < S; ++s) {
+            active_h[s] = kinds_h[s] == KIND_CUSTOM ? 1 : 0;
+            letters_h[s] = 0;
+          }
+          const int rc = cfg.correct(cfg.correct_user, l, S, nd, active_h.data(), delta.p, corr.p, letters_h.data(),
+                                     st);
+          RTE_REQUIRE(rc == 0, RTE_ERR_RUNTIME, "si_solve: correction callback failed (" + std::to_string(rc) + ")");
+          for (int s = 0; s < S; ++s)
+            if (!active_h[s]) letters_h[s] = 0;
+          RTE_CUDA(cudaMemcpyAsync(letters_d.p, letters_h.data(), S, cudaMemcpyHostToDevice, st));
+          si_custom_kinds_kernel<<<(S + 127) / 128, 128, 0, st>>>(S, sst, l, cfg.max_iters, letters_d.p);
+          RTE_CUDA(cudaGetLastError());
         }
         {
           ProfScope ps(ctx, RTE_PROF_OTHER, st, 1);

@@ -86,7 +86,7 @@ enum SrcMode : int {
 };
 
 // Per-sample SI bookkeeping kinds (rte_si_solve).
-enum Kind : int { KIND_IDLE = 0, KIND_ACCEPT = 1, KIND_DSA = 2, KIND_ROMSA = 3, KIND_SINGULAR = 4 };
+enum Kind : int { KIND_IDLE = 0, KIND_ACCEPT = 1, KIND_DSA = 2, KIND_ROMSA = 3, KIND_SINGULAR = 4, KIND_CUSTOM = 5 };
 
 // 2D sweep direction table entry: canonical (reflected) constants of one
 // unique (vx, vy) slot.

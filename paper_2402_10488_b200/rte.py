@@ -557,14 +557,67 @@ _METHODS = {"SI": capi.RTE_SI, "DSA": capi.RTE_DSA, "ROMSA": capi.RTE_ROMSA, "RO
             "ROMIG": capi.RTE_ROMIG}
 
 
-def sisa_solve(batch: TransportBatch, method: str, config: SolveConfig):
-    """Batched sisa_solve (sisa.cpp:14-54): returns (rho [S, n_dof], reports)."""
+class CorrectionStrategy:
+    """The reference's plugin point (solvers.hpp:38-51), batched: ``setup`` is
+    called once before the solve; ``correct(l, delta, active, out)`` once per
+    SI iteration with ``delta`` = rho* - rho and ``out`` torch CUDA views
+    [S, n_dof] and ``active`` a bool array of the samples to correct; it fills
+    ``out`` for those samples and returns one kind letter per sample
+    (``last_kind()``; '' = no correction).  ``label`` names the strategy in the
+    reports."""
+
+    def setup(self, batch: "TransportBatch") -> None:
+        pass
+
+    def correct(self, l: int, delta, active, out):
+        raise NotImplementedError
+
+    def label(self) -> str:
+        return "CUSTOM"
+
+
+class _DevArray:
+    """Zero-copy torch view of a device pointer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": "<f8", "data": (ptr, False), "version": 2}
+
+
+def _custom_callback(batch, strategy, errors):
+    torch = _torch()
+
+    def cb(user, l, S, nd, active_p, delta_p, corr_p, kinds_p, stream):
+        try:
+            act = np.array([bool(active_p[s]) for s in range(S)])
+            delta = torch.as_tensor(_DevArray(delta_p, (S, nd)), device=batch.device)
+            out = torch.as_tensor(_DevArray(corr_p, (S, nd)), device=batch.device)
+            kinds = strategy.correct(int(l), delta, act, out)
+            torch.cuda.synchronize(batch.device)
+            for s in range(S):
+                k = kinds[s] if kinds is not None else ""
+                kinds_p[s] = (k.encode()[:1] if k else b"\0")
+            return 0
+        except Exception as e:  # reported by rte_si_solve as RTE_ERR_RUNTIME
+            errors.append(e)
+            return 1
+    return capi.CORRECTION_FN(cb)
+
+
+def sisa_solve(batch: TransportBatch, method, config: SolveConfig):
+    """Batched sisa_solve (sisa.cpp:14-54): returns (rho [S, n_dof], reports).
+    ``method`` is a built-in strategy name ("SI", "DSA", "ROMSA", "ROMSAD",
+    "ROMIG") or a CorrectionStrategy object (RTE_CUSTOM)."""
     L = capi.load()
-    m = _METHODS[method]
+    custom = None if isinstance(method, str) else method
+    m = capi.RTE_CUSTOM if custom is not None else _METHODS[method]
+    errors = []
+    cb = capi.CORRECTION_FN() if custom is None else _custom_callback(batch, custom, errors)
+    if custom is not None:
+        custom.setup(batch)
     cfg = capi.SiConfig(m, float(config.eps_sisa), capi.RTE_NORM_REL if config.norm == "rel" else capi.RTE_NORM_ABS,
                         int(config.max_iters), int(config.fixed_iters), int(config.theta),
                         float(config.eps_romsad), 1 if config.initial_guess is not None else 0,
-                        1 if config.compute_residual else 0, int(config.check_every))
+                        1 if config.compute_residual else 0, int(config.check_every), cb, None)
     if config.initial_guess is not None:
         rho = batch._dev(config.initial_guess, (batch.S, batch.nd)).clone()
     else:
@@ -574,18 +627,20 @@ def sisa_solve(batch: TransportBatch, method: str, config: SolveConfig):
     hist = np.zeros(S * mi)
     log = ctypes.create_string_buffer(S * mi)
     _torch().cuda.synchronize(batch.device)
-    capi.check(L.rte_si_solve(batch._h, ctypes.byref(cfg), ctypes.c_void_p(rho.data_ptr()), reps, capi.dptr(hist),
-                              log), batch._h)
+    rc = L.rte_si_solve(batch._h, ctypes.byref(cfg), ctypes.c_void_p(rho.data_ptr()), reps, capi.dptr(hist), log)
+    if rc != 0 and errors:
+        raise errors[0]
+    capi.check(rc, batch._h)
     raw = log.raw
     out = []
-    label = {"SI": "SI", "DSA": "DSA", "ROMSA": "ROMSA", "ROMSAD": "ROMSAD", "ROMIG": "ROMIG"}[method]
+    label = custom.label() if custom is not None else method
     for s in range(S):
         r = reps[s]
         it = r.iterations
         lg = raw[s * mi:s * mi + it].replace(b"\0", b"").decode()
         out.append(SolveReport(bool(r.converged), int(r.n_sweep), int(it), list(hist[s * mi:s * mi + it]),
                                float(r.final_residual), label,
-                               "supplied" if (config.initial_guess is not None or method == "ROMIG") else "zero",
+                               "supplied" if (config.initial_guess is not None or m == capi.RTE_ROMIG) else "zero",
                                lg, int(r.switch_iter), bool(r.singular)))
     return rho, out
 
