@@ -716,6 +716,130 @@ def collect_snapshots(batch: TransportBatch, window: int = 3, eps_train: float =
                      np.array(nit[:], dtype=np.int32))
 
 
+# RTESNP1 snapshot files (snapshots.cpp:15-78, 224-314): one file per
+# training parameter, header | w_mu records (f^(l), delta_rho^(l)) | f_conv.
+_SNAP_MAGIC = b"RTESNP1\0"
+
+
+def snapshot_header_bytes(n_params: int) -> int:
+    """snapshots.cpp:57 -- the first stored iterate starts here."""
+    return 58 + 8 * n_params
+
+
+def snapshot_patch_offset(n_params: int) -> int:
+    """snapshots.cpp:58 -- w_mu, n_conv, converged (patched after the solve)."""
+    return 49 + 8 * n_params
+
+
+def write_snapshot_file(path: str, geometry: int, n_v: int, n_dof: int, mu, window: int, eps_train: float,
+                        f_iter, drho, f_conv, n_conv: int, converged: bool, float32: bool = False) -> None:
+    """One training parameter in the reference's RTESNP1 layout (the writer
+    sequence of snapshots.cpp:128-176): f_iter [w_mu, n_v*n_dof] and drho
+    [w_mu, n_dof] are the stored iterates (w_mu = min(n_conv, window))."""
+    import struct
+    mu = [float(v) for v in mu]
+    f_iter = np.asarray(f_iter, dtype=np.float64)
+    drho = np.asarray(drho, dtype=np.float64)
+    w_mu = min(int(n_conv), int(window))
+    kd = np.float32 if float32 else np.float64
+    try:
+        f = open(path, "wb")
+    except OSError as e:
+        raise RuntimeError("snapshots: cannot create " + path) from e
+    with f:
+        f.write(_SNAP_MAGIC)
+        f.write(struct.pack("<IIQQI", 1, int(geometry), int(n_v), int(n_dof), len(mu)))
+        f.write(struct.pack("<%dd" % len(mu), *mu))
+        f.write(struct.pack("<IdBIIB", int(window), float(eps_train), 4 if float32 else 8, w_mu, int(n_conv),
+                            1 if converged else 0))
+        for l in range(w_mu):
+            f.write(f_iter[l].astype(kd).tobytes())
+            f.write(drho[l].tobytes())
+        f.write(np.asarray(f_conv, dtype=np.float64).astype(kd).tobytes())
+
+
+def read_snapshot_file(path: str) -> dict:
+    """Header and data of one RTESNP1 file (snapshots.cpp:60-78, 270-314)."""
+    import struct
+    try:
+        f = open(path, "rb")
+    except OSError as e:
+        raise RuntimeError("snapshots: cannot open " + path) from e
+    with f:
+        def raw(n):
+            b = f.read(n)
+            if len(b) != n:
+                raise RuntimeError("snapshots: truncated file")
+            return b
+        if raw(8) != _SNAP_MAGIC:
+            raise RuntimeError("snapshots: " + path + " is not a snapshot file")
+        if struct.unpack("<I", raw(4))[0] != 1:
+            raise RuntimeError("snapshots: unsupported version in " + path)
+        geom, nv, nd, npar = struct.unpack("<IQQI", raw(24))
+        mu = list(struct.unpack("<%dd" % npar, raw(8 * npar)))
+        window, eps_train, dsize, w_mu, n_conv, conv = struct.unpack("<IdBIIB", raw(22))
+        kd = np.float32 if dsize == 4 else np.float64
+        kdim = nv * nd
+        f_iter = np.zeros((w_mu, kdim))
+        drho = np.zeros((w_mu, nd))
+        for l in range(w_mu):
+            f_iter[l] = np.frombuffer(raw(dsize * kdim), dtype=kd)
+            drho[l] = np.frombuffer(raw(8 * nd), dtype=np.float64)
+        f_conv = np.frombuffer(raw(dsize * kdim), dtype=kd).astype(np.float64)
+    return dict(geometry=geom, n_v=nv, n_dof=nd, mu=mu, window=window, eps_train=eps_train, dsize=dsize,
+                w_mu=w_mu, n_conv=n_conv, converged=bool(conv), f_iter=f_iter, drho=drho, f_conv=f_conv)
+
+
+def save_snapshots(batch: TransportBatch, snaps: Snapshots, directory: str, eps_train: float,
+                   float32: bool = False) -> list:
+    """Write the device snapshots as the reference's per-parameter store
+    (runner.cpp:44-48 names: snap_%03d.snap); returns the paths."""
+    import os
+    os.makedirs(directory, exist_ok=True)
+    mus = batch.mus
+    paths = []
+    fi = snaps.f_iter.cpu().numpy()
+    dr = snaps.drho.cpu().numpy()
+    fc = snaps.f_conv.cpu().numpy()
+    for s in range(batch.S):
+        p = os.path.join(directory, "snap_%03d.snap" % s)
+        w = int(snaps.w_mu[s])
+        write_snapshot_file(p, int(batch.mesh.geometry), batch.quad.n(), batch.nd, mus[s] if mus else [],
+                            snaps.window, eps_train, fi[s, :w], dr[s, :w], fc[s], int(snaps.n_iter[s]),
+                            bool(snaps.converged[s]), float32)
+        paths.append(p)
+    return paths
+
+
+def load_snapshots(directory: str, device: int = 0) -> Snapshots:
+    """SnapshotStore::open (snapshots.cpp:224-254): every *.snap file of the
+    directory in sorted order, one discretization; returns device Snapshots
+    usable by snapshot_matrix / pod (e.g. a store written by the reference)."""
+    import os
+    torch = _torch()
+    paths = sorted(os.path.join(directory, p) for p in os.listdir(directory) if p.endswith(".snap"))
+    if not paths:
+        raise RuntimeError("snapshots: no .snap files in " + directory)
+    recs = [read_snapshot_file(p) for p in paths]
+    g0 = recs[0]
+    for p, r in zip(paths, recs):
+        if (r["geometry"], r["n_v"], r["n_dof"]) != (g0["geometry"], g0["n_v"], g0["n_dof"]):
+            raise RuntimeError("snapshots: mixed discretizations in one store (" + p + ")")
+    window = max(r["window"] for r in recs)
+    S, kdim, nd = len(recs), g0["n_v"] * g0["n_dof"], g0["n_dof"]
+    f_iter = np.zeros((S, window, kdim))
+    drho = np.zeros((S, window, nd))
+    f_conv = np.zeros((S, kdim))
+    for s, r in enumerate(recs):
+        f_iter[s, :r["w_mu"]] = r["f_iter"]
+        drho[s, :r["w_mu"]] = r["drho"]
+        f_conv[s] = r["f_conv"]
+    dev = "cuda:%d" % device
+    return Snapshots(window, torch.from_numpy(f_iter).to(dev), torch.from_numpy(f_conv).to(dev),
+                     torch.from_numpy(drho).to(dev), np.array([r["converged"] for r in recs], dtype=np.int32),
+                     np.array([r["n_conv"] for r in recs], dtype=np.int32))
+
+
 def snapshot_matrix(batch: TransportBatch, snaps: Snapshots, kind: str, window_limit: int = 0):
     """'primary' or 'correction' columns as a torch tensor [n_cols, kdim]
     (i.e. column-major kdim x n_cols)."""

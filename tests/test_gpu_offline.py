@@ -115,3 +115,23 @@ def test_device_offline_drives_romsad_like_oracle(setup):
                                      ro.SolveConfig(eps_sisa=1e-8))
         assert reps[s].iterations == o_rep.iterations and reps[s].correction_log == o_rep.correction_log
         assert rel_l2(rho[s], o_rho) < 1e-8
+
+
+def test_snapshot_store_round_trip(setup, tmp_path):
+    """Device snapshots -> RTESNP1 files (snap_%03d.snap) -> SnapshotStore
+    reader -> identical training matrices and POD on the device."""
+    from paper_2402_10488_b200 import rte
+    tb, d = setup["tb"], setup["dsnaps"]
+    paths = rte.save_snapshots(tb, d, str(tmp_path / "snaps"), EPS_TRAIN)
+    assert len(paths) == tb.S and paths[0].endswith("snap_000.snap")
+    hdr = rte.read_snapshot_file(paths[1])
+    assert hdr["mu"] == list(setup["train"][1]) and hdr["n_v"] == 16 and hdr["n_dof"] == tb.n_dof()
+    back = rte.load_snapshots(str(tmp_path / "snaps"))
+    for kind in ("primary", "correction"):
+        a = rte.snapshot_matrix(tb, d, kind).cpu().numpy()
+        b = rte.snapshot_matrix(tb, back, kind).cpu().numpy()
+        assert np.array_equal(a, b)
+    Fa = rte.snapshot_matrix(tb, d, "correction")
+    Fb = rte.snapshot_matrix(tb, back, "correction")
+    (_, sa), (_, sb) = rte.pod(Fa, 8), rte.pod(Fb, 8)
+    assert np.array_equal(sa, sb)
