@@ -271,6 +271,7 @@ Plan2D plan2d(const rte_ctx* c, int single) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   Plan2D best{1, 1, 0};
   for (int dpl : {8, 4, 2, 1}) {
+    if (c->block == 16 && dpl > 2) continue;  // full-block cell solve: keep the register budget
     const int groups = std::max(1, (mq + nw * dpl - 1) / (nw * dpl));
     best = Plan2D{dpl, groups, groups * nw * dpl};
     const long items = (long)nbands * c->S * 4 * groups;
@@ -397,6 +398,10 @@ static void transport_apply_ex(rte_ctx* ctx, int mode, int single, const double*
   a.active = active;
   a.fout = fout;
   a.nv = ctx->nv;
+  if (ctx->block == 16) {
+    a.mt_blk = ctx->mt.p;
+    a.ms_blk = ctx->ms.p;
+  }
   {
     ProfScope ps(ctx, RTE_PROF_SWEEP, st);
     launch_sweep2d(a, st);
@@ -482,8 +487,8 @@ int rte_create(const rte_problem* p, int device, rte_ctx** out) {
       c->dvx.upload(c->vx.data(), c->nv);
       c->dw.upload(c->w.data(), c->nv);
     } else {
-      RTE_REQUIRE(c->block == 1, RTE_ERR_UNSUPPORTED,
-                  "xy: only per-cell constant coefficients (block = 1) are implemented");
+      RTE_REQUIRE(c->block == 1 || c->block == 16, RTE_ERR_INVALID,
+                  "xy: block must be 1 (sigma I per cell) or 16 (full 4x4 per-cell blocks)");
       RTE_REQUIRE(p->x0 < p->x1 && p->y0 < p->y1, RTE_ERR_INVALID, "invalid rectangular mesh");
       c->hx = (p->x1 - p->x0) / c->nx;
       c->hy = (p->y1 - p->y0) / c->ny;

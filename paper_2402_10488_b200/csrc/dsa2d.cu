@@ -85,6 +85,7 @@ struct Dsa2D {
   rte_ctx* ctx = nullptr;     // for per-kernel profiling of the fine smoother
   const double* sgt = nullptr;
   const double* sgs = nullptr;
+  bool full = false;          // full per-cell 4x4 mass blocks (sgt/sgs then point at [S][cells][16])
 };
 
 // ----------------------------------------------------------------------------
@@ -317,6 +318,25 @@ __global__ void k_fine_diag(int S, long nc, const double* __restrict__ st, const
     d[(4 + i) * NB + 4 + i] += m2x3 * sgt;
     d[(8 + i) * NB + 8 + i] += m2y3 * sgt;
   }
+}
+
+// Fine diagonal blocks for full per-cell mass blocks (intra-cell-varying
+// coefficients): D_c = Dconst + blockdiag(Mt - Ms, 3 m2x Mt, 3 m2y Mt)
+// (dsa.cpp:216-246 with the cell's 4x4 mass blocks).
+__global__ void k_fine_diag_full(int S, long nc, const double* __restrict__ mt, const double* __restrict__ ms,
+                                 double m2x3, double m2y3, double* __restrict__ D) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)S * nc) return;
+  const double* bt = mt + t * 16;
+  const double* bs = ms + t * 16;
+  double* d = D + t * NB2;
+  for (int e = 0; e < NB2; ++e) d[e] = c_dconst[e];
+  for (int i = 0; i < 4; ++i)
+    for (int k = 0; k < 4; ++k) {
+      d[i * NB + k] += bt[4 * i + k] - bs[4 * i + k];
+      d[(4 + i) * NB + 4 + k] += m2x3 * bt[4 * i + k];
+      d[(8 + i) * NB + 8 + k] += m2y3 * bt[4 * i + k];
+    }
 }
 
 // Coarse diagonal blocks: D_C = sum_pos P_pos^T D_c P_pos + Dint (Galerkin).
@@ -951,7 +971,7 @@ __global__ void __launch_bounds__(kBT) k_bicg_p(int S, unsigned n, unsigned nc, 
 
 // out = K x (x: fp32 red-black preconditioned vector, exact in fp64), with the
 // fused partial dots: mode 0 q0 = (d0, out); mode 1 q0 = (out, d0), q1 = (out, out)
-template <int mode>
+template <int mode, bool FULL>
 __global__ void __launch_bounds__(kBT, 2) k_apply_dot(int S, int nx, int ny, const double* __restrict__ sgt,
                                                       const double* __restrict__ sgs, const float* __restrict__ xin,
                                                       double* __restrict__ out, const double* __restrict__ d0,
@@ -974,7 +994,28 @@ __global__ void __launch_bounds__(kBT, 2) k_apply_dot(int S, int nx, int ny, con
 #pragma unroll
       for (int r = 0; r < NB; ++r) xl[r] = (double)xp[r * 32];
       const long fi = (long)s * nc + c;
-      fine_block_mv(sgt[fi], sgt[fi] - sgs[fi], xl, acc);
+      if (FULL) {
+        // Dconst x + blockdiag(Mt - Ms, 3 m2x Mt, 3 m2y Mt) x with the cell's 4x4 blocks
+        fine_block_mv(0.0, 0.0, xl, acc);
+        const double* bt = sgt + fi * 16;
+        const double* bs = sgs + fi * 16;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double ar = 0.0, ax = 0.0, ay = 0.0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double mt = bt[4 * i + k];
+            ar = fma(mt - bs[4 * i + k], xl[k], ar);
+            ax = fma(mt, xl[4 + k], ax);
+            ay = fma(mt, xl[8 + k], ay);
+          }
+          acc[i] += ar;
+          acc[4 + i] = fma(c_m2x3, ax, acc[4 + i]);
+          acc[8 + i] = fma(c_m2y3, ay, acc[8 + i]);
+        }
+      } else {
+        fine_block_mv(sgt[fi], sgt[fi] - sgs[fi], xl, acc);
+      }
     }
     double* yo = out + (long)s * nc * NB + c;
     const double* dd = d0 + (long)s * nc * NB + c;
@@ -1067,15 +1108,24 @@ __global__ void k_bicg_check(int S, int nblk, const double* part, double* scal, 
 
 // rhs assembly [rho part = (Ms) in, J parts = 0] and extraction of the density block
 __global__ void k_pack_rhs(int S, long nc, const double* __restrict__ in, const double* __restrict__ ss, int apply_ms,
-                           double* __restrict__ b, const int* __restrict__ kind) {
+                           int full, double* __restrict__ b, const int* __restrict__ kind) {
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long)S * nc) return;
   const long s = t / nc;
   const long c = t - s * nc;
   const bool on = !kind || kind[s] == KIND_DSA;
-  const double m = apply_ms ? ss[t] : 1.0;
   double* o = b + s * nc * NB + c;
-  for (int r = 0; r < 4; ++r) o[r * nc] = on ? m * in[t * 4 + r] : 0.0;
+  if (apply_ms && full) {
+    const double* m = ss + t * 16;
+    for (int r = 0; r < 4; ++r) {
+      double v = 0.0;
+      for (int q = 0; q < 4; ++q) v = fma(m[4 * r + q], in[t * 4 + q], v);
+      o[r * nc] = on ? v : 0.0;
+    }
+  } else {
+    const double m = apply_ms ? ss[t] : 1.0;
+    for (int r = 0; r < 4; ++r) o[r * nc] = on ? m * in[t * 4 + r] : 0.0;
+  }
   for (int r = 4; r < NB; ++r) o[r * nc] = 0.0;
 }
 
@@ -1194,6 +1244,7 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   }
   d->sgt = ctx->mt.p;
   d->sgs = ctx->ms.p;
+  d->full = ctx->block == 16;
 
   // prolongation blocks (4x4 E2 per position) for the device
   std::vector<Mat> P12(4);
@@ -1231,11 +1282,11 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
     for (int k = 0; k < 4; ++k) std::copy(nbr[k].begin(), nbr[k].end(), lv.nbr_h.begin() + k * NB2);
     lv.nbr.upload(lv.nbr_h.data(), lv.nbr_h.size());
     const size_t li = d->L.size() - 1;
-    if (li > 0) {
+    if (li > 0 || d->full) {
       lv.D.alloc((size_t)S * lv.nc * NB2);
       lv.fac.alloc((size_t)S * vstride(lv.nc, 48));
-      lv.x.alloc((size_t)S * vstride(lv.nc, NB));
     }
+    if (li > 0) lv.x.alloc((size_t)S * vstride(lv.nc, NB));
     if (li < (size_t)kMaxLevels) {
       const int fb[4][2] = {{0, 1}, {0, 2}, {1, 0}, {2, 0}};
       for (int m = 0; m < 4; ++m)
@@ -1327,16 +1378,25 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   DBuf<unsigned long long> ferr;
   ferr.alloc(1);
   RTE_CUDA(cudaMemsetAsync(ferr.p, 0, sizeof(unsigned long long), st));
+  if (d->full) {
+    // full per-cell blocks: the finest level also smooths with stored Schur factors
+    Level& f0 = d->L[0];
+    k_fine_diag_full<<<nblocks((long)S * f0.nc), 256, 0, st>>>(S, f0.nc, ctx->mt.p, ctx->ms.p, m2x3, m2y3, f0.D.p);
+    RTE_CUDA(cudaGetLastError());
+    k_coarse_factor<<<nblocks((long)S * f0.nc, 64), 64, 0, st>>>(S, f0.nx, f0.ny, 0, f0.D.p, f0.fac.p, ferr.p);
+    RTE_CUDA(cudaGetLastError());
+  }
   for (size_t l = 1; l < d->L.size(); ++l) {
     Level& lv = d->L[l];
     const Level& f = d->L[l - 1];
-    k_galerkin_diag<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, f.nx, f.ny, l == 1 ? nullptr : f.D.p, d->sgt,
-                                                                   d->sgs, d->P.p, d->Dint.p + (l - 1) * NB2, lv.D.p);
+    k_galerkin_diag<<<nblocks((long)S * lv.nc, 128), 128, 0, st>>>(S, f.nx, f.ny, (l == 1 && !d->full) ? nullptr : f.D.p,
+                                                                   d->sgt, d->sgs, d->P.p, d->Dint.p + (l - 1) * NB2,
+                                                                   lv.D.p);
     RTE_CUDA(cudaGetLastError());
     k_coarse_factor<<<nblocks((long)S * lv.nc, 64), 64, 0, st>>>(S, lv.nx, lv.ny, (int)l, lv.D.p, lv.fac.p, ferr.p);
     RTE_CUDA(cudaGetLastError());
   }
-  if (d->L.size() == 1 && l0.nc <= kMaxCoarseCells) {
+  if (d->L.size() == 1 && l0.nc <= kMaxCoarseCells && !d->full) {
     // tiny grid: the dense coarsest solve needs explicit level-0 blocks
     d->L[0].D.alloc((size_t)S * l0.nc * NB2);
     k_fine_diag<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, ctx->mt.p, ctx->ms.p, m2x3, m2y3, d->L[0].D.p);
@@ -1367,7 +1427,7 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   {
     // verify the stored factors against the fp64 blocks: max |D^-1 D - I|
     // (fp32 factors: ~1e-7 for well-conditioned blocks)
-    for (size_t l = 1; l < d->L.size(); ++l) {
+    for (size_t l = d->full ? 0 : 1; l < d->L.size(); ++l) {
       Level& lv = d->L[l];
       RTE_CUDA(cudaMemsetAsync(ferr.p, 0, sizeof(unsigned long long), st));
       k_check_factor<<<nblocks((long)S * lv.nc, 64), 64, 0, st>>>(S, lv.nx, lv.ny, (int)l, lv.D.p, lv.fac.p, ferr.p);
@@ -1383,9 +1443,11 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   }
   for (size_t l = 0; l < d->L.size(); ++l) d->L[l].D.release();
   // fine-level coefficients for the V-cycle (fp32, red-black order)
-  d->sig.alloc((size_t)S * l0.nc);
-  k_sig_rb<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->sig.p);
-  RTE_CUDA(cudaGetLastError());
+  if (!d->full) {
+    d->sig.alloc((size_t)S * l0.nc);
+    k_sig_rb<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->sig.p);
+    RTE_CUDA(cudaGetLastError());
+  }
   // Krylov workspace
   const size_t nv = (size_t)S * l0.nc * NB;
   RTE_REQUIRE(l0.nc * NB < (1L << 31), RTE_ERR_UNSUPPORTED, "dsa: more than 2^31 unknowns per sample");
@@ -1405,13 +1467,14 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
 static void gs(Dsa2D* d, int l, int color, const float* b, float* x, const int* act, bool zero_nbr, float* delta,
                bool old_zero, const float* xc, cudaStream_t st) {
   Level& lv = d->L[l];
-  GsArgs a{d->S, lv.nx, lv.ny, l, color, x, b, l == 0 ? d->sig.p : nullptr, l == 0 ? nullptr : lv.fac.p,
+  const bool fine = l == 0 && !d->full;  // closed-form fine cell solve (sigma I blocks)
+  GsArgs a{d->S, lv.nx, lv.ny, l, color, x, b, fine ? d->sig.p : nullptr, fine ? nullptr : lv.fac.p,
            act, zero_nbr ? 1 : 0, delta, old_zero ? 1 : 0, xc};
   const long n = (long)d->S * lv.ny * ((lv.nx + 1) / 2);
   ProfScope ps(l == 0 ? d->ctx : nullptr, RTE_PROF_DSA_SMOOTH0, st, 1);
   ++d->nlaunch;
   const int g = nblocks(n, 128);
-  if (l == 0)
+  if (fine)
     xc ? k_gs_rb<true, true><<<g, 128, 0, st>>>(a) : k_gs_rb<true, false><<<g, 128, 0, st>>>(a);
   else
     xc ? k_gs_rb<false, true><<<g, 128, 0, st>>>(a) : k_gs_rb<false, false><<<g, 128, 0, st>>>(a);
@@ -1468,7 +1531,8 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   const dim3 vgrid(d->nblk, S);
   // b -> rhs (also the shadow residual) ; x = p = v = 0 ; r = b
   ++d->nlaunch;
-  k_pack_rhs<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, rhs, ctx->ms.p, apply_ms, d->rhs.p, kind);
+  k_pack_rhs<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, rhs, ctx->ms.p, apply_ms, d->full ? 1 : 0, d->rhs.p,
+                                                       kind);
   RTE_CUDA(cudaMemsetAsync(d->x.p, 0, sizeof(double) * S * n, st));
   RTE_CUDA(cudaMemsetAsync(d->p.p, 0, sizeof(double) * S * n, st));
   RTE_CUDA(cudaMemsetAsync(d->v.p, 0, sizeof(double) * S * n, st));
@@ -1495,15 +1559,23 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     k_bicg_p<<<vgrid, kBT, 0, st>>>(S, un, unc, unx, d->scal.p, d->r.p, d->p.p, d->v.p, b0, d->act.p);
     vcycle(d, 0, b0, d->xa.p, d->act.p, st);
     ++d->nlaunch;
-    k_apply_dot<0><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xa.p, d->v.p, d->rhs.p, d->part.p,
-                                          d->act.p);
+    if (d->full)
+      k_apply_dot<0, true><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xa.p, d->v.p, d->rhs.p, d->part.p,
+                                                  d->act.p);
+    else
+      k_apply_dot<0, false><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xa.p, d->v.p, d->rhs.p,
+                                                   d->part.p, d->act.p);
     ++d->nlaunch;
     k_bicg_s<<<vgrid, kBT, 0, st>>>(S, un, unc, unx, d->nblk, d->part.p, d->scal.p, d->r.p, d->v.p, d->s.p, b0,
                                     d->act.p);
     vcycle(d, 0, b0, d->xb.p, d->act.p, st);
     ++d->nlaunch;
-    k_apply_dot<1><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xb.p, d->t.p, d->s.p, d->part.p,
-                                          d->act.p);
+    if (d->full)
+      k_apply_dot<1, true><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xb.p, d->t.p, d->s.p, d->part.p,
+                                                  d->act.p);
+    else
+      k_apply_dot<1, false><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xb.p, d->t.p, d->s.p,
+                                                   d->part.p, d->act.p);
     ++d->nlaunch;
     k_bicg_x<<<vgrid, kBT, 0, st>>>(S, un, unc, unx, d->nblk, d->part.p, d->scal.p, d->x.p, d->xa.p, d->xb.p,
                                     d->r.p, d->s.p, d->t.p, d->rhs.p, d->part2.p, d->act.p);

@@ -128,13 +128,14 @@ __device__ void block_dots(const double* u, long nd, int r, const double* v_smem
     for (long i = threadIdx.x; i < nd; i += blockDim.x) {
       double m;
       const double* d = delta + (long)s * nd;
-      if (block == 4) {
-        const long c = i >> 1;
-        const int rr = (int)(i & 1);
-        const double* mm = ms + ((long)s * N + c) * 4 + 2 * rr;
-        m = mm[0] * d[2 * c] + mm[1] * d[2 * c + 1];
+      const int nl = (int)(nd / N);
+      if (block == nl * nl) {  // full per-cell block (1D block 4, XY block 16)
+        const long c = i / nl;
+        const int rr = (int)(i - c * nl);
+        const double* mm = ms + ((long)s * N + c) * block + nl * rr;
+        m = 0.0;
+        for (int q = 0; q < nl; ++q) m = fma(mm[q], d[nl * c + q], m);
       } else {
-        const int nl = (int)(nd / N);
         m = ms[(long)s * N + i / nl] * d[i];
       }
 #pragma unroll

@@ -232,6 +232,8 @@ struct Sweep2DArgs {
   const int* active;
   double* fout;          // kinetic output [S][nv][ndof] (null: no kinetic store)
   int nv;
+  const double* mt_blk;  // full per-cell 4x4 blocks [S][cells][16] (intra-cell-varying
+  const double* ms_blk;  // coefficients), or null: sigma * I from sig_t / sig_s
 };
 void launch_sweep2d(const Sweep2DArgs& a, cudaStream_t st);
 

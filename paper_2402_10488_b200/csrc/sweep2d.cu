@@ -118,6 +118,61 @@ __device__ __forceinline__ void solve_cell(const DirConst& dc, double sig, doubl
   Yo1 = dc.b * fma(s3, f[3], f[1]);
 }
 
+// General cell solve for full per-cell mass blocks (intra-cell-varying
+// coefficients): B = M + I (x) (a K) + (b K) (x) I with M the reflected 4x4
+// total-interaction block; LU without pivoting (the symmetric part of B is
+// positive definite), same face-trace algebra as solve_cell.
+__device__ __forceinline__ void solve_cell_full(const DirConst& dc, const double M[16], const double q[4], double X0,
+                                                double X1, double Y0, double Y1, double f[4], double& Xo0,
+                                                double& Xo1, double& Yo0, double& Yo1) {
+  const double s3 = kSqrt3;
+  double r[4];
+  r[0] = (q[0] + Y0) + X0;
+  r[1] = fma(-s3, X0, q[1] + Y1);
+  r[2] = fma(-s3, Y0, q[2] + X1);
+  r[3] = fma(-s3, X1 + Y1, q[3]);
+  double B[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) B[e] = M[e];
+  const double a = dc.a, b = dc.b;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int o = 2 * k;  // (I (x) aK): x-mode pair (o, o+1) of y-mode k
+    B[o * 4 + o] += a;
+    B[o * 4 + o + 1] += s3 * a;
+    B[(o + 1) * 4 + o] -= s3 * a;
+    B[(o + 1) * 4 + o + 1] += 3.0 * a;
+    // (bK (x) I): y-mode pair (k, k+2) of x-mode k
+    B[k * 4 + k] += b;
+    B[k * 4 + k + 2] += s3 * b;
+    B[(k + 2) * 4 + k] -= s3 * b;
+    B[(k + 2) * 4 + k + 2] += 3.0 * b;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double piv = fast_rcp(B[k * 4 + k]);
+#pragma unroll
+    for (int i = k + 1; i < 4; ++i) {
+      const double l = B[i * 4 + k] * piv;
+#pragma unroll
+      for (int j = k + 1; j < 4; ++j) B[i * 4 + j] = fma(-l, B[k * 4 + j], B[i * 4 + j]);
+      r[i] = fma(-l, r[k], r[i]);
+    }
+    B[k * 4 + k] = piv;
+  }
+#pragma unroll
+  for (int i = 3; i >= 0; --i) {
+    double v = r[i];
+#pragma unroll
+    for (int j = i + 1; j < 4; ++j) v = fma(-B[i * 4 + j], f[j], v);
+    f[i] = v * B[i * 4 + i];
+  }
+  Xo0 = a * fma(s3, f[1], f[0]);
+  Xo1 = a * fma(s3, f[3], f[2]);
+  Yo0 = b * fma(s3, f[2], f[0]);
+  Yo1 = b * fma(s3, f[3], f[1]);
+}
+
 struct Smem {
   double* red;    // [kC][kNW][4][32]
   double* ring;   // [kRC][kRP]: comps 0..3 = reflected q, 4 = sigma_t; row fastest
@@ -174,8 +229,9 @@ __device__ __forceinline__ void issue_chunk_loads(const Sweep2DArgs& a, const Sm
 }
 
 // stage -> ring (reflected source moments + sigma_t) for columns c0..c0+kC-1
+template <bool FULL>
 __device__ __forceinline__ void convert_chunk(const Sweep2DArgs& a, const Smem& sm, int c0, int band, double sx,
-                                              double sy) {
+                                              double sy, int s, int qx, int qy) {
   const int t = threadIdx.x;
   if (t >= kC * 32) return;
   const int col = c0 + (t >> 5), row = t & 31;
@@ -188,8 +244,19 @@ __device__ __forceinline__ void convert_chunk(const Sweep2DArgs& a, const Smem& 
       q0 = r[0]; q1 = r[1]; q2 = r[2]; q3 = r[3];
     } else {
       if (a.mode & SRC_MS_RHO) {
-        const double ss = r[9];
-        q0 = ss * r[0]; q1 = ss * r[1]; q2 = ss * r[2]; q3 = ss * r[3];
+        if (FULL) {
+          // full per-cell scattering block (physical orientation; reflected below)
+          const int ix = qx ? a.nx - 1 - col : col;
+          const int iy = qy ? a.ny - 1 - (band * 32 + row) : band * 32 + row;
+          const double* m = a.ms_blk + ((long)s * a.nx * a.ny + (long)iy * a.nx + ix) * 16;
+          q0 = m[0] * r[0] + m[1] * r[1] + m[2] * r[2] + m[3] * r[3];
+          q1 = m[4] * r[0] + m[5] * r[1] + m[6] * r[2] + m[7] * r[3];
+          q2 = m[8] * r[0] + m[9] * r[1] + m[10] * r[2] + m[11] * r[3];
+          q3 = m[12] * r[0] + m[13] * r[1] + m[14] * r[2] + m[15] * r[3];
+        } else {
+          const double ss = r[9];
+          q0 = ss * r[0]; q1 = ss * r[1]; q2 = ss * r[2]; q3 = ss * r[3];
+        }
       }
       if (a.mode & SRC_G) {
         q0 += r[4]; q1 += r[5]; q2 += r[6]; q3 += r[7];
@@ -204,7 +271,7 @@ __device__ __forceinline__ void convert_chunk(const Sweep2DArgs& a, const Smem& 
   dst[128] = sg;
 }
 
-template <int D, bool KIN>
+template <int D, bool KIN, bool FULL>
 __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const Sweep2DArgs a) {
   extern __shared__ double smraw[];
   constexpr int ndir = kNW * D;
@@ -277,7 +344,7 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
     issue_chunk_loads<D>(a, sm, 0, band, qx, qy, s, ybelow, 0);
     cp_async_wait_all();
     __syncthreads();
-    convert_chunk(a, sm, 0, band, sx, sy);
+    convert_chunk<FULL>(a, sm, 0, band, sx, sy, s, qx, qy);
 
     const int yr = band * 32 + lane;
     const bool row_ok = yr < ny;
@@ -311,6 +378,16 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
         const double sig = ok ? rg[128] : 1.0;
         if (!ok) q[0] = q[1] = q[2] = q[3] = 0.0;
         const double sig2 = sig * sig;
+        double M[FULL ? 16 : 1];
+        if (FULL) {
+          // reflected full block of this lane's cell: M'_ij = s_i s_j M_ij, s = (1, sx, sy, sx sy)
+          const int ix = qx ? nx - 1 - x : x;
+          const int iyy = qy ? ny - 1 - yr : yr;
+          const double* m = a.mt_blk + ((long)s * ncell + (long)iyy * nx + (ok ? ix : 0)) * 16;
+          const double sg[4] = {1.0, sx, sy, sx * sy};
+#pragma unroll
+          for (int e = 0; e < 16; ++e) M[e] = ok ? __ldg(m + e) * sg[e >> 2] * sg[e & 3] : (e % 5 == 0 ? 1.0 : 0.0);
+        }
         const double* yst = sm.ystg + ((ys * kC + kk) * ndir + warp * D) * 2;
         const bool lane0 = lane == 0;
         const bool from_below = lane0 && band > 0;
@@ -326,7 +403,10 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
           Y0 = lane0 ? (from_below ? ys0 : dc.bcy) : Y0;
           Y1 = lane0 ? (from_below ? ys1 : 0.0) : Y1;
           double f[4], xo0, xo1, yo0, yo1;
-          solve_cell(dc, sig, sig2, q, X[d][0], X[d][1], Y0, Y1, f, xo0, xo1, yo0, yo1);
+          if (FULL)
+            solve_cell_full(dc, M, q, X[d][0], X[d][1], Y0, Y1, f, xo0, xo1, yo0, yo1);
+          else
+            solve_cell(dc, sig, sig2, q, X[d][0], X[d][1], Y0, Y1, f, xo0, xo1, yo0, yo1);
           Y[d][0] = yo0;
           Y[d][1] = yo1;
           X[d][0] = ok ? xo0 : X[d][0];
@@ -389,7 +469,7 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
           }
         }
       }
-      if (k0 + kC < nx) convert_chunk(a, sm, k0 + kC, band, sx, sy);
+      if (k0 + kC < nx) convert_chunk<FULL>(a, sm, k0 + kC, band, sx, sy, s, qx, qy);
       ys ^= 1;
       if (threadIdx.x == 0 && band + 1 < nbands) {
         __threadfence();
@@ -408,14 +488,15 @@ size_t smem_bytes() {  // NOLINT
          sizeof(DirConst) * kNW * D;
 }
 
-template <int D, bool KIN>
+template <int D, bool KIN, bool FULL>
 void launch_d(const Sweep2DArgs& a, cudaStream_t st) {
   const size_t smem = smem_bytes<D>();
   static int max_ctas = -1;
   if (max_ctas < 0) {
-    RTE_CUDA(cudaFuncSetAttribute(sweep2d_kernel<D, KIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RTE_CUDA(cudaFuncSetAttribute(sweep2d_kernel<D, KIN, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     int per_sm = 0, dev = 0, sms = 0;
-    RTE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep2d_kernel<D, KIN>, kNW * 32, smem));
+    RTE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep2d_kernel<D, KIN, FULL>, kNW * 32, smem));
     RTE_CUDA(cudaGetDevice(&dev));
     RTE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     max_ctas = std::max(1, per_sm) * sms;
@@ -423,7 +504,7 @@ void launch_d(const Sweep2DArgs& a, cudaStream_t st) {
   const int nbands = (a.ny + 31) / 32;
   const long total = (long)nbands * a.S * 4 * a.groups;
   const int grid = (int)std::min<long>(total, max_ctas);
-  sweep2d_kernel<D, KIN><<<grid, kNW * 32, smem, st>>>(a);
+  sweep2d_kernel<D, KIN, FULL><<<grid, kNW * 32, smem, st>>>(a);
   RTE_CUDA(cudaGetLastError());
 }
 
@@ -462,24 +543,32 @@ __global__ void reduce_partials_kernel(int S, long nd, int nparts, const double*
 
 }  // namespace
 
-void launch_sweep2d(const Sweep2DArgs& a, cudaStream_t st) {
-  const int dpc = a.nq_pad / a.groups / kNW;  // directions per lane
+template <bool FULL>
+void launch_full(const Sweep2DArgs& a, cudaStream_t st, int dpc) {
   if (a.fout) {
     switch (dpc) {
-      case 1: return launch_d<1, true>(a, st);
-      case 2: return launch_d<2, true>(a, st);
-      case 4: return launch_d<4, true>(a, st);
-      case 8: return launch_d<8, true>(a, st);
+      case 1: return launch_d<1, true, FULL>(a, st);
+      case 2: return launch_d<2, true, FULL>(a, st);
+      case 4: return launch_d<4, true, FULL>(a, st);
+      case 8: return launch_d<8, true, FULL>(a, st);
       default: throw Error(RTE_ERR_UNSUPPORTED, "sweep2d: unsupported direction grouping");
     }
   }
   switch (dpc) {
-    case 1: return launch_d<1, false>(a, st);
-    case 2: return launch_d<2, false>(a, st);
-    case 4: return launch_d<4, false>(a, st);
-    case 8: return launch_d<8, false>(a, st);
+    case 1: return launch_d<1, false, FULL>(a, st);
+    case 2: return launch_d<2, false, FULL>(a, st);
+    case 4: return launch_d<4, false, FULL>(a, st);
+    case 8: return launch_d<8, false, FULL>(a, st);
     default: throw Error(RTE_ERR_UNSUPPORTED, "sweep2d: unsupported direction grouping");
   }
+}
+
+void launch_sweep2d(const Sweep2DArgs& a, cudaStream_t st) {
+  const int dpc = a.nq_pad / a.groups / kNW;  // directions per lane
+  if (a.mt_blk)
+    launch_full<true>(a, st, dpc);
+  else
+    launch_full<false>(a, st, dpc);
 }
 
 void launch_reduce_partials(int S, long nd, int nparts, const double* part, double* out, const double* rho_prev,

@@ -186,7 +186,11 @@ class TransportBatch:
     """
 
     def __init__(self, problem: ProblemDefinition, mesh: Mesh, quad: AngularQuadrature,
-                 mus: Sequence[Sequence[float]], device: int = 0):
+                 mus: Sequence[Sequence[float]], device: int = 0, force_full_blocks: bool = False):
+        """transport_system.cpp:82-109 for a batch of parameter samples.  XY
+        problems whose mass blocks are sigma I per cell use the closed-form
+        cell solves; intra-cell-varying coefficients (or force_full_blocks)
+        use full 4x4 per-cell blocks."""
         if not (problem.geometry == mesh.geometry == quad.geometry):
             raise ValueError("transport system: geometry mismatch")
         if not problem.terms:
@@ -218,10 +222,19 @@ class TransportBatch:
         g = mesh.project(_vals(problem.source, px, py)) if problem.source is not None else np.zeros(mesh.n_dof())
         inflow = (problem.inflow_left, problem.inflow_right, problem.inflow_bottom, problem.inflow_top)
         if mesh.geometry == XY2D:
-            mt_s, ms_s = _scalar_blocks(mt), _scalar_blocks(ms)
-            tmt_s, tms_s = _scalar_blocks(tmt), _scalar_blocks(tms)
-            self._create(mesh, quad, mt_s, ms_s, g, True, inflow, 1, device)
-            self._affine(K, tmt_s, tms_s, psi)
+            try:
+                # per-cell constant coefficients: sigma I blocks (closed-form cell solves)
+                mt_s, ms_s = _scalar_blocks(mt), _scalar_blocks(ms)
+                tmt_s, tms_s = _scalar_blocks(tmt), _scalar_blocks(tms)
+            except capi.RteError:
+                mt_s = None
+            if mt_s is not None and not force_full_blocks:
+                self._create(mesh, quad, mt_s, ms_s, g, True, inflow, 1, device)
+                self._affine(K, tmt_s, tms_s, psi)
+            else:
+                # intra-cell-varying coefficients: full 4x4 blocks per cell (block = 16)
+                self._create(mesh, quad, mt.reshape(S, -1, 16), ms.reshape(S, -1, 16), g, True, inflow, 16, device)
+                self._affine(K, tmt.reshape(K, -1, 16), tms.reshape(K, -1, 16), psi)
         else:
             self._create(mesh, quad, mt.reshape(S, -1, 4), ms.reshape(S, -1, 4), g, True, inflow, 4, device)
             self._affine(K, tmt.reshape(K, -1, 4), tms.reshape(K, -1, 4), psi)
