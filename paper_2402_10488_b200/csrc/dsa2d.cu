@@ -235,7 +235,6 @@ __device__ __forceinline__ void face_lift(int lev, int dir, const R* v, R* y) {
 template <typename R, typename T>
 __device__ __forceinline__ void face_mv(int lev, int dir, const T* __restrict__ xs, long nc, long cn, R* y) {
   R v[NB];
-#pragma unroll
   const T* p = xs + vblk(cn, NB);
 #pragma unroll
   for (int r = 0; r < NB; ++r) v[r] = (R)p[r * 32];

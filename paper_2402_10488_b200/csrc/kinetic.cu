@@ -180,8 +180,6 @@ __global__ void k_snap_step(int S, long kdim, long nd, int l, int window, double
                             int* __restrict__ conv, int* __restrict__ n_iter, const unsigned long long* bits) {
   const int s = blockIdx.y;
   if (!active[s]) return;
-  const double ch = __longlong_as_double((long long)bits[2 * s]);
-  const bool done = ch < eps;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < kdim; i += (long)gridDim.x * blockDim.x) {
     const double v = f[(long)s * kdim + i];
     if (l <= window) f_iter[((long)s * window + (l - 1)) * kdim + i] = v;
