@@ -69,6 +69,9 @@ struct Dsa2D {
   DBuf<double> Dint;          // [levels][144] constant internal-coupling part of the coarse diagonal
   // BiCGStab (fp64, natural order [S][12][nc]); the shadow residual is the rhs
   DBuf<double> r, p, v, s, t, x, rhs;
+  DBuf<double> xprev;         // previous solution per sample (warm start), natural layout
+  DBuf<int> has_prev;         // per sample: xprev holds a solution
+  bool warm = true;           // start BiCGStab from the best multiple of the previous solution
   DBuf<float> xa, xb;         // preconditioned directions M^-1 p, M^-1 s (fp32, red-black order)
   DBuf<float2> sig;           // fine (sigma_t, sigma_a) in red-black order for the V-cycle
   DBuf<double> scal;          // per sample scalars [S][16]
@@ -1081,6 +1084,123 @@ __global__ void __launch_bounds__(kBT) k_bicg_x(int S, unsigned n, unsigned nc, 
   if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_TS] = omega;
 }
 
+// Warm start.  v = K xprev (fp64, natural layout) with partials (v, b), (v, v).
+template <bool FULL>
+__global__ void __launch_bounds__(kBT, 2) k_apply_nat(int S, int nx, int ny, const double* __restrict__ sgt,
+                                                      const double* __restrict__ sgs, const double* __restrict__ xin,
+                                                      double* __restrict__ out, const double* __restrict__ b,
+                                                      double* __restrict__ part) {
+  const int s = blockIdx.y;
+  const long nc = (long)nx * ny;
+  const double* xs = xin + (long)s * nc * NB;
+  double a0 = 0.0, a1 = 0.0;
+  for (long c = (long)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (long)gridDim.x * blockDim.x) {
+    const int iy = (int)(c / nx), ix = (int)(c - (long)iy * nx);
+    double acc[NB], v[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) acc[r] = 0.0;
+    auto nbr = [&](int dir, long cn) {
+#pragma unroll
+      for (int r = 0; r < NB; ++r) v[r] = xs[r * nc + cn];
+      face_lift(0, dir, v, acc);
+    };
+    if (ix > 0) nbr(0, c - 1);
+    if (ix < nx - 1) nbr(1, c + 1);
+    if (iy > 0) nbr(2, c - nx);
+    if (iy < ny - 1) nbr(3, c + nx);
+#pragma unroll
+    for (int r = 0; r < NB; ++r) v[r] = xs[r * nc + c];
+    const long fi = (long)s * nc + c;
+    if (FULL) {
+      fine_block_mv(0.0, 0.0, v, acc);
+      const double* bt = sgt + fi * 16;
+      const double* bs = sgs + fi * 16;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double ar = 0.0, ax = 0.0, ay = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double mt = bt[4 * i + k];
+          ar = fma(mt - bs[4 * i + k], v[k], ar);
+          ax = fma(mt, v[4 + k], ax);
+          ay = fma(mt, v[8 + k], ay);
+        }
+        acc[i] += ar;
+        acc[4 + i] = fma(c_m2x3, ax, acc[4 + i]);
+        acc[8 + i] = fma(c_m2y3, ay, acc[8 + i]);
+      }
+    } else {
+      fine_block_mv(sgt[fi], sgt[fi] - sgs[fi], v, acc);
+    }
+    double* yo = out + (long)s * nc * NB + c;
+    const double* bb = b + (long)s * nc * NB + c;
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      yo[r * nc] = acc[r];
+      a0 = fma(acc[r], bb[r * nc], a0);
+      a1 = fma(acc[r], acc[r], a1);
+    }
+  }
+  block_parts(a0, a1, 2, part, s);
+}
+
+// gamma = (K xprev, b) / (K xprev, K xprev) per sample (0 without a previous
+// solution or for an unselected sample, whose xprev is carried over);
+// x = gamma xprev, r = b - gamma K xprev; partials (b, r), (r, r)
+__global__ void __launch_bounds__(kBT) k_warm_init(int S, long n, int nblk, const double* part, const int* has_prev,
+                                                   const int* __restrict__ kind, const double* __restrict__ xprev,
+                                                   const double* __restrict__ kxp, const double* __restrict__ b,
+                                                   double* __restrict__ x, double* __restrict__ r,
+                                                   double* __restrict__ part2) {
+  const int s = blockIdx.y;
+  double q[2];
+  reduce_parts(part, s, nblk, 2, q);
+  const bool selected = !kind || kind[s] == KIND_DSA;
+  const double gam = (selected && has_prev[s] && q[1] > 0.0) ? q[0] / q[1] : 0.0;
+  const long base = (long)s * n;
+  double a0 = 0.0, a1 = 0.0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const double bi = b[base + i];
+    const double xp = xprev[base + i];
+    // unselected samples (b == 0, inactive) keep their previous solution in x
+    const double xi = selected ? gam * xp : xp;
+    const double ri = fma(-gam, kxp[base + i], bi);
+    x[base + i] = xi;
+    r[base + i] = ri;
+    a0 = fma(bi, ri, a0);
+    a1 = fma(ri, ri, a1);
+  }
+  block_parts(a0, a1, 2, part2, s);
+}
+
+// warm-start bookkeeping: bnorm2 from part (q0), rho = (b, r) and rnorm2 = (r, r) from part2
+__global__ void k_bicg_init_warm(int S, int nblk, const double* part, const double* part2, double* scal, int* act,
+                                 double tol2, int* nact) {
+  const int s = blockIdx.x;
+  double q[2], w[2];
+  reduce_parts(part, s, nblk, 1, q);
+  reduce_parts(part2, s, nblk, 2, w);
+  if (threadIdx.x != 0) return;
+  double* sc = scal + s * 16;
+  const double bn = q[0];
+  sc[SC_RHO_OLD] = 1.0;
+  sc[SC_ALPHA] = 1.0;
+  sc[SC_OMEGA] = 1.0;
+  sc[SC_BNORM2] = bn;
+  sc[SC_RNORM2] = w[1];
+  sc[SC_RHO_NEW] = w[0];
+  sc[SC_ITERS] = 0;
+  const bool done = !(bn > 0.0) || w[1] <= tol2 * bn;
+  sc[SC_CONV] = done ? 1 : 0;
+  act[s] = done ? 0 : 1;
+  if (!done) atomicAdd(nact, 1);
+}
+
+__global__ void k_mark_prev(int S, const double* scal, int* has_prev) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < S && scal[s * 16 + SC_BNORM2] > 0.0) has_prev[s] = 1;
+}
+
 // scalar bookkeeping + convergence: rnorm2 = (r, r), next rho = (rh, r)
 __global__ void k_bicg_check(int S, int nblk, const double* part, double* scal, int* act, double tol2, int maxit,
                              int* nact) {
@@ -1155,6 +1275,9 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   d->ctx = ctx;
   if (const char* e = std::getenv("RTE_DSA_NU")) d->nu = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_NU_COARSE")) d->nu_coarse = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("RTE_DSA_WARM")) d->warm = std::atoi(e) != 0;
+  d->xprev.release();
+  d->has_prev.release();
   // moments (dsa.cpp:167-192, 223-226)
   double m1x = 0, m2x = 0, m3x = 0, m1y = 0, m2y = 0, m3y = 0, m3yx = 0, m3xy = 0;
   for (int j = 0; j < ctx->nv; ++j) {
@@ -1532,10 +1655,42 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   ++d->nlaunch;
   k_pack_rhs<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, rhs, ctx->ms.p, apply_ms, d->full ? 1 : 0, d->rhs.p,
                                                        kind);
-  RTE_CUDA(cudaMemsetAsync(d->x.p, 0, sizeof(double) * S * n, st));
   RTE_CUDA(cudaMemsetAsync(d->p.p, 0, sizeof(double) * S * n, st));
-  RTE_CUDA(cudaMemsetAsync(d->v.p, 0, sizeof(double) * S * n, st));
-  RTE_CUDA(cudaMemcpyAsync(d->r.p, d->rhs.p, sizeof(double) * S * n, cudaMemcpyDeviceToDevice, st));
+  const double tol2 = d->tol * d->tol;
+  int* nact_h = nullptr;
+  RTE_CUDA(cudaMallocHost(&nact_h, sizeof(int)));
+  if (d->warm && !d->xprev.p) {
+    d->xprev.alloc((size_t)S * n);
+    d->xprev.zero(st);
+    d->has_prev.alloc(S);
+    d->has_prev.zero(st);
+  }
+  if (d->warm) {
+    // x0 = gamma xprev minimising ||b - gamma K xprev||_2 per sample (v is scratch for K xprev)
+    ++d->nlaunch;
+    if (d->full)
+      k_apply_nat<true><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xprev.p, d->v.p, d->rhs.p,
+                                               d->part.p);
+    else
+      k_apply_nat<false><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xprev.p, d->v.p, d->rhs.p,
+                                                d->part.p);
+    ++d->nlaunch;
+    k_warm_init<<<vgrid, kBT, 0, st>>>(S, n, d->nblk, d->part.p, d->has_prev.p, kind, d->xprev.p, d->v.p,
+                                       d->rhs.p, d->x.p, d->r.p, d->part2.p);
+    RTE_CUDA(cudaMemsetAsync(d->v.p, 0, sizeof(double) * S * n, st));
+  } else {
+    RTE_CUDA(cudaMemsetAsync(d->x.p, 0, sizeof(double) * S * n, st));
+    RTE_CUDA(cudaMemsetAsync(d->v.p, 0, sizeof(double) * S * n, st));
+    RTE_CUDA(cudaMemcpyAsync(d->r.p, d->rhs.p, sizeof(double) * S * n, cudaMemcpyDeviceToDevice, st));
+    DotArgs a{};
+    a.a[0] = d->rhs.p;
+    a.b[0] = d->rhs.p;
+    a.a[1] = d->rhs.p;
+    a.b[1] = d->rhs.p;
+    a.nq = 2;
+    ++d->nlaunch;
+    k_dots<<<vgrid, kBT, 0, st>>>(S, n, a, d->part2.p, nullptr);  // (b, r), (r, r) with r = b
+  }
   {
     DotArgs a{};
     a.a[0] = d->rhs.p;
@@ -1544,16 +1699,17 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     ++d->nlaunch;
     k_dots<<<vgrid, kBT, 0, st>>>(S, n, a, d->part.p, nullptr);
   }
+  RTE_CUDA(cudaMemsetAsync(d->nact.p, 0, sizeof(int), st));
   ++d->nlaunch;
-  k_bicg_init<<<(S + 127) / 128, 128, 0, st>>>(S, d->nblk, d->part.p, d->scal.p, d->act.p, nullptr);
+  k_bicg_init_warm<<<S, 32, 0, st>>>(S, d->nblk, d->part.p, d->part2.p, d->scal.p, d->act.p, tol2, d->nact.p);
   RTE_CUDA(cudaGetLastError());
-  const double tol2 = d->tol * d->tol;
-  int* nact_h = nullptr;
-  RTE_CUDA(cudaMallocHost(&nact_h, sizeof(int)));
+  RTE_CUDA(cudaMemcpyAsync(nact_h, d->nact.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RTE_CUDA(cudaStreamSynchronize(st));
   int it = 0;
+  const bool any_active = *nact_h > 0;
   float* b0 = l0.b.p;
   static const bool trace = std::getenv("RTE_DSA_TRACE") != nullptr;
-  for (; it < d->maxit; ++it) {
+  for (; any_active && it < d->maxit; ++it) {
     ++d->nlaunch;
     k_bicg_p<<<vgrid, kBT, 0, st>>>(S, un, unc, unx, d->scal.p, d->r.p, d->p.p, d->v.p, b0, d->act.p);
     vcycle(d, 0, b0, d->xa.p, d->act.p, st);
@@ -1600,9 +1756,17 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   }
   cudaFreeHost(nact_h);
   d->last_iters = it;
+  static const bool report = std::getenv("RTE_DSA_REPORT") != nullptr;
+  if (report) std::fprintf(stderr, "[dsa2d] solve: %d BiCGStab iterations%s\n", it, d->warm ? " (warm start)" : "");
   ++d->nlaunch;
   k_unpack<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, d->x.p, out, kind);
   RTE_CUDA(cudaGetLastError());
+  if (d->warm) {
+    // keep this solution (unselected samples carried their previous one in x)
+    std::swap(d->x, d->xprev);
+    ++d->nlaunch;
+    k_mark_prev<<<(S + 127) / 128, 128, 0, st>>>(S, d->scal.p, d->has_prev.p);
+  }
 }
 
 void dsa2d_destroy(void* p) { delete static_cast<Dsa2D*>(p); }
