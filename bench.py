@@ -5,11 +5,14 @@ Workload (BASELINE.json configs[4], the 2D sweep-throughput stress config):
 [0,1]^2 at 1024x1024 cells, 256 unique directions (CL(32,16): 8 polar x 32
 azimuthal per hemisphere, +/-vz folded), 16 samples with per-cell
 sigma_t ~ logU[0.1,100] and c ~ U[0.5,0.99] drawn from seed, q = 1, vacuum.
-One step = one source iteration over the whole batch: the upwind sweep of
+One step = one SI-DSA iteration over the whole batch: the upwind sweep of
 every (cell, direction, sample) with the fused source update and scalar-flux
-reduction, the per-sample change norm, and the DSA correction when the build
-provides it for XY geometry (see config.dsa).  Metric: cell*direction*sample
-sweep updates per second (updates counted over unique directions).
+reduction, the per-sample change norm, and the DSA correction (device
+BiCGStab + multigrid to a relative residual of --dsa-tol).  The default run
+is the config's "fixed 20 source iterations with DSA" (3 warm-up + 20 timed).
+Metric: cell*direction*sample sweep updates per second of the whole step
+(updates counted over unique directions); the sweep kernel alone is reported
+as sweep_only_updates_per_s and sweep_roofline.
 
 Contract: `python bench.py --gpus N --steps K --warmup W [--impl reference]`
 prints one JSON line (rank 0).  Multi-GPU: samples shard across ranks (weak
@@ -357,7 +360,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)  # configs[4]: a fixed 20 source iterations with DSA
     ap.add_argument("--dsa-tol", type=float, default=1e-8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
