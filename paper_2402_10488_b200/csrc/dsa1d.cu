@@ -13,9 +13,12 @@
 // quadrature moments (dsa.cpp:167-192).  After scaling the J rows by 3 the
 // matrix is positive-real, so block elimination without
 // inter-block pivoting is stable; each 4x4 pivot block is inverted with
-// partial pivoting.  Setup factors once per sample (block Thomas: stores
-// Dt_i^{-1}, G_i = L_i Dt_{i-1}^{-1}, U_i); each correction is one forward
-// and one backward block substitution.  Samples run in parallel.
+// partial pivoting.  The system is solved by batched block cyclic reduction
+// (one CTA per sample, ceil(log2 N) levels): setup eliminates the odd
+// equations of every level once and stores, per level, D^{-1}, L, U of the
+// eliminated equations and A = L D_{p-1}^{-1}, C = U D_{p+1}^{-1} of the kept
+// ones; each correction is then log2 N forward rhs-reduction levels and log2 N
+// back-substitution levels, every level parallel over its equations.
 #include "rte_internal.cuh"
 
 namespace rte {
@@ -142,33 +145,102 @@ __device__ void cell_blocks(const Dsa1DArgs& a, int s, int i, double* D, double*
   }
 }
 
-// Block Thomas factorization, one thread per sample.
-__global__ void dsa1d_factor(const Dsa1DArgs a) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= a.S) return;
-  double D[16], L[16], U[16], Dt[16], inv[16], prev_inv[16], G[16], GU[16];
-  for (int i = 0; i < a.N; ++i) {
-    cell_blocks(a, s, i, D, L, U);
-    double* f = a.fac + ((long)s * a.N + i) * 48;
-    if (i == 0) {
-      for (int e = 0; e < 16; ++e) Dt[e] = D[e];
-      for (int e = 0; e < 16; ++e) G[e] = 0;
-    } else {
-      mm4(L, prev_inv, G);
-      double Uprev[16];
-      const double* fp = a.fac + ((long)s * a.N + i - 1) * 48;
-      for (int e = 0; e < 16; ++e) Uprev[e] = fp[32 + e];
-      mm4(G, Uprev, GU);
-      for (int e = 0; e < 16; ++e) Dt[e] = D[e] - GU[e];
-    }
-    inv4(Dt, inv);
-    for (int e = 0; e < 16; ++e) {
-      f[e] = inv[e];
-      f[16 + e] = G[e];
-      f[32 + e] = U[e];
-      prev_inv[e] = inv[e];
-    }
+constexpr int kCrThreads = 256;
+
+// level sizes of the reduction: n_0 = N, n_{l+1} = ceil(n_l / 2) until 1
+__host__ __device__ inline int cr_levels(int N) {
+  int l = 0;
+  for (int n = N; n > 1; n = (n + 1) / 2) ++l;
+  return l;
+}
+__host__ __device__ inline long cr_entries(int N) {  // sum of n_l over all levels incl. the last (1)
+  long t = 0;
+  int n = N;
+  for (;;) {
+    t += n;
+    if (n == 1) break;
+    n = (n + 1) / 2;
   }
+  return t;
+}
+
+__device__ inline void mv4(const double* m, const double* x, double* y) {
+  for (int r = 0; r < 4; ++r) y[r] = m[4 * r] * x[0] + m[4 * r + 1] * x[1] + m[4 * r + 2] * x[2] + m[4 * r + 3] * x[3];
+}
+
+// Block cyclic reduction setup, one CTA per sample.  work: [S][2][N][48]
+// ping-pong of the current level's (D, L, U) per position; fac: per level l
+// and position p (offset off_l + p): odd p -> (D^{-1}, L, U), even p ->
+// (A, C, -); the last level's single entry holds D^{-1}.
+__global__ void __launch_bounds__(kCrThreads) dsa1d_factor_cr(const Dsa1DArgs a, double* __restrict__ work) {
+  const int s = blockIdx.x;
+  const int N = a.N;
+  double* cur = work + (long)s * 2 * N * 48;
+  double* nxt = cur + (long)N * 48;
+  double* fac = a.fac + (long)s * cr_entries(N) * 48;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    double* e = cur + (long)i * 48;
+    cell_blocks(a, s, i, e, e + 16, e + 32);
+  }
+  __syncthreads();
+  long off = 0;
+  for (int n = N; n > 1; n = (n + 1) / 2) {
+    double* f = fac + off * 48;
+    // eliminated (odd) equations: D^{-1}, L, U
+    for (int p = 1 + 2 * threadIdx.x; p < n; p += 2 * blockDim.x) {
+      const double* e = cur + (long)p * 48;
+      double* o = f + (long)p * 48;
+      inv4(e, o);
+      for (int k = 0; k < 32; ++k) o[16 + k] = e[16 + k];
+    }
+    __syncthreads();
+    // kept (even) equations: A = L D_{p-1}^{-1}, C = U D_{p+1}^{-1}; next-level blocks
+    for (int p = 2 * threadIdx.x; p < n; p += 2 * blockDim.x) {
+      const double* e = cur + (long)p * 48;
+      double D[16], L[16], U[16], A[16], C[16], t[16];
+      for (int k = 0; k < 16; ++k) {
+        D[k] = e[k];
+        L[k] = 0.0;
+        U[k] = 0.0;
+        A[k] = 0.0;
+        C[k] = 0.0;
+      }
+      if (p >= 1) {
+        const double* m = f + (long)(p - 1) * 48;  // D^{-1}, L, U of equation p-1
+        mm4(e + 16, m, A);
+        mm4(A, m + 32, t);  // A U_{p-1}
+        for (int k = 0; k < 16; ++k) D[k] -= t[k];
+        mm4(A, m + 16, t);  // A L_{p-1}
+        for (int k = 0; k < 16; ++k) L[k] = -t[k];
+      }
+      if (p + 1 < n) {
+        const double* m = f + (long)(p + 1) * 48;
+        mm4(e + 32, m, C);
+        mm4(C, m + 16, t);  // C L_{p+1}
+        for (int k = 0; k < 16; ++k) D[k] -= t[k];
+        mm4(C, m + 32, t);  // C U_{p+1}
+        for (int k = 0; k < 16; ++k) U[k] = -t[k];
+      }
+      double* o = f + (long)p * 48;
+      for (int k = 0; k < 16; ++k) {
+        o[k] = A[k];
+        o[16 + k] = C[k];
+        o[32 + k] = 0.0;
+      }
+      double* q = nxt + (long)(p / 2) * 48;
+      for (int k = 0; k < 16; ++k) {
+        q[k] = D[k];
+        q[16 + k] = L[k];
+        q[32 + k] = U[k];
+      }
+    }
+    __syncthreads();
+    double* tmp = cur;
+    cur = nxt;
+    nxt = tmp;
+    off += n;
+  }
+  if (threadIdx.x == 0) inv4(cur, fac + off * 48);
 }
 
 struct Dsa1DSolve {
@@ -177,58 +249,101 @@ struct Dsa1DSolve {
   const double* ms;      // to form Ms * delta when apply_ms
   const double* rhs;     // [S][2N]
   double* out;           // [S][2N]
-  double* work;          // [S][N][4]
+  double* work;          // [S][N][4]: reduced right-hand sides, then the solution
   const int* kind;       // optional mask: only samples with kind == KIND_DSA
   int apply_ms;
 };
 
-__global__ void dsa1d_solve(const Dsa1DSolve a) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= a.S) return;
+// Block cyclic reduction solve, one CTA per sample.
+__global__ void __launch_bounds__(kCrThreads) dsa1d_solve_cr(const Dsa1DSolve a) {
+  const int s = blockIdx.x;
   if (a.kind && a.kind[s] != KIND_DSA) return;
-  const long nd = 2L * a.N;
+  const int N = a.N;
+  const long nd = 2L * N;
   const double* r = a.rhs + (long)s * nd;
-  double* y = a.work + (long)s * a.N * 4;
-  double yp[4] = {0, 0, 0, 0};
-  for (int i = 0; i < a.N; ++i) {
-    const double* f = a.fac + ((long)s * a.N + i) * 48;
+  double* y = a.work + (long)s * N * 4;
+  const double* fac = a.fac + (long)s * cr_entries(N) * 48;
+  // rhs [(Ms) rho ; 0] per cell
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
     double r0 = r[2 * i], r1 = r[2 * i + 1];
     if (a.apply_ms) {
       if (a.block == 4) {
-        const double* m = a.ms + ((long)s * a.N + i) * 4;
+        const double* m = a.ms + ((long)s * N + i) * 4;
         const double t0 = m[0] * r0 + m[1] * r1, t1 = m[2] * r0 + m[3] * r1;
         r0 = t0;
         r1 = t1;
       } else {
-        const double sg = a.ms[(long)s * a.N + i];
+        const double sg = a.ms[(long)s * N + i];
         r0 *= sg;
         r1 *= sg;
       }
     }
-    double v[4] = {r0, r1, 0.0, 0.0};
-    if (i > 0)
-      for (int k = 0; k < 4; ++k)
-        v[k] -= f[16 + 4 * k] * yp[0] + f[16 + 4 * k + 1] * yp[1] + f[16 + 4 * k + 2] * yp[2] +
-                f[16 + 4 * k + 3] * yp[3];
-    for (int k = 0; k < 4; ++k) {
-      y[4 * i + k] = v[k];
-      yp[k] = v[k];
+    y[4 * i] = r0;
+    y[4 * i + 1] = r1;
+    y[4 * i + 2] = 0.0;
+    y[4 * i + 3] = 0.0;
+  }
+  __syncthreads();
+  // forward: at level l (stride st) kept equation p (index p*st) absorbs its odd neighbours
+  long off = 0;
+  int st = 1, L = 0;
+  for (int n = N; n > 1; n = (n + 1) / 2, st *= 2, ++L) {
+    const double* f = fac + off * 48;
+    for (int p = 2 * threadIdx.x; p < n; p += 2 * blockDim.x) {
+      const double* e = f + (long)p * 48;
+      double v[4], t[4];
+      for (int k = 0; k < 4; ++k) v[k] = y[4L * p * st + k];
+      if (p >= 1) {
+        mv4(e, y + 4L * (p - 1) * st, t);
+        for (int k = 0; k < 4; ++k) v[k] -= t[k];
+      }
+      if (p + 1 < n) {
+        mv4(e + 16, y + 4L * (p + 1) * st, t);
+        for (int k = 0; k < 4; ++k) v[k] -= t[k];
+      }
+      for (int k = 0; k < 4; ++k) y[4L * p * st + k] = v[k];
+    }
+    __syncthreads();
+    off += n;
+  }
+  if (threadIdx.x == 0) {
+    double t[4];
+    mv4(fac + off * 48, y, t);
+    for (int k = 0; k < 4; ++k) y[k] = t[k];
+  }
+  __syncthreads();
+  // backward: odd equations of each level from the top, x = D^{-1} (y - L x_{p-1} - U x_{p+1})
+  int ns[32];
+  {
+    int n = N, l = 0;
+    while (n > 1) {
+      ns[l++] = n;
+      n = (n + 1) / 2;
     }
   }
-  double xn[4] = {0, 0, 0, 0};
-  for (int i = a.N - 1; i >= 0; --i) {
-    const double* f = a.fac + ((long)s * a.N + i) * 48;
-    double v[4];
-    for (int k = 0; k < 4; ++k) v[k] = y[4 * i + k];
-    if (i < a.N - 1)
-      for (int k = 0; k < 4; ++k)
-        v[k] -= f[32 + 4 * k] * xn[0] + f[32 + 4 * k + 1] * xn[1] + f[32 + 4 * k + 2] * xn[2] +
-                f[32 + 4 * k + 3] * xn[3];
-    double x[4];
-    for (int k = 0; k < 4; ++k) x[k] = f[4 * k] * v[0] + f[4 * k + 1] * v[1] + f[4 * k + 2] * v[2] + f[4 * k + 3] * v[3];
-    for (int k = 0; k < 4; ++k) xn[k] = x[k];
-    a.out[(long)s * nd + 2 * i] = x[0];
-    a.out[(long)s * nd + 2 * i + 1] = x[1];
+  for (int l = L - 1; l >= 0; --l) {
+    const int n = ns[l];
+    const int stl = 1 << l;
+    off -= n;
+    const double* f = fac + off * 48;
+    for (int p = 1 + 2 * threadIdx.x; p < n; p += 2 * blockDim.x) {
+      const double* e = f + (long)p * 48;
+      double v[4], t[4];
+      for (int k = 0; k < 4; ++k) v[k] = y[4L * p * stl + k];
+      mv4(e + 16, y + 4L * (p - 1) * stl, t);
+      for (int k = 0; k < 4; ++k) v[k] -= t[k];
+      if (p + 1 < n) {
+        mv4(e + 32, y + 4L * (p + 1) * stl, t);
+        for (int k = 0; k < 4; ++k) v[k] -= t[k];
+      }
+      mv4(e, v, t);
+      for (int k = 0; k < 4; ++k) y[4L * p * stl + k] = t[k];
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    a.out[(long)s * nd + 2 * i] = y[4 * i];
+    a.out[(long)s * nd + 2 * i + 1] = y[4 * i + 1];
   }
 }
 
@@ -261,10 +376,13 @@ void dsa_setup(rte_ctx* ctx, cudaStream_t st) {
   d->nf = 2;
   d->dim = 2 * ctx->ndof;
   moments(ctx->vx, ctx->w, d->m1, d->m2, d->m3);
-  d->fac.alloc((size_t)ctx->S * ctx->ncells * 48);
+  d->fac.alloc((size_t)ctx->S * cr_entries(ctx->ncells) * 48);
   Dsa1DArgs a{ctx->S, ctx->ncells, ctx->block, ctx->width.p, ctx->mt.p, ctx->ms.p, d->m1, d->m2, d->m3, d->fac.p};
-  dsa1d_factor<<<(ctx->S + 63) / 64, 64, 0, st>>>(a);
+  DBuf<double> work;
+  work.alloc((size_t)ctx->S * 2 * ctx->ncells * 48);
+  dsa1d_factor_cr<<<ctx->S, kCrThreads, 0, st>>>(a, work.p);
   RTE_CUDA(cudaGetLastError());
+  RTE_CUDA(cudaStreamSynchronize(st));
 }
 
 // out = C rhs (solve_density) or C Ms rhs (correct) depending on apply_ms;
@@ -277,7 +395,7 @@ void dsa_apply(rte_ctx* ctx, const double* rhs, double* out, const int* kind, in
   }
   ctx->ws_e.alloc((size_t)ctx->S * ctx->ncells * 4);
   Dsa1DSolve a{ctx->S, ctx->ncells, ctx->block, ctx->dsa->fac.p, ctx->ms.p, rhs, out, ctx->ws_e.p, kind, apply_ms};
-  dsa1d_solve<<<(ctx->S + 31) / 32, 32, 0, st>>>(a);
+  dsa1d_solve_cr<<<ctx->S, std::min(kCrThreads, std::max(32, (ctx->ncells + 1) / 2 / 32 * 32 + 32)), 0, st>>>(a);
   RTE_CUDA(cudaGetLastError());
 }
 

@@ -101,7 +101,7 @@ struct DsaState {
   int nf = 2;
   long dim = 0;
   double m1 = 0, m2 = 0, m3 = 0;
-  DBuf<double> fac;         // slab: [S][N][48] block-Thomas factors
+  DBuf<double> fac;         // slab: [S][sum of CR level sizes][48] block cyclic reduction factors
   void* impl2d = nullptr;   // xy: multigrid/Krylov state (dsa2d.cu)
 };
 struct RomState;
