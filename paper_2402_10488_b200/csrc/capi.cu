@@ -515,6 +515,7 @@ int rte_create(const rte_problem* p, int device, rte_ctx** out) {
 void rte_destroy(rte_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
+  if (ctx->pinned_int) cudaFreeHost(ctx->pinned_int);
   delete ctx;
 }
 
@@ -694,8 +695,8 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
     const bool need_dsa = cfg.method == RTE_DSA || cfg.method == RTE_ROMSAD || cfg.method == RTE_ROMIG;
     const bool need_rom = cfg.method == RTE_ROMSA || cfg.method == RTE_ROMSAD;
     if (need_dsa && !ctx->dsa) dsa_setup(ctx, st);
-    DBuf<int> ibuf;
-    ibuf.alloc((size_t)S * 8 + 1);
+    DBuf<int>& ibuf = ctx->si_ibuf;
+    ibuf.ensure((size_t)S * 8 + 1);
     SiState sst{};
     sst.active = ibuf.p;
     sst.iters = ibuf.p + S;
@@ -704,24 +705,25 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
     sst.converged = ibuf.p + 4 * S;
     sst.singular = ibuf.p + 5 * S;
     sst.switch_iter = ibuf.p + 6 * S;
-    DBuf<int> sing;
+    DBuf<int>& sing = ctx->si_int;
     if (need_rom) {
-      sing.alloc(S);
+      sing.ensure(S);
       rom_setup(ctx, 1, sing.p, st);
     }
     sst.n_active = ibuf.p + 8 * S;
-    DBuf<double> hist, lastc;
-    hist.alloc((size_t)S * cfg.max_iters);
-    hist.zero(st);
-    lastc.alloc(S);
+    DBuf<double>& hist = ctx->si_hist;
+    DBuf<double>& lastc = ctx->si_lastc;
+    hist.ensure((size_t)S * cfg.max_iters);
+    RTE_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(double) * S * cfg.max_iters, st));
+    lastc.ensure(S);
     sst.history = hist.p;
     sst.last_change = lastc.p;
-    DBuf<char> lg;
-    lg.alloc((size_t)S * cfg.max_iters);
+    DBuf<char>& lg = ctx->si_log;
+    lg.ensure((size_t)S * cfg.max_iters);
     RTE_CUDA(cudaMemsetAsync(lg.p, 0, (size_t)S * cfg.max_iters, st));
     sst.log = lg.p;
-    DBuf<unsigned long long> bits;
-    bits.alloc((size_t)2 * S);
+    DBuf<unsigned long long>& bits = ctx->si_bits;
+    bits.ensure((size_t)2 * S);
     sst.change_bits = bits.p;
     init_state_kernel<<<(S + 127) / 128, 128, 0, st>>>(S, sst, need_rom ? sing.p : nullptr, cfg.method);
     RTE_CUDA(cudaGetLastError());
@@ -753,10 +755,10 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
     RTE_REQUIRE(cfg.method != RTE_CUSTOM || cfg.correct, RTE_ERR_INVALID, "si_solve: RTE_CUSTOM needs a callback");
     std::vector<int> kinds_h(S), active_h(S);
     std::vector<char> letters_h(S);
-    DBuf<char> letters_d;
-    letters_d.alloc(S);
-    int* n_active_host = nullptr;
-    RTE_CUDA(cudaMallocHost(&n_active_host, sizeof(int)));
+    DBuf<char>& letters_d = ctx->si_letters;
+    letters_d.ensure(S);
+    if (!ctx->pinned_int) RTE_CUDA(cudaMallocHost(&ctx->pinned_int, sizeof(int)));
+    int* n_active_host = ctx->pinned_int;
     const int fin_bx = (int)std::min<long>((nd + 255) / 256, std::max(1, 8192 / S));
     int l = 1;
     try {
@@ -807,10 +809,8 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
         }
       }
     } catch (...) {
-      cudaFreeHost(n_active_host);
       throw;
     }
-    cudaFreeHost(n_active_host);
 
     std::vector<double> resid(S, 0.0);
     if (cfg.compute_residual) {

@@ -72,6 +72,10 @@ struct Dsa2D {
   DBuf<double> xprev;         // previous solution per sample (warm start), natural layout
   DBuf<int> has_prev;         // per sample: xprev holds a solution
   bool warm = true;           // start BiCGStab from the best multiple of the previous solution
+  int* nact_h = nullptr;      // pinned poll target
+  ~Dsa2D() {
+    if (nact_h) cudaFreeHost(nact_h);
+  }
   DBuf<float> xa, xb;         // preconditioned directions M^-1 p, M^-1 s (fp32, red-black order)
   DBuf<float2> sig;           // fine (sigma_t, sigma_a) in red-black order for the V-cycle
   DBuf<double> scal;          // per sample scalars [S][16]
@@ -1657,8 +1661,8 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
                                                        kind);
   RTE_CUDA(cudaMemsetAsync(d->p.p, 0, sizeof(double) * S * n, st));
   const double tol2 = d->tol * d->tol;
-  int* nact_h = nullptr;
-  RTE_CUDA(cudaMallocHost(&nact_h, sizeof(int)));
+  if (!d->nact_h) RTE_CUDA(cudaMallocHost(&d->nact_h, sizeof(int)));
+  int* nact_h = d->nact_h;
   if (d->warm && !d->xprev.p) {
     d->xprev.alloc((size_t)S * n);
     d->xprev.zero(st);
@@ -1754,7 +1758,6 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
       }
     }
   }
-  cudaFreeHost(nact_h);
   d->last_iters = it;
   static const bool report = std::getenv("RTE_DSA_REPORT") != nullptr;
   if (report) std::fprintf(stderr, "[dsa2d] solve: %d BiCGStab iterations%s\n", it, d->warm ? " (warm start)" : "");

@@ -68,6 +68,11 @@ struct DBuf {
     RTE_CUDA(cudaMalloc(&p, count * sizeof(T)));
     n = count;
   }
+  // grow-only variant for per-context scratch reused across calls
+  void ensure(size_t count) {
+    if (p && count <= n) return;
+    alloc(count);
+  }
   void upload(const T* host, size_t count) {
     alloc(count);
     if (count) RTE_CUDA(cudaMemcpy(p, host, count * sizeof(T), cudaMemcpyHostToDevice));
@@ -137,6 +142,12 @@ struct rte_ctx {
 
   // workspace (lazily sized)
   rte::DBuf<double> ws_a, ws_b, ws_c, ws_d, ws_e, ws_part;
+  // SI driver scratch reused across rte_si_solve calls (no cudaMalloc per solve)
+  rte::DBuf<int> si_ibuf, si_int;
+  rte::DBuf<double> si_hist, si_lastc;
+  rte::DBuf<char> si_log, si_letters;
+  rte::DBuf<unsigned long long> si_bits;
+  int* pinned_int = nullptr;  // cudaMallocHost, one int for the active-count poll
   rte::DBuf<unsigned long long> ws_bits;
   rte::DBuf<unsigned int> ws_sync;
   rte::DBuf<rte::Slot2D> slot_tab;  // cached all-slot sweep table (2D)
