@@ -73,8 +73,28 @@ struct Dsa2D {
   DBuf<int> has_prev;         // per sample: xprev holds a solution
   bool warm = true;           // start BiCGStab from the best multiple of the previous solution
   int* nact_h = nullptr;      // pinned poll target
+  // CUDA graphs of one BiCGStab iteration (keyed by the iterate buffer, which
+  // alternates with the warm-start buffer, and by the stopping parameters)
+  struct Graph {
+    const void* key;
+    double tol;
+    int maxit;
+    cudaGraphExec_t exec;
+    long launches;
+  };
+  std::vector<Graph> graphs;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  void clear_graphs() {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    graphs.clear();
+  }
   ~Dsa2D() {
     if (nact_h) cudaFreeHost(nact_h);
+    clear_graphs();
+    if (gstream) cudaStreamDestroy(gstream);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
   }
   DBuf<float> xa, xb;         // preconditioned directions M^-1 p, M^-1 s (fp32, red-black order)
   DBuf<float2> sig;           // fine (sigma_t, sigma_a) in red-black order for the V-cycle
@@ -1280,6 +1300,7 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   if (const char* e = std::getenv("RTE_DSA_NU")) d->nu = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_NU_COARSE")) d->nu_coarse = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_WARM")) d->warm = std::atoi(e) != 0;
+  d->clear_graphs();
   d->xprev.release();
   d->has_prev.release();
   // moments (dsa.cpp:167-192, 223-226)
@@ -1713,50 +1734,96 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   const bool any_active = *nact_h > 0;
   float* b0 = l0.b.p;
   static const bool trace = std::getenv("RTE_DSA_TRACE") != nullptr;
-  for (; any_active && it < d->maxit; ++it) {
+  // one BiCGStab iteration on stream q (captured into a CUDA graph when possible)
+  auto iteration = [&](cudaStream_t q) {
     ++d->nlaunch;
-    k_bicg_p<<<vgrid, kBT, 0, st>>>(S, un, unc, unx, d->scal.p, d->r.p, d->p.p, d->v.p, b0, d->act.p);
-    vcycle(d, 0, b0, d->xa.p, d->act.p, st);
-    ++d->nlaunch;
-    if (d->full)
-      k_apply_dot<0, true><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xa.p, d->v.p, d->rhs.p, d->part.p,
-                                                  d->act.p);
-    else
-      k_apply_dot<0, false><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xa.p, d->v.p, d->rhs.p,
-                                                   d->part.p, d->act.p);
-    ++d->nlaunch;
-    k_bicg_s<<<vgrid, kBT, 0, st>>>(S, un, unc, unx, d->nblk, d->part.p, d->scal.p, d->r.p, d->v.p, d->s.p, b0,
-                                    d->act.p);
-    vcycle(d, 0, b0, d->xb.p, d->act.p, st);
+    k_bicg_p<<<vgrid, kBT, 0, q>>>(S, un, unc, unx, d->scal.p, d->r.p, d->p.p, d->v.p, b0, d->act.p);
+    vcycle(d, 0, b0, d->xa.p, d->act.p, q);
     ++d->nlaunch;
     if (d->full)
-      k_apply_dot<1, true><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xb.p, d->t.p, d->s.p, d->part.p,
-                                                  d->act.p);
+      k_apply_dot<0, true><<<vgrid, kBT, 0, q>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xa.p, d->v.p, d->rhs.p, d->part.p,
+                                                 d->act.p);
     else
-      k_apply_dot<1, false><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xb.p, d->t.p, d->s.p,
-                                                   d->part.p, d->act.p);
+      k_apply_dot<0, false><<<vgrid, kBT, 0, q>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xa.p, d->v.p, d->rhs.p,
+                                                  d->part.p, d->act.p);
     ++d->nlaunch;
-    k_bicg_x<<<vgrid, kBT, 0, st>>>(S, un, unc, unx, d->nblk, d->part.p, d->scal.p, d->x.p, d->xa.p, d->xb.p,
-                                    d->r.p, d->s.p, d->t.p, d->rhs.p, d->part2.p, d->act.p);
-    RTE_CUDA(cudaMemsetAsync(d->nact.p, 0, sizeof(int), st));
+    k_bicg_s<<<vgrid, kBT, 0, q>>>(S, un, unc, unx, d->nblk, d->part.p, d->scal.p, d->r.p, d->v.p, d->s.p, b0,
+                                   d->act.p);
+    vcycle(d, 0, b0, d->xb.p, d->act.p, q);
     ++d->nlaunch;
-    k_bicg_check<<<S, 32, 0, st>>>(S, d->nblk, d->part2.p, d->scal.p, d->act.p, tol2, d->maxit, d->nact.p);
+    if (d->full)
+      k_apply_dot<1, true><<<vgrid, kBT, 0, q>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xb.p, d->t.p, d->s.p, d->part.p,
+                                                 d->act.p);
+    else
+      k_apply_dot<1, false><<<vgrid, kBT, 0, q>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->xb.p, d->t.p, d->s.p,
+                                                  d->part.p, d->act.p);
+    ++d->nlaunch;
+    k_bicg_x<<<vgrid, kBT, 0, q>>>(S, un, unc, unx, d->nblk, d->part.p, d->scal.p, d->x.p, d->xa.p, d->xb.p,
+                                   d->r.p, d->s.p, d->t.p, d->rhs.p, d->part2.p, d->act.p);
+    RTE_CUDA(cudaMemsetAsync(d->nact.p, 0, sizeof(int), q));
+    ++d->nlaunch;
+    k_bicg_check<<<S, 32, 0, q>>>(S, d->nblk, d->part2.p, d->scal.p, d->act.p, tol2, d->maxit, d->nact.p);
     RTE_CUDA(cudaGetLastError());
+  };
+  static const bool graphs_off = [] {
+    const char* e = std::getenv("RTE_DSA_GRAPH");
+    return e && std::atoi(e) == 0;
+  }();
+  const bool use_graph = any_active && !trace && !graphs_off && !(ctx->prof);
+  cudaStream_t q = st;
+  const Dsa2D::Graph* g = nullptr;
+  if (use_graph) {
+    if (!d->gstream) {
+      RTE_CUDA(cudaStreamCreateWithFlags(&d->gstream, cudaStreamNonBlocking));
+      RTE_CUDA(cudaEventCreateWithFlags(&d->ev_in, cudaEventDisableTiming));
+      RTE_CUDA(cudaEventCreateWithFlags(&d->ev_out, cudaEventDisableTiming));
+    }
+    for (const auto& e : d->graphs)
+      if (e.key == d->x.p && e.tol == d->tol && e.maxit == d->maxit) g = &e;
+    if (!g) {
+      cudaGraph_t graph;
+      const long n0 = d->nlaunch;
+      RTE_CUDA(cudaStreamBeginCapture(d->gstream, cudaStreamCaptureModeThreadLocal));
+      iteration(d->gstream);
+      RTE_CUDA(cudaStreamEndCapture(d->gstream, &graph));
+      Dsa2D::Graph e{d->x.p, d->tol, d->maxit, nullptr, d->nlaunch - n0};
+      d->nlaunch = n0;
+      RTE_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
+      RTE_CUDA(cudaGraphDestroy(graph));
+      if (d->graphs.size() >= 4) d->clear_graphs();
+      d->graphs.push_back(e);
+      g = &d->graphs.back();
+    }
+    q = d->gstream;
+    RTE_CUDA(cudaEventRecord(d->ev_in, st));
+    RTE_CUDA(cudaStreamWaitEvent(q, d->ev_in, 0));
+  }
+  for (; any_active && it < d->maxit; ++it) {
+    if (g) {
+      RTE_CUDA(cudaGraphLaunch(g->exec, q));
+      d->nlaunch += g->launches;
+    } else {
+      iteration(q);
+    }
     if (trace) {
       double sc[16];
-      RTE_CUDA(cudaMemcpyAsync(sc, d->scal.p, sizeof(sc), cudaMemcpyDeviceToHost, st));
-      RTE_CUDA(cudaStreamSynchronize(st));
+      RTE_CUDA(cudaMemcpyAsync(sc, d->scal.p, sizeof(sc), cudaMemcpyDeviceToHost, q));
+      RTE_CUDA(cudaStreamSynchronize(q));
       std::fprintf(stderr, "[dsa2d] it %d rel residual %.3e alpha %.3e omega %.3e\n", it,
                    std::sqrt(sc[SC_RNORM2] / sc[SC_BNORM2]), sc[SC_ALPHA], sc[SC_OMEGA]);
     }
     if ((it & 3) == 3) {
-      RTE_CUDA(cudaMemcpyAsync(nact_h, d->nact.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-      RTE_CUDA(cudaStreamSynchronize(st));
+      RTE_CUDA(cudaMemcpyAsync(nact_h, d->nact.p, sizeof(int), cudaMemcpyDeviceToHost, q));
+      RTE_CUDA(cudaStreamSynchronize(q));
       if (*nact_h == 0) {
         ++it;
         break;
       }
     }
+  }
+  if (q != st) {
+    RTE_CUDA(cudaEventRecord(d->ev_out, q));
+    RTE_CUDA(cudaStreamWaitEvent(st, d->ev_out, 0));
   }
   d->last_iters = it;
   static const bool report = std::getenv("RTE_DSA_REPORT") != nullptr;

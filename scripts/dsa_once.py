@@ -1,5 +1,6 @@
 """One 2D DSA solve (for launch lists): python scripts/dsa_once.py NX S TOL"""
 import os, sys, time
+os.environ.setdefault("RTE_DSA_WARM", "0")  # repeated solves of one rhs: time cold solves
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2402_10488_b200 import rte, configs
@@ -25,5 +26,5 @@ for k in range(int(os.environ.get("REPS", "3"))):
     torch.cuda.synchronize()
     ts.append(time.time() - t0)
 print("solve %.3f s (min of %s), krylov iterations %d, %.2f ms/iteration"
-      % (min(ts), " ".join("%.3f" % t for t in ts), d.last_iterations(), 1e3 * min(ts) / d.last_iterations()),
+      % (min(ts), " ".join("%.3f" % t for t in ts), d.last_iterations(), 1e3 * min(ts) / max(1, d.last_iterations())),
       flush=True)
