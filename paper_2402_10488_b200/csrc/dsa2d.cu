@@ -105,6 +105,7 @@ struct Dsa2D {
   double tol = 1e-12;
   int maxit = 1000;
   int nu = 6;          // smoothing steps on the finest level
+  int gamma0 = 1, gamma = 1;  // coarse-correction cycles from the finest / coarser levels (V-cycle)
   int nu_coarse = 2;   // smoothing steps on coarser levels (C5 sweep of (nu, nu_coarse): 24 its, 0.56 s)
   int last_iters = 0;
   int nblk = 64;
@@ -1300,6 +1301,8 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   if (const char* e = std::getenv("RTE_DSA_NU")) d->nu = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_NU_COARSE")) d->nu_coarse = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_WARM")) d->warm = std::atoi(e) != 0;
+  if (const char* e = std::getenv("RTE_DSA_GAMMA0")) d->gamma0 = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("RTE_DSA_GAMMA")) d->gamma = std::max(1, std::atoi(e));
   d->clear_graphs();
   d->xprev.release();
   d->has_prev.release();
@@ -1629,18 +1632,20 @@ static void gs(Dsa2D* d, int l, int color, const float* b, float* x, const int* 
 
 // V-cycle on level l: b, x in the level's red-black layout; x need not be
 // initialised (the first half-sweep treats it as zero)
-static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cudaStream_t st) {
+static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cudaStream_t st,
+                   bool zero_init = true) {
   Level& lv = d->L[l];
   const int S = d->S;
   const bool last = (size_t)l + 1 == d->L.size();
   if (last) {
     if (d->ncoarse > 0) {
+      if (!zero_init) return;  // exact: a repeated visit changes nothing
       ++d->nlaunch;
       k_dense_apply<<<S, 256, 0, st>>>(d->ncoarse, (int)lv.nc, d->coarse_inv.p, b, x, act);
       RTE_CUDA(cudaGetLastError());
     } else {
       for (int k = 0; k < 20; ++k) {
-        gs(d, l, 0, b, x, act, k == 0, nullptr, false, nullptr, st);
+        gs(d, l, 0, b, x, act, k == 0 && zero_init, nullptr, false, nullptr, st);
         gs(d, l, 1, b, x, act, false, nullptr, false, nullptr, st);
       }
     }
@@ -1650,14 +1655,16 @@ static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cu
   // pre-smoothing: colour 0 then colour 1; the last colour-1 update is kept
   // as delta so the residual is -C delta on colour 0 and 0 on colour 1
   for (int k = 0; k < nu; ++k) {
-    gs(d, l, 0, b, x, act, k == 0, nullptr, false, nullptr, st);
-    gs(d, l, 1, b, x, act, false, k == nu - 1 ? lv.r.p : nullptr, k == 0, nullptr, st);
+    gs(d, l, 0, b, x, act, k == 0 && zero_init, nullptr, false, nullptr, st);
+    gs(d, l, 1, b, x, act, false, k == nu - 1 ? lv.r.p : nullptr, k == 0 && zero_init, nullptr, st);
   }
   Level& lc = d->L[l + 1];
   ++d->nlaunch;
   k_restrict_delta<<<nblocks((long)S * lc.nc, 128), 128, 0, st>>>(S, lv.nx, lv.ny, l, lv.r.p, lc.b.p, act);
   RTE_CUDA(cudaGetLastError());
-  vcycle(d, l + 1, lc.b.p, lc.x.p, act, st);
+  // coarse-grid correction: gamma cycles on the coarse residual equation (1 = V, 2 = W)
+  const int gam = l == 0 ? d->gamma0 : d->gamma;
+  for (int g = 0; g < gam; ++g) vcycle(d, l + 1, lc.b.p, lc.x.p, act, st, g == 0);
   // post-smoothing: colour 1 then colour 0; the first colour-1 half-sweep sees
   // its colour-0 neighbours with the coarse correction prolonged on the fly,
   // and the colour-0 half-sweep that follows overwrites them
