@@ -192,6 +192,10 @@ DSA_CASES_2D = CASES_2D + [
     ("c3_32", lambda m: prob2d_const(m, 10 * 0.001, 10 * 0.999, lambda x, y: 1.0), 32, 32, (16, 8), [[]],
      (0.0, 1.0, 0.0, 1.0)),
     ("thin_random_32", None, 32, 32, (8, 4), [[]], (0.0, 1.0, 0.0, 1.0)),
+    # 48 x 40 -> 24 x 20 -> 12 x 10 -> 6 x 5: the coarsest level (30 cells) cannot
+    # coarsen further and is smoothed instead of solved densely
+    ("partial_coarsening_48x40", lambda m: prob2d_const(m, 0.05, 2.0, lambda x, y: 1.0 + y, inflow_bottom=0.3),
+     48, 40, (8, 4), [[]], (0.0, 1.2, 0.0, 1.0)),
 ]
 
 
