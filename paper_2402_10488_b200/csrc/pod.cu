@@ -95,6 +95,141 @@ __global__ void k_rmul(long m, int n, int k, const double* __restrict__ A, const
   }
 }
 
+// ---- blocked kernels for p, q, n, k <= 128 (all POD shapes of the configs) ----
+// One CTA reads each row chunk of A and B once and accumulates the whole
+// p x q product (16 x 16 threads, 8 x 8 outputs each, columns strided by 16
+// so shared-memory reads are conflict-free).  FP64 on the CUDA cores: the
+// B200 FP64 tensor rate is not higher than the DFMA rate for this shape.
+constexpr int kW = 128;         // max columns
+constexpr int kGR = 16;         // rows per shared-memory stage
+constexpr int kGChunk = 16384;  // rows per CTA
+
+__global__ void __launch_bounds__(512) k_gram_wide(long m, int p, int q, const double* __restrict__ A,
+                                                   const double* __restrict__ B, double* __restrict__ part) {
+  // 32 x 16 threads, 4 x 8 outputs each (rows ty + 32 a, columns tx + 16 b);
+  // the next stage's rows are prefetched into registers while this one computes
+  extern __shared__ double gsm[];
+  auto sa = reinterpret_cast<double (*)[kGR][kW]>(gsm);                // [2][kGR][kW]
+  auto sb = reinterpret_cast<double (*)[kGR][kW]>(gsm + 2 * kGR * kW);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const long r0 = (long)blockIdx.x * kGChunk;
+  const long r1 = min(m, r0 + kGChunk);
+  double acc[4][8];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+  constexpr int kPer = kGR * kW / 512;  // elements per thread per matrix and stage
+  double ra[kPer], rb_[kPer];
+  auto load = [&](long rb) {
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int e = threadIdx.x + t * 512;
+      const int rr = e % kGR, cc = e / kGR;
+      const long row = rb + rr;
+      ra[t] = (row < r1 && cc < p) ? __ldg(A + (long)cc * m + row) : 0.0;
+      rb_[t] = (row < r1 && cc < q) ? __ldg(B + (long)cc * m + row) : 0.0;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int e = threadIdx.x + t * 512;
+      sa[buf][e % kGR][e / kGR] = ra[t];
+      sb[buf][e % kGR][e / kGR] = rb_[t];
+    }
+  };
+  int buf = 0;
+  load(r0);
+  store(0);
+  __syncthreads();
+  for (long rb = r0; rb < r1; rb += kGR) {
+    const bool more = rb + kGR < r1;
+    if (more) load(rb + kGR);
+#pragma unroll 4
+    for (int rr = 0; rr < kGR; ++rr) {
+      double va[4], vb[8];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) va[a] = sa[buf][rr][ty + 32 * a];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) vb[b] = sb[buf][rr][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = fma(va[a], vb[b], acc[a][b]);
+    }
+    if (more) store(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+  double* o = part + (long)blockIdx.x * kW * kW;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) o[(ty + 32 * a) * kW + tx + 16 * b] = acc[a][b];
+}
+
+__global__ void k_gram_wide_reduce(int nchunks, int p, int q, const double* __restrict__ part,
+                                   double* __restrict__ C) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= kW * kW) return;
+  const int i = e / kW, j = e % kW;
+  if (i >= p || j >= q) return;
+  double v = 0.0;
+  for (int c = 0; c < nchunks; ++c) v += part[(long)c * kW * kW + e];
+  C[(long)j * p + i] = v;  // column-major p x q
+}
+
+// Y (m x k) = A (m x n) M (n x k): 64-row tiles of A (transposed into shared
+// memory) times M held in shared memory; 16 x 16 threads, 4 rows x 8 columns each.
+__global__ void __launch_bounds__(256) k_rmul_wide(long m, int n, int k, const double* __restrict__ A,
+                                                   const double* __restrict__ M, double* __restrict__ Y) {
+  extern __shared__ double sm[];
+  double* Ms = sm;                // [n][kW] row-major
+  double* At = sm + n * kW;       // [n][64]
+  for (int e = threadIdx.x; e < n * kW; e += blockDim.x) {
+    const int l = e / kW, j = e % kW;
+    Ms[e] = j < k ? M[(long)j * n + l] : 0.0;
+  }
+  const int tr = threadIdx.x & 15, tc = threadIdx.x >> 4;
+  for (long rb = (long)blockIdx.x * 64; rb < m; rb += (long)gridDim.x * 64) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * 64; e += blockDim.x) {
+      const int l = e / 64, rr = e % 64;
+      const long row = rb + rr;
+      At[e] = row < m ? A[(long)l * m + row] : 0.0;
+    }
+    __syncthreads();
+    double acc[4][8];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+#pragma unroll 2
+    for (int l = 0; l < n; ++l) {
+      double va[4], vb[8];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) va[a] = At[l * 64 + tr + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) vb[b] = Ms[l * kW + tc + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = fma(va[a], vb[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const long row = rb + tr + 16 * a;
+      if (row >= m) continue;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int j = tc + 16 * b;
+        if (j < k) Y[(long)j * m + row] = acc[a][b];
+      }
+    }
+  }
+}
+
 // u_rho / u_iso: out[c][i] = sum_j wj U[c][j][i]
 __global__ void k_block_sum(int r, int nv, long nd, const double* __restrict__ U, const double* __restrict__ w,
                             double* __restrict__ out) {
@@ -107,6 +242,22 @@ __global__ void k_block_sum(int r, int nv, long nd, const double* __restrict__ U
 }
 
 void gram(long m, int p, int q, const double* A, const double* B, double* C_dev, cudaStream_t st) {
+  if (p <= kW && q <= kW) {
+    const int nch = (int)((m + kGChunk - 1) / kGChunk);
+    DBuf<double> part;
+    part.alloc((size_t)nch * kW * kW);
+    const int gsmem = (int)(sizeof(double) * 4 * kGR * kW);
+    static bool gcfg = false;
+    if (!gcfg) {
+      RTE_CUDA(cudaFuncSetAttribute(k_gram_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem));
+      gcfg = true;
+    }
+    k_gram_wide<<<nch, 512, gsmem, st>>>(m, p, q, A, B, part.p);
+    k_gram_wide_reduce<<<kW * kW / 256, 256, 0, st>>>(nch, p, q, part.p, C_dev);
+    RTE_CUDA(cudaGetLastError());
+    RTE_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
   const int tiles = ((p + TT - 1) / TT) * ((q + TT - 1) / TT);
   const int nch = (int)((m + kRowChunk - 1) / kRowChunk);
   DBuf<double> part;
@@ -129,6 +280,22 @@ std::vector<double> gram_host(long m, int p, int q, const double* A, const doubl
 void rmul(long m, int n, int k, const double* A, const std::vector<double>& M, double* Y, cudaStream_t st) {
   DBuf<double> dM;
   dM.upload(M.data(), M.size());
+  if (n <= kW && k <= kW) {
+    const size_t smem2 = sizeof(double) * ((size_t)n * kW + (size_t)n * 64);
+    static bool cfg2 = false;
+    if (!cfg2) {
+      RTE_CUDA(cudaFuncSetAttribute(k_rmul_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      cfg2 = true;
+    }
+    int sms = 148, dev = 0;
+    RTE_CUDA(cudaGetDevice(&dev));
+    RTE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const long tiles = (m + 63) / 64;
+    k_rmul_wide<<<(int)std::min<long>(tiles, (long)sms * 2), 256, smem2, st>>>(m, n, k, A, dM.p, Y);
+    RTE_CUDA(cudaGetLastError());
+    RTE_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
   const size_t smem = sizeof(double) * n * k;
   RTE_REQUIRE(smem <= 200 * 1024, RTE_ERR_UNSUPPORTED, "pod: too many columns");
   static bool cfg = false;
