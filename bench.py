@@ -109,13 +109,18 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def dist_init():
+def dist_init(init_group=True):
+    """One process per GPU (torchrun env).  The process group is only needed by
+    our arm (barrier + max-over-ranks timing); the reference arm runs on rank 0
+    alone and the other ranks exit without work."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 and init_group:
+        import torch
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
@@ -370,14 +375,14 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     args = ap.parse_args()
-    rank, world, local = dist_init()
+    rank, world, local = dist_init(init_group=args.impl != "reference")
     if args.impl == "reference":
         line = run_reference(args, rank, world)
     else:
         line = run_b200(args, rank, world, local)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 and args.impl != "reference":
         import torch.distributed as dist
         dist.destroy_process_group()
 
