@@ -105,6 +105,9 @@ SIGNATURES = [
     ("rte_romig", ctypes.c_int, [_vp, _vp, _ip, _vp]),
     ("rte_si_solve", ctypes.c_int, [_vp, ctypes.POINTER(SiConfig), _vp, ctypes.POINTER(SiReport), _dp,
                                     ctypes.c_char_p]),
+    ("rte_apply_kinetic", ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    ("rte_apply_streaming_collision", ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp]),
+    ("rte_kinetic_rhs", ctypes.c_int, [_vp, _vp, _vp]),
     ("rte_gmres_solve", ctypes.c_int, [_vp, ctypes.POINTER(GmresConfig), _vp, ctypes.POINTER(GmresReport), _dp,
                                        ctypes.c_int]),
     ("rte_profile_enable", ctypes.c_int, [_vp, ctypes.c_int]),

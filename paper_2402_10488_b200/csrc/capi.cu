@@ -885,52 +885,91 @@ int rte_truncation_rank(const double* s, int n, double eps_pod) {
   return kept;
 }
 
+namespace {
+// kinetic right-hand side b_j = G + g_j^bc of sample s (transport_system.cpp:615-624, 142-187)
+std::vector<double> kinetic_rhs_host(rte_ctx* ctx, int s) {
+  const long nd = ctx->ndof;
+  std::vector<double> g(nd);
+  RTE_CUDA(cudaMemcpy(g.data(), ctx->g.p + (ctx->g_shared ? 0 : (size_t)s * nd), sizeof(double) * nd,
+                      cudaMemcpyDeviceToHost));
+  std::vector<double> b((size_t)ctx->nv * nd);
+  const double s3 = kSqrt3;
+  for (int j = 0; j < ctx->nv; ++j) {
+    double* bj = b.data() + (size_t)j * nd;
+    std::copy(g.begin(), g.end(), bj);
+    const double vx = ctx->vx[j], vy = ctx->vy[j];
+    if (ctx->geom == RTE_SLAB1D) {
+      const int n = ctx->nx;
+      if (vx > 0 && ctx->inflow[0] != 0) {
+        const double a = vx * ctx->inflow[0] / std::sqrt(ctx->bounds[1] - ctx->bounds[0]);
+        bj[0] += a;
+        bj[1] += -s3 * a;
+      } else if (vx < 0 && ctx->inflow[1] != 0) {
+        const double a = -vx * ctx->inflow[1] / std::sqrt(ctx->bounds[n] - ctx->bounds[n - 1]);
+        bj[2 * (n - 1)] += a;
+        bj[2 * (n - 1) + 1] += s3 * a;
+      }
+      continue;
+    }
+    const int nx = ctx->nx, ny = ctx->ny;
+    const double sx = 1.0 / std::sqrt(ctx->hx), sy = 1.0 / std::sqrt(ctx->hy);
+    if (vx > 0 && ctx->inflow[0] != 0) {
+      const double a = vx * ctx->inflow[0] * sx * std::sqrt(ctx->hy);
+      for (int iy = 0; iy < ny; ++iy) { bj[4L * (nx * iy)] += a; bj[4L * (nx * iy) + 1] += -s3 * a; }
+    }
+    if (vx < 0 && ctx->inflow[1] != 0) {
+      const double a = -vx * ctx->inflow[1] * sx * std::sqrt(ctx->hy);
+      for (int iy = 0; iy < ny; ++iy) { bj[4L * (nx - 1 + nx * iy)] += a; bj[4L * (nx - 1 + nx * iy) + 1] += s3 * a; }
+    }
+    if (vy > 0 && ctx->inflow[2] != 0) {
+      const double a = vy * ctx->inflow[2] * sy * std::sqrt(ctx->hx);
+      for (int ix = 0; ix < nx; ++ix) { bj[4L * ix] += a; bj[4L * ix + 2] += -s3 * a; }
+    }
+    if (vy < 0 && ctx->inflow[3] != 0) {
+      const double a = -vy * ctx->inflow[3] * sy * std::sqrt(ctx->hx);
+      for (int ix = 0; ix < nx; ++ix) { bj[4L * (ix + nx * (ny - 1))] += a; bj[4L * (ix + nx * (ny - 1)) + 2] += s3 * a; }
+    }
+  }
+  return b;
+}
+}  // namespace
+
 int rte_build_rom(rte_ctx* ctx, int r, const double* U, double* u_rho, double* u_iso, double* a_r, double* b_r) {
   return guarded(ctx, [&] {
     DeviceGuard dg(ctx->device);
-    // kinetic right-hand side b_j = G + g_j^bc (transport_system.cpp:615-624, 142-187)
-    const long nd = ctx->ndof;
-    std::vector<double> g(nd);
-    RTE_CUDA(cudaMemcpy(g.data(), ctx->g.p, sizeof(double) * nd, cudaMemcpyDeviceToHost));
-    std::vector<double> b((size_t)ctx->nv * nd);
-    const double s3 = kSqrt3;
-    for (int j = 0; j < ctx->nv; ++j) {
-      double* bj = b.data() + (size_t)j * nd;
-      std::copy(g.begin(), g.end(), bj);
-      const double vx = ctx->vx[j], vy = ctx->vy[j];
-      if (ctx->geom == RTE_SLAB1D) {
-        const int n = ctx->nx;
-        if (vx > 0 && ctx->inflow[0] != 0) {
-          const double a = vx * ctx->inflow[0] / std::sqrt(ctx->bounds[1] - ctx->bounds[0]);
-          bj[0] += a;
-          bj[1] += -s3 * a;
-        } else if (vx < 0 && ctx->inflow[1] != 0) {
-          const double a = -vx * ctx->inflow[1] / std::sqrt(ctx->bounds[n] - ctx->bounds[n - 1]);
-          bj[2 * (n - 1)] += a;
-          bj[2 * (n - 1) + 1] += s3 * a;
-        }
-        continue;
-      }
-      const int nx = ctx->nx, ny = ctx->ny;
-      const double sx = 1.0 / std::sqrt(ctx->hx), sy = 1.0 / std::sqrt(ctx->hy);
-      if (vx > 0 && ctx->inflow[0] != 0) {
-        const double a = vx * ctx->inflow[0] * sx * std::sqrt(ctx->hy);
-        for (int iy = 0; iy < ny; ++iy) { bj[4L * (nx * iy)] += a; bj[4L * (nx * iy) + 1] += -s3 * a; }
-      }
-      if (vx < 0 && ctx->inflow[1] != 0) {
-        const double a = -vx * ctx->inflow[1] * sx * std::sqrt(ctx->hy);
-        for (int iy = 0; iy < ny; ++iy) { bj[4L * (nx - 1 + nx * iy)] += a; bj[4L * (nx - 1 + nx * iy) + 1] += s3 * a; }
-      }
-      if (vy > 0 && ctx->inflow[2] != 0) {
-        const double a = vy * ctx->inflow[2] * sy * std::sqrt(ctx->hx);
-        for (int ix = 0; ix < nx; ++ix) { bj[4L * ix] += a; bj[4L * ix + 2] += -s3 * a; }
-      }
-      if (vy < 0 && ctx->inflow[3] != 0) {
-        const double a = -vy * ctx->inflow[3] * sy * std::sqrt(ctx->hx);
-        for (int ix = 0; ix < nx; ++ix) { bj[4L * (ix + nx * (ny - 1))] += a; bj[4L * (ix + nx * (ny - 1)) + 2] += s3 * a; }
-      }
-    }
+    const std::vector<double> b = kinetic_rhs_host(ctx, 0);
     build_rom(ctx, r, U, b.data(), u_rho, u_iso, a_r, b_r, nullptr);
+  });
+}
+
+int rte_kinetic_rhs(rte_ctx* ctx, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    RTE_REQUIRE(out, RTE_ERR_INVALID, "kinetic_rhs: null argument");
+    DeviceGuard dg(ctx->device);
+    const size_t kdim = (size_t)ctx->nv * ctx->ndof;
+    for (int s = 0; s < ctx->S; ++s) {
+      const std::vector<double> b = kinetic_rhs_host(ctx, s);
+      RTE_CUDA(cudaMemcpyAsync(out + s * kdim, b.data(), sizeof(double) * kdim, cudaMemcpyHostToDevice,
+                               as_stream(stream)));
+      RTE_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    }
+  });
+}
+
+int rte_apply_streaming_collision(rte_ctx* ctx, int j, const double* f, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    RTE_REQUIRE(f && out, RTE_ERR_INVALID, "apply_streaming_collision: null argument");
+    RTE_REQUIRE(j >= 0 && j < ctx->nv, RTE_ERR_INVALID, "apply_streaming_collision: bad direction");
+    DeviceGuard dg(ctx->device);
+    apply_streaming_collision(ctx, j, f, out, as_stream(stream));
+  });
+}
+
+int rte_apply_kinetic(rte_ctx* ctx, const double* u, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    RTE_REQUIRE(u && out, RTE_ERR_INVALID, "apply_kinetic: null argument");
+    DeviceGuard dg(ctx->device);
+    apply_kinetic(ctx, u, out, as_stream(stream));
   });
 }
 

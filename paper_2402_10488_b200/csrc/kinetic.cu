@@ -218,7 +218,86 @@ __global__ void k_snap_update(int S, long nd, const int* kind, const double* rst
     rho[(long)s * nd + i] = rstar[(long)s * nd + i] + corr[(long)s * nd + i];
 }
 
+// (D_j + Sigma_t) f for one direction and every sample (transport_system.cpp:
+// 482-558): upwind streaming with zero inflow plus the sample's Mt blocks.
+__global__ void k_stream_coll(const TermArgs a, int S, int j, const double* __restrict__ mt) {
+  const long ncell = a.geom == RTE_SLAB1D ? a.nx : (long)a.nx * a.ny;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)S * ncell) return;
+  const int s = (int)(t / ncell);
+  const int cell = (int)(t - (long)s * ncell);
+  const int nl = a.nl;
+  const double* fs = a.u + (long)s * a.ndof;
+  double o[4] = {0, 0, 0, 0};
+  if (a.geom == RTE_SLAB1D)
+    dj_1d(a, a.vx[j], fs, cell, o);
+  else
+    dj_2d(a, a.vx[j], a.vy[j], fs, cell % a.nx, cell / a.nx, o);
+  for (int r = 0; r < nl; ++r) {
+    double v = 0.0;
+    if (a.block == 1) {
+      v = mt[(long)s * ncell + cell] * fs[(long)nl * cell + r];
+    } else {
+      const double* m = mt + ((long)s * ncell + cell) * a.block + (long)nl * r;
+      for (int q = 0; q < nl; ++q) v += m[q] * fs[(long)nl * cell + q];
+    }
+    a.out[(long)s * a.ndof + (long)nl * cell + r] = o[r] + v;
+  }
+}
+
+// out[s] += psi[s][k] * t[s] over the kinetic vectors of every sample
+__global__ void k_psi_axpy(int S, long kdim, int K, int k, const double* __restrict__ psi,
+                           const double* __restrict__ t, double* __restrict__ out, int first) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long)S * kdim) return;
+  const int s = (int)(i / kdim);
+  const double v = psi[(long)s * K + k] * t[i];
+  out[i] = first ? v : out[i] + v;
+}
+
 }  // namespace
+
+void apply_streaming_collision(rte_ctx* ctx, int j, const double* f, double* out, cudaStream_t st) {
+  DBuf<double> dvx, dvy;
+  dvx.upload(ctx->vx.data(), ctx->nv);
+  dvy.upload(ctx->vy.data(), ctx->nv);
+  TermArgs a{};
+  a.geom = ctx->geom;
+  a.nx = ctx->nx;
+  a.ny = ctx->ny;
+  a.nl = ctx->nl;
+  a.nv = ctx->nv;
+  a.block = ctx->block;
+  a.ndof = ctx->ndof;
+  a.width = ctx->width.p;
+  a.hx = ctx->hx;
+  a.hy = ctx->hy;
+  a.vx = dvx.p;
+  a.vy = dvy.p;
+  a.u = f;
+  a.out = out;
+  const long n = (long)ctx->S * ctx->ncells;
+  k_stream_coll<<<(int)((n + 127) / 128), 128, 0, st>>>(a, ctx->S, j, ctx->mt.p);
+  RTE_CUDA(cudaGetLastError());
+  RTE_CUDA(cudaStreamSynchronize(st));
+}
+
+// A_mu u = sum_k psi_k(mu_s) A_k u_s for every sample (transport_system.cpp:598-613)
+void apply_kinetic(rte_ctx* ctx, const double* u, double* out, cudaStream_t st) {
+  RTE_REQUIRE(ctx->k_terms > 0 && ctx->psi.p, RTE_ERR_INVALID,
+              "apply_kinetic: call rte_set_affine with per-term mass blocks first");
+  const long kdim = (long)ctx->nv * ctx->ndof;
+  DBuf<double> t;
+  t.alloc((size_t)ctx->S * kdim);
+  const long n = (long)ctx->S * kdim;
+  for (int k = 0; k < ctx->k_terms; ++k) {
+    apply_term_kinetic(ctx, k, ctx->S, u, t.p, st);
+    k_psi_axpy<<<(int)((n + 255) / 256), 256, 0, st>>>(ctx->S, kdim, ctx->k_terms, k, ctx->psi.p, t.p, out,
+                                                         k == 0 ? 1 : 0);
+    RTE_CUDA(cudaGetLastError());
+  }
+  RTE_CUDA(cudaStreamSynchronize(st));
+}
 
 void apply_term_kinetic(rte_ctx* ctx, int k, int ncols, const double* u, double* out, cudaStream_t st) {
   RTE_REQUIRE(ctx->k_terms > 0 && ctx->term_mt.p, RTE_ERR_INVALID,

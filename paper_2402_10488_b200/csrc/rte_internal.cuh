@@ -297,6 +297,8 @@ void rom_destroy(RomState* r);
 
 // kinetic operators and training (kinetic.cu)
 void apply_term_kinetic(rte_ctx* ctx, int k, int ncols, const double* u, double* out, cudaStream_t st);
+void apply_streaming_collision(rte_ctx* ctx, int j, const double* f, double* out, cudaStream_t st);
+void apply_kinetic(rte_ctx* ctx, const double* u, double* out, cudaStream_t st);
 void collect_snapshots(rte_ctx* ctx, int window, double eps, int max_iters, double* f_iter, double* f_conv,
                        double* drho_iter, int* conv_h, int* n_iter_h, cudaStream_t st);
 

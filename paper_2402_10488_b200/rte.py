@@ -362,6 +362,26 @@ class TransportBatch:
         self._call(capi.load().rte_density_of, f.data_ptr(), out.data_ptr(), self._stream())
         return out
 
+    def apply_kinetic(self, u):
+        """A_mu u = sum_k psi_k(mu) A_k u per sample (transport_system.cpp:598-613)."""
+        u = self._dev(u, (self.S, self.kinetic_dim()))
+        out = self._out(self.S, self.kinetic_dim())
+        self._call(capi.load().rte_apply_kinetic, u.data_ptr(), out.data_ptr(), self._stream())
+        return out
+
+    def apply_streaming_collision(self, j, f):
+        """(D_j + Sigma_t) f per sample, zero inflow (transport_system.cpp:482-558)."""
+        f = self._dev(f, (self.S, self.nd))
+        out = self._out(self.S, self.nd)
+        self._call(capi.load().rte_apply_streaming_collision, int(j), f.data_ptr(), out.data_ptr(), self._stream())
+        return out
+
+    def kinetic_rhs(self):
+        """Stacked kinetic right-hand side, block j = G + g_j^bc (transport_system.cpp:615-624)."""
+        out = self._out(self.S, self.kinetic_dim())
+        self._call(capi.load().rte_kinetic_rhs, out.data_ptr(), self._stream())
+        return out
+
     def apply_term_kinetic(self, k, u):
         """A_k u (transport_system.cpp:560-596) for kinetic columns u [n, kdim]
         (term operators are parameter independent)."""

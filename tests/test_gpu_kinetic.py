@@ -67,6 +67,37 @@ def test_apply_term_kinetic(geom):
             assert np.max(np.abs(out[c] - ref)) < 1e-12 * max(1.0, np.max(np.abs(ref)))
 
 
+@pytest.mark.parametrize("geom", [1, 2])
+def test_apply_kinetic_streaming_collision_and_rhs(geom):
+    """apply_kinetic (transport_system.cpp:598-613) per sample, the
+    streaming-collision operator and its sweep inverse (test_sweep.cpp:30-50:
+    (D_j + Sigma_t) sweep_j(r) = r), and the kinetic right-hand side; the
+    converged kinetic solution satisfies A_mu f = b (test_assembly.cpp:100-110)."""
+    osys, b = systems(geom)
+    rng = np.random.default_rng(12)
+    u = rng.uniform(-1, 1, (2, b.kinetic_dim()))
+    au = b.apply_kinetic(u).cpu().numpy()
+    kb = b.kinetic_rhs().cpu().numpy()
+    for s, o in enumerate(osys):
+        ref = o.apply_kinetic(u[s])
+        assert np.max(np.abs(au[s] - ref)) < 1e-12 * max(1.0, np.max(np.abs(ref)))
+        assert np.max(np.abs(kb[s] - o.kinetic_rhs())) < 1e-13
+    f = rng.uniform(-1, 1, (2, b.n_dof()))
+    for j in (0, b.quad.n() // 2, b.quad.n() - 1):
+        sc = b.apply_streaming_collision(j, f).cpu().numpy()
+        back = b.apply_streaming_collision(j, b.sweep_direction(j, f)).cpu().numpy()
+        for s, o in enumerate(osys):
+            ref = o.apply_streaming_collision(j, f[s])
+            assert np.max(np.abs(sc[s] - ref)) < 1e-12 * max(1.0, np.max(np.abs(ref)))
+            assert rel_l2(back[s], f[s]) < 1e-12
+    # the kinetic fixed point: A_mu f* = b
+    from paper_2402_10488_b200 import rte
+    rho, _ = rte.sisa_solve(b, "SI", rte.SolveConfig(eps_sisa=1e-13, max_iters=20000))
+    fk = b.kinetic_sweep(rho)
+    res = (b.apply_kinetic(fk) - b.kinetic_rhs()).cpu().numpy()
+    assert np.max(np.abs(res)) < 1e-9 * max(1.0, np.max(np.abs(kb)))
+
+
 def test_pin_cell_offline_and_romsad():
     """BASELINE configs[3] shape at reduced size: device training, POD,
     projections and ROMSAD(3,5) vs the oracle with the device-built model."""
