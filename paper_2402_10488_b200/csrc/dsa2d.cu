@@ -263,7 +263,9 @@ __device__ __forceinline__ void face_lift(int lev, int dir, const R* v, R* y) {
 template <typename R, typename T>
 __device__ __forceinline__ void face_mv(int lev, int dir, const T* __restrict__ xs, long nc, long cn, R* y) {
   R v[NB];
-  const T* p = xs + vblk(cn, NB);
+  // 32-bit offset inside one sample's vector (< 2^31 elements, checked at setup)
+  const int icn = (int)cn;
+  const T* p = xs + ((icn >> 5) * (32 * NB) + (icn & 31));
 #pragma unroll
   for (int r = 0; r < NB; ++r) v[r] = (R)p[r * 32];
   face_lift(lev, dir, v, y);
