@@ -1,4 +1,4 @@
-"""Committed golden fixtures (tests/golden/, made by scripts/make_golden.py
+"""Committed golden fixtures (tests/golden/, made by tests/tools/make_golden.py
 from the oracle): the oracle must keep reproducing them (CPU), and the B200
 path must match them within the north_star tolerances (GPU)."""
 import os

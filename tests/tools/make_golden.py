@@ -2,12 +2,12 @@
 be built here: Eigen3/LAPACKE absent).  The fixtures pin the oracle against
 regressions and give the GPU tests fixed expected vectors.
 
-  python scripts/make_golden.py
+  python tests/tools/make_golden.py
 """
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import numpy as np
 

@@ -3,7 +3,7 @@
 parity (iteration counts, switch iterations, scalar flux) on a subset of
 samples.  Writes one JSON document (stdout).
 
-  python scripts/run_configs.py [--parity N] [--configs c1,c2,c3,c4]
+  python tests/tools/run_configs.py [--parity N] [--configs c1,c2,c3,c4]
 """
 import argparse
 import json
@@ -11,7 +11,7 @@ import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 
