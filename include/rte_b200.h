@@ -178,10 +178,11 @@ int rte_set_affine(rte_ctx* ctx, const rte_affine* aff);
 int rte_apply_term_kinetic(rte_ctx* ctx, int k, int n_cols, const double* u_dev, double* out_dev,
                            void* stream);
 /* apply_kinetic (transport_system.cpp:598-613): out = A_mu u = sum_k psi_k(mu)
- * A_k u for every sample; u/out [S][n_dirs * n_dof].  Requires rte_set_affine. */
+ * A_k u for every sample; u/out [S][n_dirs * n_dof] (distinct buffers).
+ * Requires rte_set_affine. */
 int rte_apply_kinetic(rte_ctx* ctx, const double* u_dev, double* out_dev, void* stream);
 /* apply_streaming_collision (transport_system.cpp:482-558): out = (D_j +
- * Sigma_t) f for direction j with zero inflow; f/out [S][n_dof]. */
+ * Sigma_t) f for direction j with zero inflow; f/out [S][n_dof] (distinct). */
 int rte_apply_streaming_collision(rte_ctx* ctx, int j, const double* f_dev, double* out_dev, void* stream);
 /* kinetic_rhs (transport_system.cpp:615-624): block j = G + g_j^bc per sample;
  * out [S][n_dirs * n_dof]. */

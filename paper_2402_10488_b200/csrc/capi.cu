@@ -605,6 +605,7 @@ int rte_set_affine(rte_ctx* ctx, const rte_affine* aff) {
 
 int rte_apply_term_kinetic(rte_ctx* ctx, int k, int n_cols, const double* u, double* out, void* stream) {
   return guarded(ctx, [&] {
+    RTE_REQUIRE(u && out && u != out, RTE_ERR_INVALID, "apply_term_kinetic: null or aliased buffers");
     DeviceGuard dg(ctx->device);
     apply_term_kinetic(ctx, k, n_cols, u, out, as_stream(stream));
   });
@@ -959,6 +960,7 @@ int rte_kinetic_rhs(rte_ctx* ctx, double* out, void* stream) {
 int rte_apply_streaming_collision(rte_ctx* ctx, int j, const double* f, double* out, void* stream) {
   return guarded(ctx, [&] {
     RTE_REQUIRE(f && out, RTE_ERR_INVALID, "apply_streaming_collision: null argument");
+    RTE_REQUIRE(f != out, RTE_ERR_INVALID, "apply_streaming_collision: out must not alias f");
     RTE_REQUIRE(j >= 0 && j < ctx->nv, RTE_ERR_INVALID, "apply_streaming_collision: bad direction");
     DeviceGuard dg(ctx->device);
     apply_streaming_collision(ctx, j, f, out, as_stream(stream));
@@ -968,6 +970,7 @@ int rte_apply_streaming_collision(rte_ctx* ctx, int j, const double* f, double* 
 int rte_apply_kinetic(rte_ctx* ctx, const double* u, double* out, void* stream) {
   return guarded(ctx, [&] {
     RTE_REQUIRE(u && out, RTE_ERR_INVALID, "apply_kinetic: null argument");
+    RTE_REQUIRE(u != out, RTE_ERR_INVALID, "apply_kinetic: out must not alias u");
     DeviceGuard dg(ctx->device);
     apply_kinetic(ctx, u, out, as_stream(stream));
   });
