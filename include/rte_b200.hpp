@@ -118,6 +118,32 @@ class TransportBatch {
   void apply_Ms(const DeviceVector& x, DeviceVector& out) const {  // transport_system.cpp:373
     check(rte_apply_Ms(ctx_, x.data(), out.data(), nullptr), ctx_);
   }
+  void apply_Mt(const DeviceVector& x, DeviceVector& out) const {  // transport_system.cpp:383
+    check(rte_apply_Mt(ctx_, x.data(), out.data(), nullptr), ctx_);
+  }
+  // rho* = L rho + bbar in one sweep (the SI fixed-point map)
+  void fixed_point(const DeviceVector& rho, DeviceVector& out) const {
+    check(rte_fixed_point(ctx_, rho.data(), out.data(), nullptr), ctx_);
+  }
+  void sweep_direction(int j, const DeviceVector& rhs, DeviceVector& f) const {  // transport_system.hpp:53
+    check(rte_sweep_direction(ctx_, j, rhs.data(), f.data(), nullptr), ctx_);
+  }
+  void apply_streaming_collision(int j, const DeviceVector& f, DeviceVector& out) const {  // :482-558
+    check(rte_apply_streaming_collision(ctx_, j, f.data(), out.data(), nullptr), ctx_);
+  }
+  // kinetic vectors are [S][n_dirs * n_dof]
+  void kinetic_sweep(const DeviceVector& rho, DeviceVector& f) const {  // transport_system.cpp:420
+    check(rte_kinetic_sweep(ctx_, rho.data(), f.data(), nullptr), ctx_);
+  }
+  void density_of(const DeviceVector& f, DeviceVector& rho) const {  // transport_system.cpp:433
+    check(rte_density_of(ctx_, f.data(), rho.data(), nullptr), ctx_);
+  }
+  void apply_kinetic(const DeviceVector& u, DeviceVector& out) const {  // transport_system.cpp:598
+    check(rte_apply_kinetic(ctx_, u.data(), out.data(), nullptr), ctx_);
+  }
+  void kinetic_rhs(DeviceVector& out) const {  // transport_system.cpp:615
+    check(rte_kinetic_rhs(ctx_, out.data(), nullptr), ctx_);
+  }
 
  private:
   rte_ctx* ctx_ = nullptr;
@@ -133,6 +159,11 @@ class DsaOperator {  // dsa.hpp:29-56
     check(rte_dsa_solve_density(b_->handle(), rhs.data(), out.data(), nullptr), b_->handle());
   }
   long coupled_dim() const { return rte_dsa_coupled_dim(b_->handle()); }
+  // XY: relative residual of the iterative coupled solve (default 1e-12)
+  void set_tolerance(double tol, int max_iters = 0) const {
+    check(rte_dsa_set_tolerance(b_->handle(), tol, max_iters), b_->handle());
+  }
+  int last_iterations() const { return rte_dsa_last_iterations(b_->handle()); }
 
  private:
   TransportBatch* b_;
