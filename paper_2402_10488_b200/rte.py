@@ -584,6 +584,7 @@ class SolveReport:
     correction_log: str
     switch_iter: int
     singular: bool
+    wall_seconds: float = 0.0  # wall time of the whole batched solve (shared by its samples)
 
 
 _METHODS = {"SI": capi.RTE_SI, "DSA": capi.RTE_DSA, "ROMSA": capi.RTE_ROMSA, "ROMSAD": capi.RTE_ROMSAD,
@@ -660,7 +661,10 @@ def sisa_solve(batch: TransportBatch, method, config: SolveConfig):
     hist = np.zeros(S * mi)
     log = ctypes.create_string_buffer(S * mi)
     _torch().cuda.synchronize(batch.device)
+    import time as _time
+    t0 = _time.perf_counter()
     rc = L.rte_si_solve(batch._h, ctypes.byref(cfg), ctypes.c_void_p(rho.data_ptr()), reps, capi.dptr(hist), log)
+    wall = _time.perf_counter() - t0
     if rc != 0 and errors:
         raise errors[0]
     capi.check(rc, batch._h)
@@ -674,7 +678,7 @@ def sisa_solve(batch: TransportBatch, method, config: SolveConfig):
         out.append(SolveReport(bool(r.converged), int(r.n_sweep), int(it), list(hist[s * mi:s * mi + it]),
                                float(r.final_residual), label,
                                "supplied" if (config.initial_guess is not None or m == capi.RTE_ROMIG) else "zero",
-                               lg, int(r.switch_iter), bool(r.singular)))
+                               lg, int(r.switch_iter), bool(r.singular), wall))
     return rho, out
 
 
@@ -702,15 +706,18 @@ def gmres_solve(batch: TransportBatch, preconditioner, config: SolveConfig, romi
     reps = (capi.GmresReport * S)()
     hist = np.zeros(S * cap)
     _torch().cuda.synchronize(batch.device)
+    import time as _time
+    t0 = _time.perf_counter()
     capi.check(L.rte_gmres_solve(batch._h, ctypes.byref(cfg), ctypes.c_void_p(rho.data_ptr()), reps,
                                  capi.dptr(hist), cap), batch._h)
+    wall = _time.perf_counter() - t0
     out = []
     for s in range(S):
         r = reps[s]
         n = min(int(r.history_len), cap)
         out.append(SolveReport(bool(r.converged), int(r.n_sweep), int(r.iterations), list(hist[s * cap:s * cap + n]),
                                float(r.final_residual), "PGMRES" if preconditioner is not None else "GMRES",
-                               "zero" if guess == capi.RTE_GUESS_ZERO else "supplied", "", -1, False))
+                               "zero" if guess == capi.RTE_GUESS_ZERO else "supplied", "", -1, False, wall))
     return rho, out
 
 
