@@ -1001,7 +1001,7 @@ __global__ void __launch_bounds__(kBT) k_bicg_p(int S, unsigned n, unsigned nc, 
 // out = K x (x: fp32 red-black preconditioned vector, exact in fp64), with the
 // fused partial dots: mode 0 q0 = (d0, out); mode 1 q0 = (out, d0), q1 = (out, out)
 template <int mode, bool FULL>
-__global__ void __launch_bounds__(kBT, 2) k_apply_dot(int S, int nx, int ny, const double* __restrict__ sgt,
+__global__ void __launch_bounds__(kBT, 3) k_apply_dot(int S, int nx, int ny, const double* __restrict__ sgt,
                                                       const double* __restrict__ sgs, const float* __restrict__ xin,
                                                       double* __restrict__ out, const double* __restrict__ d0,
                                                       double* __restrict__ part, const int* __restrict__ act) {
