@@ -326,3 +326,82 @@ if len(sys.argv) > 4 and sys.argv[4] == "spectrum":
     print("largest |1 - lambda|:", ["%.3f" % v for v in srt[:12]])
     print("count > 0.5: %d, > 0.3: %d, > 0.1: %d of %d" % ((mu > 0.5).sum(), (mu > 0.3).sum(), (mu > 0.1).sum(), N))
     print("min |lambda| %.3e, max |lambda| %.3f, max |imag| %.3f" % (np.abs(ev).min(), np.abs(ev).max(), np.abs(ev.imag).max()))
+
+if len(sys.argv) > 4 and sys.argv[4] == "semicoarse":
+    # two-grid with x-semicoarsening (coarse grid nx/2 x ny) and an exact coarse solve
+    nxf = nx
+    rows, cols, vals = [], [], []
+    nxc = nxf // 2
+    def idx2(f, ix, iy, loc, nxl, nyl):
+        return f * (nxl * nyl * 4) + (iy * nxl + ix) * 4 + loc
+    for f in range(3):
+        for iy in range(nxf):
+            for ix in range(nxf):
+                Ex = Emat(ix & 1)
+                for fa in range(2):
+                    for fb in range(2):
+                        for ca in range(2):
+                            v = Ex[fa, ca]
+                            if v != 0:
+                                rows.append(idx2(f, ix, iy, fa + 2 * fb, nxf, nxf))
+                                cols.append(idx2(f, ix // 2, iy, ca + 2 * fb, nxc, nxf))
+                                vals.append(v)
+    Pxs = sp.csr_matrix((vals, (rows, cols)), shape=(3 * nxf * nxf * 4, 3 * nxc * nxf * 4))
+    Acs = (Pxs.T @ A @ Pxs).tocsc()
+    lus = spl.splu(Acs)
+    L0 = levs[0]
+    def tg2(bv):
+        x = np.zeros_like(bv)
+        for _ in range(NU):
+            x = L0.gs(bv, x, (0, 1))
+        r = bv - A @ x
+        x = x + Pxs @ lus.solve(Pxs.T @ r)
+        for _ in range(NU):
+            x = L0.gs(bv, x, (1, 0))
+        return x
+    cnt = [0]
+    def mv5(v):
+        cnt[0] += 1
+        return tg2(v)
+    x, info = spl.bicgstab(A, b, M=spl.LinearOperator((N, N), matvec=mv5), rtol=1e-8, maxiter=500)
+    print("two-grid x-semicoarsening: precond applications %d info %d" % (cnt[0], info))
+
+if len(sys.argv) > 4 and sys.argv[4] == "patch":
+    # red-black block GS over 2x2-cell patches (48 unknowns) on the finest level
+    L0 = levs[0]
+    nxl = L0.nxl
+    Ap = L0.Ap
+    pats = []
+    for py in range(0, nxl, 2):
+        for px in range(0, nxl, 2):
+            cells = [(py + a) * nxl + px + b_ for a in range(2) for b_ in range(2)]
+            ids = np.concatenate([np.arange(12 * c, 12 * c + 12) for c in cells])
+            pats.append(((px // 2 + py // 2) % 2, ids, np.linalg.inv(Ap[ids][:, ids].toarray())))
+    def patch_gs(bv, x, order):
+        bp, xp = bv[L0.perm], x[L0.perm].copy()
+        for col in order:
+            r = bp - Ap @ xp
+            for c_, ids, inv in pats:
+                if c_ == col:
+                    xp[ids] += inv @ r[ids]
+        out = np.empty_like(x); out[L0.perm] = xp
+        return out
+    NPS = int(sys.argv[5]) if len(sys.argv) > 5 else 2
+    def vc(l, bv):
+        L = levs[l]
+        if l == len(levs) - 1:
+            return coarse_lu.solve(bv)
+        x = np.zeros_like(bv)
+        for _ in range(NPS if l == 0 else NUC):
+            x = patch_gs(bv, x, (0, 1)) if l == 0 else L.gs(bv, x, (0, 1))
+        r = bv - L.A @ x
+        x = x + Ps[l] @ vcycle(l + 1, Ps[l].T @ r)
+        for _ in range(NPS if l == 0 else NUC):
+            x = patch_gs(bv, x, (1, 0)) if l == 0 else L.gs(bv, x, (1, 0))
+        return x
+    cnt = [0]
+    def mv6(v):
+        cnt[0] += 1
+        return vc(0, v)
+    x, info = spl.bicgstab(A, b, M=spl.LinearOperator((N, N), matvec=mv6), rtol=1e-8, maxiter=500)
+    print("patch (2x2) smoother x%d: precond applications %d info %d" % (NPS, cnt[0], info))
