@@ -6,7 +6,7 @@ and a red-black 12x12 block Gauss-Seidel V-cycle mirroring dsa2d.cu, then
 measures BiCGStab/GMRES preconditioner applications and analyses the slow
 modes.  DESIGN.md section 6 quotes its results.
 
-  python tests/tools/dsa_model.py NX LEVELS [plain|aux] [mode|gmres|lines N|smoothedP W|spectrum]
+  python tests/tools/dsa_model.py NX LEVELS [plain|aux] [mode|gmres|lines N|smoothedP W|spectrum|semicoarse|patch N]
 """
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
