@@ -1300,6 +1300,13 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   const int S = ctx->S;
   d->S = S;
   d->ctx = ctx;
+  // Smoothing schedule by batch size: below ~4M fine cells the V-cycle is
+  // launch-bound, so extra fine sweeps are nearly free and one coarse sweep
+  // suffices (C3 0.080 -> 0.061 s, C4 4.7 -> 4.2 ms/sample); at C5 scale
+  // (16.7M cells) the fine smoother is HBM-bound and (6, 2) is fastest.
+  const bool small = (long)S * ctx->nx * ctx->ny < (4l << 20);
+  d->nu = small ? 10 : 6;
+  d->nu_coarse = small ? 1 : 2;
   if (const char* e = std::getenv("RTE_DSA_NU")) d->nu = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_NU_COARSE")) d->nu_coarse = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_WARM")) d->warm = std::atoi(e) != 0;

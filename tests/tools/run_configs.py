@@ -114,7 +114,7 @@ def c2(args):
                           pm.discarded_fraction, pm.b_r)
     ocm = ro.ReducedModel(0, 16, b.n_dof(), 16, 4, "c", eps_c, eps_train, cm.u_rho, cm.u_iso, cm.a_r, cm.singular_values,
                           cm.discarded_fraction, cm.b_r)
-    idx = list(range(0, S, max(1, S // args.parity)))[:args.parity]
+    idx = list(range(0, S, max(1, S // args.parity)))[:args.parity] if args.parity > 0 else []
     for method in ("DSA", "ROMIG", "ROMSAD"):
         cfg = rte.SolveConfig(eps_sisa=1e-8, norm="abs", theta=theta, eps_romsad=eps_r, max_iters=500)
         ((rho, reps), tc, t) = timed_warm(lambda: rte.sisa_solve(b, method, cfg))
@@ -197,7 +197,7 @@ def c4(args):
     ocm = ro.ReducedModel(1, 128, b.n_dof(), 20, 5, "c", eps_c, eps_train, cm.u_rho, cm.u_iso, cm.a_r,
                           cm.singular_values, cm.discarded_fraction, cm.b_r)
     osys = lambda mu: ro.TransportSystem(mk(nx), om, ro.build_dg_space(om), ro.chebyshev_legendre(16, 8), mu)
-    idx = list(range(0, S, max(1, S // args.parity4)))[:args.parity4]
+    idx = list(range(0, S, max(1, S // args.parity4)))[:args.parity4] if args.parity4 > 0 else []
     for method in ("DSA", "ROMSAD"):
         cfg = rte.SolveConfig(eps_sisa=1e-8, theta=theta, eps_romsad=eps_r, max_iters=500)
         ((rho, reps), tc, t) = timed_warm(lambda: rte.sisa_solve(b, method, cfg), reps=1)
