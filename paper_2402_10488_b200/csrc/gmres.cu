@@ -313,33 +313,36 @@ void gmres_solve(rte_ctx* ctx, const rte_gmres_config& cfg, double* rho, rte_gmr
   const dim3 vg(nblk, S);
   const int hcap = std::max(1, history_cap);
 
-  DBuf<double> V, H, gv, cs, sn, yv, hist, bbar, U, LU, Z, C, W, part0, part1;
-  DBuf<GmState> sts;
-  DBuf<int> act, kind, nact;
-  DBuf<unsigned long long> zmax;
-  V.alloc((size_t)S * (m + 1) * nd);
-  H.alloc((size_t)S * (m + 1) * m);
+  // persistent per-context scratch (grow-only): no cudaMalloc per solve
+  DBuf<double>(&dd)[15] = ctx->gm_d;
+  DBuf<double>&V = dd[0], &H = dd[1], &gv = dd[2], &cs = dd[3], &sn = dd[4], &yv = dd[5], &hist = dd[6],
+  &bbar = dd[7], &U = dd[8], &LU = dd[9], &Z = dd[10], &C = dd[11], &W = dd[12], &part0 = dd[13], &part1 = dd[14];
+  DBuf<int>&act = ctx->gm_i[0], &kind = ctx->gm_i[1], &nact = ctx->gm_i[2];
+  DBuf<unsigned long long>& zmax = ctx->gm_zmax;
+  V.ensure((size_t)S * (m + 1) * nd);
+  H.ensure((size_t)S * (m + 1) * m);
   H.zero(st);
-  gv.alloc((size_t)S * (m + 1));
-  cs.alloc((size_t)S * m);
-  sn.alloc((size_t)S * m);
-  yv.alloc((size_t)S * m);
-  hist.alloc((size_t)S * hcap);
-  for (DBuf<double>* b : {&bbar, &U, &LU, &Z, &W}) b->alloc((size_t)S * nd);
-  if (pre) C.alloc((size_t)S * nd);
-  part0.alloc((size_t)S * nblk);
-  part1.alloc((size_t)S * nblk);
-  sts.alloc(S);
-  act.alloc(S);
-  kind.alloc(S);
-  nact.alloc(1);
-  zmax.alloc(S);
-  GmArgs a{S, m, nd, sts.p, V.p, H.p, gv.p, cs.p, sn.p, yv.p, hist.p, hcap, cfg.rel_tol, cfg.max_iters, nblk};
+  gv.ensure((size_t)S * (m + 1));
+  cs.ensure((size_t)S * m);
+  sn.ensure((size_t)S * m);
+  yv.ensure((size_t)S * m);
+  hist.ensure((size_t)S * hcap);
+  for (DBuf<double>* b : {&bbar, &U, &LU, &Z, &W}) b->ensure((size_t)S * nd);
+  if (pre) C.ensure((size_t)S * nd);
+  part0.ensure((size_t)S * nblk);
+  part1.ensure((size_t)S * nblk);
+  ctx->gm_states.ensure(sizeof(GmState) * S);
+  GmState* sts_p = reinterpret_cast<GmState*>(ctx->gm_states.p);
+  act.ensure(S);
+  kind.ensure(S);
+  nact.ensure(1);
+  zmax.ensure(S);
+  GmArgs a{S, m, nd, sts_p, V.p, H.p, gv.p, cs.p, sn.p, yv.p, hist.p, hcap, cfg.rel_tol, cfg.max_iters, nblk};
 
   // initial guess
   if (cfg.guess == RTE_GUESS_ROMIG) {
-    DBuf<int> stat;
-    stat.alloc(S);
+    DBuf<int>& stat = ctx->gm_i[3];
+    stat.ensure(S);
     romig(ctx, rho, stat.p, st);
     std::vector<int> hs(S);
     RTE_CUDA(cudaMemcpyAsync(hs.data(), stat.p, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
@@ -369,9 +372,9 @@ void gmres_solve(rte_ctx* ctx, const rte_gmres_config& cfg, double* rho, rte_gmr
                                                         cudaGetErrorString(e));
   };
   chk("init");
-  int* nact_h = nullptr;
-  RTE_CUDA(cudaMallocHost(&nact_h, sizeof(int)));
-  try {
+  if (!ctx->pinned_int) RTE_CUDA(cudaMallocHost(&ctx->pinned_int, sizeof(int)));
+  int* nact_h = ctx->pinned_int;
+  {
     for (;;) {
       k_gm_stage<<<vg, kT, 0, st>>>(a, rho, U.p, act.p, kind.p);
       RTE_CUDA(cudaGetLastError());
@@ -399,22 +402,18 @@ void gmres_solve(rte_ctx* ctx, const rte_gmres_config& cfg, double* rho, rte_gmr
       RTE_CUDA(cudaStreamSynchronize(st));
       if (*nact_h == 0) break;
     }
-  } catch (...) {
-    cudaFreeHost(nact_h);
-    throw;
   }
-  cudaFreeHost(nact_h);
 
   std::vector<GmState> hs(S);
-  RTE_CUDA(cudaMemcpyAsync(hs.data(), sts.p, sizeof(GmState) * S, cudaMemcpyDeviceToHost, st));
+  RTE_CUDA(cudaMemcpyAsync(hs.data(), sts_p, sizeof(GmState) * S, cudaMemcpyDeviceToHost, st));
   RTE_CUDA(cudaStreamSynchronize(st));
   // non-converged samples: ||rho - L rho - bbar||_inf (uncounted sweep, gmres.cpp:116-119)
   bool any_nc = false;
   for (int s = 0; s < S; ++s) any_nc |= !hs[s].converged;
   std::vector<double> res_nc(S, 0.0);
   if (any_nc) {
-    DBuf<unsigned long long> bits;
-    bits.alloc((size_t)2 * S);
+    DBuf<unsigned long long>& bits = ctx->gm_bits;
+    bits.ensure((size_t)2 * S);
     bits.zero(st);
     transport_apply(ctx, SRC_MS_RHO | SRC_G | SRC_BC, rho, U.p, nullptr, rho, LU.p, bits.p, st);
     std::vector<unsigned long long> hb(2 * S);

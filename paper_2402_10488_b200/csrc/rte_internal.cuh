@@ -148,6 +148,11 @@ struct rte_ctx {
   rte::DBuf<char> si_log, si_letters;
   rte::DBuf<unsigned long long> si_bits;
   int* pinned_int = nullptr;  // cudaMallocHost, one int for the active-count poll
+  // PGMRES scratch reused across rte_gmres_solve calls (grow-only)
+  rte::DBuf<double> gm_d[15];
+  rte::DBuf<int> gm_i[4];
+  rte::DBuf<unsigned long long> gm_zmax, gm_bits;
+  rte::DBuf<char> gm_states;
   rte::DBuf<unsigned long long> ws_bits;
   rte::DBuf<unsigned int> ws_sync;
   rte::DBuf<rte::Slot2D> slot_tab;  // cached all-slot sweep table (2D)
