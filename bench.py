@@ -341,6 +341,7 @@ def cpu_reference(args, budget_s=20.0):
     wall = time.perf_counter() - t0
     upd = win * win * (PHI * VZ // 2) * reps * cores
     return {"value": upd / max(times), "unit": "updates/s", "cores": cores, "kind": "port",
+            "value_1core": win * win * (PHI * VZ // 2) / probe,
             "sample": "%d SI-DSA iterations (one sweep of all %d directions as the reference does + SuperLU DSA "
                       "correction; updates counted over the %d unique slots as in our arm) on %d independent %dx%d "
                       "windows of C5 sample 0, one per process; one iteration %.3f s"

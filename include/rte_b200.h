@@ -237,6 +237,12 @@ int rte_dsa_correct(rte_ctx* ctx, const double* delta_dev, double* out_dev, void
 int rte_dsa_set_tolerance(rte_ctx* ctx, double tol, int max_iters);
 /* Krylov iterations of the last XY DSA solve (0 for slab: direct). */
 int rte_dsa_last_iterations(const rte_ctx* ctx);
+/* DsaOperator::apply_eliminated (dsa.cpp:279-293, dsa.hpp:43-46): the
+ * current-eliminated density operator S x = A_rr x - A_rJ T^{-1} A_Jr x for
+ * every sample.  The current block T is factored lazily on first use (slab:
+ * block cyclic reduction; XY: solved by CG to relative residual 1e-13).
+ * x and out are [S][ndof] device buffers and must not alias. */
+int rte_dsa_apply_eliminated(rte_ctx* ctx, const double* x_dev, double* out_dev, void* stream);
 /* DsaOperator::coupled_dim (dsa.hpp:48). */
 long rte_dsa_coupled_dim(const rte_ctx* ctx);
 

@@ -158,6 +158,10 @@ class DsaOperator {  // dsa.hpp:29-56
   void solve_density(const DeviceVector& rhs, DeviceVector& out) const {
     check(rte_dsa_solve_density(b_->handle(), rhs.data(), out.data(), nullptr), b_->handle());
   }
+  // dsa.cpp:279-293: S x = A_rr x - A_rJ T^-1 A_Jr x
+  void apply_eliminated(const DeviceVector& x, DeviceVector& out) const {
+    check(rte_dsa_apply_eliminated(b_->handle(), x.data(), out.data(), nullptr), b_->handle());
+  }
   long coupled_dim() const { return rte_dsa_coupled_dim(b_->handle()); }
   // XY: relative residual of the iterative coupled solve (default 1e-12)
   void set_tolerance(double tol, int max_iters = 0) const {

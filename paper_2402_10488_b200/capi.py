@@ -99,6 +99,7 @@ SIGNATURES = [
     ("rte_dsa_solve_density", ctypes.c_int, [_vp, _vp, _vp, _vp]),
     ("rte_dsa_correct", ctypes.c_int, [_vp, _vp, _vp, _vp]),
     ("rte_dsa_coupled_dim", ctypes.c_long, [_vp]),
+    ("rte_dsa_apply_eliminated", ctypes.c_int, [_vp, _vp, _vp, _vp]),
     ("rte_dsa_set_tolerance", ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_int]),
     ("rte_dsa_last_iterations", ctypes.c_int, [_vp]),
     ("rte_rom_load", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(Rom)]),

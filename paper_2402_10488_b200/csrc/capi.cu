@@ -642,6 +642,14 @@ int rte_dsa_correct(rte_ctx* ctx, const double* delta, double* out, void* stream
   });
 }
 
+int rte_dsa_apply_eliminated(rte_ctx* ctx, const double* x, double* out, void* stream) {
+  return guarded(ctx, [&] {
+    RTE_REQUIRE(x != out, RTE_ERR_INVALID, "dsa: apply_eliminated input and output must not alias");
+    DeviceGuard dg(ctx->device);
+    dsa_apply_eliminated(ctx, x, out, as_stream(stream));
+  });
+}
+
 long rte_dsa_coupled_dim(const rte_ctx* ctx) { return dsa_coupled_dim(ctx); }
 
 int rte_dsa_set_tolerance(rte_ctx* ctx, double tol, int max_iters) {

@@ -75,6 +75,7 @@ struct Dsa1DArgs {
   const double* ms;
   double m1, m2, m3;
   double* fac;
+  int tonly;  // 1: the current block T alone, padded with identity rho rows (apply_eliminated)
 };
 
 // Blocks of cell i (dsa.cpp:34-110, 197-215 with unknowns interleaved per cell).
@@ -142,6 +143,15 @@ __device__ void cell_blocks(const Dsa1DArgs& a, int s, int i, double* D, double*
         U[4 * (r + 2) + c] = a.m2 * dcv;
         U[4 * (r + 2) + c + 2] = -3.0 * a.m3 * djv;
       }
+  }
+  if (a.tonly) {
+    for (int r = 0; r < 4; ++r)
+      for (int c = 0; c < 4; ++c)
+        if (r < 2 || c < 2) {
+          D[4 * r + c] = r == c ? 1.0 : 0.0;
+          L[4 * r + c] = 0.0;
+          U[4 * r + c] = 0.0;
+        }
   }
 }
 
@@ -252,6 +262,7 @@ struct Dsa1DSolve {
   double* work;          // [S][N][4]: reduced right-hand sides, then the solution
   const int* kind;       // optional mask: only samples with kind == KIND_DSA
   int apply_ms;
+  int prepared;          // 1: work already holds the 4-vector rhs; the solution stays in work
 };
 
 // Block cyclic reduction solve, one CTA per sample.
@@ -264,7 +275,7 @@ __global__ void __launch_bounds__(kCrThreads) dsa1d_solve_cr(const Dsa1DSolve a)
   double* y = a.work + (long)s * N * 4;
   const double* fac = a.fac + (long)s * cr_entries(N) * 48;
   // rhs [(Ms) rho ; 0] per cell
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+  for (int i = threadIdx.x; i < N && !a.prepared; i += blockDim.x) {
     double r0 = r[2 * i], r1 = r[2 * i + 1];
     if (a.apply_ms) {
       if (a.block == 4) {
@@ -341,9 +352,48 @@ __global__ void __launch_bounds__(kCrThreads) dsa1d_solve_cr(const Dsa1DSolve a)
     }
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+  for (int i = threadIdx.x; i < N && !a.prepared; i += blockDim.x) {
     a.out[(long)s * nd + 2 * i] = y[4 * i];
     a.out[(long)s * nd + 2 * i + 1] = y[4 * i + 1];
+  }
+}
+
+// Current-eliminated operator pieces (dsa.cpp:279-293) from the coupled
+// blocks of cell i: phase 0 -> work_i = (0, 0, (A_Jr x)_i); phase 1 ->
+// out_i = (A_rr x)_i - (A_rJ y)_i with y_i = work_i[2..3] = T^{-1} A_Jr x.
+__global__ void k_elim1d(const Dsa1DArgs a, int phase, const double* __restrict__ x, double* __restrict__ work,
+                         double* __restrict__ out) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)a.S * a.N) return;
+  const int s = (int)(t / a.N), i = (int)(t - (long)s * a.N);
+  double B[3][16];
+  cell_blocks(a, s, i, B[0], B[1], B[2]);
+  const double* xs = x + (long)s * 2 * a.N;
+  const double* ys = work + (long)s * a.N * 4;
+  const int nb[3] = {i, i - 1, i + 1};
+  double acc[2] = {0.0, 0.0};
+  for (int k = 0; k < 3; ++k) {
+    const int j = nb[k];
+    if (j < 0 || j >= a.N) continue;
+    const double* m = B[k];
+    for (int r = 0; r < 2; ++r) {
+      if (phase == 0) {
+        acc[r] += m[4 * (r + 2)] * xs[2 * j] + m[4 * (r + 2) + 1] * xs[2 * j + 1];
+      } else {
+        acc[r] += m[4 * r] * xs[2 * j] + m[4 * r + 1] * xs[2 * j + 1];
+        acc[r] -= m[4 * r + 2] * ys[4 * j + 2] + m[4 * r + 3] * ys[4 * j + 3];
+      }
+    }
+  }
+  if (phase == 0) {
+    double* w = work + t * 4;
+    w[0] = 0.0;
+    w[1] = 0.0;
+    w[2] = acc[0];
+    w[3] = acc[1];
+  } else {
+    out[t * 2] = acc[0];
+    out[t * 2 + 1] = acc[1];
   }
 }
 
@@ -375,6 +425,7 @@ void dsa_setup(rte_ctx* ctx, cudaStream_t st) {
   }
   d->nf = 2;
   d->dim = 2 * ctx->ndof;
+  d->fac_t.release();
   moments(ctx->vx, ctx->w, d->m1, d->m2, d->m3);
   d->fac.alloc((size_t)ctx->S * cr_entries(ctx->ncells) * 48);
   Dsa1DArgs a{ctx->S, ctx->ncells, ctx->block, ctx->width.p, ctx->mt.p, ctx->ms.p, d->m1, d->m2, d->m3, d->fac.p};
@@ -401,6 +452,41 @@ void dsa_apply(rte_ctx* ctx, const double* rhs, double* out, const int* kind, in
 
 void dsa_solve_density(rte_ctx* ctx, const double* rhs, double* out, const int* kind, cudaStream_t st) {
   dsa_apply(ctx, rhs, out, kind, 0, st);
+}
+
+void dsa2d_apply_eliminated(rte_ctx* ctx, const double* x, double* out, cudaStream_t st);
+
+// DsaOperator::apply_eliminated (dsa.cpp:279-293): S x = A_rr x - A_rJ T^{-1} A_Jr x.
+// Slab: T (the J-J block, block tridiagonal) is factored lazily on first use
+// by the same block cyclic reduction, padded to 4x4 blocks with identity rho
+// rows, like the reference's lazily built current-block SparseLU.
+void dsa_apply_eliminated(rte_ctx* ctx, const double* x, double* out, cudaStream_t st) {
+  RTE_REQUIRE(ctx->dsa, RTE_ERR_INVALID, "dsa: rte_dsa_setup was not called");
+  if (ctx->geom == RTE_XY2D) {
+    dsa2d_apply_eliminated(ctx, x, out, st);
+    return;
+  }
+  DsaState* d = ctx->dsa;
+  const int S = ctx->S, N = ctx->ncells;
+  Dsa1DArgs a{S, N, ctx->block, ctx->width.p, ctx->mt.p, ctx->ms.p, d->m1, d->m2, d->m3, nullptr, 0};
+  if (!d->fac_t.p) {
+    d->fac_t.alloc((size_t)S * cr_entries(N) * 48);
+    Dsa1DArgs at = a;
+    at.fac = d->fac_t.p;
+    at.tonly = 1;
+    DBuf<double> work;
+    work.alloc((size_t)S * 2 * N * 48);
+    dsa1d_factor_cr<<<S, kCrThreads, 0, st>>>(at, work.p);
+    RTE_CUDA(cudaGetLastError());
+    RTE_CUDA(cudaStreamSynchronize(st));
+  }
+  ctx->ws_e.alloc((size_t)S * N * 4);
+  const int nb = (int)(((long)S * N + 255) / 256);
+  k_elim1d<<<nb, 256, 0, st>>>(a, 0, x, ctx->ws_e.p, nullptr);
+  Dsa1DSolve sv{S, N, ctx->block, d->fac_t.p, nullptr, nullptr, nullptr, ctx->ws_e.p, nullptr, 0, 1};
+  dsa1d_solve_cr<<<S, std::min(kCrThreads, std::max(32, (N + 1) / 2 / 32 * 32 + 32)), 0, st>>>(sv);
+  k_elim1d<<<nb, 256, 0, st>>>(a, 1, x, ctx->ws_e.p, out);
+  RTE_CUDA(cudaGetLastError());
 }
 
 void dsa_destroy(DsaState* d) {

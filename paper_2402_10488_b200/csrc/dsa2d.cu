@@ -1285,6 +1285,100 @@ __global__ void k_unpack(int S, long nc, const double* __restrict__ x, double* _
   for (int r = 0; r < 4; ++r) out[t * 4 + r] = x[s * nc * NB + r * nc + c];
 }
 
+// ---- apply_eliminated (dsa.cpp:279-293) ------------------------------------
+// The current block T = blockdiag(T_x, T_y) (T_x = 3 m2x Mt - 3 m3x D_Jx -
+// 3 m3yx D_Jy, dsa.cpp:216-246) is SPD, so T y = A_Jr x is solved by CG on the
+// J components of natural-layout vectors whose rho components stay zero; the
+// operator applications reuse k_apply_nat (K on (0, y) gives T y in the J rows
+// and A_rJ y in the rho rows).  Per-sample scalars el[s*4 + {rr, rr0, beta}].
+
+// r = p = J part of z, y = 0; partial (r, r)
+__global__ void __launch_bounds__(kBT) k_el_init(int S, long nc, const double* __restrict__ z, double* __restrict__ r,
+                                                 double* __restrict__ p, double* __restrict__ y,
+                                                 double* __restrict__ part) {
+  const int s = blockIdx.y;
+  const long n = nc * NB, base = (long)s * n;
+  double a0 = 0.0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const double v = i < 4 * nc ? 0.0 : z[base + i];
+    r[base + i] = v;
+    p[base + i] = v;
+    y[base + i] = 0.0;
+    a0 = fma(v, v, a0);
+  }
+  block_parts(a0, 0.0, 1, part, s);
+}
+
+__global__ void k_el_start(int S, int nblk, const double* part, double* el, int* act, double tol2, int* nact) {
+  const int s = blockIdx.x;
+  double q[1];
+  reduce_parts(part, s, nblk, 1, q);
+  if (threadIdx.x != 0) return;
+  el[s * 4 + 0] = q[0];
+  el[s * 4 + 1] = q[0];
+  const bool on = q[0] > 0.0;
+  act[s] = on ? 1 : 0;
+  if (on) atomicAdd(nact, 1);
+  (void)tol2;
+}
+
+// alpha = rr / (p, T p); y += alpha p; r -= alpha (T p) on the J rows; partial (r, r)
+__global__ void __launch_bounds__(kBT) k_el_update(int S, long nc, int nblk, const double* part, const double* el,
+                                                   const int* act, const double* __restrict__ p,
+                                                   const double* __restrict__ ap, double* __restrict__ y,
+                                                   double* __restrict__ r, double* __restrict__ part2) {
+  const int s = blockIdx.y;
+  if (!act[s]) return;
+  double q[2];
+  reduce_parts(part, s, nblk, 2, q);
+  const double alpha = el[s * 4] / q[0];
+  const long n = nc * NB, base = (long)s * n;
+  double a0 = 0.0;
+  for (long i = 4 * nc + (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    y[base + i] = fma(alpha, p[base + i], y[base + i]);
+    const double rv = fma(-alpha, ap[base + i], r[base + i]);
+    r[base + i] = rv;
+    a0 = fma(rv, rv, a0);
+  }
+  block_parts(a0, 0.0, 1, part2, s);
+}
+
+__global__ void k_el_beta(int S, int nblk, const double* part2, double* el, int* act, double tol2, int* nact) {
+  const int s = blockIdx.x;
+  if (!act[s]) return;
+  double q[1];
+  reduce_parts(part2, s, nblk, 1, q);
+  if (threadIdx.x != 0) return;
+  double* e = el + s * 4;
+  e[2] = q[0] / e[0];
+  e[0] = q[0];
+  if (q[0] <= tol2 * e[1]) {
+    act[s] = 0;
+  } else {
+    atomicAdd(nact, 1);
+  }
+}
+
+// p = r + beta p on the J rows
+__global__ void __launch_bounds__(kBT) k_el_dir(int S, long nc, const double* el, const int* act,
+                                                const double* __restrict__ r, double* __restrict__ p) {
+  const int s = blockIdx.y;
+  if (!act[s]) return;
+  const double beta = el[s * 4 + 2];
+  const long n = nc * NB, base = (long)s * n;
+  for (long i = 4 * nc + (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    p[base + i] = fma(beta, p[base + i], r[base + i]);
+}
+
+// out[s][c][r] = z_rho - w_rho (A_rr x - A_rJ y)
+__global__ void k_el_out(int S, long nc, const double* __restrict__ z, const double* __restrict__ w,
+                         double* __restrict__ out) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)S * nc) return;
+  const long s = t / nc, c = t - s * nc;
+  for (int r = 0; r < 4; ++r) out[t * 4 + r] = z[s * nc * NB + r * nc + c] - w[s * nc * NB + r * nc + c];
+}
+
 inline int nblocks(long n, int bs = 256) { return (int)((n + bs - 1) / bs); }
 
 }  // namespace
@@ -1750,6 +1844,12 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   const bool any_active = *nact_h > 0;
   float* b0 = l0.b.p;
   static const bool trace = std::getenv("RTE_DSA_TRACE") != nullptr;
+  if (trace) {
+    double sc[16];
+    RTE_CUDA(cudaMemcpy(sc, d->scal.p, sizeof(sc), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "[dsa2d] start rel residual %.3e%s\n", std::sqrt(sc[SC_RNORM2] / sc[SC_BNORM2]),
+                 d->warm ? " (warm start)" : "");
+  }
   // one BiCGStab iteration on stream q (captured into a CUDA graph when possible)
   auto iteration = [&](cudaStream_t q) {
     ++d->nlaunch;
@@ -1853,6 +1953,59 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     ++d->nlaunch;
     k_mark_prev<<<(S + 127) / 128, 128, 0, st>>>(S, d->scal.p, d->has_prev.p);
   }
+}
+
+void dsa2d_apply_eliminated(rte_ctx* ctx, const double* xin, double* out, cudaStream_t st) {
+  auto* d = static_cast<Dsa2D*>(ctx->dsa->impl2d);
+  RTE_REQUIRE(d, RTE_ERR_INVALID, "dsa: rte_dsa_setup was not called");
+  const int S = d->S;
+  Level& l0 = d->L[0];
+  const long nc = l0.nc, n = nc * NB;
+  const dim3 vgrid(d->nblk, S);
+  auto apply = [&](const double* x, double* y, const double* b) {
+    if (d->full)
+      k_apply_nat<true><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, x, y, b, d->part.p);
+    else
+      k_apply_nat<false><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, x, y, b, d->part.p);
+  };
+  // X = (x, 0, 0) in d->rhs; Z = K X in d->v (rho rows A_rr x, J rows A_Jr x)
+  k_pack_rhs<<<nblocks((long)S * nc), 256, 0, st>>>(S, nc, xin, nullptr, 0, 0, d->rhs.p, nullptr);
+  apply(d->rhs.p, d->v.p, d->rhs.p);
+  DBuf<double> el;
+  el.alloc((size_t)S * 4);
+  DBuf<int> act, nact;
+  act.alloc(S);
+  nact.alloc(1);
+  RTE_CUDA(cudaMemsetAsync(nact.p, 0, sizeof(int), st));
+  k_el_init<<<vgrid, kBT, 0, st>>>(S, nc, d->v.p, d->r.p, d->p.p, d->s.p, d->part2.p);
+  const double tol2 = 1e-26;
+  k_el_start<<<S, 32, 0, st>>>(S, d->nblk, d->part2.p, el.p, act.p, tol2, nact.p);
+  RTE_CUDA(cudaGetLastError());
+  int nh = 0;
+  RTE_CUDA(cudaMemcpyAsync(&nh, nact.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RTE_CUDA(cudaStreamSynchronize(st));
+  const int maxit = 100000;
+  int it = 0;
+  for (; nh > 0 && it < maxit; ++it) {
+    apply(d->p.p, d->t.p, d->p.p);  // T p (J rows), partial (T p, p)
+    k_el_update<<<vgrid, kBT, 0, st>>>(S, nc, d->nblk, d->part.p, el.p, act.p, d->p.p, d->t.p, d->s.p, d->r.p,
+                                       d->part2.p);
+    RTE_CUDA(cudaMemsetAsync(nact.p, 0, sizeof(int), st));
+    k_el_beta<<<S, 32, 0, st>>>(S, d->nblk, d->part2.p, el.p, act.p, tol2, nact.p);
+    k_el_dir<<<vgrid, kBT, 0, st>>>(S, nc, el.p, act.p, d->r.p, d->p.p);
+    RTE_CUDA(cudaGetLastError());
+    if ((it & 15) == 15) {
+      RTE_CUDA(cudaMemcpyAsync(&nh, nact.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      RTE_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+  RTE_REQUIRE(nh == 0, RTE_ERR_RUNTIME, "dsa: current block solve did not converge");
+  // W = K (0, y): rho rows A_rJ y; out = A_rr x - A_rJ y
+  apply(d->s.p, d->t.p, d->s.p);
+  k_el_out<<<nblocks((long)S * nc), 256, 0, st>>>(S, nc, d->v.p, d->t.p, out);
+  RTE_CUDA(cudaGetLastError());
+  RTE_CUDA(cudaStreamSynchronize(st));
+  (void)n;
 }
 
 void dsa2d_destroy(void* p) { delete static_cast<Dsa2D*>(p); }

@@ -107,6 +107,7 @@ struct DsaState {
   long dim = 0;
   double m1 = 0, m2 = 0, m3 = 0;
   DBuf<double> fac;         // slab: [S][sum of CR level sizes][48] block cyclic reduction factors
+  DBuf<double> fac_t;       // slab: CR factors of the current block T (apply_eliminated, lazy)
   void* impl2d = nullptr;   // xy: multigrid/Krylov state (dsa2d.cu)
 };
 struct RomState;
@@ -292,6 +293,7 @@ int dsa2d_last_iters(const rte_ctx* ctx);
 long dsa2d_take_launches(rte_ctx* ctx);
 void dsa2d_set_tolerance(rte_ctx* ctx, double tol, int maxit);
 long dsa_coupled_dim(const rte_ctx* ctx);
+void dsa_apply_eliminated(rte_ctx* ctx, const double* x, double* out, cudaStream_t st);
 
 // ROM
 void rom_load(rte_ctx* ctx, int which, const rte_rom* rom);

@@ -450,6 +450,15 @@ class DsaOperator:
         b._call(capi.load().rte_dsa_correct, d.data_ptr(), out.data_ptr(), b._stream())
         return out
 
+    def apply_eliminated(self, x):
+        """dsa.cpp:279-293: S x = A_rr x - A_rJ T^-1 A_Jr x per sample (the
+        current block is factored lazily on first use)."""
+        b = self.batch
+        xd = b._dev(x, (b.S, b.nd))
+        out = b._out(b.S, b.nd)
+        b._call(capi.load().rte_dsa_apply_eliminated, xd.data_ptr(), out.data_ptr(), b._stream())
+        return out
+
 
 def build_dsa(batch: TransportBatch) -> DsaOperator:
     return DsaOperator(batch)

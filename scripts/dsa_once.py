@@ -1,4 +1,4 @@
-"""One 2D DSA solve (for launch lists): python scripts/dsa_once.py NX S TOL"""
+"""One 2D DSA solve (for launch lists): python scripts/dsa_once.py NX S TOL [c3|c5|h<st>:<c>|r<a>:<b>]"""
 import os, sys, time
 os.environ.setdefault("RTE_DSA_WARM", "0")  # repeated solves of one rhs: time cold solves
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -11,6 +11,14 @@ quad = rte.chebyshev_legendre(16, 8)
 n = nx * nx
 if kind == "c3":
     st, ss = np.full((S, n), 10.0), np.full((S, n), 9.99)
+elif kind.startswith("h"):  # homogeneous h<sigma_t>:<c>
+    sg, cc = (float(v) for v in kind[1:].split(":"))
+    st, ss = np.full((S, n), sg), np.full((S, n), sg * cc)
+elif kind.startswith("r"):  # random sigma_t ~ logU[a,b] per cell, c ~ U[0.5,0.99]: r<a>:<b>
+    a_, b_ = (float(v) for v in kind[1:].split(":"))
+    rg = np.random.default_rng(5)
+    st = np.exp(np.log(a_) + (np.log(b_) - np.log(a_)) * rg.uniform(size=(S, n)))
+    ss = rg.uniform(0.5, 0.99, size=(S, n)) * st
 else:
     st, ss = configs.c5_coefficients(nx, S)
 px, py = mesh.cell_points()

@@ -17,6 +17,8 @@ nx = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 rng = np.random.default_rng(1)
 st = np.exp(np.log(0.1) + (np.log(100.0) - np.log(0.1)) * rng.uniform(size=(nx, nx))) * nx / 1024
 c = rng.uniform(0.5, 0.99, size=(nx, nx))
+if os.environ.get("HOMOG"):  # homogeneous field at a given sigma_t (same c draw mean)
+    st = np.full((nx, nx), float(os.environ["HOMOG"]) * nx / 1024); c = np.full((nx, nx), 0.745)
 ss = c * st
 h = 1.0 / nx
 def cell(x, y):
