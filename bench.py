@@ -171,7 +171,7 @@ def run_b200(args, rank, world, device):
     slots = batch.n_slots()
     upd_step = nx * nx * slots * S
     # DSA availability for XY geometry in this build
-    dsa_ok = True
+    dsa_ok, dsa = True, None
     try:
         dsa = rte.DsaOperator(batch)
         dsa.set_tolerance(args.dsa_tol, 2000)
@@ -281,9 +281,122 @@ def run_b200(args, rank, world, device):
         "gpu_launches": gpu_launches,
         "clocks": ck,
     }
+    if rank == 0 and world == 1 and not args.no_ttt:
+        batch = rho = reps = dsa = None  # free the C5 batch (~25 GB) first
+        torch.cuda.empty_cache()
+        line["time_to_tol"] = time_to_tol(device)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_reference(args, budget_s=args.cpu_seconds)
     return line
+
+
+# ---------------------------------------------------------------------------
+# Time to tolerance per parameter sample (the metric's second half) on
+# BASELINE.json configs[0..3], product path only (no oracle: parity for these
+# runs is tests/tools/run_configs.py and tests/test_gpu_*.py).  Offline stage
+# (snapshots, POD, projections) on the device; each online solve timed warm
+# (best of `reps` after a cold call) with CUDA events around the batched call.
+
+def time_to_tol(device, reps=2):
+    import torch
+    from paper_2402_10488_b200 import configs, rte
+    torch.cuda.set_device(device)
+
+    def timed(fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        out = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return out, e0.elapsed_time(e1) * 1e-3
+
+    def warm(fn):
+        out, best = timed(fn)
+        for _ in range(reps):
+            out, t = timed(fn)
+            best = min(best, t)
+        return out, best
+
+    def summary(reps_, t, S):
+        return {"per_sample_s": t / S, "batch_s": t,
+                "mean_iterations": float(np.mean([r.iterations for r in reps_])),
+                "mean_n_sweep": float(np.mean([r.n_sweep for r in reps_])),
+                "converged": int(sum(r.converged for r in reps_)), "samples": S}
+
+    def homog(mod, geom, sig_t, c):
+        t0 = mod.CoefficientTerm(absorption_weight=lambda x, y: sig_t * (1 - c),
+                                 scattering_weight=lambda x, y: sig_t * c)
+        return mod.ProblemDefinition(geom, [t0], lambda x, y: 1.0)
+
+    out = {"timing": "CUDA events around the batched solve call, warm (best of %d after a cold call); "
+                     "per_sample_s = batch_s / samples" % reps}
+    # C1: 256-cell slab, S16, sigma_t = 100, c = 0.9999, SI-DSA to 1e-8 relative change
+    b = rte.TransportBatch(homog(rte, rte.SLAB1D, 100.0, 0.9999), rte.Mesh.slab_uniform(0.0, 1.0, 256),
+                           rte.gauss_legendre(16), [[]], device=device)
+    (_, r), t = warm(lambda: rte.sisa_solve(b, "DSA", rte.SolveConfig(eps_sisa=1e-8, norm="rel")))
+    out["c1_slab"] = {"SI-DSA": summary(r, t, 1)}
+    del b
+    # C2: two-region slab, 32 training + 512 test samples, POD rank 16
+    train, test = configs.c2_params(32, 512)
+    mesh, quad = rte.Mesh.slab_uniform(0.0, 1.0, 256), rte.gauss_legendre(16)
+    eps_train, window, theta = 1e-8, 3, 3
+    t_off = time.perf_counter()
+    tb = rte.TransportBatch(configs.two_region_slab(rte), mesh, quad, train, device=device)
+    snaps = rte.collect_snapshots(tb, window, eps_train)
+    models = []
+    for kind in ("primary", "correction"):
+        U, sv = rte.pod(rte.snapshot_matrix(tb, snaps, kind), 16, device=device)
+        eps_pod = float(np.sum(sv[16:]) / np.sum(sv))
+        models.append(rte.build_reduced_model(tb, U, sv, eps_pod, eps_train, kind[0]))
+    torch.cuda.synchronize()
+    t_off = time.perf_counter() - t_off
+    del tb, snaps
+    b = rte.TransportBatch(configs.two_region_slab(rte), mesh, quad, test, device=device)
+    rte.load_rom(b, 0, models[0])
+    rte.load_rom(b, 1, models[1])
+    cfg = rte.SolveConfig(eps_sisa=1e-8, norm="abs", theta=theta, max_iters=500,
+                          eps_romsad=rte.romsad_tolerance(eps_train, models[1].discarded_fraction))
+    c2 = {"offline_wall_s": t_off, "pod_rank": 16}
+    for label, method in (("SI-DSA", "DSA"), ("ROMIG", "ROMIG"), ("ROMSAD", "ROMSAD")):
+        (_, r), t = warm(lambda: rte.sisa_solve(b, method, cfg))
+        c2[label] = summary(r, t, len(test))
+    out["c2_slab_parametric"] = c2
+    del b
+    # C3: 256^2 XY, CL(16,8), sigma_t = 10, c = 0.999, SI-DSA to 1e-8 relative change
+    b = rte.TransportBatch(homog(rte, rte.XY2D, 10.0, 0.999), rte.Mesh.rect_uniform(0, 1, 256, 0, 1, 256),
+                           rte.chebyshev_legendre(16, 8), [[]], device=device)
+    rte.DsaOperator(b)
+    (_, r), t = warm(lambda: rte.sisa_solve(b, "DSA", rte.SolveConfig(eps_sisa=1e-8, norm="rel")))
+    out["c3_xy"] = {"SI-DSA": summary(r, t, 1)}
+    del b
+    # C4: 128^2 pin cell, 40 training + 64 test samples, POD rank 20 (correction model)
+    train, test = configs.c4_params(40, 64)
+    mesh, quad, make = rte.Mesh.rect_uniform(0, 1, 128, 0, 1, 128), rte.chebyshev_legendre(16, 8), configs.pin_cell(rte)
+    theta = 5
+    t_off = time.perf_counter()
+    tb = rte.TransportBatch(make(128), mesh, quad, train, device=device)
+    snaps = rte.collect_snapshots(tb, window, eps_train)
+    U, sv = rte.pod(rte.snapshot_matrix(tb, snaps, "correction"), 20, device=device)
+    eps_pod = float(np.sum(sv[20:]) / np.sum(sv))
+    cm = rte.build_reduced_model(tb, U, sv, eps_pod, eps_train, "c")
+    torch.cuda.synchronize()
+    t_off = time.perf_counter() - t_off
+    del tb, snaps, U
+    torch.cuda.empty_cache()
+    b = rte.TransportBatch(make(128), mesh, quad, test, device=device)
+    rte.DsaOperator(b)
+    rte.load_rom(b, 1, cm)
+    cfg = rte.SolveConfig(eps_sisa=1e-8, norm="abs", theta=theta, max_iters=500,
+                          eps_romsad=rte.romsad_tolerance(eps_train, eps_pod))
+    c4 = {"offline_wall_s": t_off, "pod_rank": 20}
+    for label, method in (("SI-DSA", "DSA"), ("ROMSAD", "ROMSAD")):
+        (_, r), t = warm(lambda: rte.sisa_solve(b, method, cfg))
+        c4[label] = summary(r, t, len(test))
+    out["c4_xy_pin_cell"] = c4
+    del b
+    torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -374,6 +487,7 @@ def main():
     ap.add_argument("--samples", type=int, default=16)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ttt", action="store_true", help="skip the C1-C4 time-to-tolerance leg")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     args = ap.parse_args()
     rank, world, local = dist_init(init_group=args.impl != "reference")
