@@ -297,6 +297,9 @@ def run_b200(args, rank, world, device):
 # (snapshots, POD, projections) on the device; each online solve timed warm
 # (best of `reps` after a cold call) with CUDA events around the batched call.
 
+INNER = {1e-2: "", 0.0: "/dsa_tol_1e-12"}  # xy DSA inner tolerance: rte_si_config.dsa_inner -> label suffix
+
+
 def time_to_tol(device, reps=2):
     import torch
     from paper_2402_10488_b200 import configs, rte
@@ -330,7 +333,11 @@ def time_to_tol(device, reps=2):
         return mod.ProblemDefinition(geom, [t0], lambda x, y: 1.0)
 
     out = {"timing": "CUDA events around the batched solve call, warm (best of %d after a cold call); "
-                     "per_sample_s = batch_s / samples" % reps}
+                     "per_sample_s = batch_s / samples" % reps,
+           "xy_dsa": "unsuffixed: each DSA solve to relative residual 1e-2 * eps / change (SPEC.md:174 inner "
+                     "tolerance 1e-2 eps_SISA; iteration counts equal the exact-DSA oracle, "
+                     "tests/test_gpu_parity.py::test_2d_dsa_inner_tolerance); '/dsa_tol_1e-12': every DSA solve to "
+                     "relative residual 1e-12"}
     # C1: 256-cell slab, S16, sigma_t = 100, c = 0.9999, SI-DSA to 1e-8 relative change
     b = rte.TransportBatch(homog(rte, rte.SLAB1D, 100.0, 0.9999), rte.Mesh.slab_uniform(0.0, 1.0, 256),
                            rte.gauss_legendre(16), [[]], device=device)
@@ -367,8 +374,11 @@ def time_to_tol(device, reps=2):
     b = rte.TransportBatch(homog(rte, rte.XY2D, 10.0, 0.999), rte.Mesh.rect_uniform(0, 1, 256, 0, 1, 256),
                            rte.chebyshev_legendre(16, 8), [[]], device=device)
     rte.DsaOperator(b)
-    (_, r), t = warm(lambda: rte.sisa_solve(b, "DSA", rte.SolveConfig(eps_sisa=1e-8, norm="rel")))
-    out["c3_xy"] = {"SI-DSA": summary(r, t, 1)}
+    c3 = {}
+    for inner in INNER:
+        (_, r), t = warm(lambda: rte.sisa_solve(b, "DSA", rte.SolveConfig(eps_sisa=1e-8, norm="rel", dsa_inner=inner)))
+        c3["SI-DSA" + INNER[inner]] = summary(r, t, 1)
+    out["c3_xy"] = c3
     del b
     # C4: 128^2 pin cell, 40 training + 64 test samples, POD rank 20 (correction model)
     train, test = configs.c4_params(40, 64)
@@ -387,12 +397,13 @@ def time_to_tol(device, reps=2):
     b = rte.TransportBatch(make(128), mesh, quad, test, device=device)
     rte.DsaOperator(b)
     rte.load_rom(b, 1, cm)
-    cfg = rte.SolveConfig(eps_sisa=1e-8, norm="abs", theta=theta, max_iters=500,
-                          eps_romsad=rte.romsad_tolerance(eps_train, eps_pod))
     c4 = {"offline_wall_s": t_off, "pod_rank": 20}
-    for label, method in (("SI-DSA", "DSA"), ("ROMSAD", "ROMSAD")):
-        (_, r), t = warm(lambda: rte.sisa_solve(b, method, cfg))
-        c4[label] = summary(r, t, len(test))
+    for inner in INNER:
+        cfg = rte.SolveConfig(eps_sisa=1e-8, norm="abs", theta=theta, max_iters=500, dsa_inner=inner,
+                              eps_romsad=rte.romsad_tolerance(eps_train, eps_pod))
+        for label, method in (("SI-DSA", "DSA"), ("ROMSAD", "ROMSAD")):
+            (_, r), t = warm(lambda: rte.sisa_solve(b, method, cfg))
+            c4[label + INNER[inner]] = summary(r, t, len(test))
     out["c4_xy_pin_cell"] = c4
     del b
     torch.cuda.empty_cache()

@@ -131,6 +131,10 @@ typedef struct rte_si_config {
   int check_every;     /* host polls the active count every k iterations (0 = 4) */
   rte_correction_fn correct; /* RTE_CUSTOM only */
   void* correct_user;        /* passed through to correct */
+  double dsa_inner;    /* xy DSA only; 0: every correction solved to the DSA tolerance
+                          (rte_dsa_set_tolerance, default 1e-12 relative); c in (0,1):
+                          iteration l solves to relative residual max(tol, c * eps / change_l)
+                          ("inner tolerance 1e-2 eps_SISA"; ignored with fixed_iters) */
 } rte_si_config;
 
 typedef struct rte_si_report {

@@ -184,6 +184,7 @@ struct SolveConfig {  // solvers.hpp:13-19 (+ batch options)
   const std::vector<double>* initial_guess = nullptr;  // S * n_dof, host
   int gmres_restart = 25;        // solvers.hpp:16
   double gmres_rel_tol = 1e-11;  // solvers.hpp:17
+  double dsa_inner = 0.0;        // xy DSA inner tolerance factor (rte_si_config.dsa_inner)
 };
 
 struct SolveReport {  // solvers.hpp:21-33 (per sample)
@@ -204,6 +205,7 @@ inline std::pair<std::vector<double>, std::vector<SolveReport>> sisa_solve(Trans
   if (c.initial_guess) rho.from_host(*c.initial_guess);
   rte_si_config cfg{c.method, c.eps_sisa, c.norm, c.max_iters, c.fixed_iters, c.theta, c.eps_romsad,
                     c.initial_guess ? 1 : 0, 1, 4};
+  cfg.dsa_inner = c.dsa_inner;
   const int mi = std::max(c.max_iters, c.fixed_iters);
   std::vector<rte_si_report> reps(S);
   std::vector<double> hist((size_t)S * mi);

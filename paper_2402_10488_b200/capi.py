@@ -51,7 +51,8 @@ class SiConfig(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int), ("eps", ctypes.c_double), ("norm", ctypes.c_int),
                 ("max_iters", ctypes.c_int), ("fixed_iters", ctypes.c_int), ("theta", ctypes.c_int),
                 ("eps_romsad", ctypes.c_double), ("use_guess", ctypes.c_int), ("compute_residual", ctypes.c_int),
-                ("check_every", ctypes.c_int), ("correct", CORRECTION_FN), ("correct_user", ctypes.c_void_p)]
+                ("check_every", ctypes.c_int), ("correct", CORRECTION_FN), ("correct_user", ctypes.c_void_p),
+                ("dsa_inner", ctypes.c_double)]
 
 
 class SiReport(ctypes.Structure):

@@ -145,6 +145,9 @@ __global__ void si_decide_kernel(int S, SiState st, int l, rte_si_config cfg) {
       break;
   }
   if (kind == KIND_DSA && st.switch_iter[s] < 0) st.switch_iter[s] = l;
+  // inner tolerance relative to the outer stop test ("1e-2 eps_SISA"):
+  // the correction only has to be accurate to dsa_inner * eps / ||delta||
+  if (st.dsa_tol && kind == KIND_DSA) st.dsa_tol[s] = cfg.dsa_inner * cfg.eps / chn;
   st.kind[s] = kind;
   if (lg) st.log[(long)s * cfg.max_iters + l - 1] = lg;
   const int limit = cfg.fixed_iters > 0 ? cfg.fixed_iters : cfg.max_iters;
@@ -734,6 +737,18 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
     DBuf<unsigned long long>& bits = ctx->si_bits;
     bits.ensure((size_t)2 * S);
     sst.change_bits = bits.p;
+    DBuf<double>& dtol = ctx->si_dsatol;
+    const bool inner = cfg.dsa_inner > 0 && cfg.fixed_iters <= 0 && ctx->geom == RTE_XY2D && need_dsa;
+    if (inner) {
+      RTE_REQUIRE(cfg.dsa_inner < 1.0, RTE_ERR_INVALID, "si_solve: dsa_inner must be in [0, 1)");
+      dtol.ensure(S);
+      sst.dsa_tol = dtol.p;
+    }
+    struct TolScope {  // the per-sample tolerances apply to this solve only
+      rte_ctx* c;
+      ~TolScope() { c->dsa_tol_s = nullptr; }
+    } tol_scope{ctx};
+    ctx->dsa_tol_s = inner ? dtol.p : nullptr;
     init_state_kernel<<<(S + 127) / 128, 128, 0, st>>>(S, sst, need_rom ? sing.p : nullptr, cfg.method);
     RTE_CUDA(cudaGetLastError());
 

@@ -77,6 +77,7 @@ struct Dsa2D {
   // alternates with the warm-start buffer, and by the stopping parameters)
   struct Graph {
     const void* key;
+    const double* tols;  // per-sample tolerance array (nullptr: d->tol for all)
     double tol;
     int maxit;
     cudaGraphExec_t exec;
@@ -1202,8 +1203,9 @@ __global__ void __launch_bounds__(kBT) k_warm_init(int S, long n, int nblk, cons
 
 // warm-start bookkeeping: bnorm2 from part (q0), rho = (b, r) and rnorm2 = (r, r) from part2
 __global__ void k_bicg_init_warm(int S, int nblk, const double* part, const double* part2, double* scal, int* act,
-                                 double tol2, int* nact) {
+                                 double tol2, int* nact, const double* tol_s) {
   const int s = blockIdx.x;
+  if (tol_s) tol2 = fmax(tol2, tol_s[s] * tol_s[s]);
   double q[2], w[2];
   reduce_parts(part, s, nblk, 1, q);
   reduce_parts(part2, s, nblk, 2, w);
@@ -1230,9 +1232,10 @@ __global__ void k_mark_prev(int S, const double* scal, int* has_prev) {
 
 // scalar bookkeeping + convergence: rnorm2 = (r, r), next rho = (rh, r)
 __global__ void k_bicg_check(int S, int nblk, const double* part, double* scal, int* act, double tol2, int maxit,
-                             int* nact) {
+                             int* nact, const double* tol_s) {
   const int s = blockIdx.x;
   if (!act[s]) return;
+  if (tol_s) tol2 = fmax(tol2, tol_s[s] * tol_s[s]);
   double* sc = scal + s * 16;
   double q[2];
   reduce_parts(part, s, nblk, 2, q);
@@ -1836,7 +1839,8 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   }
   RTE_CUDA(cudaMemsetAsync(d->nact.p, 0, sizeof(int), st));
   ++d->nlaunch;
-  k_bicg_init_warm<<<S, 32, 0, st>>>(S, d->nblk, d->part.p, d->part2.p, d->scal.p, d->act.p, tol2, d->nact.p);
+  k_bicg_init_warm<<<S, 32, 0, st>>>(S, d->nblk, d->part.p, d->part2.p, d->scal.p, d->act.p, tol2, d->nact.p,
+                                    ctx->dsa_tol_s);
   RTE_CUDA(cudaGetLastError());
   RTE_CUDA(cudaMemcpyAsync(nact_h, d->nact.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   RTE_CUDA(cudaStreamSynchronize(st));
@@ -1878,7 +1882,8 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
                                    d->r.p, d->s.p, d->t.p, d->rhs.p, d->part2.p, d->act.p);
     RTE_CUDA(cudaMemsetAsync(d->nact.p, 0, sizeof(int), q));
     ++d->nlaunch;
-    k_bicg_check<<<S, 32, 0, q>>>(S, d->nblk, d->part2.p, d->scal.p, d->act.p, tol2, d->maxit, d->nact.p);
+    k_bicg_check<<<S, 32, 0, q>>>(S, d->nblk, d->part2.p, d->scal.p, d->act.p, tol2, d->maxit, d->nact.p,
+                                          ctx->dsa_tol_s);
     RTE_CUDA(cudaGetLastError());
   };
   static const bool graphs_off = [] {
@@ -1895,14 +1900,14 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
       RTE_CUDA(cudaEventCreateWithFlags(&d->ev_out, cudaEventDisableTiming));
     }
     for (const auto& e : d->graphs)
-      if (e.key == d->x.p && e.tol == d->tol && e.maxit == d->maxit) g = &e;
+      if (e.key == d->x.p && e.tols == ctx->dsa_tol_s && e.tol == d->tol && e.maxit == d->maxit) g = &e;
     if (!g) {
       cudaGraph_t graph;
       const long n0 = d->nlaunch;
       RTE_CUDA(cudaStreamBeginCapture(d->gstream, cudaStreamCaptureModeThreadLocal));
       iteration(d->gstream);
       RTE_CUDA(cudaStreamEndCapture(d->gstream, &graph));
-      Dsa2D::Graph e{d->x.p, d->tol, d->maxit, nullptr, d->nlaunch - n0};
+      Dsa2D::Graph e{d->x.p, ctx->dsa_tol_s, d->tol, d->maxit, nullptr, d->nlaunch - n0};
       d->nlaunch = n0;
       RTE_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
       RTE_CUDA(cudaGraphDestroy(graph));

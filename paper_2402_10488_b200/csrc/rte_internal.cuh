@@ -145,7 +145,7 @@ struct rte_ctx {
   rte::DBuf<double> ws_a, ws_b, ws_c, ws_d, ws_e, ws_part;
   // SI driver scratch reused across rte_si_solve calls (no cudaMalloc per solve)
   rte::DBuf<int> si_ibuf, si_int;
-  rte::DBuf<double> si_hist, si_lastc;
+  rte::DBuf<double> si_hist, si_lastc, si_dsatol;
   rte::DBuf<char> si_log, si_letters;
   rte::DBuf<unsigned long long> si_bits;
   int* pinned_int = nullptr;  // cudaMallocHost, one int for the active-count poll
@@ -172,6 +172,10 @@ struct rte_ctx {
   long prof_n[RTE_PROF_KINDS] = {0, 0, 0, 0, 0, 0};
 
   rte::DsaState* dsa = nullptr;
+  // per-sample relative tolerances for the iterative (xy) DSA solve, set by
+  // rte_si_solve for the duration of a solve when rte_si_config.dsa_inner > 0
+  // (nullptr: the DSA's own tolerance for every sample)
+  const double* dsa_tol_s = nullptr;
   rte::RomState* rom[2] = {nullptr, nullptr};
 
   std::string err;
@@ -278,6 +282,7 @@ struct SiState {
   unsigned long long* change_bits;  // [S][2]: max|delta|, max|rho*|
   double* last_change;
   int* n_active;
+  double* dsa_tol;     // [S] per-sample relative DSA tolerance (rte_si_config.dsa_inner > 0), else nullptr
 };
 void launch_si_decide(int S, const SiState& st, int l, const rte_si_config& cfg, cudaStream_t s);
 void launch_si_finalize(int S, long ndof, const SiState& st, const double* rho_star, const double* corr,

@@ -578,6 +578,7 @@ class SolveConfig:
     check_every: int = 4
     gmres_restart: int = 25       # solvers.hpp:16
     gmres_rel_tol: float = 1e-11  # solvers.hpp:17
+    dsa_inner: float = 0.0        # xy DSA: 0 = DSA tolerance; c > 0: relative c * eps / change per iteration
 
 
 @dataclass
@@ -660,7 +661,8 @@ def sisa_solve(batch: TransportBatch, method, config: SolveConfig):
     cfg = capi.SiConfig(m, float(config.eps_sisa), capi.RTE_NORM_REL if config.norm == "rel" else capi.RTE_NORM_ABS,
                         int(config.max_iters), int(config.fixed_iters), int(config.theta),
                         float(config.eps_romsad), 1 if config.initial_guess is not None else 0,
-                        1 if config.compute_residual else 0, int(config.check_every), cb, None)
+                        1 if config.compute_residual else 0, int(config.check_every), cb, None,
+                        float(config.dsa_inner))
     if config.initial_guess is not None:
         rho = batch._dev(config.initial_guess, (batch.S, batch.nd)).clone()
     else:

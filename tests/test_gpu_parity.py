@@ -250,3 +250,34 @@ def test_2d_dsa_solve_parity(case):
     assert reps[0].iterations == o_rep.iterations, (reps[0].iterations, o_rep.iterations)
     assert rel_l2(rho.cpu().numpy()[0], o_rho) < CONV_TOL
     np.testing.assert_allclose(reps[0].change_history, o_rep.change_history, rtol=1e-5, atol=1e-13)
+
+
+def _pin_cell_case(nx=32, n=6):
+    from paper_2402_10488_b200 import configs
+    _, mus = configs.c4_params(0, n)
+    make = configs.pin_cell
+    return pair_2d(lambda m: make(m)(nx), nx, nx, (16, 8), mus)
+
+
+@pytest.mark.parametrize("case", ["c3_32", "thin_random_32", "pin_cell_32x6"])
+@pytest.mark.parametrize("inner", [1e-2, 1e-3])
+def test_2d_dsa_inner_tolerance(case, inner):
+    """rte_si_config.dsa_inner (SPEC.md:174 inner tolerance 1e-2 eps_SISA):
+    each correction solved to relative residual inner * eps / change.  Outer
+    iteration counts equal the oracle's exact (SuperLU) DSA and the converged
+    flux is within the 1e-8 bar."""
+    if case == "pin_cell_32x6":
+        osys, batch = _pin_cell_case()
+    else:
+        osys, batch = _dsa_case([c for c in DSA_CASES_2D if c[0] == case][0])
+    R = rte()
+    eps = 1e-8
+    cfg = R.SolveConfig(eps_sisa=eps, max_iters=500, dsa_inner=inner)
+    rho, reps = R.sisa_solve(batch, "DSA", cfg)
+    rho = rho.cpu().numpy()
+    for s, o in enumerate(osys):
+        o_rho, o_rep = ro.sisa_solve(o, ro.DsaStrategy(ro.build_dsa(o)), ro.SolveConfig(eps_sisa=eps, max_iters=500))
+        assert reps[s].converged and o_rep.converged
+        assert reps[s].iterations == o_rep.iterations, (s, reps[s].iterations, o_rep.iterations)
+        assert rel_l2(rho[s], o_rho) < CONV_TOL
+        np.testing.assert_allclose(reps[s].change_history, o_rep.change_history, rtol=1e-2, atol=1e-13)
