@@ -131,16 +131,24 @@ class Mesh:
         capi.check(capi.load().rte_cell_points(*self._geo(), nq, capi.dptr(px), capi.dptr(py)))
         return px, py
 
+    def _check_points(self, vals, nq):
+        npc = nq if self.geometry == SLAB1D else nq * nq
+        if vals.size != self.cell_count() * npc:
+            raise ValueError("expected %d quadrature-point values (cell_points(%d)), got %d"
+                             % (self.cell_count() * npc, nq, vals.size))
+
     def weighted_mass(self, wvals, nq: int = NQ):
         nl = self.n_local()
         out = np.zeros(self.cell_count() * nl * nl)
         w = _c(wvals)
+        self._check_points(w, nq)
         capi.check(capi.load().rte_weighted_mass(*self._geo(), nq, capi.dptr(w), capi.dptr(out)))
         return out.reshape(self.cell_count(), nl, nl)
 
     def project(self, fvals, nq: int = NQ):
         out = np.zeros(self.n_dof())
         f = _c(fvals)
+        self._check_points(f, nq)
         capi.check(capi.load().rte_project(*self._geo(), nq, capi.dptr(f), capi.dptr(out)))
         return out
 
