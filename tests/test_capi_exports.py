@@ -56,3 +56,30 @@ def test_invalid_arguments_are_reported_not_raised_across_the_abi():
     h = ctypes.c_void_p()
     assert L.rte_create(ctypes.byref(p), 0, ctypes.byref(h)) == capi.RTE_ERR_INVALID
     assert b"geometry" in L.rte_last_error(None)
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """Every struct the ctypes binding mirrors has the C header's size and field
+    offsets (a C program compiled against include/rte_b200.h prints them)."""
+    import subprocess
+    from paper_2402_10488_b200 import capi
+    structs = {"rte_problem": capi.Problem, "rte_affine": capi.Affine, "rte_rom": capi.Rom,
+               "rte_si_config": capi.SiConfig, "rte_si_report": capi.SiReport,
+               "rte_gmres_config": capi.GmresConfig, "rte_gmres_report": capi.GmresReport}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "rte_b200.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append('printf("%s size %%zu\\n", sizeof(%s));' % (cname, cname))
+        for fname, _ in py._fields_:
+            lines.append('printf("%s.%s %%zu\\n", offsetof(%s, %s));' % (cname, fname, cname, fname))
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+                    str(src), "-o", str(exe)], check=True)
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                         check=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got["%s size" % cname]) == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert int(got["%s.%s" % (cname, fname)]) == getattr(py, fname).offset, (cname, fname)
