@@ -1216,7 +1216,7 @@ __global__ void __launch_bounds__(kBT) k_sl_p(int S, long nc, double* scal, cons
 // out = K x on rb fp32 vectors (fp32 coefficients, fp64 arithmetic) with fused
 // partials: mode 0 q0 = (d0, out); mode 1 q0 = (out, d0), q1 = (out, out)
 template <int mode>
-__global__ void __launch_bounds__(kBT) k_sl_apply(int S, int nx, int ny, const float2* __restrict__ sig,
+__global__ void __launch_bounds__(kBT, 5) k_sl_apply(int S, int nx, int ny, const float2* __restrict__ sig,
                                                      const float* __restrict__ xin, float* __restrict__ out,
                                                      const float* __restrict__ d0, double* __restrict__ part,
                                                      const int* __restrict__ act) {
