@@ -107,6 +107,7 @@ struct Dsa2D {
   int maxit = 1000;
   int nu = 6;          // smoothing steps on the finest level
   int gamma0 = 1, gamma = 1;  // coarse-correction cycles from the finest / coarser levels (V-cycle)
+  long cta_cells = 1024;  // levels with at most this many cells run in k_coarse_cycle (0: per-level kernels)
   int nu_coarse = 2;   // smoothing steps on coarser levels (C5 sweep of (nu, nu_coarse): 24 its, 0.56 s)
   int last_iters = 0;
   int nblk = 64;
@@ -705,16 +706,11 @@ struct GsArgs {
   const float* xc;      // if set: neighbours carry the prolonged coarse correction P x_C
 };
 
+// one own-colour cell (slot rem = iy * ceil(nx/2) + k) of sample s
 template <bool FINE, bool PROLONG>
-__global__ void __launch_bounds__(128) k_gs_rb(GsArgs a) {
+__device__ __forceinline__ void gs_body(const GsArgs& a, int s, long rem) {
   const int h = (a.nx + 1) >> 1;
-  const long per = (long)a.ny * h;
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long)a.S * per) return;
-  const int s = (int)(t / per);
-  const long rem = t - s * per;
   const int iy = (int)(rem / h), k = (int)(rem - (long)iy * h);
-  if (a.act && !a.act[s]) return;
   const int c0 = rb_cnt0(a.nx, iy);
   if (k >= (a.color ? a.nx - c0 : c0)) return;
   const int ix = 2 * k + ((a.color + iy) & 1);
@@ -764,18 +760,25 @@ __global__ void __launch_bounds__(128) k_gs_rb(GsArgs a) {
   }
 }
 
+template <bool FINE, bool PROLONG>
+__global__ void __launch_bounds__(128) k_gs_rb(GsArgs a) {
+  const int h = (a.nx + 1) >> 1;
+  const long per = (long)a.ny * h;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)a.S * per) return;
+  const int s = (int)(t / per);
+  if (a.act && !a.act[s]) return;
+  gs_body<FINE, PROLONG>(a, s, t - s * per);
+}
+
 // Restriction of the residual after a pre-smoothing cycle that ended with a
 // colour-1 half-sweep: colour-1 residuals vanish, colour-0 residuals are
 // r_f = -sum_nbr C delta_nbr (delta = last colour-1 update).
 //   b_C = sum_{f in colour-0 children} E_f^T r_f
-__global__ void k_restrict_delta(int S, int fnx, int fny, int lev, const float* __restrict__ delta,
-                                 float* __restrict__ bc, const int* __restrict__ act) {
+__device__ __forceinline__ void restrict_body(int fnx, int fny, int lev, const float* __restrict__ delta,
+                                              float* __restrict__ bc, long s, long C) {
   const int cnx = fnx / 2, cny = fny / 2;
   const long ncc = (long)cnx * cny, nf = (long)fnx * fny;
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long)S * ncc) return;
-  const long s = t / ncc, C = t - s * ncc;
-  if (act && !act[s]) return;
   const int cx = (int)(C % cnx), cy = (int)(C / cnx);
   const float* ds = delta + s * vstride(nf, NB);
   VR out[NB];
@@ -801,6 +804,16 @@ __global__ void k_restrict_delta(int S, int fnx, int fny, int lev, const float* 
   float* o = bc + s * vstride(ncc, NB) + vblk(rbidx(cnx, cx, cy), NB);
 #pragma unroll
   for (int r = 0; r < NB; ++r) o[r * 32] = (float)out[r];
+}
+
+__global__ void k_restrict_delta(int S, int fnx, int fny, int lev, const float* __restrict__ delta,
+                                 float* __restrict__ bc, const int* __restrict__ act) {
+  const long ncc = (long)(fnx / 2) * (fny / 2);
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)S * ncc) return;
+  const long s = t / ncc;
+  if (act && !act[s]) return;
+  restrict_body(fnx, fny, lev, delta, bc, s, t - s * ncc);
 }
 
 // dense coarsest operator [S][n][n] (n = 12 nc), unknown index r * nc + rb(cell)
@@ -895,22 +908,96 @@ __global__ void k_dense_inverse(int n, double* __restrict__ A, double* __restric
   }
 }
 
+// rows r0, r0 + rstep, ... of x = Ainv b for sample s, one warp per row
 template <typename T>
-__global__ void k_dense_apply(int n, int nc, const double* __restrict__ Ainv, const T* __restrict__ b,
-                              T* __restrict__ x, const int* __restrict__ act) {
+__device__ __forceinline__ void dense_apply_body(int n, int nc, const double* __restrict__ Ainv,
+                                                 const T* __restrict__ b, T* __restrict__ x, int s, int r0,
+                                                 int rstep) {
   // dense unknown e = q * nc + k  <->  blocked vector position vblk(k, NB) + 32 q
-  const int s = blockIdx.x;
-  if (act && !act[s]) return;
   const double* a = Ainv + (long)s * n * n;
   const long vs = vstride(nc, NB);
   const T* bs = b + (long)s * vs;
   auto pos = [&](int e) { return vblk(e % nc, NB) + 32 * (e / nc); };
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int r = wid; r < n; r += nw) {
+  const int lane = threadIdx.x & 31;
+  for (int r = r0; r < n; r += rstep) {
     double acc = 0.0;
     for (int c = lane; c < n; c += 32) acc = fma(a[(long)r * n + c], (double)bs[pos(c)], acc);
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) x[(long)s * vs + pos(r)] = (T)acc;
+  }
+}
+
+template <typename T>
+__global__ void k_dense_apply(int n, int nc, const double* __restrict__ Ainv, const T* __restrict__ b,
+                              T* __restrict__ x, const int* __restrict__ act) {
+  const int s = blockIdx.x;
+  if (act && !act[s]) return;
+  // rows split over blockIdx.y (one warp per row): the matrix of a sample is
+  // streamed by gridDim.y CTAs at once instead of one
+  const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  dense_apply_body(n, nc, Ainv, b, x, s, blockIdx.y * nw + wid, nw * gridDim.y);
+}
+
+// The coarse end of the V-cycle in one launch: levels with at most
+// `cta_cells` cells, down to the dense coarsest solve and back up, run by one
+// CTA per sample with __syncthreads between the dependent steps instead of a
+// kernel launch per colour half-sweep (the same per-cell arithmetic and order
+// as the per-level kernels, so results are bitwise identical).
+struct CoarseLev {
+  int nx, ny;
+  float *x, *b, *r;
+  const FacT* fac;
+};
+struct CoarseArgs {
+  int S, lev0, nlev, nu, ncoarse;
+  const double* cinv;  // dense inverse of the coarsest level (ncoarse > 0)
+  const int* act;
+  CoarseLev L[kMaxLevels];
+};
+
+__global__ void __launch_bounds__(256) k_coarse_cycle(CoarseArgs c) {
+  const int s = blockIdx.x;
+  if (c.act && !c.act[s]) return;
+  auto sweep = [&](int i, int color, bool zero_nbr, float* delta, bool old_zero, const float* xc) {
+    const CoarseLev& L = c.L[i];
+    GsArgs a{c.S, L.nx, L.ny, c.lev0 + i, color, L.x, L.b, nullptr, L.fac, nullptr, zero_nbr ? 1 : 0, delta,
+             old_zero ? 1 : 0, xc};
+    const long per = (long)L.ny * ((L.nx + 1) >> 1);
+    for (long rem = threadIdx.x; rem < per; rem += blockDim.x) {
+      if (xc)
+        gs_body<false, true>(a, s, rem);
+      else
+        gs_body<false, false>(a, s, rem);
+    }
+    __syncthreads();
+  };
+  const int last = c.nlev - 1;
+  for (int i = 0; i < last; ++i) {
+    for (int k = 0; k < c.nu; ++k) {
+      sweep(i, 0, k == 0, nullptr, false, nullptr);
+      sweep(i, 1, false, k == c.nu - 1 ? c.L[i].r : nullptr, k == 0, nullptr);
+    }
+    const CoarseLev& L = c.L[i];
+    const long ncc = (long)(L.nx / 2) * (L.ny / 2);
+    for (long C = threadIdx.x; C < ncc; C += blockDim.x)
+      restrict_body(L.nx, L.ny, c.lev0 + i, L.r, c.L[i + 1].b, s, C);
+    __syncthreads();
+  }
+  if (c.ncoarse > 0) {
+    const CoarseLev& L = c.L[last];
+    dense_apply_body(c.ncoarse, L.nx * L.ny, c.cinv, L.b, L.x, s, threadIdx.x >> 5, blockDim.x >> 5);
+    __syncthreads();
+  } else {
+    for (int k = 0; k < 20; ++k) {
+      sweep(last, 0, k == 0, nullptr, false, nullptr);
+      sweep(last, 1, false, nullptr, false, nullptr);
+    }
+  }
+  for (int i = last - 1; i >= 0; --i) {
+    for (int k = 0; k < c.nu; ++k) {
+      sweep(i, 1, false, nullptr, false, k == 0 ? c.L[i + 1].x : nullptr);
+      sweep(i, 0, false, nullptr, false, nullptr);
+    }
   }
 }
 
@@ -1727,6 +1814,7 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   if (const char* e = std::getenv("RTE_DSA_GAMMA0")) d->gamma0 = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_GAMMA")) d->gamma = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_SLOPPY")) d->sloppy = std::atoi(e) != 0;
+  if (const char* e = std::getenv("RTE_DSA_CTA_CELLS")) d->cta_cells = std::atol(e);
   if (const char* e = std::getenv("RTE_DSA_RELIABLE")) d->reliable = std::atof(e);
   d->clear_graphs();
   d->xprev.release();
@@ -2073,11 +2161,31 @@ static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cu
   Level& lv = d->L[l];
   const int S = d->S;
   const bool last = (size_t)l + 1 == d->L.size();
+  if (l > 0 && zero_init && d->gamma == 1 && lv.nc <= d->cta_cells) {
+    // this level and everything below it: one CTA per sample, one launch
+    CoarseArgs c{};
+    c.S = S;
+    c.lev0 = l;
+    c.nlev = (int)d->L.size() - l;
+    c.nu = d->nu_coarse;
+    c.ncoarse = d->ncoarse;
+    c.cinv = d->coarse_inv.p;
+    c.act = act;
+    for (int i = 0; i < c.nlev; ++i) {
+      Level& q = d->L[l + i];
+      c.L[i] = CoarseLev{q.nx, q.ny, i == 0 ? x : q.x.p, i == 0 ? const_cast<float*>(b) : q.b.p, q.r.p, q.fac.p};
+    }
+    ++d->nlaunch;
+    k_coarse_cycle<<<S, 256, 0, st>>>(c);
+    RTE_CUDA(cudaGetLastError());
+    return;
+  }
   if (last) {
     if (d->ncoarse > 0) {
       if (!zero_init) return;  // exact: a repeated visit changes nothing
       ++d->nlaunch;
-      k_dense_apply<<<S, 256, 0, st>>>(d->ncoarse, (int)lv.nc, d->coarse_inv.p, b, x, act);
+      k_dense_apply<<<dim3(S, (d->ncoarse + 63) / 64), 256, 0, st>>>(d->ncoarse, (int)lv.nc, d->coarse_inv.p, b, x,
+                                                                      act);
       RTE_CUDA(cudaGetLastError());
     } else {
       for (int k = 0; k < 20; ++k) {

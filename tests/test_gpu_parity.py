@@ -281,3 +281,20 @@ def test_2d_dsa_inner_tolerance(case, inner):
         assert reps[s].iterations == o_rep.iterations, (s, reps[s].iterations, o_rep.iterations)
         assert rel_l2(rho[s], o_rho) < CONV_TOL
         np.testing.assert_allclose(reps[s].change_history, o_rep.change_history, rtol=1e-2, atol=1e-13)
+
+
+@pytest.mark.parametrize("case", ["c3_32", "partial_coarsening_48x40"])
+def test_2d_dsa_coarse_cycle_kernel_is_bitwise_identical(case, monkeypatch):
+    """k_coarse_cycle (the levels <= RTE_DSA_CTA_CELLS cells in one CTA per
+    sample) performs the per-level kernels' arithmetic in the same order."""
+    R = rte()
+    c = [c for c in DSA_CASES_2D if c[0] == case][0]
+    rhs = np.random.default_rng(4).uniform(-1, 1, (len(c[5]), _dsa_case(c)[0][0].n_dof()))
+    out = []
+    for cells in ("0", "1024"):
+        monkeypatch.setenv("RTE_DSA_CTA_CELLS", cells)
+        _, batch = _dsa_case(c)
+        d = R.DsaOperator(batch)
+        out.append((d.solve_density(rhs).cpu().numpy(), d.last_iterations()))
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][0], out[1][0])
