@@ -2427,7 +2427,18 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   }
   d->last_iters = it;
   static const bool report = std::getenv("RTE_DSA_REPORT") != nullptr;
-  if (report) std::fprintf(stderr, "[dsa2d] solve: %d BiCGStab iterations%s\n", it, d->warm ? " (warm start)" : "");
+  if (report) {  // exact per-sample counts (the loop polls every 4 iterations)
+    std::vector<double> sc((size_t)S * 16);
+    RTE_CUDA(cudaMemcpyAsync(sc.data(), d->scal.p, sizeof(double) * sc.size(), cudaMemcpyDeviceToHost, st));
+    RTE_CUDA(cudaStreamSynchronize(st));
+    double mx = 0, sum = 0;
+    for (int k = 0; k < S; ++k) {
+      mx = std::max(mx, sc[(size_t)k * 16 + SC_ITERS]);
+      sum += sc[(size_t)k * 16 + SC_ITERS];
+    }
+    std::fprintf(stderr, "[dsa2d] solve: %d BiCGStab iterations (per sample max %.0f, mean %.2f)%s\n", it, mx, sum / S,
+                 d->warm ? " (warm start)" : "");
+  }
   ++d->nlaunch;
   k_unpack<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, d->x.p, out, kind);
   RTE_CUDA(cudaGetLastError());
