@@ -110,6 +110,7 @@ struct Dsa2D {
   long cta_cells = 1024;  // levels with at most this many cells run in k_coarse_cycle (0: per-level kernels)
   int nu_coarse = 2;   // smoothing steps on coarser levels (C5 sweep of (nu, nu_coarse): 24 its, 0.56 s)
   int last_iters = 0;
+  int poll_from = 1000000;    // poll every iteration from here on (previous solve's count)
   int nblk = 64;
   long nlaunch = 0;           // kernel launches issued (for launch accounting)
   rte_ctx* ctx = nullptr;     // for per-kernel profiling of the fine smoother
@@ -2412,7 +2413,10 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
       std::fprintf(stderr, "[dsa2d] it %d rel residual %.3e alpha %.3e omega %.3e\n", it,
                    std::sqrt(sc[SC_RNORM2] / sc[SC_BNORM2]), sc[SC_ALPHA], sc[SC_OMEGA]);
     }
-    if ((it & 3) == 3) {
+    // poll the active count every 4 iterations, and after every iteration
+    // from one below the previous solve's count on (the right-hand sides of
+    // consecutive solves converge alike), so at most a few no-op iterations run
+    if ((it & 3) == 3 || it + 2 >= d->poll_from) {
       RTE_CUDA(cudaMemcpyAsync(nact_h, d->nact.p, sizeof(int), cudaMemcpyDeviceToHost, q));
       RTE_CUDA(cudaStreamSynchronize(q));
       if (*nact_h == 0) {
@@ -2426,6 +2430,7 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     RTE_CUDA(cudaStreamWaitEvent(st, d->ev_out, 0));
   }
   d->last_iters = it;
+  if (it > 0) d->poll_from = it;
   static const bool report = std::getenv("RTE_DSA_REPORT") != nullptr;
   if (report) {  // exact per-sample counts (the loop polls every 4 iterations)
     std::vector<double> sc((size_t)S * 16);
