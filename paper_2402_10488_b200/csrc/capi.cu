@@ -272,11 +272,20 @@ Plan2D plan2d(const rte_ctx* c, int single) {
   const int nbands = (c->ny + 31) / 32;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  static const int force_dpl = [] {
+    const char* e = std::getenv("RTE_SWEEP_DPL");
+    return e ? std::atoi(e) : 0;
+  }();
   Plan2D best{1, 1, 0};
   for (int dpl : {8, 4, 2, 1}) {
     if (c->block == 16 && dpl > 2) continue;  // full-block cell solve: keep the register budget
+    if (force_dpl > 0 && dpl != force_dpl) continue;
     const int groups = std::max(1, (mq + nw * dpl - 1) / (nw * dpl));
     best = Plan2D{dpl, groups, groups * nw * dpl};
+    // padded direction slots cost as much as real ones: take a smaller
+    // per-lane direction count rather than run more than 1/4 of the lanes
+    // on padding (CL(16,8): 16 slots per quadrant -> 2 per lane, not 8)
+    if (dpl > 1 && force_dpl == 0 && 4 * (best.nq_pad - mq) > mq) continue;
     const long items = (long)nbands * c->S * 4 * groups;
     if (items >= 4L * sms) break;
   }
