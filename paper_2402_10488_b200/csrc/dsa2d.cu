@@ -944,6 +944,11 @@ __global__ void k_dense_apply(int n, int nc, const double* __restrict__ Ainv, co
 // CTA per sample with __syncthreads between the dependent steps instead of a
 // kernel launch per colour half-sweep (the same per-cell arithmetic and order
 // as the per-level kernels, so results are bitwise identical).
+#ifndef RTE_COARSE_THREADS
+#define RTE_COARSE_THREADS 512
+#endif
+constexpr int kCoarseThreads = RTE_COARSE_THREADS;  // one CTA per sample: a 32^2 level half-sweep in one pass
+
 struct CoarseLev {
   int nx, ny;
   float *x, *b, *r;
@@ -956,7 +961,7 @@ struct CoarseArgs {
   CoarseLev L[kMaxLevels];
 };
 
-__global__ void __launch_bounds__(256) k_coarse_cycle(CoarseArgs c) {
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs c) {
   const int s = blockIdx.x;
   if (c.act && !c.act[s]) return;
   auto sweep = [&](int i, int color, bool zero_nbr, float* delta, bool old_zero, const float* xc) {
@@ -1803,12 +1808,14 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   d->S = S;
   d->ctx = ctx;
   // Smoothing schedule by batch size: below ~4M fine cells the V-cycle is
-  // launch-bound, so extra fine sweeps are nearly free and one coarse sweep
-  // suffices (C3 0.080 -> 0.061 s, C4 4.7 -> 4.2 ms/sample); at C5 scale
-  // (16.7M cells) the fine smoother is HBM-bound and (6, 2) is fastest.
-  const bool small = (long)S * ctx->nx * ctx->ny < (4l << 20);
-  d->nu = small ? 10 : 6;
-  d->nu_coarse = small ? 1 : 2;
+  // latency-bound and one coarse sweep suffices; below ~0.5M cells extra fine
+  // sweeps are nearly free (C3, 65K cells: (10, 1) 27.8 ms vs (6, 1) 31.4);
+  // at C4 scale (1M cells) (6, 1) is best (1.08 vs 1.14 ms/sample with
+  // (10, 1)); at C5 scale (16.7M cells) the fine smoother is HBM-bound and
+  // (6, 2) is fastest.
+  const long cells = (long)S * ctx->nx * ctx->ny;
+  d->nu = cells < (1l << 19) ? 10 : 6;
+  d->nu_coarse = cells < (4l << 20) ? 1 : 2;
   if (const char* e = std::getenv("RTE_DSA_NU")) d->nu = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_NU_COARSE")) d->nu_coarse = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_WARM")) d->warm = std::atoi(e) != 0;
@@ -2177,7 +2184,7 @@ static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cu
       c.L[i] = CoarseLev{q.nx, q.ny, i == 0 ? x : q.x.p, i == 0 ? const_cast<float*>(b) : q.b.p, q.r.p, q.fac.p};
     }
     ++d->nlaunch;
-    k_coarse_cycle<<<S, 256, 0, st>>>(c);
+    k_coarse_cycle<<<S, kCoarseThreads, 0, st>>>(c);
     RTE_CUDA(cudaGetLastError());
     return;
   }
