@@ -70,8 +70,11 @@ struct Dsa2D {
   // BiCGStab (fp64, natural order [S][12][nc]); the shadow residual is the rhs
   DBuf<double> r, p, v, s, t, x, rhs;
   DBuf<double> xprev;         // previous solution per sample (warm start), natural layout
+  DBuf<double> xprev2;        // the one before (two-vector warm start)
+  DBuf<double> partw, partx;  // warm-start dot partials for xprev2
   DBuf<int> has_prev;         // per sample: xprev holds a solution
-  bool warm = true;           // start BiCGStab from the best multiple of the previous solution
+  int warm = 2;               // BiCGStab start: 0 zero, 1 best multiple of the previous solution,
+                              // 2 best combination of the previous two
   int* nact_h = nullptr;      // pinned poll target
   // CUDA graphs of one BiCGStab iteration (keyed by the iterate buffer, which
   // alternates with the warm-start buffer, and by the stopping parameters)
@@ -1637,7 +1640,52 @@ __global__ void k_bicg_init_warm(int S, int nblk, const double* part, const doub
 
 __global__ void k_mark_prev(int S, const double* scal, int* has_prev) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < S && scal[s * 16 + SC_BNORM2] > 0.0) has_prev[s] = 1;
+  if (s < S && scal[s * 16 + SC_BNORM2] > 0.0) has_prev[s] = min(has_prev[s] + 1, 2);
+}
+
+// Two-vector warm start: x0 = g1 xprev + g2 xprev2 minimising ||b - K x0||_2
+// per sample (normal equations of the 2x2 least-squares problem; the
+// consecutive SI-DSA corrections become nearly parallel, so a singular or
+// ill-conditioned pair falls back to the one-vector fit).  part: (K xprev, b),
+// (K xprev, K xprev); partw: (K xprev2, b), (K xprev2, K xprev2); partx:
+// (K xprev, K xprev2).  x = g1 xprev + g2 xprev2, r = b - g1 v1 - g2 v2;
+// partials (b, r), (r, r).
+__global__ void __launch_bounds__(kBT) k_warm_init2(int S, long n, int nblk, const double* part, const double* partw,
+                                                    const double* partx, const int* has_prev,
+                                                    const int* __restrict__ kind, const double* __restrict__ xprev,
+                                                    const double* __restrict__ xprev2, const double* __restrict__ v1,
+                                                    const double* __restrict__ v2, const double* __restrict__ b,
+                                                    double* __restrict__ x, double* __restrict__ r,
+                                                    double* __restrict__ part2) {
+  const int s = blockIdx.y;
+  double q[2], w[2], c[1];
+  reduce_parts(part, s, nblk, 2, q);
+  reduce_parts(partw, s, nblk, 2, w);
+  reduce_parts(partx, s, nblk, 1, c);
+  const bool selected = !kind || kind[s] == KIND_DSA;
+  double g1 = 0.0, g2 = 0.0;
+  if (selected && has_prev[s] >= 1 && q[1] > 0.0) {
+    g1 = q[0] / q[1];
+    const double det = q[1] * w[1] - c[0] * c[0];
+    if (has_prev[s] >= 2 && w[1] > 0.0 && det > 1e-10 * q[1] * w[1]) {
+      g1 = (w[1] * q[0] - c[0] * w[0]) / det;
+      g2 = (q[1] * w[0] - c[0] * q[0]) / det;
+    }
+  }
+  const long base = (long)s * n;
+  double a0 = 0.0, a1 = 0.0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const double bi = b[base + i];
+    const double xp = xprev[base + i];
+    // unselected samples (b == 0, inactive) keep their previous solution in x
+    const double xi = selected ? fma(g2, xprev2[base + i], g1 * xp) : xp;
+    const double ri = fma(-g2, v2[base + i], fma(-g1, v1[base + i], bi));
+    x[base + i] = xi;
+    r[base + i] = ri;
+    a0 = fma(bi, ri, a0);
+    a1 = fma(ri, ri, a1);
+  }
+  block_parts(a0, a1, 2, part2, s);
 }
 
 // scalar bookkeeping + convergence: rnorm2 = (r, r), next rho = (rh, r)
@@ -1818,7 +1866,7 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   d->nu_coarse = cells < (4l << 20) ? 1 : 2;
   if (const char* e = std::getenv("RTE_DSA_NU")) d->nu = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_NU_COARSE")) d->nu_coarse = std::max(1, std::atoi(e));
-  if (const char* e = std::getenv("RTE_DSA_WARM")) d->warm = std::atoi(e) != 0;
+  if (const char* e = std::getenv("RTE_DSA_WARM")) d->warm = std::max(0, std::min(2, std::atoi(e)));
   if (const char* e = std::getenv("RTE_DSA_GAMMA0")) d->gamma0 = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_GAMMA")) d->gamma = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_SLOPPY")) d->sloppy = std::atoi(e) != 0;
@@ -1826,6 +1874,7 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   if (const char* e = std::getenv("RTE_DSA_RELIABLE")) d->reliable = std::atof(e);
   d->clear_graphs();
   d->xprev.release();
+  d->xprev2.release();
   d->has_prev.release();
   // moments (dsa.cpp:167-192, 223-226)
   double m1x = 0, m2x = 0, m3x = 0, m1y = 0, m2y = 0, m3y = 0, m3yx = 0, m3xy = 0;
@@ -2249,7 +2298,36 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     d->has_prev.alloc(S);
     d->has_prev.zero(st);
   }
-  if (d->warm) {
+  if (d->warm >= 2 && !d->xprev2.p) {
+    d->xprev2.alloc((size_t)S * n);
+    d->xprev2.zero(st);
+    d->partw.alloc((size_t)S * d->nblk * 4);
+    d->partx.alloc((size_t)S * d->nblk * 4);
+  }
+  if (d->warm >= 2) {
+    // x0 from span{xprev, xprev2}; v = K xprev and t = K xprev2 are scratch
+    for (int k = 0; k < 2; ++k) {
+      const double* xp = k == 0 ? d->xprev.p : d->xprev2.p;
+      double* kx = k == 0 ? d->v.p : d->t.p;
+      double* pp = k == 0 ? d->part.p : d->partw.p;
+      ++d->nlaunch;
+      if (d->full)
+        k_apply_nat<true><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, xp, kx, d->rhs.p, pp);
+      else
+        k_apply_nat<false><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, xp, kx, d->rhs.p, pp);
+    }
+    DotArgs a{};
+    a.a[0] = d->v.p;
+    a.b[0] = d->t.p;
+    a.nq = 1;
+    ++d->nlaunch;
+    k_dots<<<vgrid, kBT, 0, st>>>(S, n, a, d->partx.p, nullptr);
+    ++d->nlaunch;
+    k_warm_init2<<<vgrid, kBT, 0, st>>>(S, n, d->nblk, d->part.p, d->partw.p, d->partx.p, d->has_prev.p, kind,
+                                        d->xprev.p, d->xprev2.p, d->v.p, d->t.p, d->rhs.p, d->x.p, d->r.p,
+                                        d->part2.p);
+    RTE_CUDA(cudaMemsetAsync(d->v.p, 0, sizeof(double) * S * n, st));
+  } else if (d->warm) {
     // x0 = gamma xprev minimising ||b - gamma K xprev||_2 per sample (v is scratch for K xprev)
     ++d->nlaunch;
     if (d->full)
@@ -2398,7 +2476,7 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
       d->nlaunch = n0;
       RTE_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
       RTE_CUDA(cudaGraphDestroy(graph));
-      if (d->graphs.size() >= 4) d->clear_graphs();
+      if (d->graphs.size() >= 8) d->clear_graphs();
       d->graphs.push_back(e);
       g = &d->graphs.back();
     }
@@ -2455,7 +2533,9 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   k_unpack<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, d->x.p, out, kind);
   RTE_CUDA(cudaGetLastError());
   if (d->warm) {
-    // keep this solution (unselected samples carried their previous one in x)
+    // keep this solution (unselected samples carried their previous one in x):
+    // xprev2 <- xprev <- x, x takes the oldest buffer
+    if (d->warm >= 2) std::swap(d->xprev2, d->xprev);
     std::swap(d->x, d->xprev);
     ++d->nlaunch;
     k_mark_prev<<<(S + 127) / 128, 128, 0, st>>>(S, d->scal.p, d->has_prev.p);
