@@ -44,6 +44,7 @@ constexpr int NB = 12;  // unknowns per cell
 constexpr int NB2 = NB * NB;
 constexpr int kMaxCoarseCells = 16;
 constexpr int kMaxLevels = 16;
+constexpr int kHist = 8;  // max ring length of the K-vector warm start
 #ifdef RTE_DSA_FAC64
 using FacT = double;
 #else
@@ -72,9 +73,14 @@ struct Dsa2D {
   DBuf<double> xprev;         // previous solution per sample (warm start), natural layout
   DBuf<double> xprev2;        // the one before (two-vector warm start)
   DBuf<double> partw, partx;  // warm-start dot partials for xprev2
+  DBuf<double> hx[kHist], hkx[kHist];  // K-vector warm start: ring of solutions and K X (natural layout)
+  DBuf<double> gram, wcoef, part4;     // [S][4][4] Gram of K X, [S][4] weights, [S][nblk][4] partials
+  DBuf<int> hcount;                    // [S] valid ring entries
+  int hhead = -1;                      // ring slot of the newest solution
   DBuf<int> has_prev;         // per sample: xprev holds a solution
-  int warm = 2;               // BiCGStab start: 0 zero, 1 best multiple of the previous solution,
-                              // 2 best combination of the previous two
+  int warm = kHist;           // BiCGStab start: 0 zero, 1 best multiple of the previous solution,
+                              // 2 best combination of the previous two, K >= 3 minimal residual over
+                              // the last K (C5 SI-DSA step: 1 414, 2 384, 4 338, 6 322, 8 320 ms)
   int* nact_h = nullptr;      // pinned poll target
   // CUDA graphs of one BiCGStab iteration (keyed by the iterate buffer, which
   // alternates with the warm-start buffer, and by the stopping parameters)
@@ -1688,6 +1694,157 @@ __global__ void __launch_bounds__(kBT) k_warm_init2(int S, long n, int nblk, con
   block_parts(a0, a1, 2, part2, s);
 }
 
+
+// ---- K-vector warm start (RTE_DSA_WARM = K in 3..8) --------------------------
+// Minimal-residual start from the span of the last K solutions of the sample
+// (projection onto previous solutions for a sequence of right-hand sides,
+// as in Fischer's method for successive linear systems): the solutions X_i
+// and K X_i are kept in a ring, with their Gram matrix G_ij = (K X_i, K X_j)
+// updated incrementally (one operator apply and one multi-dot pass per
+// solve).  x0 = sum_i w_i X_i with G w = c, c_i = (K X_i, b), over the subset
+// of ring vectors, newest first, that keeps the Cholesky factor of G well
+// conditioned (consecutive corrections become nearly parallel).
+struct HistPtrs {
+  const double* v[kHist];
+};
+
+// per-sample fixed-order reduction of kHist-wide partials part8[s][blk][q]
+__device__ __forceinline__ void reduce_parts8(const double* __restrict__ part, int s, int nblk, int nq, double* out) {
+  __shared__ double sh[kHist];
+  if (threadIdx.x < 32) {
+    for (int q = 0; q < nq; ++q) {
+      double v = 0.0;
+      for (int b = threadIdx.x; b < nblk; b += 32) v += part[((long)s * nblk + b) * kHist + q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (threadIdx.x == 0) sh[q] = v;
+    }
+  }
+  __syncthreads();
+  for (int q = 0; q < nq; ++q) out[q] = sh[q];
+}
+
+// part8[s][blk][q] = (a_q, w) for q < nq (fixed-order block reduction)
+__global__ void __launch_bounds__(kBT) k_dots4(int S, long n, int nq, HistPtrs a, const double* __restrict__ w,
+                                               double* __restrict__ part4, const int* __restrict__ act) {
+  const int s = blockIdx.y;
+  if (act && !act[s]) return;
+  double acc[kHist];
+#pragma unroll
+  for (int q = 0; q < kHist; ++q) acc[q] = 0.0;
+  const long base = (long)s * n;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const double wv = w[base + i];
+#pragma unroll
+    for (int q = 0; q < kHist; ++q)
+      if (q < nq) acc[q] = fma(a.v[q][base + i], wv, acc[q]);
+  }
+  __shared__ double red[kHist][kBT];
+#pragma unroll
+  for (int q = 0; q < kHist; ++q) red[q][threadIdx.x] = acc[q];
+  __syncthreads();
+  for (int o = kBT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+#pragma unroll
+      for (int q = 0; q < kHist; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x < nq) part4[((long)s * gridDim.x + blockIdx.x) * kHist + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// after a solve whose solution went to ring slot h: G[h][j] = G[j][h] = (K X_j, K X_h);
+// count = min(count + 1, K) for samples solved in this call, 1 for carried ones
+__global__ void k_hist_gram(int S, int K, int h, int nblk, const double* part4, double* gram, int* count,
+                            const double* scal) {
+  const int s = blockIdx.x;
+  double q[kHist];
+  reduce_parts8(part4, s, nblk, K, q);
+  if (threadIdx.x != 0) return;
+  double* g = gram + (long)s * kHist * kHist;
+  for (int j = 0; j < K; ++j) {
+    g[h * kHist + j] = q[j];
+    g[j * kHist + h] = q[j];
+  }
+  count[s] = scal[s * 16 + SC_BNORM2] > 0.0 ? min(count[s] + 1, K) : 1;
+}
+
+// per sample: w over the ring (newest first, well-conditioned subset)
+__global__ void k_hist_coef(int S, int K, int head, int nblk, const double* part4, const double* gram,
+                            const int* count, const int* __restrict__ kind, double* wcoef) {
+  const int s = blockIdx.x;
+  double c[kHist];
+  reduce_parts8(part4, s, nblk, K, c);
+  if (threadIdx.x != 0) return;
+  double* w = wcoef + (long)s * kHist;
+  for (int j = 0; j < kHist; ++j) w[j] = 0.0;
+  const bool selected = !kind || kind[s] == KIND_DSA;
+  if (!selected) return;
+  const double* g = gram + (long)s * kHist * kHist;
+  int sel[kHist], m = 0;
+  double L[kHist][kHist];
+  for (int j = 0; j < count[s]; ++j) {
+    const int slot = ((head - j) % K + K) % K;
+    const double d = g[slot * kHist + slot];
+    if (!(d > 0.0)) continue;
+    double l[kHist];
+    double piv = d;
+    for (int a = 0; a < m; ++a) {
+      double v = g[slot * kHist + sel[a]];
+      for (int b = 0; b < a; ++b) v -= L[a][b] * l[b];
+      l[a] = v / L[a][a];
+      piv -= l[a] * l[a];
+    }
+    if (piv <= 1e-10 * d) continue;  // nearly dependent on the newer ones
+    for (int a = 0; a < m; ++a) L[m][a] = l[a];
+    L[m][m] = sqrt(piv);
+    sel[m++] = slot;
+  }
+  double y[kHist];
+  for (int a = 0; a < m; ++a) {
+    double v = c[sel[a]];
+    for (int b = 0; b < a; ++b) v -= L[a][b] * y[b];
+    y[a] = v / L[a][a];
+  }
+  for (int a = m - 1; a >= 0; --a) {
+    double v = y[a];
+    for (int b = a + 1; b < m; ++b) v -= L[b][a] * w[sel[b]];
+    w[sel[a]] = v / L[a][a];
+  }
+}
+
+// x = sum w_i X_i, r = b - sum w_i K X_i (unselected samples: x = newest X); partials (b, r), (r, r)
+__global__ void __launch_bounds__(kBT) k_hist_combine(int S, long n, int K, int head, const double* wcoef,
+                                                      HistPtrs X, HistPtrs KX, const int* __restrict__ kind,
+                                                      const double* __restrict__ b, double* __restrict__ x,
+                                                      double* __restrict__ r, double* __restrict__ part2) {
+  const int s = blockIdx.y;
+  const bool selected = !kind || kind[s] == KIND_DSA;
+  double w[kHist];
+#pragma unroll
+  for (int j = 0; j < kHist; ++j) w[j] = j < K ? wcoef[(long)s * kHist + j] : 0.0;
+  const long base = (long)s * n;
+  double a0 = 0.0, a1 = 0.0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const double bi = b[base + i];
+    double xi = 0.0, ri = bi;
+    if (selected) {
+#pragma unroll
+      for (int j = 0; j < kHist; ++j)
+        if (w[j] != 0.0) {
+          xi = fma(w[j], X.v[j][base + i], xi);
+          ri = fma(-w[j], KX.v[j][base + i], ri);
+        }
+    } else {
+      xi = X.v[head][base + i];
+    }
+    x[base + i] = xi;
+    r[base + i] = ri;
+    a0 = fma(bi, ri, a0);
+    a1 = fma(ri, ri, a1);
+  }
+  block_parts(a0, a1, 2, part2, s);
+}
+
 // scalar bookkeeping + convergence: rnorm2 = (r, r), next rho = (rh, r)
 __global__ void k_bicg_check(int S, int nblk, const double* part, double* scal, int* act, double tol2, int maxit,
                              int* nact, const double* tol_s) {
@@ -1866,7 +2023,7 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   d->nu_coarse = cells < (4l << 20) ? 1 : 2;
   if (const char* e = std::getenv("RTE_DSA_NU")) d->nu = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_NU_COARSE")) d->nu_coarse = std::max(1, std::atoi(e));
-  if (const char* e = std::getenv("RTE_DSA_WARM")) d->warm = std::max(0, std::min(2, std::atoi(e)));
+  if (const char* e = std::getenv("RTE_DSA_WARM")) d->warm = std::max(0, std::min(kHist, std::atoi(e)));
   if (const char* e = std::getenv("RTE_DSA_GAMMA0")) d->gamma0 = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_GAMMA")) d->gamma = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_SLOPPY")) d->sloppy = std::atoi(e) != 0;
@@ -1875,6 +2032,12 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   d->clear_graphs();
   d->xprev.release();
   d->xprev2.release();
+  for (int j = 0; j < kHist; ++j) {
+    d->hx[j].release();
+    d->hkx[j].release();
+  }
+  d->gram.release();
+  d->hhead = -1;
   d->has_prev.release();
   // moments (dsa.cpp:167-192, 223-226)
   double m1x = 0, m2x = 0, m3x = 0, m1y = 0, m2y = 0, m3y = 0, m3yx = 0, m3xy = 0;
@@ -2292,19 +2455,50 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   const double tol2 = d->tol * d->tol;
   if (!d->nact_h) RTE_CUDA(cudaMallocHost(&d->nact_h, sizeof(int)));
   int* nact_h = d->nact_h;
-  if (d->warm && !d->xprev.p) {
+  if (d->warm && d->warm < 3 && !d->xprev.p) {
     d->xprev.alloc((size_t)S * n);
     d->xprev.zero(st);
     d->has_prev.alloc(S);
     d->has_prev.zero(st);
   }
-  if (d->warm >= 2 && !d->xprev2.p) {
+  const int K = d->warm;
+  if (K >= 3 && !d->gram.p) {
+    for (int j = 0; j < K; ++j) {
+      d->hx[j].alloc((size_t)S * n);
+      d->hx[j].zero(st);
+      d->hkx[j].alloc((size_t)S * n);
+      d->hkx[j].zero(st);
+    }
+    d->gram.alloc((size_t)S * kHist * kHist);
+    d->gram.zero(st);
+    d->wcoef.alloc((size_t)S * kHist);
+    d->part4.alloc((size_t)S * d->nblk * kHist);
+    d->hcount.alloc(S);
+    d->hcount.zero(st);
+    d->hhead = K - 1;
+  }
+  if (K >= 3) {
+    HistPtrs X{}, KX{};
+    for (int j = 0; j < K; ++j) {
+      X.v[j] = d->hx[j].p;
+      KX.v[j] = d->hkx[j].p;
+    }
+    ++d->nlaunch;
+    k_dots4<<<vgrid, kBT, 0, st>>>(S, n, K, KX, d->rhs.p, d->part4.p, nullptr);
+    ++d->nlaunch;
+    k_hist_coef<<<S, 32, 0, st>>>(S, K, d->hhead, d->nblk, d->part4.p, d->gram.p, d->hcount.p, kind, d->wcoef.p);
+    ++d->nlaunch;
+    k_hist_combine<<<vgrid, kBT, 0, st>>>(S, n, K, d->hhead, d->wcoef.p, X, KX, kind, d->rhs.p, d->x.p, d->r.p,
+                                          d->part2.p);
+    RTE_CUDA(cudaMemsetAsync(d->v.p, 0, sizeof(double) * S * n, st));
+  } else if (d->warm >= 2 && !d->xprev2.p) {
     d->xprev2.alloc((size_t)S * n);
     d->xprev2.zero(st);
     d->partw.alloc((size_t)S * d->nblk * 4);
     d->partx.alloc((size_t)S * d->nblk * 4);
   }
-  if (d->warm >= 2) {
+  if (K >= 3) {
+  } else if (d->warm >= 2) {
     // x0 from span{xprev, xprev2}; v = K xprev and t = K xprev2 are scratch
     for (int k = 0; k < 2; ++k) {
       const double* xp = k == 0 ? d->xprev.p : d->xprev2.p;
@@ -2476,7 +2670,7 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
       d->nlaunch = n0;
       RTE_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
       RTE_CUDA(cudaGraphDestroy(graph));
-      if (d->graphs.size() >= 8) d->clear_graphs();
+      if (d->graphs.size() >= 16) d->clear_graphs();
       d->graphs.push_back(e);
       g = &d->graphs.back();
     }
@@ -2532,7 +2726,27 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   ++d->nlaunch;
   k_unpack<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, d->x.p, out, kind);
   RTE_CUDA(cudaGetLastError());
-  if (d->warm) {
+  if (K >= 3) {
+    // the solution becomes the newest ring entry (its buffer swaps with the
+    // oldest one, which the next solve overwrites), then K X and the Gram row
+    const int h = (d->hhead + 1) % K;
+    std::swap(d->x, d->hx[h]);
+    ++d->nlaunch;
+    if (d->full)
+      k_apply_nat<true><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->hx[h].p, d->hkx[h].p, d->rhs.p,
+                                               d->part2.p);
+    else
+      k_apply_nat<false><<<vgrid, kBT, 0, st>>>(S, l0.nx, l0.ny, d->sgt, d->sgs, d->hx[h].p, d->hkx[h].p,
+                                                d->rhs.p, d->part2.p);
+    HistPtrs KX{};
+    for (int j = 0; j < K; ++j) KX.v[j] = d->hkx[j].p;
+    ++d->nlaunch;
+    k_dots4<<<vgrid, kBT, 0, st>>>(S, n, K, KX, d->hkx[h].p, d->part4.p, nullptr);
+    ++d->nlaunch;
+    k_hist_gram<<<S, 32, 0, st>>>(S, K, h, d->nblk, d->part4.p, d->gram.p, d->hcount.p, d->scal.p);
+    RTE_CUDA(cudaGetLastError());
+    d->hhead = h;
+  } else if (d->warm) {
     // keep this solution (unselected samples carried their previous one in x):
     // xprev2 <- xprev <- x, x takes the oldest buffer
     if (d->warm >= 2) std::swap(d->xprev2, d->xprev);
