@@ -2016,10 +2016,11 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   // latency-bound and one coarse sweep suffices; below ~0.5M cells extra fine
   // sweeps are nearly free (C3, 65K cells: (10, 1) 27.8 ms vs (6, 1) 31.4);
   // at C4 scale (1M cells) (6, 1) is best (1.08 vs 1.14 ms/sample with
-  // (10, 1)); at C5 scale (16.7M cells) the fine smoother is HBM-bound and
-  // (6, 2) is fastest.
+  // (10, 1)); at C5 scale (16.7M cells) the fine smoother is HBM-bound and,
+  // with the history warm start, (4, 2) is fastest (SI-DSA step 314 ms vs
+  // (3, 2) 335, (5, 2) 319, (6, 2) 320, (8, 2) 332, (4, 1) 318, (4, 3) 333).
   const long cells = (long)S * ctx->nx * ctx->ny;
-  d->nu = cells < (1l << 19) ? 10 : 6;
+  d->nu = cells < (1l << 19) ? 10 : cells < (4l << 20) ? 6 : 4;
   d->nu_coarse = cells < (4l << 20) ? 1 : 2;
   if (const char* e = std::getenv("RTE_DSA_NU")) d->nu = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_NU_COARSE")) d->nu_coarse = std::max(1, std::atoi(e));
