@@ -252,7 +252,8 @@ def run_b200(args, rank, world, device):
     # read (48 B), (sigma_t, sigma_a) (8 B) = 152 B; per V-cycle of 4 nu
     # half-sweeps one starts from x = 0 (104 B), one also reads x_old and
     # writes delta (248 B), one also reads the coarse correction (176 B).
-    nu = int(os.environ.get("RTE_DSA_NU", "6"))
+    cells = S * nx * nx  # the library's smoothing schedule by batch size (dsa2d.cu, dsa2d_setup)
+    nu = int(os.environ.get("RTE_DSA_NU", 10 if cells < (1 << 19) else 6 if cells < (4 << 20) else 4))
     gs_cell = (104 + 248 + 176 + (4 * nu - 3) * 152) / (4 * nu)
     gs_ms = ms_k[5] / max(n_k[5], 1)
     gs_bytes = gs_cell * S * nx * nx / 2
