@@ -2822,7 +2822,17 @@ long dsa2d_take_launches(rte_ctx* ctx) {
 
 int dsa2d_last_iters(const rte_ctx* ctx) {
   if (!ctx->dsa || !ctx->dsa->impl2d) return 0;
-  return static_cast<Dsa2D*>(ctx->dsa->impl2d)->last_iters;
+  const auto* d = static_cast<const Dsa2D*>(ctx->dsa->impl2d);
+  if (!d->scal.p) return d->last_iters;
+  // exact count (max over the samples of the last solve; the solve loop only
+  // polls the active count, so its trip count can overshoot by up to 3)
+  std::vector<double> sc((size_t)d->S * 16);
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpy(sc.data(), d->scal.p, sizeof(double) * sc.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return d->last_iters;
+  double mx = 0;
+  for (int k = 0; k < d->S; ++k) mx = std::max(mx, sc[(size_t)k * 16 + SC_ITERS]);
+  return (int)mx;
 }
 
 void dsa2d_set_tolerance(rte_ctx* ctx, double tol, int maxit) {

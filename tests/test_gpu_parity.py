@@ -298,3 +298,27 @@ def test_2d_dsa_coarse_cycle_kernel_is_bitwise_identical(case, monkeypatch):
         out.append((d.solve_density(rhs).cpu().numpy(), d.last_iterations()))
     assert out[0][1] == out[1][1]
     assert np.array_equal(out[0][0], out[1][0])
+
+
+def test_2d_dsa_history_warm_start():
+    """The warm start is the minimal-residual combination of the sample's
+    previous solutions: a repeated right-hand side and a linear combination of
+    earlier ones start (nearly) converged, and every solve still matches the
+    oracle's SuperLU solution."""
+    R = rte()
+    osys, batch = _dsa_case(DSA_CASES_2D[3])  # c3_32, one sample
+    d = R.DsaOperator(batch)
+    od = ro.build_dsa(osys[0])
+    rng = np.random.default_rng(11)
+    b1, b2 = (rng.uniform(-1, 1, (1, osys[0].n_dof())) for _ in range(2))
+    x1 = d.solve_density(b1).cpu().numpy()
+    n1 = d.last_iterations()
+    x2 = d.solve_density(b2).cpu().numpy()
+    assert n1 > 0 and d.last_iterations() > 0
+    x1b = d.solve_density(b1).cpu().numpy()
+    assert d.last_iterations() <= 1
+    b3 = 0.3 * b1 - 2.0 * b2
+    x3 = d.solve_density(b3).cpu().numpy()
+    assert d.last_iterations() <= 1
+    for b, x in ((b1, x1), (b2, x2), (b1, x1b), (b3, x3)):
+        assert rel_l2(x[0], od.solve_density(b[0])) < 1e-9
