@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from oracle import rte_oracle as ro
-from paper_2402_10488_b200 import configs, rte
+from paper_2402_10488_b200 import configs, reports, rte
 from tests.problems import homog, pin_cell, rel_l2, two_region_slab
 
 
@@ -115,9 +115,16 @@ def c2(args):
     ocm = ro.ReducedModel(0, 16, b.n_dof(), 16, 4, "c", eps_c, eps_train, cm.u_rho, cm.u_iso, cm.a_r, cm.singular_values,
                           cm.discarded_fraction, cm.b_r)
     idx = list(range(0, S, max(1, S // args.parity)))[:args.parity] if args.parity > 0 else []
+    table = reports.MetricsTable("c2_slab_parametric", [], [("snapshot_seconds", offline["snapshot_s"]),
+                                                             ("pod_seconds", offline["pod_s"]),
+                                                             ("projection_seconds", offline["projection_s"])])
     for method in ("DSA", "ROMIG", "ROMSAD"):
         cfg = rte.SolveConfig(eps_sisa=1e-8, norm="abs", theta=theta, eps_romsad=eps_r, max_iters=500)
         ((rho, reps), tc, t) = timed_warm(lambda: rte.sisa_solve(b, method, cfg))
+        if method == "DSA":
+            t_dsa = t
+        label, rp, rc = {"DSA": ("DSA", 0, 0), "ROMIG": ("ROMIG", 16, 0), "ROMSAD": ("ROMSAD-3,3", 0, 16)}[method]
+        table.rows.append(reports.metrics_row(label, reps, t / t_dsa, rp, rc))
         rho = rho.cpu().numpy()
         if method == "DSA":
             strat = lambda o: ro.DsaStrategy(ro.build_dsa(o))
@@ -141,6 +148,7 @@ def c2(args):
                       "mean_n_sweep": float(np.mean([r.n_sweep for r in reps])),
                       "converged": int(sum(r.converged for r in reps)),
                       "parity": check_gmres(osys, test, reps, rho, idx[:4], True, opm if rg else None)}
+    out["summary_v1"] = reports.serialize_summary(table)  # the reference runner's summary format
     return out
 
 
@@ -204,9 +212,15 @@ def c4(args):
                           cm.singular_values, cm.discarded_fraction, cm.b_r)
     osys = lambda mu: ro.TransportSystem(mk(nx), om, ro.build_dg_space(om), ro.chebyshev_legendre(16, 8), mu)
     idx = list(range(0, S, max(1, S // args.parity4)))[:args.parity4] if args.parity4 > 0 else []
+    table = reports.MetricsTable("c4_xy_pin_cell", [], [("snapshot_seconds", t_snap), ("pod_seconds", t_pod),
+                                                         ("projection_seconds", t_b)])
     for method, inner in (("DSA", 0.0), ("ROMSAD", 0.0), ("DSA", 1e-2), ("ROMSAD", 1e-2)):
         cfg = rte.SolveConfig(eps_sisa=1e-8, theta=theta, eps_romsad=eps_r, max_iters=500, dsa_inner=inner)
         ((rho, reps), tc, t) = timed_warm(lambda: rte.sisa_solve(b, method, cfg), reps=1)
+        if method == "DSA" and inner == 0:
+            t_dsa = t
+        label = ("DSA" if method == "DSA" else "ROMSAD-3,5") + ("" if inner == 0 else " dsa_inner=%g" % inner)
+        table.rows.append(reports.metrics_row(label, reps, t / t_dsa, 0, 0 if method == "DSA" else 20))
         rho = rho.cpu().numpy()
         strat = (lambda o: ro.DsaStrategy(ro.build_dsa(o))) if method == "DSA" else \
             (lambda o: ro.RomsadStrategy(ocm, ro.build_dsa(o), theta, eps_r))
@@ -224,6 +238,7 @@ def c4(args):
                      "mean_n_sweep": float(np.mean([r.n_sweep for r in greps])),
                      "converged": int(sum(r.converged for r in greps)),
                      "parity": check_gmres(osys, test, greps, grho.cpu().numpy(), idx[:1], True) if idx else None}
+    out["summary_v1"] = reports.serialize_summary(table)
     return out
 
 
