@@ -74,7 +74,7 @@ struct Dsa2D {
   DBuf<double> xprev2;        // the one before (two-vector warm start)
   DBuf<double> partw, partx;  // warm-start dot partials for xprev2
   DBuf<double> hx[kHist], hkx[kHist];  // K-vector warm start: ring of solutions and K X (natural layout)
-  DBuf<double> gram, wcoef, part4;     // [S][4][4] Gram of K X, [S][4] weights, [S][nblk][4] partials
+  DBuf<double> gram, wcoef, parth;     // [S][4][4] Gram of K X, [S][4] weights, [S][nblk][4] partials
   DBuf<int> hcount;                    // [S] valid ring entries
   int hhead = -1;                      // ring slot of the newest solution
   DBuf<int> has_prev;         // per sample: xprev holds a solution
@@ -1725,8 +1725,8 @@ __device__ __forceinline__ void reduce_parts8(const double* __restrict__ part, i
 }
 
 // part8[s][blk][q] = (a_q, w) for q < nq (fixed-order block reduction)
-__global__ void __launch_bounds__(kBT) k_dots4(int S, long n, int nq, HistPtrs a, const double* __restrict__ w,
-                                               double* __restrict__ part4, const int* __restrict__ act) {
+__global__ void __launch_bounds__(kBT) k_dots_hist(int S, long n, int nq, HistPtrs a, const double* __restrict__ w,
+                                               double* __restrict__ parth, const int* __restrict__ act) {
   const int s = blockIdx.y;
   if (act && !act[s]) return;
   double acc[kHist];
@@ -1749,16 +1749,16 @@ __global__ void __launch_bounds__(kBT) k_dots4(int S, long n, int nq, HistPtrs a
       for (int q = 0; q < kHist; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x < nq) part4[((long)s * gridDim.x + blockIdx.x) * kHist + threadIdx.x] = red[threadIdx.x][0];
+  if (threadIdx.x < nq) parth[((long)s * gridDim.x + blockIdx.x) * kHist + threadIdx.x] = red[threadIdx.x][0];
 }
 
 // after a solve whose solution went to ring slot h: G[h][j] = G[j][h] = (K X_j, K X_h);
 // count = min(count + 1, K) for samples solved in this call, 1 for carried ones
-__global__ void k_hist_gram(int S, int K, int h, int nblk, const double* part4, double* gram, int* count,
+__global__ void k_hist_gram(int S, int K, int h, int nblk, const double* parth, double* gram, int* count,
                             const double* scal) {
   const int s = blockIdx.x;
   double q[kHist];
-  reduce_parts8(part4, s, nblk, K, q);
+  reduce_parts8(parth, s, nblk, K, q);
   if (threadIdx.x != 0) return;
   double* g = gram + (long)s * kHist * kHist;
   for (int j = 0; j < K; ++j) {
@@ -1769,11 +1769,11 @@ __global__ void k_hist_gram(int S, int K, int h, int nblk, const double* part4, 
 }
 
 // per sample: w over the ring (newest first, well-conditioned subset)
-__global__ void k_hist_coef(int S, int K, int head, int nblk, const double* part4, const double* gram,
+__global__ void k_hist_coef(int S, int K, int head, int nblk, const double* parth, const double* gram,
                             const int* count, const int* __restrict__ kind, double* wcoef) {
   const int s = blockIdx.x;
   double c[kHist];
-  reduce_parts8(part4, s, nblk, K, c);
+  reduce_parts8(parth, s, nblk, K, c);
   if (threadIdx.x != 0) return;
   double* w = wcoef + (long)s * kHist;
   for (int j = 0; j < kHist; ++j) w[j] = 0.0;
@@ -2482,7 +2482,7 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     d->gram.alloc((size_t)S * kHist * kHist);
     d->gram.zero(st);
     d->wcoef.alloc((size_t)S * kHist);
-    d->part4.alloc((size_t)S * d->nblk * kHist);
+    d->parth.alloc((size_t)S * d->nblk * kHist);
     d->hcount.alloc(S);
     d->hcount.zero(st);
     d->hhead = K - 1;
@@ -2494,9 +2494,9 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
       KX.v[j] = d->hkx[j].p;
     }
     ++d->nlaunch;
-    k_dots4<<<vgrid, kBT, 0, st>>>(S, n, K, KX, d->rhs.p, d->part4.p, nullptr);
+    k_dots_hist<<<vgrid, kBT, 0, st>>>(S, n, K, KX, d->rhs.p, d->parth.p, nullptr);
     ++d->nlaunch;
-    k_hist_coef<<<S, 32, 0, st>>>(S, K, d->hhead, d->nblk, d->part4.p, d->gram.p, d->hcount.p, kind, d->wcoef.p);
+    k_hist_coef<<<S, 32, 0, st>>>(S, K, d->hhead, d->nblk, d->parth.p, d->gram.p, d->hcount.p, kind, d->wcoef.p);
     ++d->nlaunch;
     k_hist_combine<<<vgrid, kBT, 0, st>>>(S, n, K, d->hhead, d->wcoef.p, X, KX, kind, d->rhs.p, d->x.p, d->r.p,
                                           d->part2.p);
@@ -2751,9 +2751,9 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     HistPtrs KX{};
     for (int j = 0; j < K; ++j) KX.v[j] = d->hkx[j].p;
     ++d->nlaunch;
-    k_dots4<<<vgrid, kBT, 0, st>>>(S, n, K, KX, d->hkx[h].p, d->part4.p, nullptr);
+    k_dots_hist<<<vgrid, kBT, 0, st>>>(S, n, K, KX, d->hkx[h].p, d->parth.p, nullptr);
     ++d->nlaunch;
-    k_hist_gram<<<S, 32, 0, st>>>(S, K, h, d->nblk, d->part4.p, d->gram.p, d->hcount.p, d->scal.p);
+    k_hist_gram<<<S, 32, 0, st>>>(S, K, h, d->nblk, d->parth.p, d->gram.p, d->hcount.p, d->scal.p);
     RTE_CUDA(cudaGetLastError());
     d->hhead = h;
   } else if (d->warm) {
