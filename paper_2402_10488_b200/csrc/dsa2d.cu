@@ -1708,7 +1708,7 @@ struct HistPtrs {
   const double* v[kHist];
 };
 
-// per-sample fixed-order reduction of kHist-wide partials part8[s][blk][q]
+// per-sample fixed-order reduction of kHist-wide partials parth[s][blk][q]
 __device__ __forceinline__ void reduce_parts8(const double* __restrict__ part, int s, int nblk, int nq, double* out) {
   __shared__ double sh[kHist];
   if (threadIdx.x < 32) {
@@ -1724,7 +1724,7 @@ __device__ __forceinline__ void reduce_parts8(const double* __restrict__ part, i
   for (int q = 0; q < nq; ++q) out[q] = sh[q];
 }
 
-// part8[s][blk][q] = (a_q, w) for q < nq (fixed-order block reduction)
+// parth[s][blk][q] = (a_q, w) for q < nq (fixed-order block reduction)
 __global__ void __launch_bounds__(kBT) k_dots_hist(int S, long n, int nq, HistPtrs a, const double* __restrict__ w,
                                                double* __restrict__ parth, const int* __restrict__ act) {
   const int s = blockIdx.y;
