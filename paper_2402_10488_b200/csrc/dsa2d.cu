@@ -1466,10 +1466,10 @@ __global__ void __launch_bounds__(kBT) k_sl_fold(int S, int nx, long nc, float* 
 
 // reliable update, part 2: r = b - K x with the fp64 operator (x, b natural),
 // stored as the sloppy residual r_l; partials (r, r), (b, r)
-__global__ void __launch_bounds__(kBT) k_sl_resid(int S, int nx, int ny, const double* __restrict__ sgt,
-                                                     const double* __restrict__ sgs, const double* __restrict__ xin,
-                                                     const double* __restrict__ b, float* __restrict__ rl,
-                                                     double* __restrict__ part, const int* act, const int* upd) {
+__global__ void __launch_bounds__(kBT, 2) k_sl_resid(int S, int nx, int ny, const double* __restrict__ sgt,
+                                                        const double* __restrict__ sgs, const double* __restrict__ xin,
+                                                        const double* __restrict__ b, float* __restrict__ rl,
+                                                        double* __restrict__ part, const int* act, const int* upd) {
   const int s = blockIdx.y;
   if (!act[s] || !upd[s]) return;
   const long nc = (long)nx * ny;
@@ -1480,15 +1480,16 @@ __global__ void __launch_bounds__(kBT) k_sl_resid(int S, int nx, int ny, const d
     double acc[NB], v[NB];
 #pragma unroll
     for (int r = 0; r < NB; ++r) acc[r] = 0.0;
-    auto nbr = [&](int dir, long cn) {
+    // one neighbour at a time (keeps 12 loaded values live, not 48: 2 CTAs/SM without spills)
+#pragma unroll 1
+    for (int dir = 0; dir < 4; ++dir) {
+      const bool ok = dir == 0 ? ix > 0 : dir == 1 ? ix < nx - 1 : dir == 2 ? iy > 0 : iy < ny - 1;
+      if (!ok) continue;
+      const long cn = dir == 0 ? c - 1 : dir == 1 ? c + 1 : dir == 2 ? c - nx : c + nx;
 #pragma unroll
       for (int r = 0; r < NB; ++r) v[r] = xs[r * nc + cn];
       face_lift(0, dir, v, acc);
-    };
-    if (ix > 0) nbr(0, c - 1);
-    if (ix < nx - 1) nbr(1, c + 1);
-    if (iy > 0) nbr(2, c - nx);
-    if (iy < ny - 1) nbr(3, c + nx);
+    }
 #pragma unroll
     for (int r = 0; r < NB; ++r) v[r] = xs[r * nc + c];
     const long fi = (long)s * nc + c;
@@ -1546,15 +1547,16 @@ __global__ void __launch_bounds__(kBT, 2) k_apply_nat(int S, int nx, int ny, con
     double acc[NB], v[NB];
 #pragma unroll
     for (int r = 0; r < NB; ++r) acc[r] = 0.0;
-    auto nbr = [&](int dir, long cn) {
+    // one neighbour at a time (keeps 12 loaded values live, not 48)
+#pragma unroll 1
+    for (int dir = 0; dir < 4; ++dir) {
+      const bool ok = dir == 0 ? ix > 0 : dir == 1 ? ix < nx - 1 : dir == 2 ? iy > 0 : iy < ny - 1;
+      if (!ok) continue;
+      const long cn = dir == 0 ? c - 1 : dir == 1 ? c + 1 : dir == 2 ? c - nx : c + nx;
 #pragma unroll
       for (int r = 0; r < NB; ++r) v[r] = xs[r * nc + cn];
       face_lift(0, dir, v, acc);
-    };
-    if (ix > 0) nbr(0, c - 1);
-    if (ix < nx - 1) nbr(1, c + 1);
-    if (iy > 0) nbr(2, c - nx);
-    if (iy < ny - 1) nbr(3, c + nx);
+    }
 #pragma unroll
     for (int r = 0; r < NB; ++r) v[r] = xs[r * nc + c];
     const long fi = (long)s * nc + c;
