@@ -129,3 +129,28 @@ def test_c4_full_size_methods_agree():
     for s in range(len(test)):
         assert rel(rr[s], rd[s]) < 1e-7 and rel(rg[s], rd[s]) < 1e-7
         assert rep_r[s].n_sweep <= rep_d[s].n_sweep + 5
+
+
+def test_c5_dsa_fast_paths_match_the_plain_solver(monkeypatch):
+    """At full C5 size (4 of the samples), three SI-DSA iterations with the
+    production DSA (mixed-precision recurrences, history warm start) and with
+    the plain one (fp64 recurrences, cold start: RTE_DSA_SLOPPY=0,
+    RTE_DSA_WARM=0) agree to the DSA tolerance: the fast paths change the
+    cost of each correction, not its value."""
+    import torch
+    from paper_2402_10488_b200 import configs, rte
+    st, ss = configs.c5_coefficients(NX, 4)
+    mesh = rte.Mesh.rect_uniform(0, 1, NX, 0, 1, NX)
+    g = mesh.project(np.ones(mesh.cell_points()[0].size))
+    out = []
+    for env in ({}, {"RTE_DSA_SLOPPY": "0", "RTE_DSA_WARM": "0"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        b = rte.TransportBatch.from_cells(mesh, rte.chebyshev_legendre(32, 16), st, ss, g)
+        rte.DsaOperator(b).set_tolerance(1e-10, 2000)
+        rho, reps = rte.sisa_solve(b, "DSA", rte.SolveConfig(fixed_iters=3, max_iters=3, compute_residual=False))
+        out.append((rho.cpu().numpy(), [r.change_history for r in reps]))
+        del b, rho
+        torch.cuda.empty_cache()
+    assert rel(out[0][0], out[1][0]) < 1e-8
+    np.testing.assert_allclose(out[0][1], out[1][1], rtol=1e-6)
