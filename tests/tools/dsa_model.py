@@ -6,7 +6,7 @@ and a red-black 12x12 block Gauss-Seidel V-cycle mirroring dsa2d.cu, then
 measures BiCGStab/GMRES preconditioner applications and analyses the slow
 modes.  DESIGN.md section 6 quotes its results.
 
-  python tests/tools/dsa_model.py NX LEVELS [plain|aux] [mode|gmres|lines N|smoothedP W|spectrum|semicoarse|patch N]
+  python tests/tools/dsa_model.py NX LEVELS [plain|aux] [mode|gmres|lines N|smoothedP W|spectrum|semicoarse|patch N|bicgstabl]
 """
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
@@ -181,6 +181,50 @@ t = time.time()
 x, info = spl.bicgstab(A, b, M=M, rtol=1e-8, maxiter=500, callback=cb)
 print("levels", len(levs), "aux" if AUX else "plain", "bicgstab its", its[0], "info", info,
       "relres %.2e" % (np.linalg.norm(b - A @ x) / np.linalg.norm(b)), "%.1f s" % (time.time() - t))
+
+def bicgstab_l(Bop, b, ell, tol=1e-8, maxit=400):
+    """BiCGStab(ell) (Sleijpen-Fokkema) on B y = b; returns (y, B applications)."""
+    y = np.zeros_like(b); r = [b.copy()] + [None] * ell; u = [np.zeros_like(b)] + [None] * ell
+    rt = b.copy(); rho0, alpha, omega = 1.0, 0.0, 1.0
+    nb = np.linalg.norm(b); napp = 0
+    while napp < maxit:
+        rho0 = -omega * rho0
+        for j in range(ell):
+            rho1 = r[j] @ rt; beta = alpha * rho1 / rho0; rho0 = rho1
+            for i in range(j + 1):
+                u[i] = r[i] - beta * u[i]
+            u[j + 1] = Bop(u[j]); napp += 1
+            alpha = rho0 / (u[j + 1] @ rt)
+            for i in range(j + 1):
+                r[i] = r[i] - alpha * u[i + 1]
+            r[j + 1] = Bop(r[j]); napp += 1
+            y = y + alpha * u[0]
+        tau = np.zeros((ell + 1, ell + 1)); sig = np.zeros(ell + 1); gp = np.zeros(ell + 1)
+        for j in range(1, ell + 1):
+            for i in range(1, j):
+                tau[i, j] = (r[j] @ r[i]) / sig[i]
+                r[j] = r[j] - tau[i, j] * r[i]
+            sig[j] = r[j] @ r[j]; gp[j] = (r[0] @ r[j]) / sig[j]
+        g = np.zeros(ell + 1); g[ell] = gp[ell]; omega = g[ell]
+        for j in range(ell - 1, 0, -1):
+            g[j] = gp[j] - sum(tau[j, i] * g[i] for i in range(j + 1, ell + 1))
+        gpp = np.zeros(ell + 1)
+        for j in range(1, ell):
+            gpp[j] = g[j + 1] + sum(tau[j, i] * g[i + 1] for i in range(j + 1, ell))
+        y = y + g[1] * r[0]; r[0] = r[0] - gp[ell] * r[ell]; u[0] = u[0] - g[ell] * u[ell]
+        for j in range(1, ell):
+            u[0] = u[0] - g[j] * u[j]; y = y + gpp[j] * r[j]; r[0] = r[0] - gp[j] * r[j]
+        if np.linalg.norm(r[0]) <= tol * nb:
+            break
+    return y, napp
+
+if len(sys.argv) > 4 and sys.argv[4] == "bicgstabl":
+    Bop = lambda v: A @ vcycle(0, v)
+    for ell in (1, 2, 4):
+        yv, napp = bicgstab_l(Bop, b, ell)
+        xv = vcycle(0, yv)
+        print("BiCGStab(%d): %d preconditioner applications, true relres %.2e" %
+              (ell, napp, np.linalg.norm(b - A @ xv) / np.linalg.norm(b)), flush=True)
 
 if len(sys.argv) > 4 and sys.argv[4] == "mode":
     e = rng.standard_normal(N)
