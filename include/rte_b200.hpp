@@ -100,11 +100,30 @@ class DeviceVector {
 // per-cell coefficients (slab: full 2x2 blocks or scalars; xy: scalars).
 class TransportBatch {
  public:
-  TransportBatch(const rte_problem& p, int device = 0) {
+  TransportBatch(const rte_problem& p, int device = 0) : n_dirs_(p.n_dirs), device_(device) {
     check(rte_create(&p, device, &ctx_), nullptr);
   }
-  ~TransportBatch() { rte_destroy(ctx_); }
+  // Affine decomposition (problem.hpp:24-29): per-term total / scattering
+  // mass blocks [K][cells][block] and psi [S][K] with psi[s][0] == 1; needed
+  // by the kinetic term operators and the reduced models.
+  void set_affine(int k_terms, const std::vector<double>& term_mt, const std::vector<double>& term_ms,
+                  const std::vector<double>& psi) {
+    rte_affine a{k_terms, term_mt.data(), term_ms.data(), psi.data()};
+    check(rte_set_affine(ctx_, &a), ctx_);
+    k_terms_ = k_terms;
+  }
+  int n_dirs() const { return n_dirs_; }
+  long kinetic_dim() const { return (long)n_dirs_ * n_dof(); }
+  int k_terms() const { return k_terms_; }
+  int device() const { return device_; }
+  ~TransportBatch() {
+    if (ctx_) rte_destroy(ctx_);
+  }
   TransportBatch(const TransportBatch&) = delete;
+  TransportBatch(TransportBatch&& o) noexcept
+      : ctx_(o.ctx_), n_dirs_(o.n_dirs_), device_(o.device_), k_terms_(o.k_terms_) {
+    o.ctx_ = nullptr;
+  }
   rte_ctx* handle() const { return ctx_; }
   long n_dof() const { return rte_n_dof(ctx_); }
   int n_samples() const { return rte_n_samples(ctx_); }
@@ -147,6 +166,7 @@ class TransportBatch {
 
  private:
   rte_ctx* ctx_ = nullptr;
+  int n_dirs_ = 0, device_ = 0, k_terms_ = 0;
 };
 
 class DsaOperator {  // dsa.hpp:29-56
@@ -253,6 +273,131 @@ inline std::pair<std::vector<double>, std::vector<SolveReport>> gmres_solve(Tran
     r.final_residual = reps[s].final_residual;
   }
   return {rho.to_host(), out};
+}
+
+// ---- reduced models: offline stage and online strategies -------------------
+
+// ReducedModel (reduced_model.hpp:19-44), column-major like the reference's
+// Eigen storage: u_rho / u_iso n_dof x r, a_r K blocks of r x r.
+struct ReducedModel {
+  int rank = 0, k_affine = 0;
+  std::vector<double> u_rho, u_iso, a_r, b_r;
+  std::vector<double> singular_values;  // the first `rank` POD singular values
+  double eps_pod = 0.0, eps_train = 0.0;
+  double discarded_fraction = 0.0;      // sum_{k > r} sigma_k / sum sigma_k
+};
+
+// RomsadStrategy tolerance eta * max(eps_train, eps_pod) (strategies.cpp:30-32).
+inline double romsad_tolerance(double eps_train, double eps_pod, double eta = 0.1) {
+  return eta * std::max(eps_train, eps_pod);
+}
+
+// Upload a model: which = 0 primary (ROMIG), 1 correction (ROMSA / ROMSAD).
+inline void load_rom(TransportBatch& b, int which, const ReducedModel& m) {
+  rte_rom r{m.rank, m.k_affine, m.u_rho.data(), m.u_iso.data(), m.a_r.data(), m.b_r.data(), m.eps_pod, m.eps_train};
+  check(rte_rom_load(b.handle(), which, &r), b.handle());
+}
+
+// romig (strategies.cpp:8-28) for every sample: rho0 [S * n_dof]; throws
+// std::runtime_error for a singular reduced operator or a failed Galerkin
+// residual check, as the reference does.
+inline std::vector<double> romig(TransportBatch& b) {
+  const int S = b.n_samples();
+  DeviceVector rho((long)S * b.n_dof());
+  std::vector<int> status(S);
+  check(rte_romig(b.handle(), rho.data(), status.data(), nullptr), b.handle());
+  for (int s = 0; s < S; ++s) {
+    if (status[s] == 1) throw std::runtime_error("romig: reduced operator is singular at sample " + std::to_string(s));
+    if (status[s] == 2) throw std::runtime_error("romig: Galerkin residual check failed at sample " + std::to_string(s));
+  }
+  return rho.to_host();
+}
+
+// collect_snapshots (snapshots.cpp:118-194) for every training sample of the
+// batch at once, kept in device memory.
+struct Snapshots {
+  int window = 0;
+  DeviceVector f_iter, f_conv, drho;  // [S][window][kdim], [S][kdim], [S][window][n_dof]
+  std::vector<int> converged, n_iter;
+};
+
+inline Snapshots collect_snapshots(TransportBatch& b, int window, double eps_train, int max_iters = 2000) {
+  const int S = b.n_samples();
+  const long kdim = b.kinetic_dim();
+  Snapshots sn{window, DeviceVector((long)S * window * kdim), DeviceVector((long)S * kdim),
+               DeviceVector((long)S * window * b.n_dof()), std::vector<int>(S), std::vector<int>(S)};
+  cudaMemset(sn.f_iter.data(), 0, sizeof(double) * sn.f_iter.size());
+  cudaMemset(sn.drho.data(), 0, sizeof(double) * sn.drho.size());
+  check(rte_collect_snapshots(b.handle(), window, eps_train, max_iters, sn.f_iter.data(), sn.f_conv.data(),
+                              sn.drho.data(), sn.converged.data(), sn.n_iter.data()),
+        b.handle());
+  return sn;
+}
+
+// Training matrix (PrimarySource / CorrectionSource, snapshots.cpp:316-376):
+// correction = false: converged solutions; true: f - f^(l).  Column-major
+// kdim x n_cols on the device; *n_cols receives the column count.
+inline DeviceVector snapshot_matrix(TransportBatch& b, Snapshots& sn, bool correction, int* n_cols,
+                                    int window_limit = 0) {
+  int n = 0;
+  const int kind = correction ? 1 : 0;
+  check(rte_snapshot_columns(b.handle(), sn.window, sn.f_iter.data(), sn.f_conv.data(), sn.n_iter.data(),
+                             sn.converged.data(), kind, window_limit, nullptr, &n),
+        b.handle());
+  DeviceVector F((long)n * b.kinetic_dim());
+  check(rte_snapshot_columns(b.handle(), sn.window, sn.f_iter.data(), sn.f_conv.data(), sn.n_iter.data(),
+                             sn.converged.data(), kind, window_limit, F.data(), &n),
+        b.handle());
+  *n_cols = n;
+  return F;
+}
+
+// POD (pod.cpp): the first rank_max left singular vectors of F (m x n,
+// column-major, device) and all n singular values.
+inline std::pair<DeviceVector, std::vector<double>> pod(const DeviceVector& F, long m, int n, int rank_max,
+                                                        int device = 0) {
+  DeviceVector U((long)rank_max * m);
+  std::vector<double> sigma(n);
+  cudaDeviceSynchronize();
+  check(rte_pod(device, m, n, F.data(), rank_max, U.data(), sigma.data(), nullptr), nullptr);
+  return {std::move(U), sigma};
+}
+
+// truncation_rank (pod.cpp:117-139).
+inline int truncation_rank(const std::vector<double>& sigma, double eps_pod) {
+  const int r = rte_truncation_rank(sigma.data(), (int)sigma.size(), eps_pod);
+  if (r < 0) throw std::runtime_error("pod: snapshot matrix is zero");
+  return r;
+}
+
+// build_reduced_model (reduced_model.cpp:106-199) from a rank-r basis U
+// (kdim x r, column-major, device) with the batch's affine term operators.
+inline ReducedModel build_reduced_model(TransportBatch& b, const DeviceVector& U, int r,
+                                        const std::vector<double>& all_singular_values, double eps_pod,
+                                        double eps_train) {
+  const long nd = b.n_dof();
+  const int K = b.k_terms();
+  ReducedModel m;
+  m.rank = r;
+  m.k_affine = K;
+  m.u_rho.resize((size_t)r * nd);
+  m.u_iso.resize((size_t)r * nd);
+  m.a_r.resize((size_t)K * r * r);
+  m.b_r.resize(r);
+  cudaDeviceSynchronize();
+  check(rte_build_rom(b.handle(), r, U.data(), m.u_rho.data(), m.u_iso.data(), m.a_r.data(), m.b_r.data()),
+        b.handle());
+  m.eps_pod = eps_pod;
+  m.eps_train = eps_train;
+  double total = 0.0, tail = 0.0;
+  for (size_t k = 0; k < all_singular_values.size(); ++k) {
+    total += all_singular_values[k];
+    if ((int)k >= r) tail += all_singular_values[k];
+  }
+  m.singular_values.assign(all_singular_values.begin(),
+                           all_singular_values.begin() + std::min<size_t>(r, all_singular_values.size()));
+  m.discarded_fraction = total > 0 ? tail / total : 0.0;
+  return m;
 }
 
 }  // namespace rte_b200

@@ -14,11 +14,11 @@ from tests.problems import homog, rel_l2
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def build_demo():
+def build_demo(name="host_api_demo"):
     from paper_2402_10488_b200 import build
     build.build()
-    exe = os.path.join(ROOT, "paper_2402_10488_b200", "_build", "host_api_demo")
-    src = os.path.join(ROOT, "tests", "cpp", "host_api_demo.cpp")
+    exe = os.path.join(ROOT, "paper_2402_10488_b200", "_build", name)
+    src = os.path.join(ROOT, "tests", "cpp", name + ".cpp")
     lib_dir = os.path.join(ROOT, "paper_2402_10488_b200")
     subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-O2", "-std=c++17", "-I", os.path.join(ROOT, "include"),
                            src, "-o", exe, "-L" + lib_dir, "-lrte_b200", "-Xlinker", "-rpath=" + lib_dir])
@@ -27,6 +27,7 @@ def build_demo():
 
 def test_cpp_host_api_compiles():
     assert os.path.exists(build_demo())
+    assert os.path.exists(build_demo("rom_pipeline_demo"))
 
 
 @pytest.mark.gpu
@@ -45,3 +46,49 @@ def test_cpp_host_api_c1_parity():
     assert r["pgmres_converged"] == 1 and r["pgmres_iterations"] == grep_.iterations
     assert r["pgmres_n_sweep"] == grep_.n_sweep
     assert rel_l2(np.array(r["pgmres_rho"]), grho) < 1e-8
+
+
+@pytest.mark.gpu
+def test_cpp_rom_pipeline_matches_the_python_mirror():
+    """The C++ wrapper's offline stage (collect_snapshots, snapshot_matrix,
+    pod, build_reduced_model) and ROMSAD solve (tests/cpp/rom_pipeline_demo.cpp)
+    reproduce the Python host mirror's pipeline on the same inputs: same POD
+    spectrum, iteration counts, correction logs and switch iterations, and
+    the oracle's ROMSAD with the same reduced model."""
+    from paper_2402_10488_b200 import rte
+    exe = build_demo("rom_pipeline_demo")
+    r = json.loads(subprocess.run([exe], capture_output=True, text=True, check=True).stdout)
+
+    def problem(mod):
+        t0 = mod.CoefficientTerm(absorption_weight=lambda x, y: 0.2, scattering_weight=lambda x, y: 0.5)
+        t1 = mod.CoefficientTerm(psi=lambda mu: mu[0], scattering_weight=lambda x, y: 0.3)
+        return mod.ProblemDefinition(mod.SLAB1D, [t0, t1], lambda x, y: 1.0, inflow_left=0.3, n_params=1,
+                                     param_ranges=[(0.0, 1.0)])
+    mesh = rte.Mesh.slab_uniform(0.0, 1.0, 64)
+    quad = rte.gauss_legendre(8)
+    tb = rte.TransportBatch(problem(rte), mesh, quad, [[m] for m in (0.1, 0.3, 0.5, 0.7, 0.9)])
+    snaps = rte.collect_snapshots(tb, 3, 1e-10)
+    F = rte.snapshot_matrix(tb, snaps, "correction")
+    U, sv = rte.pod(F, 4)
+    assert F.shape[0] == r["n_cols"]
+    np.testing.assert_allclose(sv, r["sigma"], rtol=1e-12, atol=1e-14 * sv[0])
+    eps_pod = float(np.sum(sv[4:]) / np.sum(sv))
+    model = rte.build_reduced_model(tb, U, sv, eps_pod, 1e-10, "c")
+    test = [[0.2], [0.45], [0.8]]
+    b = rte.TransportBatch(problem(rte), mesh, quad, test)
+    rte.load_rom(b, 1, model)
+    cfg = rte.SolveConfig(eps_sisa=1e-10, theta=3, eps_romsad=rte.romsad_tolerance(1e-10, eps_pod))
+    rho, reps = rte.sisa_solve(b, "ROMSAD", cfg)
+    rho = rho.cpu().numpy()
+    om = ro.Mesh.slab_uniform(0.0, 1.0, 64)
+    ocm = ro.ReducedModel(0, 8, b.n_dof(), 4, 2, "c", eps_pod, 1e-10, model.u_rho, model.u_iso, model.a_r,
+                          model.singular_values, model.discarded_fraction, model.b_r)
+    for s, (c, p) in enumerate(zip(r["samples"], reps)):
+        assert c["converged"] == 1 and c["iterations"] == p.iterations and c["log"] == p.correction_log
+        assert c["switch_iter"] == p.switch_iter
+        assert rel_l2(np.array(c["rho"]), rho[s]) < 1e-12
+        o = ro.TransportSystem(problem(ro), om, ro.build_dg_space(om), ro.gauss_legendre(8), test[s])
+        o_rho, o_rep = ro.sisa_solve(o, ro.RomsadStrategy(ocm, ro.build_dsa(o), 3, cfg.eps_romsad),
+                                     ro.SolveConfig(eps_sisa=1e-10))
+        assert o_rep.iterations == p.iterations and o_rep.correction_log == p.correction_log
+        assert rel_l2(rho[s], o_rho) < 1e-8
