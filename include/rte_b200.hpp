@@ -205,6 +205,8 @@ struct SolveConfig {  // solvers.hpp:13-19 (+ batch options)
   int gmres_restart = 25;        // solvers.hpp:16
   double gmres_rel_tol = 1e-11;  // solvers.hpp:17
   double dsa_inner = 0.0;        // xy DSA inner tolerance factor (rte_si_config.dsa_inner)
+  rte_correction_fn correct = nullptr;  // RTE_CUSTOM (see the CorrectionStrategy overload of sisa_solve)
+  void* correct_user = nullptr;
 };
 
 struct SolveReport {  // solvers.hpp:21-33 (per sample)
@@ -215,6 +217,7 @@ struct SolveReport {  // solvers.hpp:21-33 (per sample)
   double final_residual = 0;
   std::string correction_log;
   int switch_iter = -1;
+  std::string strategy;  // label of a caller strategy (CorrectionStrategy overload)
 };
 
 // sisa_solve (solvers.hpp:70-72) for all samples: returns rho [S * n_dof].
@@ -226,6 +229,8 @@ inline std::pair<std::vector<double>, std::vector<SolveReport>> sisa_solve(Trans
   rte_si_config cfg{c.method, c.eps_sisa, c.norm, c.max_iters, c.fixed_iters, c.theta, c.eps_romsad,
                     c.initial_guess ? 1 : 0, 1, 4};
   cfg.dsa_inner = c.dsa_inner;
+  cfg.correct = c.correct;
+  cfg.correct_user = c.correct_user;
   const int mi = std::max(c.max_iters, c.fixed_iters);
   std::vector<rte_si_report> reps(S);
   std::vector<double> hist((size_t)S * mi);
@@ -244,6 +249,72 @@ inline std::pair<std::vector<double>, std::vector<SolveReport>> sisa_solve(Trans
       if (log[(size_t)s * mi + l]) r.correction_log.push_back(log[(size_t)s * mi + l]);
   }
   return {rho.to_host(), out};
+}
+
+// The reference's plugin point (solvers.hpp:38-51), one instance per sample:
+// setup() before the solve; correct(l, delta) once per SI iteration with
+// delta = rho* - rho (host vector, n_dof) returns the correction; last_kind()
+// is the correction-log letter (0: no correction).  Existing host-side
+// strategies port unchanged; the device loop calls them through RTE_CUSTOM.
+class CorrectionStrategy {
+ public:
+  virtual ~CorrectionStrategy() = default;
+  virtual void setup(TransportBatch& /*batch*/, int /*sample*/) {}
+  virtual std::vector<double> correct(int l, const std::vector<double>& delta) = 0;
+  virtual char last_kind() const = 0;
+  virtual std::string label() const = 0;
+};
+
+namespace detail {
+struct StrategyCall {
+  std::vector<CorrectionStrategy*>* strategies;
+  std::string error;
+};
+inline int strategy_trampoline(void* user, int l, int n_samples, long n_dof, const int* active, const double* delta,
+                               double* corr, char* kind, void* stream) {
+  auto* call = static_cast<StrategyCall*>(user);
+  try {
+    std::vector<double> d((size_t)n_dof);
+    for (int s = 0; s < n_samples; ++s) {
+      if (!active[s]) continue;
+      CorrectionStrategy* st = (*call->strategies)[s];
+      cudaMemcpyAsync(d.data(), delta + (long)s * n_dof, sizeof(double) * n_dof, cudaMemcpyDeviceToHost,
+                      static_cast<cudaStream_t>(stream));
+      cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+      const std::vector<double> c = st->correct(l, d);
+      if ((long)c.size() != n_dof) throw std::invalid_argument("strategy: correction has the wrong size");
+      cudaMemcpyAsync(corr + (long)s * n_dof, c.data(), sizeof(double) * n_dof, cudaMemcpyHostToDevice,
+                      static_cast<cudaStream_t>(stream));
+      cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+      kind[s] = st->last_kind();
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    call->error = e.what();
+    return 1;
+  }
+}
+}  // namespace detail
+
+// sisa_solve (solvers.hpp:70-72) with one caller strategy per sample (RTE_CUSTOM).
+inline std::pair<std::vector<double>, std::vector<SolveReport>> sisa_solve(TransportBatch& b,
+                                                                           std::vector<CorrectionStrategy*> strategies,
+                                                                           SolveConfig c) {
+  const int S = b.n_samples();
+  if ((int)strategies.size() != S) throw std::invalid_argument("sisa_solve: one strategy per sample");
+  for (int s = 0; s < S; ++s) strategies[s]->setup(b, s);
+  detail::StrategyCall call{&strategies, {}};
+  c.method = RTE_CUSTOM;
+  c.correct = detail::strategy_trampoline;
+  c.correct_user = &call;
+  try {
+    auto res = sisa_solve(b, c);
+    for (int s = 0; s < S; ++s) res.second[s].strategy = strategies[s]->label();
+    return res;
+  } catch (const std::runtime_error&) {
+    if (!call.error.empty()) throw std::runtime_error(call.error);
+    throw;
+  }
 }
 
 // gmres_solve (solvers.hpp:80-82, gmres.cpp:15-124) for all samples:

@@ -59,6 +59,16 @@ rte_b200::TransportBatch make_batch(const Slab& sl, const rte_b200::AngularQuadr
   return b;
 }
 
+// test_solvers.cpp:30-62's stub: no correction, log letter 'Z'
+class ZeroCorrection : public rte_b200::CorrectionStrategy {
+ public:
+  std::vector<double> correct(int, const std::vector<double>& delta) override {
+    return std::vector<double>(delta.size(), 0.0);
+  }
+  char last_kind() const override { return 'Z'; }
+  std::string label() const override { return "ZERO"; }
+};
+
 }  // namespace
 
 int main() {
@@ -117,6 +127,21 @@ int main() {
     for (long i = 0; i < nd; ++i) std::printf(i ? ", %.17g" : "%.17g", res.first[s * nd + i]);
     std::printf("]}");
   }
-  std::printf("]}\n");
+  // the plugin point: per-sample ZeroCorrection strategies reproduce plain SI
+  rte_b200::SolveConfig scfg;
+  scfg.method = RTE_SI;
+  scfg.eps_sisa = 1e-10;
+  auto si = rte_b200::sisa_solve(b, scfg);
+  std::vector<ZeroCorrection> zs(test.size());
+  std::vector<rte_b200::CorrectionStrategy*> zp;
+  for (auto& z : zs) zp.push_back(&z);
+  auto zr = rte_b200::sisa_solve(b, zp, scfg);
+  bool same = si.first == zr.first;
+  for (size_t s = 0; s < test.size(); ++s)
+    same = same && si.second[s].iterations == zr.second[s].iterations &&
+           zr.second[s].correction_log == std::string(si.second[s].iterations - 1, 'Z') &&
+           zr.second[s].strategy == "ZERO";
+  std::printf("], \"zero_strategy_equals_si\": %s, \"si_iterations\": %d}\n", same ? "true" : "false",
+              si.second[0].iterations);
   return 0;
 }

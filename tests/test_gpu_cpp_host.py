@@ -92,3 +92,4 @@ def test_cpp_rom_pipeline_matches_the_python_mirror():
                                      ro.SolveConfig(eps_sisa=1e-10))
         assert o_rep.iterations == p.iterations and o_rep.correction_log == p.correction_log
         assert rel_l2(rho[s], o_rho) < 1e-8
+    assert r["zero_strategy_equals_si"] and r["si_iterations"] > 1  # the C++ CorrectionStrategy plugin point
