@@ -84,11 +84,14 @@ class DeviceVector {
   long size() const { return n_; }
   std::vector<double> to_host() const {
     std::vector<double> h(n_);
-    cudaMemcpy(h.data(), p_, sizeof(double) * n_, cudaMemcpyDeviceToHost);
+    if (cudaMemcpy(h.data(), p_, sizeof(double) * n_, cudaMemcpyDeviceToHost) != cudaSuccess)
+      throw std::runtime_error("DeviceVector: device-to-host copy failed");
     return h;
   }
   void from_host(const std::vector<double>& h) {
-    cudaMemcpy(p_, h.data(), sizeof(double) * n_, cudaMemcpyHostToDevice);
+    if ((long)h.size() != n_) throw std::invalid_argument("DeviceVector: host vector has the wrong size");
+    if (cudaMemcpy(p_, h.data(), sizeof(double) * n_, cudaMemcpyHostToDevice) != cudaSuccess)
+      throw std::runtime_error("DeviceVector: host-to-device copy failed");
   }
 
  private:
@@ -397,8 +400,9 @@ inline Snapshots collect_snapshots(TransportBatch& b, int window, double eps_tra
   const long kdim = b.kinetic_dim();
   Snapshots sn{window, DeviceVector((long)S * window * kdim), DeviceVector((long)S * kdim),
                DeviceVector((long)S * window * b.n_dof()), std::vector<int>(S), std::vector<int>(S)};
-  cudaMemset(sn.f_iter.data(), 0, sizeof(double) * sn.f_iter.size());
-  cudaMemset(sn.drho.data(), 0, sizeof(double) * sn.drho.size());
+  if (cudaMemset(sn.f_iter.data(), 0, sizeof(double) * sn.f_iter.size()) != cudaSuccess ||
+      cudaMemset(sn.drho.data(), 0, sizeof(double) * sn.drho.size()) != cudaSuccess)
+    throw std::runtime_error("collect_snapshots: cudaMemset failed");
   check(rte_collect_snapshots(b.handle(), window, eps_train, max_iters, sn.f_iter.data(), sn.f_conv.data(),
                               sn.drho.data(), sn.converged.data(), sn.n_iter.data()),
         b.handle());
