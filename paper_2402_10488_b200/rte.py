@@ -655,6 +655,23 @@ def _custom_callback(batch, strategy, errors):
     return capi.CORRECTION_FN(cb)
 
 
+def si_config(config: SolveConfig, method_code: int, callback=None) -> "capi.SiConfig":
+    """SolveConfig -> rte_si_config (include/rte_b200.h); raises ValueError for
+    settings the reference would reject (solvers.hpp:13-19)."""
+    if config.norm not in ("abs", "rel"):
+        raise ValueError("solve config: norm must be 'abs' or 'rel'")
+    if config.max_iters < 1 or config.fixed_iters < 0 or config.check_every < 0:
+        raise ValueError("solve config: max_iters >= 1, fixed_iters >= 0, check_every >= 0")
+    if not 0.0 <= config.dsa_inner < 1.0:
+        raise ValueError("solve config: dsa_inner must be in [0, 1)")
+    return capi.SiConfig(method_code, float(config.eps_sisa),
+                         capi.RTE_NORM_REL if config.norm == "rel" else capi.RTE_NORM_ABS,
+                         int(config.max_iters), int(config.fixed_iters), int(config.theta),
+                         float(config.eps_romsad), 1 if config.initial_guess is not None else 0,
+                         1 if config.compute_residual else 0, int(config.check_every),
+                         callback if callback is not None else capi.CORRECTION_FN(), None, float(config.dsa_inner))
+
+
 def sisa_solve(batch: TransportBatch, method, config: SolveConfig):
     """Batched sisa_solve (sisa.cpp:14-54): returns (rho [S, n_dof], reports).
     ``method`` is a built-in strategy name ("SI", "DSA", "ROMSA", "ROMSAD",
@@ -666,11 +683,7 @@ def sisa_solve(batch: TransportBatch, method, config: SolveConfig):
     cb = capi.CORRECTION_FN() if custom is None else _custom_callback(batch, custom, errors)
     if custom is not None:
         custom.setup(batch)
-    cfg = capi.SiConfig(m, float(config.eps_sisa), capi.RTE_NORM_REL if config.norm == "rel" else capi.RTE_NORM_ABS,
-                        int(config.max_iters), int(config.fixed_iters), int(config.theta),
-                        float(config.eps_romsad), 1 if config.initial_guess is not None else 0,
-                        1 if config.compute_residual else 0, int(config.check_every), cb, None,
-                        float(config.dsa_inner))
+    cfg = si_config(config, m, cb)
     if config.initial_guess is not None:
         rho = batch._dev(config.initial_guess, (batch.S, batch.nd)).clone()
     else:

@@ -83,3 +83,18 @@ def test_struct_layouts_match_the_header(tmp_path):
         assert int(got["%s size" % cname]) == ctypes.sizeof(py), cname
         for fname, _ in py._fields_:
             assert int(got["%s.%s" % (cname, fname)]) == getattr(py, fname).offset, (cname, fname)
+
+
+def test_solve_config_maps_onto_the_c_struct():
+    """rte.SolveConfig -> rte_si_config field by field (no device needed)."""
+    from paper_2402_10488_b200 import capi, rte
+    c = rte.SolveConfig(eps_sisa=1e-8, norm="rel", max_iters=77, fixed_iters=0, theta=5, eps_romsad=3e-9,
+                        compute_residual=False, check_every=2, dsa_inner=1e-2)
+    s = rte.si_config(c, capi.RTE_ROMSAD)
+    assert (s.method, s.eps, s.norm, s.max_iters, s.fixed_iters, s.theta) == (capi.RTE_ROMSAD, 1e-8, capi.RTE_NORM_REL,
+                                                                             77, 0, 5)
+    assert (s.eps_romsad, s.use_guess, s.compute_residual, s.check_every, s.dsa_inner) == (3e-9, 0, 0, 2, 1e-2)
+    import pytest
+    for bad in (dict(norm="l2"), dict(max_iters=0), dict(dsa_inner=1.5)):
+        with pytest.raises(ValueError):
+            rte.si_config(rte.SolveConfig(**bad), capi.RTE_DSA)
