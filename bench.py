@@ -14,6 +14,10 @@ Metric: cell*direction*sample sweep updates per second of the whole step
 (updates counted over unique directions); the sweep kernel alone is reported
 as sweep_only_updates_per_s and sweep_roofline.
 
+The line also carries `time_to_tol`: time to tolerance per parameter sample
+for BASELINE.json configs[0..3] (SI-DSA, ROMIG, ROMSAD; offline stage on the
+device), the metric's second half (rank 0 at N=1; --no-ttt skips it).
+
 Contract: `python bench.py --gpus N --steps K --warmup W [--impl reference]`
 prints one JSON line (rank 0).  Multi-GPU: samples shard across ranks (weak
 scaling, no collective on the data path); timing is on the device, max over
