@@ -222,28 +222,34 @@ class TransportBatch:
             tmt.append(mesh.weighted_mass(tot))
             tms.append(mesh.weighted_mass(sc))
         tmt, tms = np.stack(tmt), np.stack(tms)  # [K][cells][nl][nl]
-        mt = np.zeros((S,) + tmt.shape[1:])
-        ms = np.zeros_like(mt)
-        for k in range(K):  # build_masses accumulation order (transport_system.cpp:136-137)
-            mt = mt + psi[:, k, None, None, None] * tmt[k][None]
-            ms = ms + psi[:, k, None, None, None] * tms[k][None]
+
+        def combine(terms):  # build_masses accumulation order (transport_system.cpp:136-137)
+            out = np.zeros((S,) + terms.shape[1:])
+            for k in range(K):
+                out = out + psi[:, k].reshape((S,) + (1,) * (terms.ndim - 1)) * terms[k][None]
+            return out
         g = mesh.project(_vals(problem.source, px, py)) if problem.source is not None else np.zeros(mesh.n_dof())
         inflow = (problem.inflow_left, problem.inflow_right, problem.inflow_bottom, problem.inflow_top)
         if mesh.geometry == XY2D:
-            try:
-                # per-cell constant coefficients: sigma I blocks (closed-form cell solves)
-                mt_s, ms_s = _scalar_blocks(mt), _scalar_blocks(ms)
-                tmt_s, tms_s = _scalar_blocks(tmt), _scalar_blocks(tms)
-            except capi.RteError:
-                mt_s = None
-            if mt_s is not None and not force_full_blocks:
-                self._create(mesh, quad, mt_s, ms_s, g, True, inflow, 1, device)
+            tmt_s = None
+            if not force_full_blocks:
+                try:
+                    # every term sigma I per cell -> so is every combination: the
+                    # samples' scalars are combined from the K term scalars (the
+                    # same arithmetic, in the same order, as combining the blocks)
+                    tmt_s, tms_s = _scalar_blocks(tmt), _scalar_blocks(tms)
+                except capi.RteError:
+                    tmt_s = None
+            if tmt_s is not None:
+                self._create(mesh, quad, combine(tmt_s), combine(tms_s), g, True, inflow, 1, device)
                 self._affine(K, tmt_s, tms_s, psi)
             else:
+                mt, ms = combine(tmt), combine(tms)
                 # intra-cell-varying coefficients: full 4x4 blocks per cell (block = 16)
                 self._create(mesh, quad, mt.reshape(S, -1, 16), ms.reshape(S, -1, 16), g, True, inflow, 16, device)
                 self._affine(K, tmt.reshape(K, -1, 16), tms.reshape(K, -1, 16), psi)
         else:
+            mt, ms = combine(tmt), combine(tms)
             self._create(mesh, quad, mt.reshape(S, -1, 4), ms.reshape(S, -1, 4), g, True, inflow, 4, device)
             self._affine(K, tmt.reshape(K, -1, 4), tms.reshape(K, -1, 4), psi)
         self.problem, self.mus = problem, mus
@@ -417,14 +423,15 @@ class TransportBatch:
 def _scalar_blocks(m):
     """Per-cell mass blocks -> scalar sigma (the B200 2D path needs sigma*I)."""
     nl = m.shape[-1]
-    d = np.diagonal(m, axis1=-2, axis2=-1)
-    off = m - d[..., None] * np.eye(nl)
-    scale = np.maximum(np.max(np.abs(d), axis=-1), 1e-300)
-    if np.any(np.max(np.abs(off), axis=(-2, -1)) > 1e-12 * scale) or \
-            np.any(np.max(np.abs(d - d[..., :1]), axis=-1) > 1e-12 * scale):
+    f = np.ascontiguousarray(m).reshape(-1, nl * nl)
+    d0 = f[:, 0]
+    # |m - d0 I| covers both the off-diagonal entries and unequal diagonals
+    err = np.abs(f - d0[:, None] * np.eye(nl).ravel()).max(axis=1)
+    scale = np.maximum(np.abs(f[:, ::nl + 1]).max(axis=1), 1e-300)
+    if np.any(err > 1e-12 * scale):
         raise capi.RteError(capi.RTE_ERR_UNSUPPORTED,
                             "xy geometry: coefficients must be constant per cell in this build")
-    return np.ascontiguousarray(d[..., 0])
+    return np.ascontiguousarray(d0).reshape(m.shape[:-2])
 
 
 class DsaOperator:
