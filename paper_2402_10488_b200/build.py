@@ -36,7 +36,8 @@ def _compile(src, force):
             os.path.join(os.path.dirname(HERE), "include", "rte_b200.h")]
     if not force and not _stale(obj, deps):
         return obj, ""
-    cmd = [NVCC] + ARCH + FLAGS + DEFINES + ["-c", path, "-o", obj]
+    omp = ["-Xcompiler", "-fopenmp"] if src.endswith(".cpp") else []  # host setup helpers
+    cmd = [NVCC] + ARCH + FLAGS + DEFINES + omp + ["-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed for %s:\n%s%s" % (src, r.stdout, r.stderr))
@@ -53,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if log:
                 print("==", os.path.basename(o), "\n", log)
     if force or _stale(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-lpthread", "-ldl", "-lrt"]
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-lgomp", "-lpthread", "-ldl", "-lrt"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n%s%s" % (r.stdout, r.stderr))

@@ -71,15 +71,20 @@ int rte_cell_points(int geometry, int nx, int ny, const double* bounds, double x
     return RTE_OK;
   }
   const double hx = (x1 - x0) / nx, hy = (y1 - y0) / ny;
-  for (int iy = 0; iy < ny; ++iy)
-    for (int ix = 0; ix < nx; ++ix) {
-      const double xc = x0 + ix * hx + 0.5 * hx, yc = y0 + iy * hy + 0.5 * hy;
-      for (int qy = 0; qy < nq; ++qy)
-        for (int qx = 0; qx < nq; ++qx, ++k) {
-          px[k] = xc + 0.5 * hx * g[qx];
-          py[k] = yc + 0.5 * hy * g[qy];
-        }
-    }
+  const long nc = (long)nx * ny;
+  // cells are independent: one thread per cell range, same per-cell arithmetic
+#pragma omp parallel for schedule(static)
+  for (long cell = 0; cell < nc; ++cell) {
+    const int iy = (int)(cell / nx), ix = (int)(cell - (long)iy * nx);
+    const double xc = x0 + ix * hx + 0.5 * hx, yc = y0 + iy * hy + 0.5 * hy;
+    long kk = cell * nq * nq;
+    for (int qy = 0; qy < nq; ++qy)
+      for (int qx = 0; qx < nq; ++qx, ++kk) {
+        px[kk] = xc + 0.5 * hx * g[qx];
+        py[kk] = yc + 0.5 * hy * g[qy];
+      }
+  }
+  (void)k;
   return RTE_OK;
 }
 
@@ -104,9 +109,10 @@ int rte_weighted_mass(int geometry, int nx, int ny, const double* bounds, double
     return RTE_OK;
   }
   const double hx = (x1 - x0) / nx, hy = (y1 - y0) / ny;
-  long cell = 0;
-  for (int iy = 0; iy < ny; ++iy)
-    for (int ix = 0; ix < nx; ++ix, ++cell) {
+  const long ncells = (long)nx * ny;
+#pragma omp parallel for schedule(static)
+  for (long cell = 0; cell < ncells; ++cell) {
+      const int iy = (int)(cell / nx), ix = (int)(cell - (long)iy * nx);
       const double xc = x0 + ix * hx + 0.5 * hx, yc = y0 + iy * hy + 0.5 * hy;
       double m[16] = {0};
       for (int qy = 0; qy < nq; ++qy) {
@@ -149,6 +155,7 @@ int rte_project(int geometry, int nx, int ny, const double* bounds, double x0, d
   }
   const double hx = (x1 - x0) / nx, hy = (y1 - y0) / ny;
   const long nc = (long)nx * ny;
+#pragma omp parallel for schedule(static)
   for (long c = 0; c < nc; ++c) {
     double o[4] = {0, 0, 0, 0};
     for (int qy = 0; qy < nq; ++qy) {
