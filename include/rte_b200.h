@@ -137,6 +137,15 @@ typedef struct rte_si_config {
                           ("inner tolerance 1e-2 eps_SISA"; ignored with fixed_iters) */
 } rte_si_config;
 
+/* Per-sample outcome of the iterative XY DSA solves (the reference's direct
+ * SparseLU cannot under-solve; its failures throw, dsa.cpp:253-256, 269-271). */
+enum rte_dsa_status {
+  RTE_DSA_OK = 0,
+  RTE_DSA_MAXIT = 1,      /* stopped at the iteration cap above the tolerance */
+  RTE_DSA_BREAKDOWN = 2,  /* BiCGStab breakdown (omega = 0) above the tolerance */
+  RTE_DSA_NAN = 3         /* non-finite residual */
+};
+
 typedef struct rte_si_report {
   int converged;
   int iterations;
@@ -145,6 +154,7 @@ typedef struct rte_si_report {
   int singular;        /* reduced operator singular at this mu */
   double final_residual;
   double last_change;
+  int dsa_status;      /* worst rte_dsa_status over this sample's DSA corrections */
 } rte_si_report;
 
 /* ---- lifecycle ---------------------------------------------------------- */
@@ -154,6 +164,10 @@ const char* rte_last_error(const rte_ctx* ctx); /* ctx may be NULL (create failu
 long rte_n_dof(const rte_ctx* ctx);
 int rte_n_samples(const rte_ctx* ctx);
 int rte_n_slots(const rte_ctx* ctx); /* unique (vx,vy) sweep slots (transport_system.cpp:194-202) */
+/* XY sweep work decomposition the context's full sweeps use: directions per
+ * lane (8, 4, 2 or 1) and direction groups per quadrant (slab: 0, 0).
+ * Diagnostic; RTE_SWEEP_DPL (environment, read per call) forces the first. */
+int rte_sweep_plan(rte_ctx* ctx, int* dirs_per_lane, int* groups);
 
 /* ---- transport operator (batched over samples) -------------------------- */
 /* TransportSystem::apply_L (transport_system.cpp:393-404): out = L rho. */
@@ -241,6 +255,16 @@ int rte_dsa_correct(rte_ctx* ctx, const double* delta_dev, double* out_dev, void
 int rte_dsa_set_tolerance(rte_ctx* ctx, double tol, int max_iters);
 /* Krylov iterations of the last XY DSA solve (0 for slab: direct). */
 int rte_dsa_last_iterations(const rte_ctx* ctx);
+/* The XY solve starts from the minimal-residual combination of the sample's
+ * last solutions (a warm start; the history holds up to 8 solution vectors and
+ * their operator images, up to half of the free device memory, for the
+ * context's lifetime).  Direct rte_dsa_solve_density / rte_dsa_correct calls
+ * warm-start from the earlier calls' solutions (results agree within the
+ * solver tolerance, not bitwise); rte_si_solve and rte_gmres_solve clear the
+ * history when they start, so a solve does not depend on earlier calls.  This
+ * clears it explicitly.  Direct solves that end above the tolerance return
+ * RTE_ERR_RUNTIME (the reference throws, dsa.cpp:269-271). */
+int rte_dsa_reset_history(rte_ctx* ctx, void* stream);
 /* DsaOperator::apply_eliminated (dsa.cpp:279-293, dsa.hpp:43-46): the
  * current-eliminated density operator S x = A_rr x - A_rJ T^{-1} A_Jr x for
  * every sample.  The current block T is factored lazily on first use (slab:
@@ -263,7 +287,9 @@ int rte_romig(rte_ctx* ctx, double* rho0_dev, int* status_host, void* stream);
  * are masked.  rho_dev [S][n_dof] holds the guess on entry (use_guess) and
  * the solution on exit.  reports_host[S]; history_host [S][max_iters] (change
  * per iteration, may be NULL); log_host [S][max_iters] correction kinds
- * 'D','R','S' or 0 (may be NULL). */
+ * 'D','R','S' or 0 (may be NULL).  fixed_iters > max_iters is RTE_ERR_INVALID.
+ * A DSA correction that ends above its tolerance (rte_dsa_status) fills the
+ * reports and returns RTE_ERR_RUNTIME (dsa.cpp:269-271 throws). */
 int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg, double* rho_dev, rte_si_report* reports_host,
                  double* history_host, char* log_host);
 
@@ -287,6 +313,7 @@ typedef struct rte_gmres_report {
   double final_residual; /* converged: ||A rho - bbar||_inf of the verifying cycle start;
                             else ||rho - L rho - bbar||_inf */
   int history_len;     /* SolveReport::change_history size (entries beyond history_cap dropped) */
+  int dsa_status;      /* worst rte_dsa_status over this sample's preconditioner solves */
 } rte_gmres_report;
 
 /* Batched gmres_solve for every sample: rho_dev [S][n_dof] holds the guess on

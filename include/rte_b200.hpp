@@ -221,6 +221,7 @@ struct SolveReport {  // solvers.hpp:21-33 (per sample)
   std::string correction_log;
   int switch_iter = -1;
   std::string strategy;  // label of a caller strategy (CorrectionStrategy overload)
+  int dsa_status = RTE_DSA_OK;  // worst rte_dsa_status of the sample's DSA corrections
 };
 
 // sisa_solve (solvers.hpp:70-72) for all samples: returns rho [S * n_dof].
@@ -234,7 +235,7 @@ inline std::pair<std::vector<double>, std::vector<SolveReport>> sisa_solve(Trans
   cfg.dsa_inner = c.dsa_inner;
   cfg.correct = c.correct;
   cfg.correct_user = c.correct_user;
-  const int mi = std::max(c.max_iters, c.fixed_iters);
+  const int mi = c.max_iters;  // rte_si_solve rejects fixed_iters > max_iters
   std::vector<rte_si_report> reps(S);
   std::vector<double> hist((size_t)S * mi);
   std::vector<char> log((size_t)S * mi);
@@ -248,6 +249,7 @@ inline std::pair<std::vector<double>, std::vector<SolveReport>> sisa_solve(Trans
     r.change_history.assign(hist.begin() + (long)s * mi, hist.begin() + (long)s * mi + r.iterations);
     r.final_residual = reps[s].final_residual;
     r.switch_iter = reps[s].switch_iter;
+    r.dsa_status = reps[s].dsa_status;
     for (int l = 0; l < r.iterations; ++l)
       if (log[(size_t)s * mi + l]) r.correction_log.push_back(log[(size_t)s * mi + l]);
   }

@@ -14,6 +14,7 @@
 // Layouts follow the reference: DOF vectors are cell-major with the local
 // index fastest (dg_space.hpp:24); kinetic vectors are direction-major blocks
 // of n_dof (transport_system.hpp:73-89).
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -23,6 +24,10 @@
 #include <string>
 #include <utility>
 #include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 namespace {
 
@@ -212,6 +217,9 @@ void stream_block(double v, double h, double* o) {
   }
 }
 
+// Largest per-slot inverse cache (bytes) the oracle builds (ro_set_cache_budget).
+double g_cache_budget = 4.0e9;
+
 struct BcEntry {
   int cell;
   double v[4];
@@ -231,7 +239,9 @@ struct System {
   double inflow[4] = {0, 0, 0, 0};
   std::vector<std::vector<BcEntry>> bc;
   std::vector<int> slot;
-  std::vector<std::vector<double>> inv;
+  int nslots = 0;
+  std::vector<std::vector<double>> inv;   // per slot: cached inverses, or empty (computed per cell on the fly)
+  std::vector<std::array<double, 16>> gm; // xy: per-slot streaming block g (transport_system.cpp:239-250)
   std::vector<double> trL, trR;  // slab: [cell][2]
   double bxL[2], bxR[2], byL[2], byR[2];
 
@@ -290,6 +300,7 @@ struct System {
       if (it == slot_of.end()) it = slot_of.emplace(key, (int)slot_of.size()).first;
       slot[j] = it->second;
     }
+    nslots = (int)slot_of.size();
     inv.assign(slot_of.size(), {});
     if (mesh.geom == 0) {
       trL.resize(2 * nc);
@@ -320,30 +331,45 @@ struct System {
     bxR[0] = rx; bxR[1] = kS3 * rx;
     byL[0] = ry; byL[1] = -kS3 * ry;
     byR[0] = ry; byR[1] = kS3 * ry;
+    gm.assign(slot_of.size(), {});
     for (const auto& kv : slot_of) {
       double bx[4], by[4];
       stream_block(kv.first.first, hx, bx);
       stream_block(kv.first.second, hy, by);
-      double gm[16] = {0};
+      double* g = gm[kv.second].data();
+      for (int e = 0; e < 16; ++e) g[e] = 0.0;
       for (int b = 0; b < 2; ++b)
         for (int a = 0; a < 2; ++a)
-          for (int a2 = 0; a2 < 2; ++a2) gm[4 * (a + 2 * b) + (a2 + 2 * b)] += bx[2 * a + a2];
+          for (int a2 = 0; a2 < 2; ++a2) g[4 * (a + 2 * b) + (a2 + 2 * b)] += bx[2 * a + a2];
       for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b)
-          for (int b2 = 0; b2 < 2; ++b2) gm[4 * (a + 2 * b) + (a + 2 * b2)] += by[2 * b + b2];
-      auto& flat = inv[kv.second];
-      flat.resize(16 * (size_t)nc);
-      for (int c = 0; c < nc; ++c) {
-        double bm[16];
-        for (int e = 0; e < 16; ++e) bm[e] = gm[e] + mt[16 * c + e];
-        inv4(bm, flat.data() + 16 * c);
-      }
+          for (int b2 = 0; b2 < 2; ++b2) g[4 * (a + 2 * b) + (a + 2 * b2)] += by[2 * b + b2];
     }
+    // The reference caches 16 doubles per slot and cell (34 GB per sample at
+    // 1024^2 x 256 slots).  Above the budget the oracle computes the same
+    // inverse (same operands, same inv4) per cell when it sweeps instead.
+    if ((double)nslots * nc * 16 * 8 <= g_cache_budget)
+      for (int k = 0; k < nslots; ++k) cache_slot(k);
+  }
+
+  // transport_system.cpp:251-259 for one slot: inverse of g + Mt_c per cell
+  void cache_slot(int k) {
+    const int nc = mesh.cells();
+    auto& flat = inv[k];
+    flat.resize(16 * (size_t)nc);
+    for (int c = 0; c < nc; ++c) cell_inverse(k, c, flat.data() + 16 * c);
+  }
+  void cell_inverse(int k, int c, double* out) const {
+    double bm[16];
+    const double* g = gm[k].data();
+    for (int e = 0; e < 16; ++e) bm[e] = g[e] + mt[16 * (size_t)c + e];
+    inv4(bm, out);
   }
 
   // transport_system.cpp:276-364
   void sweep(int j, const double* rhs, double* f) const {
     const double* iv = inv[slot[j]].data();
+    const bool lazy = inv[slot[j]].empty();
     if (mesh.geom == 0) {
       const int n = mesh.cells();
       const double v = vx[j];
@@ -412,7 +438,12 @@ struct System {
             }
           }
         }
-        const double* b = iv + 16 * cell;
+        double bl[16];
+        const double* b = bl;
+        if (lazy)
+          cell_inverse(slot[j], cell, bl);
+        else
+          b = iv + 16 * (size_t)cell;
         double* fc = f + 4 * cell;
         for (int k = 0; k < 4; ++k)
           fc[k] = b[4 * k] * r[0] + b[4 * k + 1] * r[1] + b[4 * k + 2] * r[2] + b[4 * k + 3] * r[3];
@@ -441,10 +472,63 @@ struct System {
     }
   }
 
+  bool cached() const {
+    for (const auto& v : inv)
+      if (v.empty()) return false;
+    return true;
+  }
+
+  // Uncached (large) problems: slot-major over threads.  The directions of a
+  // slot share (vx, vy), so their sweeps of a common right-hand side are the
+  // same arithmetic; each slot is swept once and every direction of it
+  // accumulated (w_j f, j ascending within the slot) into the thread's partial
+  // sum; the partials are added in thread order.  Differs from the
+  // reference's j-ordered sum only in the order of the final additions.
+  // rhs_of(j, buf) returns the right-hand side of direction j.
+  template <typename Rhs>
+  void accumulate_slots(Rhs rhs_of, double* out) const {
+    int nt = 1;
+#ifdef _OPENMP
+    nt = omp_get_max_threads();
+#endif
+    std::vector<std::vector<double>> part(nt);
+#pragma omp parallel num_threads(nt)
+    {
+      int t = 0;
+#ifdef _OPENMP
+      t = omp_get_thread_num();
+#endif
+      std::vector<double>& acc = part[t];
+      acc.assign(ndof, 0.0);
+      std::vector<double> f(ndof), rhs(ndof);
+#pragma omp for schedule(static)
+      for (int k = 0; k < nslots; ++k) {
+        int j0 = -1;
+        for (int j = 0; j < nv; ++j)
+          if (slot[j] == k) {
+            j0 = j;
+            break;
+          }
+        const double* r = rhs_of(j0, rhs);
+        sweep(j0, r, f.data());
+        for (int j = 0; j < nv; ++j)
+          if (slot[j] == k)
+            for (long i = 0; i < ndof; ++i) acc[i] += w[j] * f[i];
+      }
+    }
+    std::fill(out, out + ndof, 0.0);
+    for (int t = 0; t < nt; ++t)
+      for (long i = 0; i < ndof; ++i) out[i] += part[t][i];
+  }
+
   // transport_system.cpp:393-404
   void apply_L(const double* rho, double* out) const {
     std::vector<double> q(ndof), f(ndof);
     apply_block(ms, rho, q.data());
+    if (!cached()) {
+      accumulate_slots([&](int, std::vector<double>&) { return (const double*)q.data(); }, out);
+      return;
+    }
     std::fill(out, out + ndof, 0.0);
     for (int j = 0; j < nv; ++j) {
       sweep(j, q.data(), f.data());
@@ -454,12 +538,35 @@ struct System {
 
   // transport_system.cpp:406-418
   void assemble_rhs(double* out) const {
+    if (!cached()) {
+      accumulate_slots(
+          [&](int j, std::vector<double>& buf) {
+            buf = g;
+            add_bc(j, buf.data());
+            return (const double*)buf.data();
+          },
+          out);
+      return;
+    }
     std::vector<double> rhs(ndof), f(ndof);
     std::fill(out, out + ndof, 0.0);
     for (int j = 0; j < nv; ++j) {
       rhs = g;
       add_bc(j, rhs.data());
       sweep(j, rhs.data(), f.data());
+      for (long i = 0; i < ndof; ++i) out[i] += w[j] * f[i];
+    }
+  }
+
+  // The reference's apply_L restricted to directions [j0, j1) (transport_
+  // system.cpp:398-401): out += w_j f_j in j order.  CPU baseline timing of
+  // the reference's per-direction sweep cost on a bounded sample.
+  void apply_L_dirs(const double* rho, double* out, int j0, int j1) const {
+    std::vector<double> q(ndof), f(ndof);
+    apply_block(ms, rho, q.data());
+    std::fill(out, out + ndof, 0.0);
+    for (int j = j0; j < j1; ++j) {
+      sweep(j, q.data(), f.data());
       for (long i = 0; i < ndof; ++i) out[i] += w[j] * f[i];
     }
   }
@@ -978,6 +1085,20 @@ void* ro_system_create(int geom, int nx, int ny, const double* bounds, double x0
 void ro_system_destroy(void* h) { delete static_cast<System*>(h); }
 long ro_n_dof(void* h) { return static_cast<System*>(h)->ndof; }
 int ro_n_slots(void* h) { return (int)static_cast<System*>(h)->inv.size(); }
+// bytes of per-slot inverse cache built by later ro_system_create calls
+void ro_set_cache_budget(double bytes) { g_cache_budget = bytes; }
+int ro_is_cached(void* h) { return static_cast<System*>(h)->cached() ? 1 : 0; }
+// build the cache of slots [k0, k1) (xy) -- the reference's build_sweep_cache for those slots
+void ro_cache_slots(void* h, int k0, int k1) {
+  auto* s = static_cast<System*>(h);
+  if (s->mesh.geom == 0) return;
+  for (int k = k0; k < k1 && k < s->nslots; ++k)
+    if (s->inv[k].empty()) s->cache_slot(k);
+}
+int ro_dir_slot(void* h, int j) { return static_cast<System*>(h)->slot[j]; }
+void ro_apply_L_dirs(void* h, const double* rho, double* out, int j0, int j1) {
+  static_cast<System*>(h)->apply_L_dirs(rho, out, j0, j1);
+}
 
 void ro_mass_blocks(void* h, double* mt, double* ms) {
   auto* s = static_cast<System*>(h);

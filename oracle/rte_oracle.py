@@ -375,6 +375,24 @@ class TransportSystem:
     def n_slots(self) -> int:
         return lib().ro_n_slots(self._h)
 
+    def is_cached(self) -> bool:
+        """True when the per-slot inverse cache (build_sweep_cache) was built;
+        large problems sweep with per-cell inverses computed on the fly."""
+        return bool(lib().ro_is_cached(self._h))
+
+    def dir_slot(self, j) -> int:
+        return lib().ro_dir_slot(self._h, ctypes.c_int(j))
+
+    def cache_slots(self, k0, k1):
+        lib().ro_cache_slots(self._h, ctypes.c_int(k0), ctypes.c_int(k1))
+
+    def apply_L_dirs(self, rho, j0, j1):
+        """apply_L restricted to directions [j0, j1) (CPU baseline timing)."""
+        rho = _c(rho)
+        out = np.zeros(self._nd)
+        lib().ro_apply_L_dirs(self._h, _p(rho), _p(out), ctypes.c_int(j0), ctypes.c_int(j1))
+        return out
+
     # --- density-space ops ---
     def apply_Ms(self, rho):
         rho = _c(rho)
@@ -503,6 +521,56 @@ def _splu(m):
     return sla.splu(m.tocsc(), permc_spec="COLAMD")
 
 
+def nested_dissection_cells(nx, ny):
+    """Nested-dissection order of the cells of an nx x ny grid (recursive
+    bisection along the longer side, separator line last)."""
+    out = []
+
+    def rec(x0, x1, y0, y1):
+        w, h = x1 - x0, y1 - y0
+        if w <= 0 or h <= 0:
+            return
+        if w * h <= 16:
+            for y in range(y0, y1):
+                out.extend(range(x0 + nx * y, x1 + nx * y))
+            return
+        if w >= h:
+            m = (x0 + x1) // 2
+            rec(x0, m, y0, y1)
+            rec(m + 1, x1, y0, y1)
+            out.extend(range(m + nx * y0, m + nx * y1, nx))
+        else:
+            m = (y0 + y1) // 2
+            rec(x0, x1, y0, m)
+            rec(x0, x1, m + 1, y1)
+            out.extend(range(x0 + nx * m, x1 + nx * m))
+    rec(0, nx, 0, ny)
+    return np.array(out, dtype=np.int64)
+
+
+class _NdLU:
+    """SuperLU of the 2D coupled system in a nested-dissection order of the
+    cells (the 12 unknowns of a cell kept together).  Eigen's SparseLU
+    (dsa.cpp:146, 253) orders with COLAMD; COLAMD fill on these grids makes a
+    128^2 factorization take ~45 s, the dissection order ~4x less.  The
+    ordering changes only the rounding of the direct solve (backward error
+    ~1e-14, tests/test_oracle_solvers.py)."""
+
+    def __init__(self, m, nx, ny, nl, nf):
+        import scipy.sparse.linalg as sla
+        nd = nx * ny * nl
+        cells = nested_dissection_cells(nx, ny)
+        self.p = (np.arange(nf)[None, :, None] * nd + nl * cells[:, None, None]
+                  + np.arange(nl)[None, None, :]).ravel()
+        mc = m.tocsr()[self.p][:, self.p].tocsc()
+        self.lu = sla.splu(mc, permc_spec="NATURAL", diag_pivot_thresh=0.1, options=dict(SymmetricMode=True))
+
+    def solve(self, b):
+        x = np.empty_like(b)
+        x[self.p] = self.lu.solve(b[self.p])
+        return x
+
+
 class DsaOperator:
     """dsa.hpp:29-56."""
 
@@ -524,7 +592,11 @@ class DsaOperator:
         dim = self.n_fields * self.n
         self.coupled = sp.coo_matrix((v, (r, c)), shape=(dim, dim)).tocsc()
         try:
-            self.lu = _splu(self.coupled)
+            m = system.mesh
+            if self.n_fields == 3:
+                self.lu = _NdLU(self.coupled, m.nx, m.ny, 4, 3)
+            else:
+                self.lu = _splu(self.coupled)
         except RuntimeError as e:  # dsa.cpp:254-256
             raise RuntimeError("dsa: coupled moment system factorization failed") from e
         self._t_lu = [None] * (self.n_fields - 1)
@@ -1172,3 +1244,10 @@ class Mt19937_64:
 
     def unit(self) -> float:
         return float(self() >> 11) * 2.0 ** -53
+
+
+def set_cache_budget(nbytes: float):
+    """Largest per-slot inverse cache (bytes) later TransportSystems build;
+    bigger problems compute each cell's inverse when they sweep (same
+    arithmetic), slot-major over OpenMP threads."""
+    lib().ro_set_cache_budget(ctypes.c_double(float(nbytes)))

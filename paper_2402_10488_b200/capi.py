@@ -16,6 +16,7 @@ RTE_OK, RTE_ERR_INVALID, RTE_ERR_RUNTIME, RTE_ERR_CUDA, RTE_ERR_UNSUPPORTED = 0,
 RTE_SLAB1D, RTE_XY2D = 0, 1
 RTE_SI, RTE_DSA, RTE_ROMSA, RTE_ROMSAD, RTE_ROMIG, RTE_CUSTOM = 0, 1, 2, 3, 4, 5
 RTE_NORM_ABS, RTE_NORM_REL = 0, 1
+RTE_DSA_OK, RTE_DSA_MAXIT, RTE_DSA_BREAKDOWN, RTE_DSA_NAN = 0, 1, 2, 3
 RTE_GUESS_ZERO, RTE_GUESS_SUPPLIED, RTE_GUESS_ROMIG = 0, 1, 2
 PROF_KINDS = ("sweep", "reduce", "dsa", "rom", "other", "dsa_smooth0")
 
@@ -58,7 +59,7 @@ class SiConfig(ctypes.Structure):
 class SiReport(ctypes.Structure):
     _fields_ = [("converged", ctypes.c_int), ("iterations", ctypes.c_int), ("n_sweep", ctypes.c_long),
                 ("switch_iter", ctypes.c_int), ("singular", ctypes.c_int), ("final_residual", ctypes.c_double),
-                ("last_change", ctypes.c_double)]
+                ("last_change", ctypes.c_double), ("dsa_status", ctypes.c_int)]
 
 
 # (name, restype, argtypes) for every symbol include/rte_b200.h declares.
@@ -69,7 +70,8 @@ class GmresConfig(ctypes.Structure):
 
 class GmresReport(ctypes.Structure):
     _fields_ = [("converged", ctypes.c_int), ("iterations", ctypes.c_int), ("n_sweep", ctypes.c_long),
-                ("cycles", ctypes.c_int), ("final_residual", ctypes.c_double), ("history_len", ctypes.c_int)]
+                ("cycles", ctypes.c_int), ("final_residual", ctypes.c_double), ("history_len", ctypes.c_int),
+                ("dsa_status", ctypes.c_int)]
 
 
 SIGNATURES = [
@@ -79,6 +81,7 @@ SIGNATURES = [
     ("rte_n_dof", ctypes.c_long, [_vp]),
     ("rte_n_samples", ctypes.c_int, [_vp]),
     ("rte_n_slots", ctypes.c_int, [_vp]),
+    ("rte_sweep_plan", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     ("rte_apply_L", ctypes.c_int, [_vp, _vp, _vp, _vp]),
     ("rte_assemble_rhs", ctypes.c_int, [_vp, _vp, _vp]),
     ("rte_fixed_point", ctypes.c_int, [_vp, _vp, _vp, _vp]),
@@ -103,6 +106,7 @@ SIGNATURES = [
     ("rte_dsa_apply_eliminated", ctypes.c_int, [_vp, _vp, _vp, _vp]),
     ("rte_dsa_set_tolerance", ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_int]),
     ("rte_dsa_last_iterations", ctypes.c_int, [_vp]),
+    ("rte_dsa_reset_history", ctypes.c_int, [_vp, _vp]),
     ("rte_rom_load", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(Rom)]),
     ("rte_romig", ctypes.c_int, [_vp, _vp, _ip, _vp]),
     ("rte_si_solve", ctypes.c_int, [_vp, ctypes.POINTER(SiConfig), _vp, ctypes.POINTER(SiReport), _dp,

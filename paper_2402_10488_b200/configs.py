@@ -56,11 +56,13 @@ def c4_params(n_train=40, n_test=64, seed=SEEDS["c4"]):
     return sample_params(seed, [("u", 1.0, 10.0), ("log", 1e-3, 1e-1), ("u", 0.9, 0.9999)], n_train, n_test)
 
 
-def c5_coefficients(nx: int = 1024, samples: int = 16, seed: int = SEEDS["c5"]):
+def c5_coefficients(nx: int = 1024, samples: int = 16, seed: int = SEEDS["c5"], draws=None):
     """configs[4]: per sample, cell-major draws: sigma_t ~ logU[0.1,100] for all
-    cells, then c ~ U[0.5,0.99] for all cells.  Returns (sigma_t, sigma_s)."""
+    cells, then c ~ U[0.5,0.99] for all cells.  Returns (sigma_t, sigma_s).
+    ``draws(seed, n)`` replaces the unit-draw generator (the CPU reference arm
+    passes the oracle's restatement, so it never maps the product library)."""
     n = nx * nx
-    u = unit_draws(seed, 2 * n * samples)
+    u = (draws or unit_draws)(seed, 2 * n * samples)
     st = np.empty((samples, n))
     ss = np.empty((samples, n))
     for s in range(samples):

@@ -272,10 +272,9 @@ Plan2D plan2d(const rte_ctx* c, int single) {
   const int nbands = (c->ny + 31) / 32;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  static const int force_dpl = [] {
-    const char* e = std::getenv("RTE_SWEEP_DPL");
-    return e ? std::atoi(e) : 0;
-  }();
+  // development knob (read per call so tests can force each production plan)
+  const char* dpl_env = std::getenv("RTE_SWEEP_DPL");
+  const int force_dpl = dpl_env ? std::atoi(dpl_env) : 0;
   Plan2D best{1, 1, 0};
   for (int dpl : {8, 4, 2, 1}) {
     if (c->block == 16 && dpl > 2) continue;  // full-block cell solve: keep the register budget
@@ -506,6 +505,15 @@ int rte_create(const rte_problem* p, int device, rte_ctx** out) {
       c->hy = (p->y1 - p->y0) / c->ny;
     }
     build_slots(c);
+    if (c->geom == RTE_XY2D) {
+      // the 2D sweep writes kinetic output for at most two original directions
+      // per (vx, vy) slot (the +/-vz pair of a product quadrature)
+      std::vector<int> per_slot(c->nslots, 0);
+      for (int j = 0; j < c->nv; ++j) ++per_slot[c->dir_slot[j]];
+      for (int k = 0; k < c->nslots; ++k)
+        RTE_REQUIRE(per_slot[k] <= 2, RTE_ERR_UNSUPPORTED,
+                    "rte_create: more than two directions share one (vx, vy) slot");
+    }
     const size_t nblk = (size_t)c->S * c->ncells * c->block;
     c->mt_h.assign(p->mt, p->mt + nblk);
     c->ms_h.assign(p->ms, p->ms + nblk);
@@ -535,6 +543,17 @@ const char* rte_last_error(const rte_ctx* ctx) { return ctx ? ctx->err.c_str() :
 long rte_n_dof(const rte_ctx* ctx) { return ctx->ndof; }
 int rte_n_samples(const rte_ctx* ctx) { return ctx->S; }
 int rte_n_slots(const rte_ctx* ctx) { return ctx->nslots; }
+
+int rte_sweep_plan(rte_ctx* ctx, int* dpl, int* groups) {
+  return guarded(ctx, [&] {
+    RTE_REQUIRE(dpl && groups, RTE_ERR_INVALID, "sweep_plan: null argument");
+    *dpl = *groups = 0;
+    if (ctx->geom != RTE_XY2D) return;
+    const Plan2D p = plan2d(ctx, -1);
+    *dpl = p.dpl;
+    *groups = p.groups;
+  });
+}
 
 int rte_apply_L(rte_ctx* ctx, const double* rho, double* out, void* stream) {
   return guarded(ctx, [&] {
@@ -643,14 +662,28 @@ int rte_dsa_setup(rte_ctx* ctx, void* stream) {
 int rte_dsa_solve_density(rte_ctx* ctx, const double* rhs, double* out, void* stream) {
   return guarded(ctx, [&] {
     DeviceGuard dg(ctx->device);
+    RTE_REQUIRE(ctx->dsa, RTE_ERR_INVALID, "dsa: rte_dsa_setup was not called");
+    dsa_status_reset(ctx, as_stream(stream));
     dsa_apply(ctx, rhs, out, nullptr, 0, as_stream(stream));
+    dsa_status_check(ctx, as_stream(stream), "dsa: solve_density");
   });
 }
 
 int rte_dsa_correct(rte_ctx* ctx, const double* delta, double* out, void* stream) {
   return guarded(ctx, [&] {
     DeviceGuard dg(ctx->device);
+    RTE_REQUIRE(ctx->dsa, RTE_ERR_INVALID, "dsa: rte_dsa_setup was not called");
+    dsa_status_reset(ctx, as_stream(stream));
     dsa_apply(ctx, delta, out, nullptr, 1, as_stream(stream));
+    dsa_status_check(ctx, as_stream(stream), "dsa: correct");
+  });
+}
+
+int rte_dsa_reset_history(rte_ctx* ctx, void* stream) {
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    RTE_REQUIRE(ctx->dsa, RTE_ERR_INVALID, "dsa: rte_dsa_setup was not called");
+    dsa_history_reset(ctx, as_stream(stream));
   });
 }
 
@@ -708,7 +741,8 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
     DeviceGuard dg(ctx->device);
     rte_si_config cfg = *cfg_in;
     RTE_REQUIRE(cfg.max_iters >= 1, RTE_ERR_INVALID, "si_solve: max_iters must be >= 1");
-    if (cfg.fixed_iters > 0) cfg.max_iters = std::max(cfg.max_iters, cfg.fixed_iters);
+    // history_host / log_host rows are max_iters long
+    RTE_REQUIRE(cfg.fixed_iters <= cfg.max_iters, RTE_ERR_INVALID, "si_solve: fixed_iters must not exceed max_iters");
     const int every = cfg.check_every > 0 ? cfg.check_every : 4;
     cudaStream_t st = nullptr;
     const int S = ctx->S;
@@ -716,6 +750,10 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
     const bool need_dsa = cfg.method == RTE_DSA || cfg.method == RTE_ROMSAD || cfg.method == RTE_ROMIG;
     const bool need_rom = cfg.method == RTE_ROMSA || cfg.method == RTE_ROMSAD;
     if (need_dsa && !ctx->dsa) dsa_setup(ctx, st);
+    if (need_dsa) {  // a solve does not depend on earlier calls' warm-start history
+      dsa_history_reset(ctx, st);
+      dsa_status_reset(ctx, st);
+    }
     DBuf<int>& ibuf = ctx->si_ibuf;
     ibuf.ensure((size_t)S * 8 + 1);
     SiState sst{};
@@ -862,6 +900,8 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
     RTE_CUDA(cudaMemcpy(hi.data(), ibuf.p, sizeof(int) * S * 8, cudaMemcpyDeviceToHost));
     std::vector<double> hl(S);
     RTE_CUDA(cudaMemcpy(hl.data(), lastc.p, sizeof(double) * S, cudaMemcpyDeviceToHost));
+    std::vector<int> dstat(S, RTE_DSA_OK);
+    if (need_dsa) dsa_status_read(ctx, dstat.data(), st);
     if (reports) {
       for (int s = 0; s < S; ++s) {
         rte_si_report& r = reports[s];
@@ -872,10 +912,12 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
         r.singular = hi[5 * S + s];
         r.final_residual = resid[s];
         r.last_change = hl[s];
+        r.dsa_status = dstat[s];
       }
     }
     if (history) RTE_CUDA(cudaMemcpy(history, hist.p, sizeof(double) * S * cfg.max_iters, cudaMemcpyDeviceToHost));
     if (log) RTE_CUDA(cudaMemcpy(log, lg.p, (size_t)S * cfg.max_iters, cudaMemcpyDeviceToHost));
+    if (need_dsa) dsa_status_check(ctx, st, "si_solve: DSA correction");
   });
 }
 

@@ -450,6 +450,36 @@ void dsa_apply(rte_ctx* ctx, const double* rhs, double* out, const int* kind, in
   RTE_CUDA(cudaGetLastError());
 }
 
+void dsa2d_status_reset(rte_ctx* ctx, cudaStream_t st);
+void dsa2d_status_read(rte_ctx* ctx, int* host, cudaStream_t st);
+void dsa2d_history_reset(rte_ctx* ctx, cudaStream_t st);
+
+// Per-sample rte_dsa_status of the solves since the last reset.  The slab
+// solve is a direct block cyclic reduction (no iteration to fall short).
+void dsa_status_reset(rte_ctx* ctx, cudaStream_t st) {
+  if (ctx->dsa && ctx->dsa->impl2d) dsa2d_status_reset(ctx, st);
+}
+void dsa_status_read(rte_ctx* ctx, int* host, cudaStream_t st) {
+  if (ctx->dsa && ctx->dsa->impl2d)
+    dsa2d_status_read(ctx, host, st);
+  else
+    std::fill(host, host + ctx->S, 0);
+}
+void dsa_history_reset(rte_ctx* ctx, cudaStream_t st) {
+  if (ctx->dsa && ctx->dsa->impl2d) dsa2d_history_reset(ctx, st);
+}
+// throws RTE_ERR_RUNTIME naming the first sample whose solve fell short
+void dsa_status_check(rte_ctx* ctx, cudaStream_t st, const char* what) {
+  std::vector<int> f(ctx->S);
+  dsa_status_read(ctx, f.data(), st);
+  for (int s = 0; s < ctx->S; ++s)
+    if (f[s] != RTE_DSA_OK) {
+      static const char* why[] = {"ok", "iteration cap reached", "breakdown", "non-finite residual"};
+      throw Error(RTE_ERR_RUNTIME, std::string(what) + ": coupled moment system solve failed at sample " +
+                                       std::to_string(s) + " (" + why[f[s] & 3] + ")");
+    }
+}
+
 void dsa_solve_density(rte_ctx* ctx, const double* rhs, double* out, const int* kind, cudaStream_t st) {
   dsa_apply(ctx, rhs, out, kind, 0, st);
 }

@@ -111,6 +111,8 @@ struct Dsa2D {
   DBuf<double> scal;          // per sample scalars [S][16]
   DBuf<double> part, part2;   // dot partials [S][nblk][4] (two sets: producer / consumer overlap)
   DBuf<int> act;              // per-sample active flag
+  DBuf<int> fail;             // [S] worst rte_dsa_status since the last dsa2d_status_reset
+  bool fail_init = false;
   DBuf<int> nact;
   double tol = 1e-12;
   int maxit = 1000;
@@ -1078,7 +1080,14 @@ __global__ void k_dots(int S, long n, DotArgs d, double* __restrict__ part, cons
 
 // scalar state per sample (scal[s*16 + k])
 enum { SC_RHO_OLD = 0, SC_ALPHA, SC_OMEGA, SC_RHO, SC_BNORM2, SC_RNORM2, SC_ITERS, SC_CONV, SC_RHV, SC_TS, SC_TT,
-       SC_RHO_NEW, SC_RMAX };
+       SC_RHO_NEW, SC_RMAX, SC_FAIL };
+
+// why a sample stopped without meeting its tolerance (SC_FAIL, rte_si_report.dsa_status)
+__device__ __forceinline__ double fail_code(double rn, const double* sc) {
+  if (!(rn == rn)) return (double)RTE_DSA_NAN;
+  if (sc[SC_OMEGA] == 0.0) return (double)RTE_DSA_BREAKDOWN;
+  return (double)RTE_DSA_MAXIT;
+}
 
 // natural SoA element i of a sample -> red-black position (32-bit index math)
 __device__ __forceinline__ unsigned nat2rb(unsigned i, unsigned nc, unsigned nx) {
@@ -1102,6 +1111,7 @@ __global__ void k_bicg_init(int S, int nblk, const double* part, double* scal, i
   sc[SC_RHO_NEW] = bn;  // (rh, r) with rh = r = b
   sc[SC_ITERS] = 0;
   sc[SC_CONV] = 0;
+  sc[SC_FAIL] = 0;
   act[s] = (mask ? mask[s] : 1) && bn > 0.0;
   if (!(bn > 0.0)) sc[SC_CONV] = 1;
 }
@@ -1526,6 +1536,7 @@ __global__ void k_sl_relcheck(int S, int nblk, const double* part, double* scal,
   const bool conv = rn <= tol2 * sc[SC_BNORM2];
   if (conv || !(rn == rn) || sc[SC_ITERS] >= maxit || sc[SC_OMEGA] == 0.0) {
     sc[SC_CONV] = conv ? 1 : 0;
+    if (!conv) sc[SC_FAIL] = fail_code(rn, sc);
     act[s] = 0;
   } else {
     atomicAdd(nact, 1);
@@ -1640,10 +1651,18 @@ __global__ void k_bicg_init_warm(int S, int nblk, const double* part, const doub
   sc[SC_RNORM2] = w[1];
   sc[SC_RHO_NEW] = w[0];
   sc[SC_ITERS] = 0;
+  sc[SC_FAIL] = 0;
   const bool done = !(bn > 0.0) || w[1] <= tol2 * bn;
   sc[SC_CONV] = done ? 1 : 0;
   act[s] = done ? 0 : 1;
   if (!done) atomicAdd(nact, 1);
+}
+
+// per-sample failure codes of this solve folded into the running status
+// (the worst code since the last dsa2d_status_reset)
+__global__ void k_fail_accum(int S, const double* scal, int* fail) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < S) fail[s] = max(fail[s], (int)scal[s * 16 + SC_FAIL]);
 }
 
 __global__ void k_mark_prev(int S, const double* scal, int* has_prev) {
@@ -1866,6 +1885,7 @@ __global__ void k_bicg_check(int S, int nblk, const double* part, double* scal, 
   sc[SC_ITERS] += 1;
   if (rn <= tol2 * sc[SC_BNORM2] || !(rn == rn) || sc[SC_ITERS] >= maxit || sc[SC_OMEGA] == 0.0) {
     sc[SC_CONV] = (rn <= tol2 * sc[SC_BNORM2]) ? 1 : 0;
+    if (!(rn <= tol2 * sc[SC_BNORM2])) sc[SC_FAIL] = fail_code(rn, sc);
     act[s] = 0;
   } else {
     atomicAdd(nact, 1);
@@ -2735,6 +2755,13 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     std::fprintf(stderr, "[dsa2d] solve: %d BiCGStab iterations (per sample max %.0f, mean %.2f)%s\n", it, mx, sum / S,
                  d->warm ? " (warm start)" : "");
   }
+  if (!d->fail_init) {
+    d->fail.ensure(S);
+    d->fail.zero(st);
+    d->fail_init = true;
+  }
+  ++d->nlaunch;
+  k_fail_accum<<<(S + 127) / 128, 128, 0, st>>>(S, d->scal.p, d->fail.p);
   ++d->nlaunch;
   k_unpack<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, d->x.p, out, kind);
   RTE_CUDA(cudaGetLastError());
@@ -2844,6 +2871,36 @@ int dsa2d_last_iters(const rte_ctx* ctx) {
   double mx = 0;
   for (int k = 0; k < d->S; ++k) mx = std::max(mx, sc[(size_t)k * 16 + SC_ITERS]);
   return (int)mx;
+}
+
+void dsa2d_status_reset(rte_ctx* ctx, cudaStream_t st) {
+  auto* d = static_cast<Dsa2D*>(ctx->dsa->impl2d);
+  d->fail.ensure(d->S);
+  d->fail.zero(st);
+  d->fail_init = true;
+}
+
+void dsa2d_status_read(rte_ctx* ctx, int* host, cudaStream_t st) {
+  auto* d = static_cast<Dsa2D*>(ctx->dsa->impl2d);
+  if (!d->fail_init) {
+    std::fill(host, host + d->S, 0);
+    return;
+  }
+  RTE_CUDA(cudaMemcpyAsync(host, d->fail.p, sizeof(int) * d->S, cudaMemcpyDeviceToHost, st));
+  RTE_CUDA(cudaStreamSynchronize(st));
+}
+
+// forget the warm-start history (the solutions of earlier solves): the next
+// solve starts from zero, so its result does not depend on earlier calls
+void dsa2d_history_reset(rte_ctx* ctx, cudaStream_t st) {
+  auto* d = static_cast<Dsa2D*>(ctx->dsa->impl2d);
+  if (d->hcount.p) d->hcount.zero(st);
+  if (d->gram.p) d->gram.zero(st);
+  if (d->has_prev.p) d->has_prev.zero(st);
+  if (d->xprev.p) d->xprev.zero(st);
+  if (d->xprev2.p) d->xprev2.zero(st);
+  if (d->gram.p) d->hhead = d->warm - 1;
+  d->poll_from = 1000000;
 }
 
 void dsa2d_set_tolerance(rte_ctx* ctx, double tol, int maxit) {

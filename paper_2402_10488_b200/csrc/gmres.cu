@@ -309,6 +309,10 @@ void gmres_solve(rte_ctx* ctx, const rte_gmres_config& cfg, double* rho, rte_gmr
   const long nd = ctx->ndof;
   const bool pre = cfg.preconditioned != 0;
   if (pre && !ctx->dsa) dsa_setup(ctx, st);
+  if (pre) {  // a solve does not depend on earlier calls' warm-start history
+    dsa_history_reset(ctx, st);
+    dsa_status_reset(ctx, st);
+  }
   const int nblk = (int)std::min<long>(256, std::max<long>(1, (nd + 4095) / 4096));
   const dim3 vg(nblk, S);
   const int hcap = std::max(1, history_cap);
@@ -421,9 +425,12 @@ void gmres_solve(rte_ctx* ctx, const rte_gmres_config& cfg, double* rho, rte_gmr
     RTE_CUDA(cudaStreamSynchronize(st));
     for (int s = 0; s < S; ++s) std::memcpy(&res_nc[s], &hb[2 * s], sizeof(double));
   }
+  std::vector<int> dstat(S, RTE_DSA_OK);
+  if (pre) dsa_status_read(ctx, dstat.data(), st);
   if (reports) {
     for (int s = 0; s < S; ++s) {
       rte_gmres_report& r = reports[s];
+      r.dsa_status = dstat[s];
       r.converged = hs[s].converged;
       r.iterations = hs[s].total;
       r.n_sweep = 1 + (long)hs[s].steps;  // bbar + one apply_A per cycle start and inner step
@@ -434,6 +441,7 @@ void gmres_solve(rte_ctx* ctx, const rte_gmres_config& cfg, double* rho, rte_gmr
   }
   if (history && history_cap > 0)
     RTE_CUDA(cudaMemcpy(history, hist.p, sizeof(double) * S * history_cap, cudaMemcpyDeviceToHost));
+  if (pre) dsa_status_check(ctx, st, "gmres: DSA preconditioner");
 }
 
 }  // namespace rte

@@ -344,6 +344,8 @@ void collect_snapshots(rte_ctx* ctx, int window, double eps, int max_iters, doub
   const int S = ctx->S;
   const long nd = ctx->ndof, kdim = (long)ctx->nv * nd;
   if (!ctx->dsa) dsa_setup(ctx, st);
+  dsa_history_reset(ctx, st);
+  dsa_status_reset(ctx, st);
   DBuf<double> rho, rstar, delta, corr, f;
   rho.alloc((size_t)S * nd);
   rstar.alloc((size_t)S * nd);
@@ -384,6 +386,7 @@ void collect_snapshots(rte_ctx* ctx, int window, double eps, int max_iters, doub
   }
   RTE_CUDA(cudaMemcpy(conv_h, conv, sizeof(int) * S, cudaMemcpyDeviceToHost));
   RTE_CUDA(cudaMemcpy(n_iter_h, n_iter, sizeof(int) * S, cudaMemcpyDeviceToHost));
+  dsa_status_check(ctx, st, "collect_snapshots: DSA correction");
 }
 
 }  // namespace rte

@@ -3,11 +3,11 @@
 // Replaces pod_truncate (pod.cpp:141-304: dgesdd in-core or out-of-core TSQR)
 // and build_reduced_model (reduced_model.cpp:106-199).
 //
-// POD: shifted CholeskyQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa
-// 2020), whose backward error matches Householder QR for condition numbers up
-// to 1/u, so small singular values keep the accuracy the reference's
-// Householder/SVD path gives (a plain Gram eigen-decomposition would square
-// the condition number).  The only O(m) work -- the Gram products
+// POD: repeated (shifted) CholeskyQR (Fukaya, Kannan, Nakatsukasa, Yamamoto,
+// Yanagisawa 2020): shifted passes until the basis is well conditioned, then
+// CholeskyQR2, so small singular values keep the accuracy the reference's
+// Householder/SVD path gives, also past 1/u (a plain Gram eigen-decomposition
+// would square the condition number).  The only O(m) work -- the Gram products
 // F^T F and the right-multiplications F R^{-1}, Q W -- runs on the device
 // with deterministic two-stage reductions; the n x n factors (n <= 128)
 // are handled on the host: Cholesky and a one-sided Jacobi SVD of R (high
@@ -444,34 +444,48 @@ int snapshot_columns(int S, int window, long kdim, const double* f_iter, const d
 
 // F: m x n column-major on device (m >= n).  sigma (n values) to host; the
 // first rank_max left singular vectors to U (m x rank_max).
+__global__ void k_transpose(long m, int n, const double* __restrict__ A, double* __restrict__ T) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * n) return;
+  const long i = t % m, j = t / m;  // A(i, j), column-major m x n -> T(j, i), n x m
+  T[i * n + j] = A[t];
+}
+
+// R (n x n, column-major) -> F = Q R with Q (m x n) orthonormal in *q_out
+// (one of the two work buffers)
+static std::vector<double> cholesky_qr(long m, int n, const double* F, DBuf<double>& Q1, DBuf<double>& Q2,
+                                       const double** q_out, cudaStream_t st);
+
 void pod(long m, int n, const double* F, int rank_max, double* U, double* sigma, cudaStream_t st) {
   RTE_REQUIRE(n >= 1 && n <= 128, RTE_ERR_UNSUPPORTED, "pod: 1..128 snapshot columns supported");
-  RTE_REQUIRE(m >= n, RTE_ERR_UNSUPPORTED, "pod: wide snapshot matrices (rows < columns) not supported");
-  RTE_REQUIRE(rank_max >= 0 && rank_max <= n, RTE_ERR_INVALID, "pod: rank_max out of range");
-  std::vector<double> G = gram_host(m, n, n, F, F, st);
-  double fro2 = 0.0;
-  for (int i = 0; i < n; ++i) fro2 += G[(size_t)i * n + i];
-  RTE_REQUIRE(fro2 > 0, RTE_ERR_INVALID, "pod: snapshot matrix is zero");
-  const double u = 1.1102230246251565e-16;
-  const double shift = 11.0 * ((double)m * n + (double)n * (n + 1)) * u * fro2;
-  DBuf<double> Q1, Q2;
-  Q1.alloc((size_t)m * n);
-  Q2.alloc((size_t)m * n);
-  std::vector<double> Rtot((size_t)n * n, 0.0);
-  for (int i = 0; i < n; ++i) Rtot[(size_t)i * n + i] = 1.0;
-  const double* src = F;
-  DBuf<double>* dst = &Q1;
-  for (int pass = 0; pass < 3; ++pass) {
-    std::vector<double> Gp = pass == 0 ? G : gram_host(m, n, n, src, src, st);
-    if (pass == 0)
-      for (int i = 0; i < n; ++i) Gp[(size_t)i * n + i] += shift;
-    std::vector<double> R;
-    RTE_REQUIRE(cholesky_upper(Gp, n, R), RTE_ERR_RUNTIME, "pod: CholeskyQR breakdown");
-    rmul(m, n, n, src, inv_upper(R, n), dst->p, st);
-    Rtot = matmul_cm(R, Rtot, n);
-    src = dst->p;
-    dst = dst == &Q1 ? &Q2 : &Q1;
+  RTE_REQUIRE(m >= 1, RTE_ERR_INVALID, "pod: empty snapshot matrix");
+  RTE_REQUIRE(rank_max >= 0 && rank_max <= std::min<long>(m, n), RTE_ERR_INVALID, "pod: rank_max out of range");
+  if (m < n) {
+    // wide (more snapshots than unknowns, test_pod.cpp:183-193): F^T = Q R,
+    // so F = R^T Q^T and the left singular vectors of F are those of R^T (m x m)
+    DBuf<double> FT, Q1, Q2;
+    FT.alloc((size_t)m * n);
+    k_transpose<<<(int)((m * n + 255) / 256), 256, 0, st>>>(m, n, F, FT.p);
+    RTE_CUDA(cudaGetLastError());
+    const double* q = nullptr;
+    std::vector<double> R = cholesky_qr(n, (int)m, FT.p, Q1, Q2, &q, st);
+    const int k = (int)m;
+    std::vector<double> RT((size_t)k * k);
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j) RT[(size_t)j * k + i] = R[(size_t)i * k + j];
+    std::vector<double> s, W;
+    jacobi_svd_left(RT, k, s, W);
+    for (int i = 0; i < n; ++i) sigma[i] = i < k ? s[i] : 0.0;
+    if (rank_max > 0)
+      RTE_CUDA(cudaMemcpyAsync(U, W.data(), sizeof(double) * (size_t)k * rank_max, cudaMemcpyHostToDevice, st));
+    RTE_CUDA(cudaStreamSynchronize(st));
+    return;
   }
+  DBuf<double> Q1, Q2;
+  const double* src = nullptr;
+  std::vector<double> Rtot = cholesky_qr(m, n, F, Q1, Q2, &src, st);
+  // F = Q Rtot, Rtot = W diag(s) V^T (one-sided Jacobi: high relative
+  // accuracy), so the left singular vectors of F are Q W
   std::vector<double> s, W;
   jacobi_svd_left(Rtot, n, s, W);
   for (int k = 0; k < n; ++k) sigma[k] = s[k];
@@ -479,6 +493,54 @@ void pod(long m, int n, const double* F, int rank_max, double* U, double* sigma,
     std::vector<double> Wr(W.begin(), W.begin() + (size_t)n * rank_max);
     rmul(m, n, rank_max, src, Wr, U, st);
   }
+}
+
+static std::vector<double> cholesky_qr(long m, int n, const double* F, DBuf<double>& Q1, DBuf<double>& Q2,
+                                       const double** q_out, cudaStream_t st) {
+  // Repeated CholeskyQR: a pass whose Gram is too ill-conditioned for a plain
+  // Cholesky (kappa(Q) > 1e7, or breakdown) is shifted (Fukaya et al. 2020:
+  // G + s I with s = 11 (m n + n (n + 1)) u ||Q||_F^2), which cuts the
+  // condition number by ~sqrt(s) per pass; two plain passes (CholeskyQR2)
+  // finish once it is below 1e7.  Snapshot matrices with decaying spectra
+  // far past 1/u (the reference's POD KAT, test_pod.cpp:16-36: sigma_k =
+  // 10^(-k/2), kappa 3e19) need two shifted passes; well-conditioned ones
+  // run CholeskyQR2 directly.
+  const double u = 1.1102230246251565e-16;
+  Q1.alloc((size_t)m * n);
+  Q2.alloc((size_t)m * n);
+  std::vector<double> Rtot((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) Rtot[(size_t)i * n + i] = 1.0;
+  const double* src = F;
+  DBuf<double>* dst = &Q1;
+  int plain = 0;
+  for (int pass = 0; plain < 2; ++pass) {
+    RTE_REQUIRE(pass < 10, RTE_ERR_RUNTIME, "pod: CholeskyQR did not reach an orthonormal basis in 10 passes");
+    std::vector<double> G = gram_host(m, n, n, src, src, st);
+    double fro2 = 0.0;
+    for (int i = 0; i < n; ++i) fro2 += G[(size_t)i * n + i];
+    RTE_REQUIRE(fro2 > 0 && std::isfinite(fro2), RTE_ERR_INVALID, "pod: snapshot matrix is zero or not finite");
+    std::vector<double> R;
+    bool ok = cholesky_upper(G, n, R);
+    if (ok) {
+      std::vector<double> sv, Wv;
+      jacobi_svd_left(R, n, sv, Wv);
+      ok = sv[n - 1] > 0 && sv[0] / sv[n - 1] <= 1e7;
+    }
+    if (ok) {
+      ++plain;
+    } else {
+      plain = 0;
+      const double shift = 11.0 * ((double)m * n + (double)n * (n + 1)) * u * fro2;
+      for (int i = 0; i < n; ++i) G[(size_t)i * n + i] += shift;
+      RTE_REQUIRE(cholesky_upper(G, n, R), RTE_ERR_RUNTIME, "pod: shifted CholeskyQR breakdown");
+    }
+    rmul(m, n, n, src, inv_upper(R, n), dst->p, st);
+    Rtot = matmul_cm(R, Rtot, n);
+    src = dst->p;
+    dst = dst == &Q1 ? &Q2 : &Q1;
+  }
+  *q_out = src;
+  return Rtot;
 }
 
 // build_reduced_model: U (kdim x r) on device, sample 0's discretization.

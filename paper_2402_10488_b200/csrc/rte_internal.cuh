@@ -299,6 +299,10 @@ long dsa2d_take_launches(rte_ctx* ctx);
 void dsa2d_set_tolerance(rte_ctx* ctx, double tol, int maxit);
 long dsa_coupled_dim(const rte_ctx* ctx);
 void dsa_apply_eliminated(rte_ctx* ctx, const double* x, double* out, cudaStream_t st);
+void dsa_status_reset(rte_ctx* ctx, cudaStream_t st);
+void dsa_status_read(rte_ctx* ctx, int* host, cudaStream_t st);  // [S] rte_dsa_status
+void dsa_status_check(rte_ctx* ctx, cudaStream_t st, const char* what);
+void dsa_history_reset(rte_ctx* ctx, cudaStream_t st);
 
 // ROM
 void rom_load(rte_ctx* ctx, int which, const rte_rom* rom);

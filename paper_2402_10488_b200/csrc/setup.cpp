@@ -94,6 +94,7 @@ int rte_weighted_mass(int geometry, int nx, int ny, const double* bounds, double
   std::vector<double> g(nq), gw(nq);
   gl(nq, g.data(), gw.data());
   if (geometry == RTE_SLAB1D) {
+    if (!bounds) return RTE_ERR_INVALID;
     for (int i = 0; i < nx; ++i) {
       const double h = bounds[i + 1] - bounds[i], xc = 0.5 * (bounds[i] + bounds[i + 1]);
       double m[4] = {0, 0, 0, 0};
@@ -140,6 +141,7 @@ int rte_project(int geometry, int nx, int ny, const double* bounds, double x0, d
   auto p0 = [](double h) { return 1.0 / std::sqrt(h); };
   auto p1 = [](double h, double rel) { return std::sqrt(12.0 / (h * h * h)) * rel; };
   if (geometry == RTE_SLAB1D) {
+    if (!bounds) return RTE_ERR_INVALID;
     for (int i = 0; i < nx; ++i) {
       const double h = bounds[i + 1] - bounds[i];
       double o0 = 0, o1 = 0;

@@ -323,6 +323,13 @@ class TransportBatch:
     def n_slots(self) -> int:
         return capi.load().rte_n_slots(self._h)
 
+    def sweep_plan(self):
+        """(directions per lane, direction groups per quadrant) of the XY
+        sweep kernel for this batch ((0, 0) for slabs)."""
+        d, g = ctypes.c_int(), ctypes.c_int()
+        capi.check(capi.load().rte_sweep_plan(self._h, ctypes.byref(d), ctypes.byref(g)), self._h)
+        return d.value, g.value
+
     def _dev(self, x, shape=None):
         torch = _torch()
         t = torch.as_tensor(x, dtype=torch.float64, device="cuda:%d" % self.device).contiguous()
@@ -447,6 +454,12 @@ class DsaOperator:
     def set_tolerance(self, tol: float, max_iters: int = 0) -> None:
         """XY only: relative residual of the iterative coupled solve."""
         self.batch._call(capi.load().rte_dsa_set_tolerance, float(tol), int(max_iters))
+
+    def reset_history(self) -> None:
+        """Clear the XY warm-start history (rte_dsa_reset_history): the next
+        direct solve starts from zero.  rte_si_solve / rte_gmres_solve clear
+        it themselves."""
+        self.batch._call(capi.load().rte_dsa_reset_history, None)
 
     def last_iterations(self) -> int:
         return capi.load().rte_dsa_last_iterations(self.batch._h)
@@ -610,6 +623,7 @@ class SolveReport:
     switch_iter: int
     singular: bool
     wall_seconds: float = 0.0  # wall time of the whole batched solve (shared by its samples)
+    dsa_status: int = 0  # worst rte_dsa_status of the sample's DSA solves (0 = every solve met its tolerance)
 
 
 _METHODS = {"SI": capi.RTE_SI, "DSA": capi.RTE_DSA, "ROMSA": capi.RTE_ROMSA, "ROMSAD": capi.RTE_ROMSAD,
@@ -669,6 +683,8 @@ def si_config(config: SolveConfig, method_code: int, callback=None) -> "capi.SiC
         raise ValueError("solve config: norm must be 'abs' or 'rel'")
     if config.max_iters < 1 or config.fixed_iters < 0 or config.check_every < 0:
         raise ValueError("solve config: max_iters >= 1, fixed_iters >= 0, check_every >= 0")
+    if config.fixed_iters > config.max_iters:
+        raise ValueError("solve config: fixed_iters must not exceed max_iters")
     if not 0.0 <= config.dsa_inner < 1.0:
         raise ValueError("solve config: dsa_inner must be in [0, 1)")
     return capi.SiConfig(method_code, float(config.eps_sisa),
@@ -695,7 +711,7 @@ def sisa_solve(batch: TransportBatch, method, config: SolveConfig):
         rho = batch._dev(config.initial_guess, (batch.S, batch.nd)).clone()
     else:
         rho = batch._out(batch.S, batch.nd)
-    S, mi = batch.S, max(config.max_iters, config.fixed_iters)
+    S, mi = batch.S, config.max_iters
     reps = (capi.SiReport * S)()
     hist = np.zeros(S * mi)
     log = ctypes.create_string_buffer(S * mi)
@@ -706,7 +722,13 @@ def sisa_solve(batch: TransportBatch, method, config: SolveConfig):
     wall = _time.perf_counter() - t0
     if rc != 0 and errors:
         raise errors[0]
-    capi.check(rc, batch._h)
+    if rc != 0:
+        # a failed DSA correction still fills the reports (attached to the error)
+        try:
+            capi.check(rc, batch._h)
+        except capi.RteError as e:
+            e.dsa_status = [int(reps[s].dsa_status) for s in range(S)]
+            raise
     raw = log.raw
     out = []
     label = custom.label() if custom is not None else method
@@ -717,7 +739,7 @@ def sisa_solve(batch: TransportBatch, method, config: SolveConfig):
         out.append(SolveReport(bool(r.converged), int(r.n_sweep), int(it), list(hist[s * mi:s * mi + it]),
                                float(r.final_residual), label,
                                "supplied" if (config.initial_guess is not None or m == capi.RTE_ROMIG) else "zero",
-                               lg, int(r.switch_iter), bool(r.singular), wall))
+                               lg, int(r.switch_iter), bool(r.singular), wall, int(r.dsa_status)))
     return rho, out
 
 
@@ -756,7 +778,8 @@ def gmres_solve(batch: TransportBatch, preconditioner, config: SolveConfig, romi
         n = min(int(r.history_len), cap)
         out.append(SolveReport(bool(r.converged), int(r.n_sweep), int(r.iterations), list(hist[s * cap:s * cap + n]),
                                float(r.final_residual), "PGMRES" if preconditioner is not None else "GMRES",
-                               "zero" if guess == capi.RTE_GUESS_ZERO else "supplied", "", -1, False, wall))
+                               "zero" if guess == capi.RTE_GUESS_ZERO else "supplied", "", -1, False, wall,
+                               int(r.dsa_status)))
     return rho, out
 
 

@@ -25,7 +25,8 @@ t0 = time.time()
 rho, reps = rte.sisa_solve(b, "DSA", rte.SolveConfig(eps_sisa=1e-8, norm=norm, max_iters=200))
 torch.cuda.synchronize()
 t = time.time() - t0
-ms = (ctypes.c_double * 5)(); nk = (ctypes.c_long * 5)()
+NK = len(capi.PROF_KINDS)  # rte_profile_read writes RTE_PROF_KINDS entries
+ms = (ctypes.c_double * NK)(); nk = (ctypes.c_long * NK)()
 L.rte_profile_read(b._h, ms, nk)
 r = reps[0]
 print("C3 %s: converged=%s iterations=%d n_sweep=%d residual=%.2e time-to-tol=%.3f s" % (norm, r.converged, r.iterations,
