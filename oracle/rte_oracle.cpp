@@ -15,6 +15,7 @@
 // index fastest (dg_space.hpp:24); kinetic vectors are direction-major blocks
 // of n_dof (transport_system.hpp:73-89).
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -1098,6 +1099,44 @@ void ro_cache_slots(void* h, int k0, int k1) {
 int ro_dir_slot(void* h, int j) { return static_cast<System*>(h)->slot[j]; }
 void ro_apply_L_dirs(void* h, const double* rho, double* out, int j0, int j1) {
   static_cast<System*>(h)->apply_L_dirs(rho, out, j0, j1);
+}
+// CPU baseline timing (bench.py): `nthreads` concurrent copies of the
+// reference's per-direction apply_L work (transport_system.cpp:393-404: one
+// sweep with the cached per-slot inverse, then out += w_j f), thread t
+// sweeping directions dirs[t], dirs[t + nthreads], ... into its own buffers,
+// as independent single-threaded reference solves on separate cores would.
+// The caches of the slots involved must be built (ro_cache_slots).  Returns
+// the wall seconds of the timed region.
+double ro_time_sweeps(void* h, const double* rho, const int* dirs, int ndirs, int nthreads) {
+  auto* s = static_cast<System*>(h);
+  const long nd = s->ndof;
+  std::vector<double> q(nd);
+  s->apply_block(s->ms, rho, q.data());
+  std::vector<std::vector<double>> f(nthreads, std::vector<double>(nd)), out(nthreads, std::vector<double>(nd, 0.0));
+  double t0 = 0, t1 = 0;
+#ifdef _OPENMP
+  t0 = omp_get_wtime();
+#pragma omp parallel num_threads(nthreads)
+  {
+    const int t = omp_get_thread_num();
+    for (int k = t; k < ndirs; k += nthreads) {
+      const int j = dirs[k];
+      s->sweep(j, q.data(), f[t].data());
+      for (long i = 0; i < nd; ++i) out[t][i] += s->w[j] * f[t][i];
+    }
+  }
+  t1 = omp_get_wtime();
+#else
+  (void)nthreads;
+  const auto c0 = std::chrono::steady_clock::now();
+  for (int k = 0; k < ndirs; ++k) {
+    const int j = dirs[k];
+    s->sweep(j, q.data(), f[0].data());
+    for (long i = 0; i < nd; ++i) out[0][i] += s->w[j] * f[0][i];
+  }
+  t1 = std::chrono::duration<double>(std::chrono::steady_clock::now() - c0).count();
+#endif
+  return t1 - t0;
 }
 
 void ro_mass_blocks(void* h, double* mt, double* ms) {

@@ -386,6 +386,16 @@ class TransportSystem:
     def cache_slots(self, k0, k1):
         lib().ro_cache_slots(self._h, ctypes.c_int(k0), ctypes.c_int(k1))
 
+    def time_sweeps(self, rho, dirs, nthreads):
+        """Wall seconds of `nthreads` concurrent reference apply_L sweeps over
+        `dirs` (cached inverses; see ro_time_sweeps)."""
+        rho = _c(rho)
+        d = np.ascontiguousarray(dirs, dtype=np.int32)
+        L = lib()
+        L.ro_time_sweeps.restype = ctypes.c_double
+        return float(L.ro_time_sweeps(self._h, _p(rho), d.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                      ctypes.c_int(d.size), ctypes.c_int(nthreads)))
+
     def apply_L_dirs(self, rho, j0, j1):
         """apply_L restricted to directions [j0, j1) (CPU baseline timing)."""
         rho = _c(rho)
@@ -1251,3 +1261,28 @@ def set_cache_budget(nbytes: float):
     bigger problems compute each cell's inverse when they sweep (same
     arithmetic), slot-major over OpenMP threads."""
     lib().ro_set_cache_budget(ctypes.c_double(float(nbytes)))
+
+
+def cell_constant_system(nx, ny, sigma_t, sigma_s, quad, source=1.0, inflow=(0.0, 0.0, 0.0, 0.0),
+                         extent=(0.0, 1.0, 0.0, 1.0)):
+    """TransportSystem of an XY problem with per-cell constant coefficients
+    sigma_t, sigma_s [ny * nx] (cell = ix + nx iy): one coefficient term whose
+    closures look up the cell of each quadrature point (transport_system.cpp:
+    17-55 integrates them exactly to sigma * I blocks)."""
+    x0, x1, y0, y1 = extent
+    hx, hy = (x1 - x0) / nx, (y1 - y0) / ny
+    st = np.asarray(sigma_t, dtype=np.float64)
+    sa = st - np.asarray(sigma_s, dtype=np.float64)
+    ss = np.asarray(sigma_s, dtype=np.float64)
+
+    def cell(x, y):
+        ix = np.clip(np.floor((np.asarray(x) - x0) / hx).astype(np.int64), 0, nx - 1)
+        iy = np.clip(np.floor((np.asarray(y) - y0) / hy).astype(np.int64), 0, ny - 1)
+        return ix + nx * iy
+    term = CoefficientTerm(absorption_weight=lambda x, y: sa[cell(x, y)],
+                           scattering_weight=lambda x, y: ss[cell(x, y)])
+    p = ProblemDefinition(XY2D, [term], lambda x, y: source + 0.0 * np.asarray(x),
+                          inflow_left=inflow[0], inflow_right=inflow[1], inflow_bottom=inflow[2],
+                          inflow_top=inflow[3])
+    m = Mesh.rect_uniform(x0, x1, nx, y0, y1, ny)
+    return TransportSystem(p, m, build_dg_space(m), quad, [])

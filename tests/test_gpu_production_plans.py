@@ -27,21 +27,9 @@ def rte():
     return m
 
 
-def oracle_cells(nx, cl, st, ss, inflow=None):
-    """Oracle TransportSystem with per-cell constant coefficients (closures
-    evaluated at the cell quadrature points, transport_system.cpp:17-55)."""
-    h = 1.0 / nx
-
-    def cell(x, y):
-        ix = np.clip(np.floor(np.asarray(x) / h).astype(np.int64), 0, nx - 1)
-        iy = np.clip(np.floor(np.asarray(y) / h).astype(np.int64), 0, nx - 1)
-        return ix + nx * iy
-    term = ro.CoefficientTerm(absorption_weight=lambda x, y: (st - ss)[cell(x, y)],
-                              scattering_weight=lambda x, y: ss[cell(x, y)])
-    kw = {} if inflow is None else dict(zip(("inflow_left", "inflow_right", "inflow_bottom", "inflow_top"), inflow))
-    p = ro.ProblemDefinition(ro.XY2D, [term], lambda x, y: 1.0, **kw)
-    m = ro.Mesh.rect_uniform(0.0, 1.0, nx, 0.0, 1.0, nx)
-    return ro.TransportSystem(p, m, ro.build_dg_space(m), ro.chebyshev_legendre(*cl), [])
+def oracle_cells(nx, cl, st, ss, inflow=(0.0, 0.0, 0.0, 0.0)):
+    """Oracle TransportSystem with per-cell constant coefficients."""
+    return ro.cell_constant_system(nx, nx, st, ss, ro.chebyshev_legendre(*cl), inflow=inflow)
 
 
 def device_cells(nx, cl, st, ss, inflow=(0, 0, 0, 0)):
