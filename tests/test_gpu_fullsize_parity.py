@@ -5,7 +5,10 @@
 * C3 (configs[2]): the full 256^2 CL(16,8) SI-DSA solve against the oracle's
   golden record (tests/tools/make_c3_golden.py: exact SuperLU DSA);
 * C4 (configs[3]): all 64 test samples, SI-DSA and ROMSAD(3,5), with the DSA
-  solved to 1e-12 and with the inner tolerance tied to the stop test.
+  solved to 1e-12 and with the inner tolerance tied to the stop test
+  (dsa_inner = 1e-3; at 1e-2 iteration counts and logs still match on every
+  sample but the converged flux of a few samples drifts to 4e-8, above the
+  1e-8 bar: the correction of a diffusive sample is ~100x its delta).
 
 The bar (north_star): identical iteration counts, correction logs and ROMSAD
 switch iterations, flux within 1e-8 relative L2 at convergence.  A sample
@@ -128,7 +131,7 @@ def test_c3_full_size_si_dsa_golden():
     b = R.TransportBatch(homog(R, R.XY2D, 10 * 0.001, 10 * 0.999, 1.0), mesh, R.chebyshev_legendre(16, 8), [[]])
     summaries = []
     for norm in ("rel", "abs"):
-        for inner in (0.0, 1e-2):
+        for inner in (0.0, 1e-3):
             rho, reps = R.sisa_solve(b, "DSA", R.SolveConfig(eps_sisa=1e-8, norm=norm, dsa_inner=inner))
             r = reps[0]
             err = rel_l2(rho.cpu().numpy()[0], g["rho_" + norm])
@@ -158,7 +161,7 @@ def test_c4_all_samples_si_dsa_and_romsad():
     R.load_rom(b, 1, cm)
     eps_r = R.romsad_tolerance(eps_train, cm.discarded_fraction)
     dev = {}
-    for inner in (0.0, 1e-2):
+    for inner in (0.0, 1e-3):
         cfg = R.SolveConfig(eps_sisa=eps, norm="abs", theta=theta, eps_romsad=eps_r, max_iters=500, dsa_inner=inner)
         for m in ("DSA", "ROMSAD"):
             rho, reps = R.sisa_solve(b, m, cfg)
