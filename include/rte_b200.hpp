@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -67,6 +68,133 @@ inline AngularQuadrature chebyshev_legendre(int n_phi, int n_vz) {  // quadratur
   return q;
 }
 
+// ---- problem setup (problem.hpp:10-44, mesh.hpp:12-36) ----------------------
+
+using Params = std::vector<double>;
+using SpatialFn = std::function<double(double, double)>;  // (x, y); y ignored in slab
+using ParamFn = std::function<double(const Params&)>;
+
+// problem.hpp:24-29: sigma_a += psi(mu) absorption_weight(x), sigma_s +=
+// psi(mu) scattering_weight(x); terms[0] must have psi == 1.
+struct CoefficientTerm {
+  ParamFn psi;
+  SpatialFn absorption_weight;
+  SpatialFn scattering_weight;
+  std::string name;
+};
+
+struct ProblemDefinition {  // problem.hpp:31-44
+  int geometry = RTE_SLAB1D;
+  std::vector<CoefficientTerm> terms;
+  SpatialFn source;  // isotropic source G(x)
+  double inflow_left = 0, inflow_right = 0, inflow_bottom = 0, inflow_top = 0;
+  int n_params = 0;
+  std::vector<std::pair<double, double>> param_ranges;
+};
+
+constexpr int kCellRule = 6;  // per-axis Gauss points of the cell rules (transport_system.cpp:18)
+
+struct Mesh {  // mesh.hpp:12-36
+  int geometry = RTE_SLAB1D;
+  std::vector<double> bounds;  // slab boundaries
+  double x0 = 0, x1 = 1, y0 = 0, y1 = 1;
+  int nx = 0, ny = 1;
+
+  static Mesh slab(std::vector<double> b) {
+    if (b.size() < 2) throw std::invalid_argument("slab mesh needs at least one cell");
+    for (size_t i = 1; i < b.size(); ++i)
+      if (!(b[i - 1] < b[i])) throw std::invalid_argument("slab mesh boundaries must be strictly increasing");
+    Mesh m;
+    m.nx = (int)b.size() - 1;
+    m.bounds = std::move(b);
+    return m;
+  }
+  static Mesh slab_uniform(double a, double b, int n) {
+    if (n < 1 || !(a < b)) throw std::invalid_argument("invalid slab mesh");
+    std::vector<double> x(n + 1);
+    for (int i = 0; i <= n; ++i) x[i] = a + (b - a) * i / n;
+    x[n] = b;
+    return slab(std::move(x));
+  }
+  static Mesh rect_uniform(double x0, double x1, int nx, double y0, double y1, int ny) {
+    if (nx < 1 || ny < 1 || !(x0 < x1) || !(y0 < y1)) throw std::invalid_argument("invalid rectangular mesh");
+    Mesh m;
+    m.geometry = RTE_XY2D;
+    m.x0 = x0, m.x1 = x1, m.y0 = y0, m.y1 = y1, m.nx = nx, m.ny = ny;
+    return m;
+  }
+  int cell_count() const { return geometry == RTE_SLAB1D ? nx : nx * ny; }
+  int n_local() const { return geometry == RTE_SLAB1D ? 2 : 4; }
+  long n_dof() const { return (long)cell_count() * n_local(); }
+  int points_per_cell(int nq = kCellRule) const { return geometry == RTE_SLAB1D ? nq : nq * nq; }
+  const double* bounds_ptr() const { return bounds.empty() ? nullptr : bounds.data(); }
+  // Gauss points of every cell's rule, cell-major (rte_cell_points).
+  void cell_points(std::vector<double>& px, std::vector<double>& py, int nq = kCellRule) const {
+    px.assign((size_t)cell_count() * points_per_cell(nq), 0.0);
+    py.assign(px.size(), 0.0);
+    check(rte_cell_points(geometry, nx, ny, bounds_ptr(), x0, x1, y0, y1, nq, px.data(), py.data()), nullptr);
+  }
+  // weighted_mass (transport_system.cpp:17-55) from values at the cell points.
+  std::vector<double> weighted_mass(const std::vector<double>& wvals, int nq = kCellRule) const {
+    std::vector<double> out((size_t)cell_count() * n_local() * n_local());
+    check(rte_weighted_mass(geometry, nx, ny, bounds_ptr(), x0, x1, y0, y1, nq, wvals.data(), out.data()), nullptr);
+    return out;
+  }
+  // project (dg_space.cpp:31-71) from values at the cell points.
+  std::vector<double> project(const std::vector<double>& fvals, int nq = kCellRule) const {
+    std::vector<double> out((size_t)n_dof());
+    check(rte_project(geometry, nx, ny, bounds_ptr(), x0, x1, y0, y1, nq, fvals.data(), out.data()), nullptr);
+    return out;
+  }
+};
+
+namespace detail {
+// Per-cell blocks [cells][nl*nl] -> scalars when every block is d0 I to
+// 1e-12 (the closed-form XY cell solve needs sigma I); false otherwise.
+inline bool scalar_blocks(const std::vector<double>& m, int nl, std::vector<double>& out) {
+  const size_t nb = (size_t)nl * nl, nc = m.size() / nb;
+  out.assign(nc, 0.0);
+  for (size_t c = 0; c < nc; ++c) {
+    const double* f = m.data() + c * nb;
+    const double d0 = f[0];
+    double err = 0.0, scale = 1e-300;
+    for (int i = 0; i < nl; ++i)
+      for (int j = 0; j < nl; ++j) {
+        err = std::max(err, std::fabs(f[i * nl + j] - (i == j ? d0 : 0.0)));
+        if (i == j) scale = std::max(scale, std::fabs(f[i * nl + j]));
+      }
+    if (err > 1e-12 * scale) return false;
+    out[c] = d0;
+  }
+  return true;
+}
+
+// build_masses accumulation (transport_system.cpp:133-138): out_s = sum_k psi_sk term_k, k ascending.
+inline std::vector<double> combine_terms(const std::vector<std::vector<double>>& terms, const std::vector<double>& psi,
+                                         int S) {
+  const int K = (int)terms.size();
+  const size_t n = terms[0].size();
+  std::vector<double> out((size_t)S * n, 0.0);
+  for (int s = 0; s < S; ++s)
+    for (int k = 0; k < K; ++k) {
+      const double p = psi[(size_t)s * K + k];
+      double* o = out.data() + (size_t)s * n;
+      const double* t = terms[k].data();
+      for (size_t e = 0; e < n; ++e) {
+        const double v = p * t[e];
+        o[e] = o[e] + v;
+      }
+    }
+  return out;
+}
+
+inline std::vector<double> flatten(const std::vector<std::vector<double>>& v) {
+  std::vector<double> out;
+  for (const auto& x : v) out.insert(out.end(), x.begin(), x.end());
+  return out;
+}
+}  // namespace detail
+
 // Device buffer of S x n doubles (sample-major).
 class DeviceVector {
  public:
@@ -105,6 +233,93 @@ class TransportBatch {
  public:
   TransportBatch(const rte_problem& p, int device = 0) : n_dirs_(p.n_dirs), device_(device) {
     check(rte_create(&p, device, &ctx_), nullptr);
+  }
+  // The reference constructor (transport_system.cpp:82-109) for a batch of
+  // parameter samples mus: evaluates psi_k(mu) and the coefficient closures
+  // at the 6x6 (slab: 6) Gauss points, forms the per-term mass blocks
+  // (weighted_mass) and the source load vector (project), combines the
+  // samples' blocks in build_masses order and uploads everything.  XY
+  // problems whose blocks are all sigma I per cell use the closed-form cell
+  // solves (per-cell scalars); intra-cell-varying coefficients (or
+  // force_full_blocks) use full 4x4 blocks.  Same inputs, same arithmetic as
+  // rte.TransportBatch (paper_2402_10488_b200/rte.py).
+  TransportBatch(const ProblemDefinition& problem, const Mesh& mesh, const AngularQuadrature& quad,
+                 const std::vector<Params>& mus, int device = 0, bool force_full_blocks = false)
+      : n_dirs_(quad.n()), device_(device) {
+    if (problem.geometry != mesh.geometry || mesh.geometry != quad.geometry)
+      throw std::invalid_argument("transport system: geometry mismatch");
+    if (problem.terms.empty()) throw std::invalid_argument("transport system: no coefficient terms");
+    if (mus.empty()) throw std::invalid_argument("transport system: no parameter samples");
+    const int S = (int)mus.size(), K = (int)problem.terms.size();
+    std::vector<double> psi((size_t)S * K);
+    for (int s = 0; s < S; ++s)
+      for (int k = 0; k < K; ++k) {
+        const auto& t = problem.terms[k];
+        psi[(size_t)s * K + k] = t.psi ? t.psi(mus[s]) : 1.0;
+      }
+    for (int s = 0; s < S; ++s)
+      if (std::abs(psi[(size_t)s * K] - 1.0) > 0)
+        throw std::invalid_argument("transport system: term 0 must be parameter independent (psi == 1)");
+    std::vector<double> px, py;
+    mesh.cell_points(px, py);
+    const size_t np = px.size();
+    std::vector<std::vector<double>> tmt(K), tms(K);
+    std::vector<double> tot(np), sc(np);
+    for (int k = 0; k < K; ++k) {
+      const auto& t = problem.terms[k];
+      for (size_t i = 0; i < np; ++i) {
+        const double a = t.absorption_weight ? t.absorption_weight(px[i], py[i]) : 0.0;
+        sc[i] = t.scattering_weight ? t.scattering_weight(px[i], py[i]) : 0.0;
+        double v = 0.0;  // transport_system.cpp:125-130
+        if (t.absorption_weight) v += a;
+        if (t.scattering_weight) v += sc[i];
+        tot[i] = v;
+      }
+      tmt[k] = mesh.weighted_mass(tot);
+      tms[k] = mesh.weighted_mass(sc);
+    }
+    std::vector<double> g((size_t)mesh.n_dof(), 0.0);
+    if (problem.source) {
+      std::vector<double> f(np);
+      for (size_t i = 0; i < np; ++i) f[i] = problem.source(px[i], py[i]);
+      g = mesh.project(f);
+    }
+    int block = mesh.geometry == RTE_SLAB1D ? 4 : 16;
+    if (mesh.geometry == RTE_XY2D && !force_full_blocks) {
+      std::vector<std::vector<double>> st(K), ss(K);
+      bool scalar = true;
+      for (int k = 0; k < K && scalar; ++k)
+        scalar = detail::scalar_blocks(tmt[k], 4, st[k]) && detail::scalar_blocks(tms[k], 4, ss[k]);
+      if (scalar) {
+        block = 1;
+        tmt = std::move(st);
+        tms = std::move(ss);
+      }
+    }
+    const std::vector<double> mt = detail::combine_terms(tmt, psi, S), ms = detail::combine_terms(tms, psi, S);
+    std::vector<double> dirs;
+    for (const auto& d : quad.directions) dirs.insert(dirs.end(), d.begin(), d.end());
+    rte_problem p{};
+    p.geometry = mesh.geometry;
+    p.nx = mesh.nx;
+    p.ny = std::max(mesh.ny, 1);
+    p.bounds = mesh.bounds_ptr();
+    p.x0 = mesh.x0, p.x1 = mesh.x1, p.y0 = mesh.y0, p.y1 = mesh.y1;
+    p.n_dirs = quad.n();
+    p.dirs = dirs.data();
+    p.weights = quad.weights.data();
+    p.inflow[0] = problem.inflow_left;
+    p.inflow[1] = problem.inflow_right;
+    p.inflow[2] = problem.inflow_bottom;
+    p.inflow[3] = problem.inflow_top;
+    p.n_samples = S;
+    p.block = block;
+    p.mt = mt.data();
+    p.ms = ms.data();
+    p.source = g.data();
+    p.source_shared = 1;
+    check(rte_create(&p, device, &ctx_), nullptr);
+    set_affine(K, detail::flatten(tmt), detail::flatten(tms), psi);
   }
   // Affine decomposition (problem.hpp:24-29): per-term total / scattering
   // mass blocks [K][cells][block] and psi [S][K] with psi[s][0] == 1; needed

@@ -93,3 +93,40 @@ def test_cpp_rom_pipeline_matches_the_python_mirror():
         assert o_rep.iterations == p.iterations and o_rep.correction_log == p.correction_log
         assert rel_l2(rho[s], o_rho) < 1e-8
     assert r["zero_strategy_equals_si"] and r["si_iterations"] > 1  # the C++ CorrectionStrategy plugin point
+
+
+def test_cpp_pin_cell_compiles():
+    assert os.path.exists(build_demo("pin_cell_demo"))
+
+
+@pytest.mark.gpu
+def test_cpp_problem_setup_c4_pin_cell(tmp_path):
+    """BASELINE configs[3] (C4, 128^2 pin cell, CL(16,8), all 64 test samples)
+    set up in C++ from a ProblemDefinition (tests/cpp/pin_cell_demo.cpp:
+    closures, psi, weighted_mass, project, build_masses combination) and
+    solved with SI-DSA: bitwise equal to the Python host mirror's solve of the
+    same parameters, identical iteration counts / logs to the oracle
+    (SuperLU DSA) on the first and last sample with flux within 1e-8."""
+    from paper_2402_10488_b200 import configs, rte
+    from tests.tools import parity_workers as pw
+    exe = build_demo("pin_cell_demo")
+    out = tmp_path / "rho.bin"
+    eps = 1e-8
+    r = json.loads(subprocess.run([exe, "128", "64", repr(eps), str(out)], capture_output=True, text=True,
+                                  check=True).stdout)
+    mus = [s["mu"] for s in r["samples"]]
+    assert len(mus) == 64 and r["k_terms"] == 5
+    rho_cpp = np.fromfile(str(out)).reshape(64, -1)
+    _, test = configs.c4_params(40, 64)
+    np.testing.assert_allclose(np.array(mus), np.array(test), rtol=1e-15, atol=0)
+    mesh = rte.Mesh.rect_uniform(0, 1, 128, 0, 1, 128)
+    b = rte.TransportBatch(configs.pin_cell(rte)(128), mesh, rte.chebyshev_legendre(16, 8), mus)
+    rho_py, reps = rte.sisa_solve(b, "DSA", rte.SolveConfig(eps_sisa=eps, norm="abs", max_iters=500))
+    rho_py = rho_py.cpu().numpy()
+    for s, (c, p) in enumerate(zip(r["samples"], reps)):
+        assert c["converged"] == 1 and c["iterations"] == p.iterations and c["log"] == p.correction_log, s
+    assert np.array_equal(rho_cpp, rho_py)
+    for s in (0, 63):
+        o = pw.solve_sample(("c4", mus[s], ["DSA"], eps, "abs", 3, 0.0, None, None, True))["DSA"]
+        assert r["samples"][s]["iterations"] == o["iterations"] and r["samples"][s]["log"] == o["log"]
+        assert rel_l2(rho_cpp[s], o["rho"]) < 1e-8
