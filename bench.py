@@ -40,7 +40,10 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FLOP_PER_UPDATE = 66      # FP64 instructions of the on-the-fly cell solve (sweep2d.cu)
+# FP64 flops of one on-the-fly cell solve + weighted accumulation (sweep2d.cu
+# solve_cell + the acc update): 8 DADD + 19 DMUL + 44 DFMA (= 2 flops) = 115;
+# the peak it is divided by (rte_probe_dfma) counts 2 flops per DFMA too
+FLOP_PER_UPDATE = 115
 BYTES_PER_UPDATE = 40     # sigma_t + 4 source moments (operand-stream accounting)
 PHI, VZ = 32, 16          # CL(32,16) -> 256 unique (vx, vy) slots
 
@@ -53,7 +56,10 @@ def bench_config(args, slots):
     nx, S = args.nx, args.samples
     return {"workload": "c5_2d_sweep_stress", "cells": "%dx%d" % (nx, nx), "directions_unique": slots,
             "quadrature": "CL(%d,%d) folded" % (PHI, VZ), "samples_per_gpu": S,
-            "dsa": "device BiCGStab+multigrid to rel. residual %g (reference: SuperLU)" % args.dsa_tol,
+            "dsa": ("device BiCGStab+multigrid to rel. residual max(%g, min(0.1, %g * 2^-53 ||rho*|| / ||delta||)) "
+                    "(round-off floor rule, rte_si_config.dsa_floor; reference: SuperLU)" % (args.dsa_tol, args.dsa_floor)
+                    if args.dsa_floor > 0 else
+                    "device BiCGStab+multigrid to rel. residual %g (reference: SuperLU)" % args.dsa_tol),
             "l2": "inputs (%.1f GB per step) exceed the 126 MB L2" % (S * nx * nx * 4 * 8 * 3 / 1e9)}
 
 
@@ -186,13 +192,14 @@ def run_b200(args, rank, world, device):
         dsa_ok = False
     method = "DSA" if dsa_ok else "SI"
 
-    def solve(iters, guess):
+    def solve(iters, guess, floor=args.dsa_floor):
         cfg = rte.SolveConfig(fixed_iters=iters, max_iters=iters, compute_residual=False,
-                              initial_guess=guess, check_every=max(iters, 1))
+                              initial_guess=guess, check_every=max(iters, 1), dsa_floor=floor)
         return rte.sisa_solve(batch, method, cfg)
 
     rho, _ = solve(args.warmup, None)
     torch.cuda.synchronize()
+    rho_start = rho.clone() if (args.dsa_floor > 0 and not args.no_strict) else None
     L.rte_profile_enable(batch._h, 1)
     L.rte_profile_read(batch._h, None, None)
     clocks = Clocks(device)
@@ -212,6 +219,22 @@ def run_b200(args, rank, world, device):
     capi.check(L.rte_profile_read(batch._h, ms_k, n_k), batch._h)
     L.rte_profile_enable(batch._h, 0)
     ms_max = max_over_ranks(ms_total, world, device)
+    # the same K iterations from the same start with every DSA solve to the
+    # strict tolerance: its time, and how far the two final fluxes differ
+    strict = None
+    if rho_start is not None:
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record()
+        rho_s, _ = solve(args.steps, rho_start, floor=0.0)
+        e1.record()
+        torch.cuda.synchronize()
+        ms_s = max_over_ranks(e0.elapsed_time(e1), world, device)
+        rel = ((rho_s - rho).norm(dim=1) / rho_s.norm(dim=1)).max().item()
+        strict = {"ms_per_step": ms_s / args.steps, "value": aggregate_value(upd_step, args.steps, world, ms_s),
+                  "final_flux_max_rel_l2_vs_floor_rule": rel,
+                  "dsa": "every DSA solve to rel. residual %g" % args.dsa_tol}
+        del rho_s, rho_start
     value = aggregate_value(upd_step, args.steps, world, ms_max)
     n_dof = batch.n_dof()
     batch = rho = reps = dsa = None  # release the timed context (~55 GB at C5) before the e2e one
@@ -231,7 +254,7 @@ def run_b200(args, rank, world, device):
         if dsa_ok:
             rte.DsaOperator(b2).set_tolerance(args.dsa_tol, 2000)
         cfg = rte.SolveConfig(fixed_iters=args.steps, max_iters=args.steps, compute_residual=False,
-                              check_every=args.steps)
+                              check_every=args.steps, dsa_floor=args.dsa_floor)
         r2, _ = rte.sisa_solve(b2, method, cfg)
         out_h.copy_(r2)
         torch.cuda.synchronize()
@@ -291,6 +314,7 @@ def run_b200(args, rank, world, device):
         "kernel_launches": {k: int(n_k[i]) for i, k in enumerate(capi.PROF_KINDS)},
         "gpu_launches": gpu_launches,
         "clocks": ck,
+        "strict_dsa": strict,
     }
     if rank == 0 and world == 1 and not args.no_ttt:
         models = {}
@@ -683,6 +707,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)  # configs[4]: a fixed 20 source iterations with DSA
     ap.add_argument("--dsa-tol", type=float, default=1e-8)
+    ap.add_argument("--dsa-floor", type=float, default=1.0,
+                    help="rte_si_config.dsa_floor (0: every DSA solve to --dsa-tol)")
+    ap.add_argument("--no-strict", action="store_true", help="skip the strict-DSA comparison leg")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--nx", type=int, default=1024)

@@ -135,6 +135,11 @@ typedef struct rte_si_config {
                           (rte_dsa_set_tolerance, default 1e-12 relative); c in (0,1):
                           iteration l solves to relative residual max(tol, c * eps / change_l)
                           ("inner tolerance 1e-2 eps_SISA"; ignored with fixed_iters) */
+  double dsa_floor;    /* xy DSA only; c > 0: iteration l also accepts relative residual
+                          min(0.1, c * 2^-53 * ||rho*||_inf / ||rho* - rho||_inf): the accuracy
+                          below which the correction cannot move the iterate by more than about
+                          c ulps of rho* times the correction's gain (round-off floor of the
+                          outer iteration; applies with fixed_iters too).  0: off */
 } rte_si_config;
 
 /* Per-sample outcome of the iterative XY DSA solves (the reference's direct
@@ -353,6 +358,18 @@ int rte_project(int geometry, int nx, int ny, const double* bounds, double x0, d
                 double y1, int nq, const double* fvals, double* out);
 /* cases.cpp:11-13: n unit draws (gen() >> 11) * 2^-53 of std::mt19937_64(seed). */
 int rte_unit_draws(unsigned long long seed, long n, double* out);
+
+/* Bounds checking without compute-sanitizer (not available on the GPU pool).
+ * With RTE_GUARD=1 in the environment every library device allocation is
+ * padded by 4 KB guard zones of 0xFF bytes (its user region starts filled
+ * with the same pattern: NaN as fp64/fp32), so out-of-bounds writes are
+ * counted here and out-of-bounds / uninitialised reads surface as NaN.
+ * rte_guard_check: violations found so far (freed and live buffers) and the
+ * number of guard checks made; RTE_ERR_UNSUPPORTED without RTE_GUARD.
+ * rte_guard_selftest: writes one element past a 10-double allocation (the
+ * check must then report it). */
+int rte_guard_check(long* violations, long* checked);
+int rte_guard_selftest(int device);
 
 #ifdef __cplusplus
 }

@@ -423,6 +423,7 @@ struct SolveConfig {  // solvers.hpp:13-19 (+ batch options)
   int gmres_restart = 25;        // solvers.hpp:16
   double gmres_rel_tol = 1e-11;  // solvers.hpp:17
   double dsa_inner = 0.0;        // xy DSA inner tolerance factor (rte_si_config.dsa_inner)
+  double dsa_floor = 0.0;        // xy DSA round-off floor factor (rte_si_config.dsa_floor)
   rte_correction_fn correct = nullptr;  // RTE_CUSTOM (see the CorrectionStrategy overload of sisa_solve)
   void* correct_user = nullptr;
 };
@@ -448,6 +449,7 @@ inline std::pair<std::vector<double>, std::vector<SolveReport>> sisa_solve(Trans
   rte_si_config cfg{c.method, c.eps_sisa, c.norm, c.max_iters, c.fixed_iters, c.theta, c.eps_romsad,
                     c.initial_guess ? 1 : 0, 1, 4};
   cfg.dsa_inner = c.dsa_inner;
+  cfg.dsa_floor = c.dsa_floor;
   cfg.correct = c.correct;
   cfg.correct_user = c.correct_user;
   const int mi = c.max_iters;  // rte_si_solve rejects fixed_iters > max_iters

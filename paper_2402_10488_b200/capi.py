@@ -53,7 +53,7 @@ class SiConfig(ctypes.Structure):
                 ("max_iters", ctypes.c_int), ("fixed_iters", ctypes.c_int), ("theta", ctypes.c_int),
                 ("eps_romsad", ctypes.c_double), ("use_guess", ctypes.c_int), ("compute_residual", ctypes.c_int),
                 ("check_every", ctypes.c_int), ("correct", CORRECTION_FN), ("correct_user", ctypes.c_void_p),
-                ("dsa_inner", ctypes.c_double)]
+                ("dsa_inner", ctypes.c_double), ("dsa_floor", ctypes.c_double)]
 
 
 class SiReport(ctypes.Structure):
@@ -127,6 +127,8 @@ SIGNATURES = [
     ("rte_project", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, ctypes.c_double, ctypes.c_double,
                                    ctypes.c_double, ctypes.c_double, ctypes.c_int, _dp, _dp]),
     ("rte_unit_draws", ctypes.c_int, [ctypes.c_ulonglong, ctypes.c_long, _dp]),
+    ("rte_guard_check", ctypes.c_int, [ctypes.POINTER(ctypes.c_long), ctypes.POINTER(ctypes.c_long)]),
+    ("rte_guard_selftest", ctypes.c_int, [ctypes.c_int]),
 ]
 
 _lib = None

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <utility>
 
@@ -147,7 +148,14 @@ __global__ void si_decide_kernel(int S, SiState st, int l, rte_si_config cfg) {
   if (kind == KIND_DSA && st.switch_iter[s] < 0) st.switch_iter[s] = l;
   // inner tolerance relative to the outer stop test ("1e-2 eps_SISA"):
   // the correction only has to be accurate to dsa_inner * eps / ||delta||
-  if (st.dsa_tol && kind == KIND_DSA) st.dsa_tol[s] = cfg.dsa_inner * cfg.eps / chn;
+  // and (dsa_floor) to the round-off floor of the iterate: below
+  // 2^-53 ||rho*|| / ||delta|| relative, the correction cannot change rho*
+  // beyond a few ulps times its gain
+  if (st.dsa_tol && kind == KIND_DSA) {
+    double t = (cfg.dsa_inner > 0 && cfg.fixed_iters <= 0) ? cfg.dsa_inner * cfg.eps / chn : 0.0;
+    if (cfg.dsa_floor > 0) t = fmax(t, ch > 0 ? fmin(0.1, cfg.dsa_floor * 0x1p-53 * rm / ch) : 0.1);
+    st.dsa_tol[s] = t;
+  }
   st.kind[s] = kind;
   if (lg) st.log[(long)s * cfg.max_iters + l - 1] = lg;
   const int limit = cfg.fixed_iters > 0 ? cfg.fixed_iters : cfg.max_iters;
@@ -455,6 +463,73 @@ void launch_density_of(int S, int nv, long nd, const double* w, const double* f,
 }  // namespace rte
 
 // ===========================================================================
+
+// ---- guard mode (rte_internal.cuh, RTE_GUARD=1) ------------------------------
+namespace rte {
+namespace guard_detail {
+struct GuardState {
+  std::mutex mu;
+  std::map<void*, size_t> live;  // base -> user bytes
+  long violations = 0, checked = 0;
+  std::string first;
+};
+GuardState& guard_state() {
+  static GuardState* g = new GuardState();  // never destroyed: buffers may be released at exit
+  return *g;
+}
+// 0 if both guard zones of the allocation at base still hold 0xFF bytes
+int guard_zones_bad(void* base, size_t user_bytes) {
+  std::vector<unsigned char> h(kGuardBytes);
+  int bad = 0;
+  const char* zones[2] = {static_cast<char*>(base), static_cast<char*>(base) + kGuardBytes + user_bytes};
+  for (const char* z : zones) {
+    if (cudaMemcpy(h.data(), z, kGuardBytes, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+    for (unsigned char c : h)
+      if (c != 0xFF) {
+        ++bad;
+        break;
+      }
+  }
+  return bad;
+}
+void guard_note(GuardState& g, int bad, size_t bytes) {
+  ++g.checked;
+  if (!bad) return;
+  g.violations += bad;
+  if (g.first.empty()) g.first = "guard zone overwritten next to a " + std::to_string(bytes) + "-byte allocation";
+}
+}  // namespace guard_detail
+using namespace guard_detail;
+
+bool guard_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RTE_GUARD");
+    return e && std::atoi(e) > 0;
+  }();
+  return on;
+}
+void guard_register(void* base, size_t user_bytes) {
+  GuardState& g = guard_state();
+  std::lock_guard<std::mutex> lk(g.mu);
+  g.live[base] = user_bytes;
+}
+void guard_release(void* base) {
+  GuardState& g = guard_state();
+  std::lock_guard<std::mutex> lk(g.mu);
+  auto it = g.live.find(base);
+  if (it == g.live.end()) return;
+  cudaDeviceSynchronize();
+  guard_note(g, guard_zones_bad(base, it->second), it->second);
+  g.live.erase(it);
+}
+}  // namespace rte
+
+namespace rte {
+__global__ void guard_selftest_kernel(double* p, int n) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) p[n] = 1.0;  // one element past the end
+}
+}  // namespace rte
+
 extern "C" {
 
 int rte_create(const rte_problem* p, int device, rte_ctx** out) {
@@ -785,7 +860,9 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
     bits.ensure((size_t)2 * S);
     sst.change_bits = bits.p;
     DBuf<double>& dtol = ctx->si_dsatol;
-    const bool inner = cfg.dsa_inner > 0 && cfg.fixed_iters <= 0 && ctx->geom == RTE_XY2D && need_dsa;
+    RTE_REQUIRE(cfg.dsa_floor >= 0, RTE_ERR_INVALID, "si_solve: dsa_floor must be >= 0");
+    const bool inner = ((cfg.dsa_inner > 0 && cfg.fixed_iters <= 0) || cfg.dsa_floor > 0) && ctx->geom == RTE_XY2D &&
+                       need_dsa;
     if (inner) {
       RTE_REQUIRE(cfg.dsa_inner < 1.0, RTE_ERR_INVALID, "si_solve: dsa_inner must be in [0, 1)");
       dtol.ensure(S);
@@ -1091,6 +1168,32 @@ int rte_unit_draws(unsigned long long seed, long n, double* out) {
   return guarded(nullptr, [&] {
     std::mt19937_64 gen(seed);
     for (long i = 0; i < n; ++i) out[i] = static_cast<double>(gen() >> 11) * 0x1p-53;
+  });
+}
+
+
+int rte_guard_check(long* violations, long* checked) {
+  return guarded(nullptr, [&] {
+    using namespace rte;
+    GuardState& g = guard_state();
+    std::lock_guard<std::mutex> lk(g.mu);
+    if (guard_enabled()) {
+      RTE_CUDA(cudaDeviceSynchronize());
+      for (auto& kv : g.live) guard_note(g, guard_zones_bad(kv.first, kv.second), kv.second);
+    }
+    if (violations) *violations = g.violations;
+    if (checked) *checked = g.checked;
+    RTE_REQUIRE(guard_enabled(), RTE_ERR_UNSUPPORTED, "guard: RTE_GUARD is not set for this process");
+  });
+}
+
+int rte_guard_selftest(int device) {
+  return guarded(nullptr, [&] {
+    DeviceGuard dg(device);
+    rte::DBuf<double> b;
+    b.alloc(10);
+    rte::guard_selftest_kernel<<<1, 32>>>(b.p, 10);
+    RTE_CUDA(cudaDeviceSynchronize());
   });
 }
 

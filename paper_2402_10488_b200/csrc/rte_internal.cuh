@@ -33,6 +33,18 @@ struct Error : std::runtime_error {
     if (!(cond)) throw ::rte::Error((code), (msg)); \
   } while (0)
 
+// Guard mode (RTE_GUARD=1, read once): every device allocation gets a 4 KB
+// guard zone on each side filled with 0xFF bytes (NaN as fp64/fp32, -1 as
+// int) and its user region is filled with the same pattern, so an
+// out-of-bounds write is found by the guard check (rte_guard_check, and at
+// release) and an out-of-bounds or uninitialised read turns into NaN that the
+// parity tests see.  This is the bounds checking the GPU pool allows
+// (compute-sanitizer is not available there).
+constexpr size_t kGuardBytes = 4096;
+bool guard_enabled();
+void guard_register(void* base, size_t user_bytes);
+void guard_release(void* base);
+
 // Owning device buffer.
 template <typename T>
 struct DBuf {
@@ -57,7 +69,15 @@ struct DBuf {
   }
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (guard_enabled()) {
+        char* base = reinterpret_cast<char*>(p) - kGuardBytes;
+        guard_release(base);
+        cudaFree(base);
+      } else {
+        cudaFree(p);
+      }
+    }
     p = nullptr;
     n = 0;
   }
@@ -65,7 +85,17 @@ struct DBuf {
     if (count == n && p) return;
     release();
     if (count == 0) return;
-    RTE_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (guard_enabled()) {
+      char* base = nullptr;
+      const size_t bytes = count * sizeof(T);
+      RTE_CUDA(cudaMalloc(&base, bytes + 2 * kGuardBytes));
+      RTE_CUDA(cudaMemset(base, 0xFF, bytes + 2 * kGuardBytes));
+      RTE_CUDA(cudaDeviceSynchronize());
+      guard_register(base, bytes);
+      p = reinterpret_cast<T*>(base + kGuardBytes);
+    } else {
+      RTE_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
     n = count;
   }
   // grow-only variant for per-context scratch reused across calls

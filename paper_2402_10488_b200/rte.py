@@ -607,6 +607,7 @@ class SolveConfig:
     gmres_restart: int = 25       # solvers.hpp:16
     gmres_rel_tol: float = 1e-11  # solvers.hpp:17
     dsa_inner: float = 0.0        # xy DSA: 0 = DSA tolerance; c > 0: relative c * eps / change per iteration
+    dsa_floor: float = 0.0        # xy DSA: c > 0: relative min(0.1, c u ||rho*|| / ||delta||) per iteration (round-off floor)
 
 
 @dataclass
@@ -687,12 +688,15 @@ def si_config(config: SolveConfig, method_code: int, callback=None) -> "capi.SiC
         raise ValueError("solve config: fixed_iters must not exceed max_iters")
     if not 0.0 <= config.dsa_inner < 1.0:
         raise ValueError("solve config: dsa_inner must be in [0, 1)")
+    if not config.dsa_floor >= 0.0:
+        raise ValueError("solve config: dsa_floor must be >= 0")
     return capi.SiConfig(method_code, float(config.eps_sisa),
                          capi.RTE_NORM_REL if config.norm == "rel" else capi.RTE_NORM_ABS,
                          int(config.max_iters), int(config.fixed_iters), int(config.theta),
                          float(config.eps_romsad), 1 if config.initial_guess is not None else 0,
                          1 if config.compute_residual else 0, int(config.check_every),
-                         callback if callback is not None else capi.CORRECTION_FN(), None, float(config.dsa_inner))
+                         callback if callback is not None else capi.CORRECTION_FN(), None, float(config.dsa_inner),
+                         float(config.dsa_floor))
 
 
 def sisa_solve(batch: TransportBatch, method, config: SolveConfig):

@@ -28,3 +28,18 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Guard mode (RTE_GUARD=1, tests/test_gpu_guard.py): record the library's
+    guard-zone check over every allocation made by this session."""
+    path = os.environ.get("RTE_GUARD_REPORT")
+    if not path or not os.environ.get("RTE_GUARD"):
+        return
+    import ctypes
+    import json
+    from paper_2402_10488_b200 import capi
+    v, c = ctypes.c_long(), ctypes.c_long()
+    rc = capi.load().rte_guard_check(ctypes.byref(v), ctypes.byref(c))
+    with open(path, "w") as f:
+        json.dump({"rc": rc, "violations": v.value, "checked": c.value, "exitstatus": int(exitstatus)}, f)
