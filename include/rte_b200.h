@@ -292,7 +292,9 @@ int rte_romig(rte_ctx* ctx, double* rho0_dev, int* status_host, void* stream);
  * are masked.  rho_dev [S][n_dof] holds the guess on entry (use_guess) and
  * the solution on exit.  reports_host[S]; history_host [S][max_iters] (change
  * per iteration, may be NULL); log_host [S][max_iters] correction kinds
- * 'D','R','S' or 0 (may be NULL).  fixed_iters > max_iters is RTE_ERR_INVALID.
+ * 'D','R','S' or 0 (may be NULL).  Of each row only the first W entries are
+ * written (W = the largest iteration count of the batch; entries past a
+ * sample's own count are 0); the rest is left untouched.  fixed_iters > max_iters is RTE_ERR_INVALID.
  * A DSA correction that ends above its tolerance (rte_dsa_status) fills the
  * reports and returns RTE_ERR_RUNTIME (dsa.cpp:269-271 throws). */
 int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg, double* rho_dev, rte_si_report* reports_host,

@@ -19,7 +19,7 @@ BUILD = os.path.join(HERE, "_build") if not os.environ.get("RTE_BUILD_OUT") else
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
-SOURCES = ["capi.cu", "sweep1d.cu", "sweep2d.cu", "dsa1d.cu", "dsa2d.cu", "rom.cu", "kinetic.cu", "pod.cu", "gmres.cu", "setup.cpp"]
+SOURCES = ["capi.cu", "sweep1d.cu", "si1d.cu", "sweep2d.cu", "dsa1d.cu", "dsa2d.cu", "rom.cu", "kinetic.cu", "pod.cu", "gmres.cu", "setup.cpp"]
 
 
 def _stale(obj, deps):
@@ -32,8 +32,8 @@ def _stale(obj, deps):
 def _compile(src, force):
     path = os.path.join(CSRC, src)
     obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
-    deps = [path, os.path.join(CSRC, "rte_internal.cuh"),
-            os.path.join(os.path.dirname(HERE), "include", "rte_b200.h")]
+    deps = [path, os.path.join(os.path.dirname(HERE), "include", "rte_b200.h")] + \
+        [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     if not force and not _stale(obj, deps):
         return obj, ""
     omp = ["-Xcompiler", "-fopenmp"] if src.endswith(".cpp") else []  # host setup helpers

@@ -3,6 +3,7 @@
 // (sisa.cpp:14-54 for S samples at once) and small bookkeeping kernels.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -176,6 +177,16 @@ __global__ void si_custom_kinds_kernel(int S, SiState st, int l, int max_iters, 
   }
   st.log[(long)s * max_iters + l - 1] = c;
   if (c == 'D' && st.switch_iter[s] < 0) st.switch_iter[s] = l;
+}
+
+// rows [S][stride] -> packed [S][width] (history and log of rte_si_solve)
+__global__ void compact_rows_kernel(int S, int stride, int width, const double* __restrict__ hist,
+                                    double* __restrict__ hc, const char* __restrict__ lg, char* __restrict__ lc) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)S * width) return;
+  const long s = t / width, l = t - s * width;
+  hc[t] = hist[s * stride + l];
+  lc[t] = lg[s * stride + l];
 }
 
 __global__ void si_finalize_kernel(int S, long nd, const int* __restrict__ kind, const double* __restrict__ rho_star,
@@ -371,6 +382,9 @@ static void transport_apply_ex(rte_ctx* ctx, int mode, int single, const double*
     a.rho_prev = rho_prev;
     a.delta = delta;
     a.change_bits = change_bits;
+    slab_cache_ensure(ctx, st);
+    a.cache = ctx->slab_cache.p;
+    a.cache_sc = ctx->slab_sc.p;
     ProfScope ps(ctx, RTE_PROF_SWEEP, st);
     launch_sweep1d(a, st);
     return;
@@ -611,6 +625,7 @@ void rte_destroy(rte_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
   if (ctx->pinned_int) cudaFreeHost(ctx->pinned_int);
+  if (ctx->pinned_hist) cudaFreeHost(ctx->pinned_hist);
   delete ctx;
 }
 
@@ -908,7 +923,58 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
     if (!ctx->pinned_int) RTE_CUDA(cudaMallocHost(&ctx->pinned_int, sizeof(int)));
     int* n_active_host = ctx->pinned_int;
     const int fin_bx = (int)std::min<long>((nd + 255) / 256, std::max(1, 8192 / S));
-    int l = 1;
+    // slab: the whole loop in one launch (si1d.cu) when a sample fits one CTA
+    static const bool fuse1d = [] {
+      const char* e = std::getenv("RTE_SI1D_FUSED");
+      return !e || std::atoi(e) != 0;
+    }();
+    bool fused = false;
+    if (fuse1d && ctx->geom == RTE_SLAB1D && cfg.method != RTE_CUSTOM) {
+      Si1DArgs fa{};
+      Sweep1DArgs& a = fa.sw;
+      a.S = S;
+      a.N = ctx->ncells;
+      a.nv = ctx->nv;
+      a.ndof = nd;
+      a.width = ctx->width.p;
+      a.vx = ctx->dvx.p;
+      a.w = ctx->dw.p;
+      a.block = ctx->block;
+      a.mt = ctx->mt.p;
+      a.ms = ctx->ms.p;
+      a.g = ctx->g.p;
+      a.g_shared = ctx->g_shared;
+      a.inflow_l = ctx->inflow[0];
+      a.inflow_r = ctx->inflow[1];
+      a.mode = SRC_MS_RHO | SRC_G | SRC_BC;
+      a.j_single = -1;
+      slab_cache_ensure(ctx, st);
+      a.cache = ctx->slab_cache.p;
+      a.cache_sc = ctx->slab_sc.p;
+      fa.st = sst;
+      fa.cfg = cfg;
+      fa.rho = rho;
+      fa.fac = need_dsa ? ctx->dsa->fac_c.p : nullptr;
+      if (need_rom) rom_fill_si1d(ctx, fa);
+      static const bool clk = std::getenv("RTE_SI1D_CLOCKS") != nullptr;  // development: phase clocks
+      DBuf<long long> pc;
+      if (clk) {
+        pc.alloc(4);
+        pc.zero(st);
+        fa.phase_clk = pc.p;
+      }
+      {
+        ProfScope ps(ctx, RTE_PROF_OTHER, st, 1);
+        fused = si1d_fused(fa, st);
+      }
+      if (clk && fused) {
+        long long h[4];
+        RTE_CUDA(cudaMemcpy(h, pc.p, sizeof(h), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "[si1d] sample 0 clocks: sweep %lld, epilogue+decide %lld, correction %lld, total %lld\n",
+                     h[0], h[1], h[2], h[3]);
+      }
+    }
+    int l = fused ? cfg.max_iters + 1 : 1;
     try {
       for (; l <= cfg.max_iters; ++l) {
         bits.zero(st);
@@ -992,8 +1058,37 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
         r.dsa_status = dstat[s];
       }
     }
-    if (history) RTE_CUDA(cudaMemcpy(history, hist.p, sizeof(double) * S * cfg.max_iters, cudaMemcpyDeviceToHost));
-    if (log) RTE_CUDA(cudaMemcpy(log, lg.p, (size_t)S * cfg.max_iters, cudaMemcpyDeviceToHost));
+    // history / log rows: only the first `width` entries (the batch's largest
+    // iteration count) are copied, packed, through pinned staging
+    int width = 0;
+    for (int s = 0; s < S; ++s) width = std::max(width, hi[S + s]);
+    if ((history || log) && width > 0) {
+      const size_t nh = (size_t)S * width;
+      DBuf<double>& hc = ctx->si_hist_c;
+      DBuf<char>& lc = ctx->si_log_c;
+      hc.ensure(nh);
+      lc.ensure(nh);
+      compact_rows_kernel<<<(unsigned)((nh + 255) / 256), 256, 0, st>>>(S, cfg.max_iters, width, hist.p, hc.p, lg.p,
+                                                                          lc.p);
+      RTE_CUDA(cudaGetLastError());
+      const size_t need = nh * (sizeof(double) + 1);
+      if (ctx->pinned_hist_bytes < need) {
+        if (ctx->pinned_hist) cudaFreeHost(ctx->pinned_hist);
+        ctx->pinned_hist = nullptr;
+        ctx->pinned_hist_bytes = 0;
+        RTE_CUDA(cudaMallocHost(&ctx->pinned_hist, need));
+        ctx->pinned_hist_bytes = need;
+      }
+      double* hh = reinterpret_cast<double*>(ctx->pinned_hist);
+      char* lh = reinterpret_cast<char*>(hh + nh);
+      RTE_CUDA(cudaMemcpyAsync(hh, hc.p, sizeof(double) * nh, cudaMemcpyDeviceToHost, st));
+      RTE_CUDA(cudaMemcpyAsync(lh, lc.p, nh, cudaMemcpyDeviceToHost, st));
+      RTE_CUDA(cudaStreamSynchronize(st));
+      for (int s = 0; s < S; ++s) {
+        if (history) std::memcpy(history + (size_t)s * cfg.max_iters, hh + (size_t)s * width, sizeof(double) * width);
+        if (log) std::memcpy(log + (size_t)s * cfg.max_iters, lh + (size_t)s * width, width);
+      }
+    }
     if (need_dsa) dsa_status_check(ctx, st, "si_solve: DSA correction");
   });
 }

@@ -20,8 +20,10 @@
 // ones; each correction is then log2 N forward rhs-reduction levels and log2 N
 // back-substitution levels, every level parallel over its equations.
 #include "rte_internal.cuh"
+#include "slab_dev.cuh"
 
 namespace rte {
+using namespace slab;
 
 namespace {
 
@@ -155,29 +157,6 @@ __device__ void cell_blocks(const Dsa1DArgs& a, int s, int i, double* D, double*
   }
 }
 
-constexpr int kCrThreads = 256;
-
-// level sizes of the reduction: n_0 = N, n_{l+1} = ceil(n_l / 2) until 1
-__host__ __device__ inline int cr_levels(int N) {
-  int l = 0;
-  for (int n = N; n > 1; n = (n + 1) / 2) ++l;
-  return l;
-}
-__host__ __device__ inline long cr_entries(int N) {  // sum of n_l over all levels incl. the last (1)
-  long t = 0;
-  int n = N;
-  for (;;) {
-    t += n;
-    if (n == 1) break;
-    n = (n + 1) / 2;
-  }
-  return t;
-}
-
-__device__ inline void mv4(const double* m, const double* x, double* y) {
-  for (int r = 0; r < 4; ++r) y[r] = m[4 * r] * x[0] + m[4 * r + 1] * x[1] + m[4 * r + 2] * x[2] + m[4 * r + 3] * x[3];
-}
-
 // Block cyclic reduction setup, one CTA per sample.  work: [S][2][N][48]
 // ping-pong of the current level's (D, L, U) per position; fac: per level l
 // and position p (offset off_l + p): odd p -> (D^{-1}, L, U), even p ->
@@ -253,6 +232,29 @@ __global__ void __launch_bounds__(kCrThreads) dsa1d_factor_cr(const Dsa1DArgs a,
   if (threadIdx.x == 0) inv4(cur, fac + off * 48);
 }
 
+// Interleaved factor table -> compact component-major layout (slab_dev.cuh
+// crc_*), one CTA per sample.
+__global__ void dsa1d_repack_kernel(int N, const double* __restrict__ fac, double* __restrict__ fc) {
+  const int s = blockIdx.x;
+  const double* f = fac + (long)s * cr_entries(N) * 48;
+  double* o = fc + (long)s * crc_doubles(N);
+  long off = 0, co = 0;
+  for (int n = N; n > 1; n = (n + 1) / 2) {
+    const int ne = (n + 1) / 2, no = n / 2;
+    for (int t = threadIdx.x; t < ne * 32; t += blockDim.x) {
+      const int c = t / ne, m = t - c * ne;  // component c of kept equation p = 2m
+      o[co + t] = f[(off + 2 * m) * 48 + c];
+    }
+    for (int t = threadIdx.x; t < no * 48; t += blockDim.x) {
+      const int c = t / no, m = t - c * no;  // component c of eliminated equation p = 2m + 1
+      o[co + (long)ne * 32 + t] = f[(off + 2 * m + 1) * 48 + c];
+    }
+    off += n;
+    co += crc_level_size(n);
+  }
+  for (int t = threadIdx.x; t < 16; t += blockDim.x) o[co + t] = f[off * 48 + t];
+}
+
 struct Dsa1DSolve {
   int S, N, block;
   const double* fac;
@@ -295,63 +297,7 @@ __global__ void __launch_bounds__(kCrThreads) dsa1d_solve_cr(const Dsa1DSolve a)
     y[4 * i + 3] = 0.0;
   }
   __syncthreads();
-  // forward: at level l (stride st) kept equation p (index p*st) absorbs its odd neighbours
-  long off = 0;
-  int st = 1, L = 0;
-  for (int n = N; n > 1; n = (n + 1) / 2, st *= 2, ++L) {
-    const double* f = fac + off * 48;
-    for (int p = 2 * threadIdx.x; p < n; p += 2 * blockDim.x) {
-      const double* e = f + (long)p * 48;
-      double v[4], t[4];
-      for (int k = 0; k < 4; ++k) v[k] = y[4L * p * st + k];
-      if (p >= 1) {
-        mv4(e, y + 4L * (p - 1) * st, t);
-        for (int k = 0; k < 4; ++k) v[k] -= t[k];
-      }
-      if (p + 1 < n) {
-        mv4(e + 16, y + 4L * (p + 1) * st, t);
-        for (int k = 0; k < 4; ++k) v[k] -= t[k];
-      }
-      for (int k = 0; k < 4; ++k) y[4L * p * st + k] = v[k];
-    }
-    __syncthreads();
-    off += n;
-  }
-  if (threadIdx.x == 0) {
-    double t[4];
-    mv4(fac + off * 48, y, t);
-    for (int k = 0; k < 4; ++k) y[k] = t[k];
-  }
-  __syncthreads();
-  // backward: odd equations of each level from the top, x = D^{-1} (y - L x_{p-1} - U x_{p+1})
-  int ns[32];
-  {
-    int n = N, l = 0;
-    while (n > 1) {
-      ns[l++] = n;
-      n = (n + 1) / 2;
-    }
-  }
-  for (int l = L - 1; l >= 0; --l) {
-    const int n = ns[l];
-    const int stl = 1 << l;
-    off -= n;
-    const double* f = fac + off * 48;
-    for (int p = 1 + 2 * threadIdx.x; p < n; p += 2 * blockDim.x) {
-      const double* e = f + (long)p * 48;
-      double v[4], t[4];
-      for (int k = 0; k < 4; ++k) v[k] = y[4L * p * stl + k];
-      mv4(e + 16, y + 4L * (p - 1) * stl, t);
-      for (int k = 0; k < 4; ++k) v[k] -= t[k];
-      if (p + 1 < n) {
-        mv4(e + 32, y + 4L * (p + 1) * stl, t);
-        for (int k = 0; k < 4; ++k) v[k] -= t[k];
-      }
-      mv4(e, v, t);
-      for (int k = 0; k < 4; ++k) y[4L * p * stl + k] = t[k];
-    }
-    __syncthreads();
-  }
+  cr_solve_cta(N, fac, y);
   for (int i = threadIdx.x; i < N && !a.prepared; i += blockDim.x) {
     a.out[(long)s * nd + 2 * i] = y[4 * i];
     a.out[(long)s * nd + 2 * i + 1] = y[4 * i + 1];
@@ -432,6 +378,9 @@ void dsa_setup(rte_ctx* ctx, cudaStream_t st) {
   DBuf<double> work;
   work.alloc((size_t)ctx->S * 2 * ctx->ncells * 48);
   dsa1d_factor_cr<<<ctx->S, kCrThreads, 0, st>>>(a, work.p);
+  RTE_CUDA(cudaGetLastError());
+  d->fac_c.alloc((size_t)ctx->S * crc_doubles(ctx->ncells));
+  dsa1d_repack_kernel<<<ctx->S, 256, 0, st>>>(ctx->ncells, d->fac.p, d->fac_c.p);
   RTE_CUDA(cudaGetLastError());
   RTE_CUDA(cudaStreamSynchronize(st));
 }

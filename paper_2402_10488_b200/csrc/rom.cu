@@ -9,6 +9,7 @@
 //   rhs_r = U_iso^T (Ms delta),  c = A_r^{-1} rhs_r,  corr = U_rho c,
 // done by one CTA per sample with fixed-order block reductions.
 #include "rte_internal.cuh"
+#include "slab_dev.cuh"
 
 namespace rte {
 
@@ -22,6 +23,7 @@ struct RomState {
 };
 
 namespace {
+using namespace slab;
 
 // Complete-pivoting LU of the r x r row-major matrix in place.
 __device__ int fullpiv_lu(double* a, int r, int* rp, int* cp) {
@@ -82,21 +84,6 @@ __device__ int fullpiv_lu(double* a, int r, int* rp, int* cp) {
   return rank;
 }
 
-__device__ void fullpiv_solve(const double* a, int r, const int* rp, const int* cp, const double* b, double* y,
-                              double* x) {
-  for (int i = 0; i < r; ++i) {
-    double t = b[rp[i]];
-    for (int k = 0; k < i; ++k) t -= a[i * r + k] * y[k];
-    y[i] = t;
-  }
-  for (int i = r - 1; i >= 0; --i) {
-    double t = y[i];
-    for (int k = i + 1; k < r; ++k) t -= a[i * r + k] * y[k];
-    y[i] = t / a[i * r + i];
-  }
-  for (int i = 0; i < r; ++i) x[cp[i]] = y[i];
-}
-
 // A(mu_s) = sum_k psi_k a_r[k] (reduced_model.cpp:32-39), row-major.
 __device__ void assemble(const double* a_r, const double* psi, int r, int K, double* out) {
   for (int i = 0; i < r; ++i)
@@ -117,47 +104,6 @@ __global__ void rom_factor_kernel(int S, int r, int K, const double* a_r, const 
   sing[s] = rank < r ? 1 : 0;
 }
 
-template <int CH>
-__device__ void block_dots(const double* u, long nd, int r, const double* v_smem_or_null, const double* ms,
-                           int block, int N, const double* delta, int s, double* out_smem, double* red) {
-  // out[k] = sum_i u[k*nd + i] * (Ms delta)_i, fixed-order reduction
-  for (int k0 = 0; k0 < r; k0 += CH) {
-    double acc[CH];
-#pragma unroll
-    for (int c = 0; c < CH; ++c) acc[c] = 0.0;
-    for (long i = threadIdx.x; i < nd; i += blockDim.x) {
-      double m;
-      const double* d = delta + (long)s * nd;
-      const int nl = (int)(nd / N);
-      if (block == nl * nl) {  // full per-cell block (1D block 4, XY block 16)
-        const long c = i / nl;
-        const int rr = (int)(i - c * nl);
-        const double* mm = ms + ((long)s * N + c) * block + nl * rr;
-        m = 0.0;
-        for (int q = 0; q < nl; ++q) m = fma(mm[q], d[nl * c + q], m);
-      } else {
-        m = ms[(long)s * N + i / nl] * d[i];
-      }
-#pragma unroll
-      for (int c = 0; c < CH; ++c)
-        if (k0 + c < r) acc[c] = fma(u[(long)(k0 + c) * nd + i], m, acc[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      double v = acc[c];
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if ((threadIdx.x & 31) == 0) red[(threadIdx.x >> 5) * CH + c] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < CH && k0 + (int)threadIdx.x < r) {
-      double t = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w * CH + threadIdx.x];
-      out_smem[k0 + threadIdx.x] = t;
-    }
-    __syncthreads();
-  }
-}
-
 struct RomCorrectArgs {
   int S, r, N, block;
   long nd;
@@ -176,7 +122,7 @@ __global__ void rom_correct_kernel(const RomCorrectArgs a) {
   __shared__ double rhs[128], y[128], c[128], red[32 * 8];
   const int s = blockIdx.x;
   if (a.kind[s] != KIND_ROMSA) return;
-  block_dots<8>(a.u_iso, a.nd, a.r, nullptr, a.ms, a.block, a.N, a.delta, s, rhs, red);
+  block_dots<8>(a.u_iso, a.nd, a.r, nullptr, a.ms, a.block, a.N, a.delta + (long)s * a.nd, s, rhs, red);
   if (threadIdx.x == 0)
     fullpiv_solve(a.lu + (long)s * a.r * a.r, a.r, a.rp + (long)s * a.r, a.cp + (long)s * a.r, rhs, y, c);
   __syncthreads();
@@ -298,6 +244,17 @@ void rom_correct(rte_ctx* ctx, const double* delta, double* corr, const int* kin
                    m->cp.p, ctx->ms.p, delta, corr, kind};
   rom_correct_kernel<<<ctx->S, 256, 0, st>>>(a);
   RTE_CUDA(cudaGetLastError());
+}
+
+void rom_fill_si1d(rte_ctx* ctx, Si1DArgs& a) {
+  RomState* m = ctx->rom[1];
+  RTE_REQUIRE(m && m->factored, RTE_ERR_INVALID, "rom: correction model not set up");
+  a.r = m->r;
+  a.u_rho = m->u_rho.p;
+  a.u_iso = m->u_iso.p;
+  a.lu = m->lu.p;
+  a.rp = m->rp.p;
+  a.cp = m->cp.p;
 }
 
 void romig(rte_ctx* ctx, double* rho0, int* status_dev, cudaStream_t st) {

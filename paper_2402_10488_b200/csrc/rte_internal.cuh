@@ -137,6 +137,7 @@ struct DsaState {
   long dim = 0;
   double m1 = 0, m2 = 0, m3 = 0;
   DBuf<double> fac;         // slab: [S][sum of CR level sizes][48] block cyclic reduction factors
+  DBuf<double> fac_c;       // slab: the same factors in the compact layout (slab_dev.cuh crc_*), fused SI
   DBuf<double> fac_t;       // slab: CR factors of the current block T (apply_eliminated, lazy)
   void* impl2d = nullptr;   // xy: multigrid/Krylov state (dsa2d.cu)
 };
@@ -159,6 +160,8 @@ struct rte_ctx {
 
   // device problem data
   rte::DBuf<double> width;   // slab widths [N]
+  rte::DBuf<double> slab_cache, slab_sc;  // slab sweep cache (Sweep1DArgs::cache)
+  bool slab_cache_tried = false;
   rte::DBuf<double> dvx, dw; // slab directions [nv]
   rte::DBuf<double> mt, ms;  // [S][cells][block]
   rte::DBuf<double> g;       // [S or 1][ndof]
@@ -177,8 +180,12 @@ struct rte_ctx {
   rte::DBuf<int> si_ibuf, si_int;
   rte::DBuf<double> si_hist, si_lastc, si_dsatol;
   rte::DBuf<char> si_log, si_letters;
+  rte::DBuf<double> si_hist_c;  // packed history rows (rte_si_solve readback)
+  rte::DBuf<char> si_log_c;
   rte::DBuf<unsigned long long> si_bits;
   int* pinned_int = nullptr;  // cudaMallocHost, one int for the active-count poll
+  void* pinned_hist = nullptr;  // cudaMallocHost staging of the packed SI history / log
+  size_t pinned_hist_bytes = 0;
   // PGMRES scratch reused across rte_gmres_solve calls (grow-only)
   rte::DBuf<double> gm_d[15];
   rte::DBuf<int> gm_i[4];
@@ -263,8 +270,18 @@ struct Sweep1DArgs {
   const double* rho_prev;
   double* delta;
   unsigned long long* change_bits;  // [S][2]
+  // per-context sweep cache (slab_cache_ensure; null: cell blocks on the fly):
+  // cache [S][nv][5][32 * CPL] = B^-1 (4) and the trace gain beta of the cell at
+  // sweep position p = lane * CPL + k stored at k * 32 + lane; cache_sc [N] = h^-1/2
+  const double* cache;
+  const double* cache_sc;
 };
 void launch_sweep1d(const Sweep1DArgs& a, cudaStream_t st);
+int sweep1d_cpl(int N);  // cells per lane of the slab sweep (0: unsupported)
+// Builds the slab sweep cache once per context (the reference's per-slot
+// inverse cache, build_sweep_cache transport_system.cpp:189-227, plus the
+// trace gains); leaves it empty when it would exceed the memory budget.
+void slab_cache_ensure(rte_ctx* ctx, cudaStream_t st);
 
 struct Sweep2DArgs {
   int S, nx, ny;
@@ -319,6 +336,27 @@ void launch_si_finalize(int S, long ndof, const SiState& st, const double* rho_s
                         double* rho, cudaStream_t s);
 void launch_residual(int S, long ndof, const double* rho, const double* rho_star, double* resid,
                      cudaStream_t s);
+
+// Fused slab SI loop (si1d.cu): one CTA per sample runs every iteration of
+// rte_si_solve (sweep, stop test / strategy choice, DSA or ROMSA correction)
+// with its state in shared memory.
+struct Si1DArgs {
+  Sweep1DArgs sw;  // mode SRC_MS_RHO | SRC_G | SRC_BC; rho is read from shared memory
+  SiState st;
+  rte_si_config cfg;
+  double* rho;        // [S][ndof] initial guess in, solution out
+  const double* fac;  // [S][crc_doubles(N)] DSA factors, compact layout (null: no DSA)
+  // ROMSA correction model (r = 0: none)
+  int r;
+  const double* u_rho;
+  const double* u_iso;
+  const double* lu;
+  const int* rp;
+  const int* cp;
+  long long* phase_clk;  // optional [4]: summed SM clocks of sample 0's sweep / decide / correction / total
+};
+bool si1d_fused(const Si1DArgs& a, cudaStream_t st);  // false: does not fit one CTA
+void rom_fill_si1d(rte_ctx* ctx, Si1DArgs& a);          // the correction model's device arrays
 
 // DSA
 void dsa_setup(rte_ctx* ctx, cudaStream_t st);

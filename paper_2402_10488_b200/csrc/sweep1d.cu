@@ -21,170 +21,33 @@
 // rho = sum_j w_j f_j is accumulated in shared memory in the fixed order
 // j = 0..n-1 (deterministic, like transport_system.cpp:398-401).
 #include "rte_internal.cuh"
+#include "slab_dev.cuh"
 
 namespace rte {
 namespace {
-
-__device__ __forceinline__ void cell_block(const Sweep1DArgs& a, int s, int i, double v, double* binv) {
-  const double h = a.width[i];
-  double b0, b1, b2, b3;
-  // streaming_block_1d (transport_system.cpp:74-78): v>0: v(E_R - S), else v(-E_L - S)
-  if (v > 0) {
-    b0 = v * (1.0 / h);
-    b1 = v * (kSqrt3 / h);
-    b2 = v * (kSqrt3 / h - 2.0 * kSqrt3 / h);
-    b3 = v * (3.0 / h);
-  } else {
-    b0 = v * (-(1.0 / h));
-    b1 = v * (kSqrt3 / h);
-    b2 = v * (kSqrt3 / h - 2.0 * kSqrt3 / h);
-    b3 = v * (-(3.0 / h));
-  }
-  if (a.block == 4) {
-    const double* m = a.mt + ((long)s * a.N + i) * 4;
-    b0 += m[0];
-    b1 += m[1];
-    b2 += m[2];
-    b3 += m[3];
-  } else {
-    const double sg = a.mt[(long)s * a.N + i];
-    b0 += sg;
-    b3 += sg;
-  }
-  const double id = 1.0 / (b0 * b3 - b2 * b1);
-  binv[0] = b3 * id;
-  binv[1] = -b1 * id;
-  binv[2] = -b2 * id;
-  binv[3] = b0 * id;
-}
+using namespace slab;
 
 __device__ __forceinline__ unsigned long long dbits(double x) {
   return (unsigned long long)__double_as_longlong(x);
 }
 
-template <int CPL>
-__global__ void __launch_bounds__(512) sweep1d_kernel(const Sweep1DArgs a) {
+template <int CPL, bool CACHED>
+__global__ void __launch_bounds__(256) sweep1d_kernel(const Sweep1DArgs a) {
   extern __shared__ double sm[];
   const int s = blockIdx.x;
   if (a.active && !a.active[s]) return;
-  const int N = a.N;
   const long nd = a.ndof;
+  constexpr int NV = 2 * 32 * CPL;  // lane-major vector length (slab_dev.cuh)
   double* q = sm;
-  double* acc = sm + nd;
-  double* stage = sm + 2 * nd;
-  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // ---- source q (apply_Ms + G, or the raw rhs) ----
-  for (long i = threadIdx.x; i < nd; i += blockDim.x) {
-    double v = 0.0;
-    const long si = (long)s * nd + i;
-    if (a.mode & SRC_RAW) {
-      v = a.rho[si];
-    } else {
-      if (a.mode & SRC_MS_RHO) {
-        const long c = i >> 1;
-        const int r = (int)(i & 1);
-        if (a.block == 4) {
-          const double* m = a.ms + ((long)s * N + c) * 4 + 2 * r;
-          v = m[0] * a.rho[(long)s * nd + 2 * c] + m[1] * a.rho[(long)s * nd + 2 * c + 1];
-        } else {
-          v = a.ms[(long)s * N + c] * a.rho[si];
-        }
-      }
-      if (a.mode & SRC_G) v += a.g[(a.g_shared ? 0 : (long)s * nd) + i];
-    }
-    q[i] = v;
-    acc[i] = 0.0;
-  }
-  __syncthreads();
-
-  const int jlo = a.j_single >= 0 ? a.j_single : 0;
-  const int jn = a.j_single >= 0 ? 1 : a.nv;
-  for (int r0 = 0; r0 < jn; r0 += nw) {
-    const int jj = r0 + warp;
-    if (jj < jn) {
-      const int j = jlo + jj;
-      const double v = a.vx[j];
-      const double c = fabs(v);
-      const bool fwd = v > 0;
-      double u0 = 0.0;
-      if (a.mode & SRC_BC) u0 = fwd ? a.inflow_l : a.inflow_r;
-      // pass 1: compose the lane's affine maps u -> A + B u
-      double A = 0.0, B = 1.0;
-      for (int k = 0; k < CPL; ++k) {
-        const int p = lane * CPL + k;
-        if (p < N) {
-          const int i = fwd ? p : N - 1 - p;
-          double bi[4];
-          cell_block(a, s, i, v, bi);
-          const double sc = 1.0 / sqrt(a.width[i]);
-          const double tin0 = sc, tin1 = fwd ? -kSqrt3 * sc : kSqrt3 * sc;
-          const double tout0 = sc, tout1 = fwd ? kSqrt3 * sc : -kSqrt3 * sc;
-          const double r0v = q[2 * i], r1v = q[2 * i + 1];
-          const double y0 = bi[0] * r0v + bi[1] * r1v, y1 = bi[2] * r0v + bi[3] * r1v;
-          const double z0 = bi[0] * tin0 + bi[1] * tin1, z1 = bi[2] * tin0 + bi[3] * tin1;
-          const double al = tout0 * y0 + tout1 * y1;
-          const double be = c * (tout0 * z0 + tout1 * z1);
-          A = al + be * A;
-          B = be * B;
-        }
-      }
-      // inclusive warp scan of the affine maps
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const double Ap = __shfl_up_sync(0xffffffffu, A, d);
-        const double Bp = __shfl_up_sync(0xffffffffu, B, d);
-        if (lane >= d) {
-          A = A + B * Ap;
-          B = B * Bp;
-        }
-      }
-      const double Ae = __shfl_up_sync(0xffffffffu, A, 1);
-      const double Be = __shfl_up_sync(0xffffffffu, B, 1);
-      double u = lane == 0 ? u0 : Ae + Be * u0;
-      // pass 2: cell solves with the exact incoming trace
-      double* st = stage + (long)warp * nd;
-      double* fo = nullptr;
-      if (a.fout) fo = a.fout + (a.j_single >= 0 ? (long)s * nd : ((long)s * a.nv + j) * nd);
-      for (int k = 0; k < CPL; ++k) {
-        const int p = lane * CPL + k;
-        if (p < N) {
-          const int i = fwd ? p : N - 1 - p;
-          double bi[4];
-          cell_block(a, s, i, v, bi);
-          const double sc = 1.0 / sqrt(a.width[i]);
-          const double tin0 = sc, tin1 = fwd ? -kSqrt3 * sc : kSqrt3 * sc;
-          const double tout0 = sc, tout1 = fwd ? kSqrt3 * sc : -kSqrt3 * sc;
-          const double cu = c * u;
-          const double r0v = q[2 * i] + cu * tin0, r1v = q[2 * i + 1] + cu * tin1;
-          const double f0 = bi[0] * r0v + bi[1] * r1v, f1 = bi[2] * r0v + bi[3] * r1v;
-          u = tout0 * f0 + tout1 * f1;
-          st[2 * i] = f0;
-          st[2 * i + 1] = f1;
-          if (fo) {
-            fo[2 * i] = f0;
-            fo[2 * i + 1] = f1;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    const int cnt = min(nw, jn - r0);
-    for (long i = threadIdx.x; i < nd; i += blockDim.x) {
-      double t = acc[i];
-      for (int k = 0; k < cnt; ++k) {
-        const double wj = a.j_single >= 0 ? 1.0 : a.w[r0 + k];
-        t = t + wj * stage[(long)k * nd + i];
-      }
-      acc[i] = t;
-    }
-    __syncthreads();
-  }
+  double* acc = sm + NV;
+  double* stage = sm + 2 * NV;
+  const int lane = threadIdx.x & 31;
+  sweep_cta<CPL, CACHED>(a, s, a.rho ? a.rho + (long)s * nd : nullptr, false, q, acc, stage);
 
   if (a.out) {
     double mx_d = 0.0, mx_r = 0.0;
     for (long i = threadIdx.x; i < nd; i += blockDim.x) {
-      const double o = acc[i];
+      const double o = acc[lane_major_dof<CPL>(i)];
       a.out[(long)s * nd + i] = o;
       if (a.delta) {
         const double dd = o - a.rho_prev[(long)s * nd + i];
@@ -210,25 +73,86 @@ __global__ void __launch_bounds__(512) sweep1d_kernel(const Sweep1DArgs a) {
 
 template <int CPL>
 void launch_cpl(const Sweep1DArgs& a, cudaStream_t st) {
-  const long nd = a.ndof;
+  const long nv = 2 * 32 * CPL;  // lane-major vector length
   const int jn = a.j_single >= 0 ? 1 : a.nv;
-  int nw = 16;
+  int nw = 8;  // 256 threads: at 512 ptxas caps the kernel at 64 registers and spills
   const long budget = 200 * 1024;
-  while (nw > 1 && (long)(2 + nw) * nd * 8 > budget) nw >>= 1;
+  while (nw > 1 && (long)(2 + nw) * nv * 8 > budget) nw >>= 1;
   nw = std::min(nw, std::max(1, jn));
-  const size_t smem = (size_t)(2 + nw) * nd * 8;
+  const size_t smem = (size_t)(2 + nw) * nv * 8;
   RTE_REQUIRE(smem <= (size_t)(227 * 1024), RTE_ERR_UNSUPPORTED, "sweep1d: slab too large for one CTA");
   static bool configured = false;
   if (!configured) {
-    RTE_CUDA(cudaFuncSetAttribute(sweep1d_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RTE_CUDA(cudaFuncSetAttribute(sweep1d_kernel<CPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    RTE_CUDA(cudaFuncSetAttribute(sweep1d_kernel<CPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   227 * 1024));
     configured = true;
   }
-  sweep1d_kernel<CPL><<<a.S, nw * 32, smem, st>>>(a);
+  if (a.cache)
+    sweep1d_kernel<CPL, true><<<a.S, nw * 32, smem, st>>>(a);
+  else
+    sweep1d_kernel<CPL, false><<<a.S, nw * 32, smem, st>>>(a);
   RTE_CUDA(cudaGetLastError());
 }
 
+// One thread per (sample, direction, sweep position): the cell block inverse
+// and trace gain exactly as the on-the-fly path computes them.
+__global__ void slab_cache_kernel(Sweep1DArgs a, int cpl, double* cache, double* sc_out) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int N = a.N;
+  if (t >= (long)a.S * a.nv * N) return;
+  const int p = (int)(t % N);
+  const long sj = t / N;
+  const int j = (int)(sj % a.nv), s = (int)(sj / a.nv);
+  const double v = a.vx[j];
+  const bool fwd = v > 0;
+  const int i = fwd ? p : N - 1 - p;
+  double bi[4];
+  cell_block(a, s, i, v, bi);
+  const double sc = 1.0 / sqrt(a.width[i]);
+  const double be = trace_gain(bi, sc, fabs(v), fwd);
+  const long stride = 32L * cpl;
+  double* e = cache + sj * 5 * stride + (long)(p % cpl) * 32 + p / cpl;
+  e[0] = bi[0];
+  e[stride] = bi[1];
+  e[2 * stride] = bi[2];
+  e[3 * stride] = bi[3];
+  e[4 * stride] = be;
+  if (sj == 0) sc_out[i] = sc;
+}
+
 }  // namespace
+
+int sweep1d_cpl(int N) {
+  for (int c = 1; c <= 128; c *= 2)
+    if (N <= 32 * c) return c;
+  return 0;
+}
+
+void slab_cache_ensure(rte_ctx* ctx, cudaStream_t st) {
+  if (ctx->slab_cache_tried) return;
+  ctx->slab_cache_tried = true;
+  const int cpl = sweep1d_cpl(ctx->ncells);
+  if (!cpl) return;
+  const size_t n = (size_t)ctx->S * ctx->nv * 5 * 32 * cpl;
+  size_t fr = 0, tot = 0;
+  RTE_CUDA(cudaMemGetInfo(&fr, &tot));
+  if (n * sizeof(double) > std::min<size_t>(fr / 4, (size_t)4 << 30)) return;  // on the fly instead
+  ctx->slab_cache.alloc(n);
+  ctx->slab_sc.alloc(ctx->ncells);
+  Sweep1DArgs a{};
+  a.S = ctx->S;
+  a.N = ctx->ncells;
+  a.nv = ctx->nv;
+  a.width = ctx->width.p;
+  a.vx = ctx->dvx.p;
+  a.block = ctx->block;
+  a.mt = ctx->mt.p;
+  const long total = (long)ctx->S * ctx->nv * ctx->ncells;
+  slab_cache_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a, cpl, ctx->slab_cache.p, ctx->slab_sc.p);
+  RTE_CUDA(cudaGetLastError());
+}
 
 void launch_sweep1d(const Sweep1DArgs& a, cudaStream_t st) {
   const int N = a.N;

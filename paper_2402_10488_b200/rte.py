@@ -717,12 +717,13 @@ def sisa_solve(batch: TransportBatch, method, config: SolveConfig):
         rho = batch._out(batch.S, batch.nd)
     S, mi = batch.S, config.max_iters
     reps = (capi.SiReport * S)()
-    hist = np.zeros(S * mi)
-    log = ctypes.create_string_buffer(S * mi)
+    hist = np.empty(S * mi)  # only the rows' first max(iterations) entries are written
+    log = np.empty(S * mi, dtype=np.uint8)
     _torch().cuda.synchronize(batch.device)
     import time as _time
     t0 = _time.perf_counter()
-    rc = L.rte_si_solve(batch._h, ctypes.byref(cfg), ctypes.c_void_p(rho.data_ptr()), reps, capi.dptr(hist), log)
+    rc = L.rte_si_solve(batch._h, ctypes.byref(cfg), ctypes.c_void_p(rho.data_ptr()), reps, capi.dptr(hist),
+                        log.ctypes.data_as(ctypes.c_char_p))
     wall = _time.perf_counter() - t0
     if rc != 0 and errors:
         raise errors[0]
@@ -733,14 +734,16 @@ def sisa_solve(batch: TransportBatch, method, config: SolveConfig):
         except capi.RteError as e:
             e.dsa_status = [int(reps[s].dsa_status) for s in range(S)]
             raise
-    raw = log.raw
+    raw = log.tobytes()
     out = []
     label = custom.label() if custom is not None else method
+    width = max((reps[s].iterations for s in range(S)), default=0)
+    rows = hist.reshape(S, mi)[:, :width].tolist()  # one conversion for the batch
     for s in range(S):
         r = reps[s]
         it = r.iterations
         lg = raw[s * mi:s * mi + it].replace(b"\0", b"").decode()
-        out.append(SolveReport(bool(r.converged), int(r.n_sweep), int(it), list(hist[s * mi:s * mi + it]),
+        out.append(SolveReport(bool(r.converged), int(r.n_sweep), int(it), rows[s][:it],
                                float(r.final_residual), label,
                                "supplied" if (config.initial_guess is not None or m == capi.RTE_ROMIG) else "zero",
                                lg, int(r.switch_iter), bool(r.singular), wall, int(r.dsa_status)))
