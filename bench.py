@@ -385,11 +385,27 @@ def time_to_tol(device, reps=2, models_out=None):
         return out, best
 
     def host_timed(fn):
+        """Online setup time (steady state): fn(tm) builds the batch and
+        records its parts in tm; a first, discarded construction absorbs the
+        process's one-time costs (lazy kernel-module loading, first
+        allocations), then the second construction is timed."""
+        import gc
+        fn({})
+        gc.collect()  # the discarded batch is released before, not inside, the timed setup
+        torch.cuda.synchronize()
+        tm = {}
+        t0 = time.perf_counter()
+        out = fn(tm)
+        torch.cuda.synchronize()
+        return out, time.perf_counter() - t0, tm
+
+    def part(tm, key, fn):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         out = fn()
         torch.cuda.synchronize()
-        return out, time.perf_counter() - t0
+        tm[key] = tm.get(key, 0.0) + time.perf_counter() - t0
+        return out
 
     def summary(reps_, t, S, setup=0.0):
         return {"per_sample_s": t / S, "batch_s": t, "online_setup_s": setup,
@@ -404,7 +420,8 @@ def time_to_tol(device, reps=2, models_out=None):
         return mod.ProblemDefinition(geom, [t0], lambda x, y: 1.0)
 
     out = {"timing": "CUDA events around the batched solve call, warm (best of %d after a cold call); "
-                     "per_sample_s = batch_s / samples; per_sample_with_setup_s adds the online setup "
+                     "per_sample_s = batch_s / samples; per_sample_with_setup_s adds the online setup (steady state: the "
+                     "second construction in the process, setup_breakdown_s its parts) "
                      "(per-parameter system assembly on the host + upload, DSA setup, ROM upload; offline stage "
                      "excluded), SURVEY s8(d)" % reps,
            "xy_dsa": "unsuffixed: each DSA solve to relative residual 1e-3 * eps / change (SPEC.md:174 inner "
@@ -413,14 +430,15 @@ def time_to_tol(device, reps=2, models_out=None):
                      "tests/test_gpu_fullsize_parity.py); '/dsa_tol_1e-12': every DSA solve to "
                      "relative residual 1e-12"}
     # C1: 256-cell slab, S16, sigma_t = 100, c = 0.9999, SI-DSA to 1e-8 relative change
-    def c1_setup():
-        b = rte.TransportBatch(homog(rte, rte.SLAB1D, 100.0, 0.9999), rte.Mesh.slab_uniform(0.0, 1.0, 256),
-                               rte.gauss_legendre(16), [[]], device=device)
-        rte.DsaOperator(b)
+    def c1_setup(tm):
+        b = part(tm, "system_s", lambda: rte.TransportBatch(homog(rte, rte.SLAB1D, 100.0, 0.9999),
+                                                             rte.Mesh.slab_uniform(0.0, 1.0, 256),
+                                                             rte.gauss_legendre(16), [[]], device=device))
+        part(tm, "dsa_setup_s", lambda: rte.DsaOperator(b))
         return b
-    b, t_set = host_timed(c1_setup)
+    b, t_set, tm = host_timed(c1_setup)
     (_, r), t = warm(lambda: rte.sisa_solve(b, "DSA", rte.SolveConfig(eps_sisa=1e-8, norm="rel")))
-    out["c1_slab"] = {"SI-DSA": summary(r, t, 1, t_set)}
+    out["c1_slab"] = {"SI-DSA": summary(r, t, 1, t_set), "setup_breakdown_s": tm}
     del b
     # C2: two-region slab, 32 training + 512 test samples, POD rank 16
     train, test = configs.c2_params(32, 512)
@@ -437,13 +455,14 @@ def time_to_tol(device, reps=2, models_out=None):
     torch.cuda.synchronize()
     t_off = time.perf_counter() - t_off
     del tb, snaps
-    def c2_setup():
-        b = rte.TransportBatch(configs.two_region_slab(rte), mesh, quad, test, device=device)
-        rte.DsaOperator(b)
-        rte.load_rom(b, 0, models[0])
-        rte.load_rom(b, 1, models[1])
+    def c2_setup(tm):
+        b = part(tm, "system_s", lambda: rte.TransportBatch(configs.two_region_slab(rte), mesh, quad, test,
+                                                             device=device))
+        part(tm, "dsa_setup_s", lambda: rte.DsaOperator(b))
+        part(tm, "rom_load_s", lambda: rte.load_rom(b, 0, models[0]))
+        part(tm, "rom_load_s", lambda: rte.load_rom(b, 1, models[1]))
         return b
-    b, t_set = host_timed(c2_setup)
+    b, t_set, tm = host_timed(c2_setup)
     cfg = rte.SolveConfig(eps_sisa=1e-8, norm="abs", theta=theta, max_iters=500,
                           eps_romsad=rte.romsad_tolerance(eps_train, models[1].discarded_fraction))
     c2 = {"offline_wall_s": t_off, "pod_rank": 16}
@@ -452,19 +471,22 @@ def time_to_tol(device, reps=2, models_out=None):
     for label, method in (("SI-DSA", "DSA"), ("ROMIG", "ROMIG"), ("ROMSAD", "ROMSAD")):
         (_, r), t = warm(lambda: rte.sisa_solve(b, method, cfg))
         c2[label] = summary(r, t, len(test), t_set)
+    c2["setup_breakdown_s"] = tm
     out["c2_slab_parametric"] = c2
     del b
     # C3: 256^2 XY, CL(16,8), sigma_t = 10, c = 0.999, SI-DSA to 1e-8 relative change
-    def c3_setup():
-        b = rte.TransportBatch(homog(rte, rte.XY2D, 10.0, 0.999), rte.Mesh.rect_uniform(0, 1, 256, 0, 1, 256),
-                               rte.chebyshev_legendre(16, 8), [[]], device=device)
-        rte.DsaOperator(b)
+    def c3_setup(tm):
+        b = part(tm, "system_s", lambda: rte.TransportBatch(homog(rte, rte.XY2D, 10.0, 0.999),
+                                                             rte.Mesh.rect_uniform(0, 1, 256, 0, 1, 256),
+                                                             rte.chebyshev_legendre(16, 8), [[]], device=device))
+        part(tm, "dsa_setup_s", lambda: rte.DsaOperator(b))
         return b
-    b, t_set = host_timed(c3_setup)
+    b, t_set, tm = host_timed(c3_setup)
     c3 = {}
     for inner in INNER:
         (_, r), t = warm(lambda: rte.sisa_solve(b, "DSA", rte.SolveConfig(eps_sisa=1e-8, norm="rel", dsa_inner=inner)))
         c3["SI-DSA" + INNER[inner]] = summary(r, t, 1, t_set)
+    c3["setup_breakdown_s"] = tm
     out["c3_xy"] = c3
     del b
     # C4: 128^2 pin cell, 40 training + 64 test samples, POD rank 20 (correction model)
@@ -481,13 +503,15 @@ def time_to_tol(device, reps=2, models_out=None):
     t_off = time.perf_counter() - t_off
     del tb, snaps, U
     torch.cuda.empty_cache()
-    def c4_setup():
-        b = rte.TransportBatch(make(128), mesh, quad, test, device=device)
-        rte.DsaOperator(b)
-        rte.load_rom(b, 1, cm)
+    prob4 = make(128)
+
+    def c4_setup(tm):
+        b = part(tm, "system_s", lambda: rte.TransportBatch(prob4, mesh, quad, test, device=device))
+        part(tm, "dsa_setup_s", lambda: rte.DsaOperator(b))
+        part(tm, "rom_load_s", lambda: rte.load_rom(b, 1, cm))
         return b
-    b, t_set = host_timed(c4_setup)
-    c4 = {"offline_wall_s": t_off, "pod_rank": 20}
+    b, t_set, tm = host_timed(c4_setup)
+    c4 = {"offline_wall_s": t_off, "pod_rank": 20, "setup_breakdown_s": tm}
     if models_out is not None:
         models_out["c4"] = cm
     for inner in INNER:

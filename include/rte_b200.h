@@ -358,6 +358,13 @@ int rte_weighted_mass(int geometry, int nx, int ny, const double* bounds, double
 /* project (dg_space.cpp:31-71) from values at the cell points. */
 int rte_project(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0,
                 double y1, int nq, const double* fvals, double* out);
+/* Batch assembly helpers (the TransportSystem constructor's build_masses,
+ * transport_system.cpp:111-140, for S samples): rte_scalar_blocks reduces
+ * per-cell blocks [n][nl*nl] to scalars when every block is d0 I to 1e-12
+ * (else RTE_ERR_UNSUPPORTED); rte_combine_terms forms out[s][e] =
+ * sum_k psi[s][k] terms[k][e] in ascending k, products rounded before adds. */
+int rte_scalar_blocks(long n, int nl, const double* m, double* out);
+int rte_combine_terms(int S, int K, long n, const double* psi, const double* terms, double* out);
 /* cases.cpp:11-13: n unit draws (gen() >> 11) * 2^-53 of std::mt19937_64(seed). */
 int rte_unit_draws(unsigned long long seed, long n, double* out);
 

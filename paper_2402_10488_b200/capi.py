@@ -127,6 +127,8 @@ SIGNATURES = [
     ("rte_project", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, ctypes.c_double, ctypes.c_double,
                                    ctypes.c_double, ctypes.c_double, ctypes.c_int, _dp, _dp]),
     ("rte_unit_draws", ctypes.c_int, [ctypes.c_ulonglong, ctypes.c_long, _dp]),
+    ("rte_scalar_blocks", ctypes.c_int, [ctypes.c_long, ctypes.c_int, _dp, _dp]),
+    ("rte_combine_terms", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_long, _dp, _dp, _dp]),
     ("rte_guard_check", ctypes.c_int, [ctypes.POINTER(ctypes.c_long), ctypes.POINTER(ctypes.c_long)]),
     ("rte_guard_selftest", ctypes.c_int, [ctypes.c_int]),
 ]

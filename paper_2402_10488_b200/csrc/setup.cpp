@@ -4,6 +4,7 @@
 // projection (dg_space.cpp:31-71).  They turn ProblemDefinition-style
 // coefficient closures, evaluated by the caller at the returned points, into
 // the per-cell blocks and load vectors rte_create consumes.
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -178,3 +179,45 @@ int rte_project(int geometry, int nx, int ny, const double* bounds, double x0, d
 }
 
 }  // extern "C"
+
+// ---- per-parameter system assembly helpers (the host side of the
+// TransportSystem constructor for a batch, transport_system.cpp:82-140) ----
+
+// Per-cell blocks [n][nl*nl] -> scalars d0 when every block is d0 I to 1e-12
+// relative (the closed-form XY cell solve needs sigma I blocks).
+int rte_scalar_blocks(long n, int nl, const double* m, double* out) {
+  if (n < 0 || nl < 1 || (n && (!m || !out))) return RTE_ERR_INVALID;
+  const long nb = (long)nl * nl;
+  int bad = 0;
+  for (long c = 0; c < n; ++c) {
+    const double* f = m + c * nb;
+    const double d0 = f[0];
+    double err = 0.0, scale = 1e-300;
+    for (int i = 0; i < nl; ++i)
+      for (int j = 0; j < nl; ++j) {
+        err = std::max(err, std::fabs(f[i * nl + j] - (i == j ? d0 : 0.0)));
+        if (i == j) scale = std::max(scale, std::fabs(f[i * nl + j]));
+      }
+    if (err > 1e-12 * scale) bad |= 1;
+    out[c] = d0;
+  }
+  return bad ? RTE_ERR_UNSUPPORTED : RTE_OK;
+}
+
+// build_masses accumulation order (transport_system.cpp:133-138) for a batch:
+// out[s][e] = sum_k psi[s][k] * terms[k][e], k ascending, each product rounded
+// before the add (no contraction).
+__attribute__((optimize("fp-contract=off")))  // product and sum rounded separately, as numpy does
+int rte_combine_terms(int S, int K, long n, const double* psi, const double* terms, double* out) {
+  if (S < 1 || K < 1 || n < 0 || !psi || !terms || !out) return RTE_ERR_INVALID;
+  for (int s = 0; s < S; ++s) {
+    double* o = out + (long)s * n;
+    for (long e = 0; e < n; ++e) o[e] = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const double p = psi[(long)s * K + k];
+      const double* t = terms + (long)k * n;
+      for (long e = 0; e < n; ++e) o[e] = o[e] + p * t[e];
+    }
+  }
+  return RTE_OK;
+}

@@ -224,9 +224,10 @@ class TransportBatch:
         tmt, tms = np.stack(tmt), np.stack(tms)  # [K][cells][nl][nl]
 
         def combine(terms):  # build_masses accumulation order (transport_system.cpp:136-137)
-            out = np.zeros((S,) + terms.shape[1:])
-            for k in range(K):
-                out = out + psi[:, k].reshape((S,) + (1,) * (terms.ndim - 1)) * terms[k][None]
+            t = np.ascontiguousarray(terms)
+            out = np.empty((S,) + t.shape[1:])
+            ps = np.ascontiguousarray(psi)
+            capi.check(capi.load().rte_combine_terms(S, K, t[0].size, capi.dptr(ps), capi.dptr(t), capi.dptr(out)))
             return out
         g = mesh.project(_vals(problem.source, px, py)) if problem.source is not None else np.zeros(mesh.n_dof())
         inflow = (problem.inflow_left, problem.inflow_right, problem.inflow_bottom, problem.inflow_top)
@@ -428,17 +429,17 @@ class TransportBatch:
 
 
 def _scalar_blocks(m):
-    """Per-cell mass blocks -> scalar sigma (the B200 2D path needs sigma*I)."""
+    """Per-cell mass blocks -> scalar sigma (the B200 2D path needs sigma*I);
+    rte_scalar_blocks (OpenMP) raises RTE_ERR_UNSUPPORTED otherwise."""
     nl = m.shape[-1]
     f = np.ascontiguousarray(m).reshape(-1, nl * nl)
-    d0 = f[:, 0]
-    # |m - d0 I| covers both the off-diagonal entries and unequal diagonals
-    err = np.abs(f - d0[:, None] * np.eye(nl).ravel()).max(axis=1)
-    scale = np.maximum(np.abs(f[:, ::nl + 1]).max(axis=1), 1e-300)
-    if np.any(err > 1e-12 * scale):
+    out = np.empty(f.shape[0])
+    rc = capi.load().rte_scalar_blocks(f.shape[0], nl, capi.dptr(f), capi.dptr(out))
+    if rc == capi.RTE_ERR_UNSUPPORTED:
         raise capi.RteError(capi.RTE_ERR_UNSUPPORTED,
                             "xy geometry: coefficients must be constant per cell in this build")
-    return np.ascontiguousarray(d0).reshape(m.shape[:-2])
+    capi.check(rc)
+    return out.reshape(m.shape[:-2])
 
 
 class DsaOperator:

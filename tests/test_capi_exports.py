@@ -98,3 +98,28 @@ def test_solve_config_maps_onto_the_c_struct():
     for bad in (dict(norm="l2"), dict(max_iters=0), dict(dsa_inner=1.5)):
         with pytest.raises(ValueError):
             rte.si_config(rte.SolveConfig(**bad), capi.RTE_DSA)
+
+
+def test_batch_assembly_helpers_match_numpy():
+    """rte_combine_terms / rte_scalar_blocks (setup.cpp) against the numpy
+    formulas they replace in rte.TransportBatch: bitwise."""
+    import numpy as np
+    from paper_2402_10488_b200 import capi
+    L = capi.load()
+    rng = np.random.default_rng(5)
+    S, K, n = 7, 4, 1000
+    psi = rng.uniform(-2, 3, (S, K))
+    terms = rng.uniform(-1, 1, (K, n))
+    out = np.empty((S, n))
+    assert L.rte_combine_terms(S, K, n, capi.dptr(psi), capi.dptr(terms), capi.dptr(out)) == 0
+    ref = np.zeros((S, n))
+    for k in range(K):
+        ref = ref + psi[:, k][:, None] * terms[k][None]
+    assert np.array_equal(out, ref)
+    d0 = rng.uniform(0.5, 2, 50)
+    blocks = d0[:, None, None] * np.eye(4)[None]
+    sc = np.empty(50)
+    assert L.rte_scalar_blocks(50, 4, capi.dptr(np.ascontiguousarray(blocks)), capi.dptr(sc)) == 0
+    assert np.array_equal(sc, d0)
+    blocks[3, 0, 1] = 1e-6
+    assert L.rte_scalar_blocks(50, 4, capi.dptr(np.ascontiguousarray(blocks)), capi.dptr(sc)) == capi.RTE_ERR_UNSUPPORTED
