@@ -94,14 +94,33 @@ __device__ void assemble(const double* a_r, const double* psi, int r, int K, dou
     }
 }
 
+// One warp per sample (r <= 32; larger ranks: one thread per sample).
 __global__ void rom_factor_kernel(int S, int r, int K, const double* a_r, const double* psi, double* lu, int* rp,
                                   int* cp, int* sing) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double am[4][32 * 32];
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  const int s = blockIdx.x * 4 + w;
   if (s >= S) return;
-  double* a = lu + (long)s * r * r;
-  assemble(a_r, psi + (long)s * K, r, K, a);
-  const int rank = fullpiv_lu(a, r, rp + (long)s * r, cp + (long)s * r);
-  sing[s] = rank < r ? 1 : 0;
+  if (r > 32) {  // serial fallback
+    if (ln) return;
+    double* a = lu + (long)s * r * r;
+    assemble(a_r, psi + (long)s * K, r, K, a);
+    const int rank = fullpiv_lu(a, r, rp + (long)s * r, cp + (long)s * r);
+    sing[s] = rank < r ? 1 : 0;
+    return;
+  }
+  double* a = am[w];
+  const double* ps = psi + (long)s * K;
+  for (int e = ln; e < r * r; e += 32) {  // assemble (reduced_model.cpp:32-39), row-major
+    const int i = e / r, j = e - i * r;
+    double t = 0.0;
+    for (int k = 0; k < K; ++k) t = t + ps[k] * a_r[(long)k * r * r + (long)j * r + i];
+    a[e] = t;
+  }
+  __syncwarp();
+  const int rank = warp_fullpiv_lu(a, r, rp + (long)s * r, cp + (long)s * r);
+  for (int e = ln; e < r * r; e += 32) lu[(long)s * r * r + e] = a[e];
+  if (ln == 0) sing[s] = rank < r ? 1 : 0;
 }
 
 struct RomCorrectArgs {
@@ -123,8 +142,12 @@ __global__ void rom_correct_kernel(const RomCorrectArgs a) {
   const int s = blockIdx.x;
   if (a.kind[s] != KIND_ROMSA) return;
   block_dots<8>(a.u_iso, a.nd, a.r, nullptr, a.ms, a.block, a.N, a.delta + (long)s * a.nd, s, rhs, red);
-  if (threadIdx.x == 0)
+  if (a.r <= 32) {
+    if (threadIdx.x < 32)
+      warp_fullpiv_solve(a.lu + (long)s * a.r * a.r, a.r, a.rp + (long)s * a.r, a.cp + (long)s * a.r, rhs, c);
+  } else if (threadIdx.x == 0) {
     fullpiv_solve(a.lu + (long)s * a.r * a.r, a.r, a.rp + (long)s * a.r, a.cp + (long)s * a.r, rhs, y, c);
+  }
   __syncthreads();
   for (long i = threadIdx.x; i < a.nd; i += blockDim.x) {
     double t = 0.0;
@@ -149,17 +172,65 @@ struct RomigArgs {
 
 __global__ void romig_kernel(const RomigArgs a) {
   __shared__ double c[128], y[128], b[128];
+  __shared__ double am[32 * 32];
   __shared__ int ok;
   const int s = blockIdx.x;
   const int r = a.r;
-  if (threadIdx.x == 0) {
-    double* A = a.work + (long)s * r * r;
-    // keep an unfactored copy for the residual check in y/b scratch space
-    double* lu = A;
+  int* rp = a.rp + (long)s * r;
+  int* cp = a.cp + (long)s * r;
+  if (r <= 32) {
+    // one warp: assemble, complete-pivoting LU, solve, Galerkin residual check
+    if (threadIdx.x < 32) {
+      const int ln = threadIdx.x;
+      const double* ps = a.psi + (long)s * a.K;
+      for (int e = ln; e < r * r; e += 32) {
+        const int i = e / r, j = e - i * r;
+        double t = 0.0;
+        for (int k = 0; k < a.K; ++k) t = t + ps[k] * a.a_r[(long)k * r * r + (long)j * r + i];
+        am[e] = t;
+      }
+      if (ln < r) b[ln] = a.b_r[ln];
+      __syncwarp();
+      const int rank = warp_fullpiv_lu(am, r, rp, cp);
+      if (rank < r) {
+        if (ln == 0) {
+          a.status[s] = 1;
+          ok = 0;
+        }
+      } else {
+        warp_fullpiv_solve(am, r, rp, cp, b, c);
+        __syncwarp();
+        // Galerkin residual check (strategies.cpp:20-27), lane i = row i
+        double resid = 0.0, rs = 0.0, cm = 0.0, bm = 0.0;
+        if (ln < r) {
+          double t = 0.0;
+          for (int j = 0; j < r; ++j) {
+            double aij = 0.0;
+            for (int k = 0; k < a.K; ++k) aij = aij + ps[k] * a.a_r[(long)k * r * r + (long)j * r + ln];
+            t += aij * c[j];
+            rs += fabs(aij);
+          }
+          resid = fabs(b[ln] - t);
+          cm = fabs(c[ln]);
+          bm = fabs(b[ln]);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          resid = fmax(resid, __shfl_xor_sync(0xffffffffu, resid, o));
+          rs = fmax(rs, __shfl_xor_sync(0xffffffffu, rs, o));
+          cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+          bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+        }
+        if (ln == 0) {
+          const double scale = rs * cm + bm;
+          const bool good = !(resid > 1e-10 * fmax(scale, 1e-300));
+          a.status[s] = good ? 0 : 2;
+          ok = good ? 1 : 0;
+        }
+      }
+    }
+  } else if (threadIdx.x == 0) {
+    double* lu = a.work + (long)s * r * r;
     assemble(a.a_r, a.psi + (long)s * a.K, r, a.K, lu);
-    // row-abs-sum and residual need A: recompute entries from a_r on the fly
-    int* rp = a.rp + (long)s * r;
-    int* cp = a.cp + (long)s * r;
     for (int i = 0; i < r; ++i) b[i] = a.b_r[i];
     const int rank = fullpiv_lu(lu, r, rp, cp);
     ok = 1;
@@ -230,8 +301,8 @@ void rom_load(rte_ctx* ctx, int which, const rte_rom* rom) {
 void rom_setup(rte_ctx* ctx, int which, int* singular_dev, cudaStream_t st) {
   RomState* m = ctx->rom[which];
   RTE_REQUIRE(m, RTE_ERR_INVALID, "rom: model not loaded");
-  rom_factor_kernel<<<(ctx->S + 31) / 32, 32, 0, st>>>(ctx->S, m->r, m->K, m->a_r.p, ctx->psi.p, m->lu.p, m->rp.p,
-                                                        m->cp.p, m->sing.p);
+  rom_factor_kernel<<<(ctx->S + 3) / 4, 128, 0, st>>>(ctx->S, m->r, m->K, m->a_r.p, ctx->psi.p, m->lu.p, m->rp.p,
+                                                       m->cp.p, m->sing.p);
   RTE_CUDA(cudaGetLastError());
   if (singular_dev) RTE_CUDA(cudaMemcpyAsync(singular_dev, m->sing.p, sizeof(int) * ctx->S, cudaMemcpyDeviceToDevice, st));
   m->factored = true;

@@ -43,7 +43,7 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 template <int CPL, bool CACHED, bool FAC_SMEM>
 __global__ void __launch_bounds__(256) si1d_kernel(const Si1DArgs a) {
   extern __shared__ double sm[];
-  __shared__ double red[32], rom_rhs[128], rom_y[128], rom_c[128], rom_red[32 * 8];
+  __shared__ double red[32], rom_rhs[32], rom_c[32], rom_red[32 * 8];
   __shared__ int kind_sh, done_sh;
   constexpr int NP = 32 * CPL, NV = 2 * NP;  // lane-major vectors (slab_dev.cuh)
   const int s = blockIdx.x;
@@ -166,12 +166,13 @@ __global__ void __launch_bounds__(256) si1d_kernel(const Si1DArgs a) {
         rho[le] = acc[le] + y[(e & 1) * N + (e >> 1)];
       }
     } else if (kind == KIND_ROMSA) {
+      // natural-layout delta and the sample's LU factors (r <= 32) in the CR region
+      double* lu = y + nd;
       for (long e = threadIdx.x; e < nd; e += blockDim.x) y[e] = q[lane_major_dof<CPL>(e)];
+      for (int e = threadIdx.x; e < a.r * a.r; e += blockDim.x) lu[e] = __ldg(a.lu + (long)s * a.r * a.r + e);
       __syncthreads();
       block_dots<8>(a.u_iso, nd, a.r, nullptr, a.sw.ms, a.sw.block, N, y, s, rom_rhs, rom_red);
-      if (threadIdx.x == 0)
-        fullpiv_solve(a.lu + (long)s * a.r * a.r, a.r, a.rp + (long)s * a.r, a.cp + (long)s * a.r, rom_rhs, rom_y,
-                      rom_c);
+      if (threadIdx.x < 32) warp_fullpiv_solve(lu, a.r, a.rp + (long)s * a.r, a.cp + (long)s * a.r, rom_rhs, rom_c);
       __syncthreads();
       for (long e = threadIdx.x; e < nd; e += blockDim.x) {
         double t = 0.0;
@@ -211,7 +212,8 @@ void launch_one(const Si1DArgs& a, int nw, size_t smem, cudaStream_t st) {
 template <int CPL>
 bool launch_cpl(const Si1DArgs& a, cudaStream_t st) {
   const long nv = 2 * 32 * CPL;  // lane-major vector length
-  const long budget = 220 * 1024;  // dynamic; + 5.3 KB static (ROM scratch)
+  const long budget = 220 * 1024;  // dynamic; + static (ROM scratch)
+  if ((long)a.r * a.r > 3 * nv) return false;  // the ROMSA LU copy shares the CR region with delta
   int nw = 8;  // 256 threads: at 512 ptxas caps the kernel at 64 registers and spills
   while (nw > 1 && (long)(7 + nw) * nv * 8 > budget) nw >>= 1;
   nw = std::min(nw, std::max(1, a.sw.nv));
@@ -248,7 +250,7 @@ bool launch_cpl(const Si1DArgs& a, cudaStream_t st) {
 // the caller uses the per-kernel loop.
 bool si1d_fused(const Si1DArgs& a, cudaStream_t st) {
   const int N = a.sw.N;
-  if (a.r > 128) return false;
+  if (a.r > 32) return false;  // warp_fullpiv_solve; LU in the CR region
   if (N <= 32) return launch_cpl<1>(a, st);
   if (N <= 64) return launch_cpl<2>(a, st);
   if (N <= 128) return launch_cpl<4>(a, st);

@@ -495,6 +495,106 @@ __device__ inline void fullpiv_solve(const double* a, int r, const int* rp, cons
   for (int i = 0; i < r; ++i) x[cp[i]] = y[i];
 }
 
+// Complete-pivoting LU (FullPivLU semantics, rom.cu fullpiv_lu) of the
+// r x r row-major matrix a in shared memory by one warp, r <= 32, lane i owns
+// row i: the same pivot choices (first maximum in column-major order) and the
+// same per-element arithmetic as the serial version, so the factors are
+// bitwise equal.  Returns the rank (|pivot| > eps r max|pivot|) on all lanes.
+__device__ __forceinline__ int warp_fullpiv_lu(double* a, int r, int* rp, int* cp) {
+  const int ln = threadIdx.x & 31;
+  if (ln < r) {
+    rp[ln] = ln;
+    cp[ln] = ln;
+  }
+  __syncwarp();
+  double maxpiv = 0.0;
+  int nz = r;
+  for (int k = 0; k < r; ++k) {
+    // this lane's row: first maximum over columns k..r-1
+    double big = 0.0;
+    int bj = k;
+    if (ln >= k && ln < r)
+      for (int j = k; j < r; ++j) {
+        const double v = fabs(a[ln * r + j]);
+        if (v > big) {
+          big = v;
+          bj = j;
+        }
+      }
+    int bi = ln;
+    // warp arg-max: larger value, then smaller column, then smaller row
+    for (int o = 16; o > 0; o >>= 1) {
+      const double b2 = __shfl_xor_sync(0xffffffffu, big, o);
+      const int j2 = __shfl_xor_sync(0xffffffffu, bj, o), i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (b2 > big || (b2 == big && (j2 < bj || (j2 == bj && i2 < bi)))) {
+        big = b2;
+        bj = j2;
+        bi = i2;
+      }
+    }
+    if (big == 0.0) {
+      nz = k;
+      break;
+    }
+    maxpiv = fmax(maxpiv, big);
+    if (bi != k) {  // row swap (lane = column)
+      if (ln < r) {
+        const double t = a[k * r + ln];
+        a[k * r + ln] = a[bi * r + ln];
+        a[bi * r + ln] = t;
+      }
+      if (ln == 0) {
+        const int t = rp[k];
+        rp[k] = rp[bi];
+        rp[bi] = t;
+      }
+    }
+    __syncwarp();
+    if (bj != k) {  // column swap (lane = row)
+      if (ln < r) {
+        const double t = a[ln * r + k];
+        a[ln * r + k] = a[ln * r + bj];
+        a[ln * r + bj] = t;
+      }
+      if (ln == 0) {
+        const int t = cp[k];
+        cp[k] = cp[bj];
+        cp[bj] = t;
+      }
+    }
+    __syncwarp();
+    const double piv = a[k * r + k];
+    if (ln > k && ln < r) {
+      const double l = a[ln * r + k] / piv;
+      a[ln * r + k] = l;
+      for (int j = k + 1; j < r; ++j) a[ln * r + j] -= l * a[k * r + j];
+    }
+    __syncwarp();
+  }
+  const double thr = 2.220446049250313e-16 * r * maxpiv;
+  const bool ok = ln < nz && fabs(a[ln * r + ln]) > thr;
+  return __popc(__ballot_sync(0xffffffffu, ok));
+}
+
+// fullpiv_solve by one warp (r <= 32; lane j owns row / unknown j), LU in
+// shared memory: forward substitution subtracts in the same (ascending)
+// order as the serial version, backward in descending order.
+__device__ __forceinline__ void warp_fullpiv_solve(const double* a, int r, const int* rp, const int* cp,
+                                                   const double* b, double* x) {
+  const int j = threadIdx.x & 31;
+  double t = j < r ? b[rp[j]] : 0.0;
+  for (int i = 0; i < r; ++i) {  // L y = P b (unit lower)
+    const double yi = __shfl_sync(0xffffffffu, t, i);
+    if (j > i && j < r) t -= a[j * r + i] * yi;
+  }
+  for (int i = r - 1; i >= 0; --i) {  // U z = y
+    if (j == i) t = t / a[i * r + i];
+    const double zi = __shfl_sync(0xffffffffu, t, i);
+    if (j < i) t -= a[j * r + i] * zi;
+  }
+  if (j < r) x[cp[j]] = t;
+}
+
 template <int CH>
 __device__ inline void block_dots(const double* u, long nd, int r, const double* v_smem_or_null, const double* ms,
                            int block, int N, const double* d, int s, double* out_smem, double* red) {
