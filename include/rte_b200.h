@@ -358,6 +358,12 @@ int rte_weighted_mass(int geometry, int nx, int ny, const double* bounds, double
 /* project (dg_space.cpp:31-71) from values at the cell points. */
 int rte_project(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0,
                 double y1, int nq, const double* fvals, double* out);
+/* The same for a weight / function that is one constant at every point
+ * (identical arithmetic; no per-point value array). */
+int rte_weighted_mass_const(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0,
+                            double y1, int nq, double w, double* out);
+int rte_project_const(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0,
+                      double y1, int nq, double f, double* out);
 /* Batch assembly helpers (the TransportSystem constructor's build_masses,
  * transport_system.cpp:111-140, for S samples): rte_scalar_blocks reduces
  * per-cell blocks [n][nl*nl] to scalars when every block is d0 I to 1e-12

@@ -36,7 +36,8 @@ def _compile(src, force):
         [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     if not force and not _stale(obj, deps):
         return obj, ""
-    omp = ["-Xcompiler", "-fopenmp"] if src.endswith(".cpp") else []  # host setup helpers
+    # host setup helpers: OpenMP; no FMA contraction (bitwise the numpy / reference arithmetic)
+    omp = ["-Xcompiler", "-fopenmp", "-Xcompiler", "-ffp-contract=off"] if src.endswith(".cpp") else []
     cmd = [NVCC] + ARCH + FLAGS + DEFINES + omp + ["-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -128,6 +128,12 @@ SIGNATURES = [
                                    ctypes.c_double, ctypes.c_double, ctypes.c_int, _dp, _dp]),
     ("rte_unit_draws", ctypes.c_int, [ctypes.c_ulonglong, ctypes.c_long, _dp]),
     ("rte_scalar_blocks", ctypes.c_int, [ctypes.c_long, ctypes.c_int, _dp, _dp]),
+    ("rte_weighted_mass_const", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, ctypes.c_double,
+                                               ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                               ctypes.c_double, _dp]),
+    ("rte_project_const", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, ctypes.c_double,
+                                         ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                         ctypes.c_double, _dp]),
     ("rte_combine_terms", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_long, _dp, _dp, _dp]),
     ("rte_guard_check", ctypes.c_int, [ctypes.POINTER(ctypes.c_long), ctypes.POINTER(ctypes.c_long)]),
     ("rte_guard_selftest", ctypes.c_int, [ctypes.c_int]),

@@ -89,8 +89,9 @@ int rte_cell_points(int geometry, int nx, int ny, const double* bounds, double x
   return RTE_OK;
 }
 
-int rte_weighted_mass(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0, double y1,
-                      int nq, const double* wv, double* out) {
+// ws: point stride of the values (1: one value per point, 0: one constant)
+static int weighted_mass_impl(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0,
+                              double y1, int nq, const double* wv, long ws, double* out) {
   if (nq < 1 || nq > 32 || !wv || !out) return RTE_ERR_INVALID;
   std::vector<double> g(nq), gw(nq);
   gl(nq, g.data(), gw.data());
@@ -101,7 +102,7 @@ int rte_weighted_mass(int geometry, int nx, int ny, const double* bounds, double
       double m[4] = {0, 0, 0, 0};
       for (int q = 0; q < nq; ++q) {
         const double x = xc + 0.5 * h * g[q];
-        const double ww = 0.5 * h * gw[q] * wv[(long)i * nq + q];
+        const double ww = 0.5 * h * gw[q] * wv[((long)i * nq + q) * ws];
         const double p[2] = {1.0 / std::sqrt(h), std::sqrt(12.0 / (h * h * h)) * (x - xc)};
         for (int r = 0; r < 2; ++r)
           for (int c = 0; c < 2; ++c) m[2 * r + c] += (ww * p[r]) * p[c];
@@ -123,7 +124,7 @@ int rte_weighted_mass(int geometry, int nx, int ny, const double* bounds, double
         for (int qx = 0; qx < nq; ++qx) {
           const double x = xc + 0.5 * hx * g[qx];
           const double px0 = 1.0 / std::sqrt(hx), px1 = std::sqrt(12.0 / (hx * hx * hx)) * (x - xc);
-          const double ww = 0.25 * hx * hy * gw[qx] * gw[qy] * wv[cell * nq * nq + qy * nq + qx];
+          const double ww = 0.25 * hx * hy * gw[qx] * gw[qy] * wv[(cell * nq * nq + qy * nq + qx) * ws];
           const double p[4] = {px0 * py0, px1 * py0, px0 * py1, px1 * py1};
           for (int r = 0; r < 4; ++r)
             for (int c = 0; c < 4; ++c) m[4 * r + c] += (ww * p[r]) * p[c];
@@ -134,8 +135,8 @@ int rte_weighted_mass(int geometry, int nx, int ny, const double* bounds, double
   return RTE_OK;
 }
 
-int rte_project(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0, double y1, int nq,
-                const double* fv, double* out) {
+static int project_impl(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0, double y1,
+                        int nq, const double* fv, long ws, double* out) {
   if (nq < 1 || nq > 32 || !fv || !out) return RTE_ERR_INVALID;
   std::vector<double> g(nq), gw(nq);
   gl(nq, g.data(), gw.data());
@@ -147,7 +148,7 @@ int rte_project(int geometry, int nx, int ny, const double* bounds, double x0, d
       const double h = bounds[i + 1] - bounds[i];
       double o0 = 0, o1 = 0;
       for (int q = 0; q < nq; ++q) {
-        const double rel = 0.5 * h * g[q], wq = 0.5 * h * gw[q], f = fv[(long)i * nq + q];
+        const double rel = 0.5 * h * g[q], wq = 0.5 * h * gw[q], f = fv[((long)i * nq + q) * ws];
         o0 += wq * f * p0(h);
         o1 += wq * f * p1(h, rel);
       }
@@ -165,7 +166,7 @@ int rte_project(int geometry, int nx, int ny, const double* bounds, double x0, d
       const double ry = 0.5 * hy * g[qy];
       for (int qx = 0; qx < nq; ++qx) {
         const double rx = 0.5 * hx * g[qx];
-        const double wq = 0.25 * hx * hy * gw[qx] * gw[qy], f = fv[c * nq * nq + qy * nq + qx];
+        const double wq = 0.25 * hx * hy * gw[qx] * gw[qy], f = fv[(c * nq * nq + qy * nq + qx) * ws];
         const double bx0 = p0(hx), bx1 = p1(hx, rx), by0 = p0(hy), by1 = p1(hy, ry);
         o[0] += wq * f * bx0 * by0;
         o[1] += wq * f * bx1 * by0;
@@ -176,6 +177,23 @@ int rte_project(int geometry, int nx, int ny, const double* bounds, double x0, d
     for (int e = 0; e < 4; ++e) out[4 * c + e] = o[e];
   }
   return RTE_OK;
+}
+
+int rte_weighted_mass(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0, double y1,
+                      int nq, const double* wv, double* out) {
+  return weighted_mass_impl(geometry, nx, ny, bounds, x0, x1, y0, y1, nq, wv, 1, out);
+}
+int rte_weighted_mass_const(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0,
+                            double y1, int nq, double w, double* out) {
+  return weighted_mass_impl(geometry, nx, ny, bounds, x0, x1, y0, y1, nq, &w, 0, out);
+}
+int rte_project(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0, double y1, int nq,
+                const double* fv, double* out) {
+  return project_impl(geometry, nx, ny, bounds, x0, x1, y0, y1, nq, fv, 1, out);
+}
+int rte_project_const(int geometry, int nx, int ny, const double* bounds, double x0, double x1, double y0, double y1,
+                      int nq, double f, double* out) {
+  return project_impl(geometry, nx, ny, bounds, x0, x1, y0, y1, nq, &f, 0, out);
 }
 
 }  // extern "C"
@@ -207,7 +225,7 @@ int rte_scalar_blocks(long n, int nl, const double* m, double* out) {
 // build_masses accumulation order (transport_system.cpp:133-138) for a batch:
 // out[s][e] = sum_k psi[s][k] * terms[k][e], k ascending, each product rounded
 // before the add (no contraction).
-__attribute__((optimize("fp-contract=off")))  // product and sum rounded separately, as numpy does
+// products and sums rounded separately, as numpy does (setup.cpp is built with -ffp-contract=off)
 int rte_combine_terms(int S, int K, long n, const double* psi, const double* terms, double* out) {
   if (S < 1 || K < 1 || n < 0 || !psi || !terms || !out) return RTE_ERR_INVALID;
   for (int s = 0; s < S; ++s) {

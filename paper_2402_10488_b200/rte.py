@@ -138,18 +138,27 @@ class Mesh:
                              % (self.cell_count() * npc, nq, vals.size))
 
     def weighted_mass(self, wvals, nq: int = NQ):
+        """weighted_mass (transport_system.cpp:17-55) from values at the cell
+        points, or from one constant (a scalar: same arithmetic, no array)."""
         nl = self.n_local()
-        out = np.zeros(self.cell_count() * nl * nl)
-        w = _c(wvals)
-        self._check_points(w, nq)
-        capi.check(capi.load().rte_weighted_mass(*self._geo(), nq, capi.dptr(w), capi.dptr(out)))
+        out = np.empty(self.cell_count() * nl * nl)
+        if np.ndim(wvals) == 0:
+            capi.check(capi.load().rte_weighted_mass_const(*self._geo(), nq, float(wvals), capi.dptr(out)))
+        else:
+            w = _c(wvals)
+            self._check_points(w, nq)
+            capi.check(capi.load().rte_weighted_mass(*self._geo(), nq, capi.dptr(w), capi.dptr(out)))
         return out.reshape(self.cell_count(), nl, nl)
 
     def project(self, fvals, nq: int = NQ):
-        out = np.zeros(self.n_dof())
-        f = _c(fvals)
-        self._check_points(f, nq)
-        capi.check(capi.load().rte_project(*self._geo(), nq, capi.dptr(f), capi.dptr(out)))
+        """project (dg_space.cpp:31-71) from values at the cell points or a constant."""
+        out = np.empty(self.n_dof())
+        if np.ndim(fvals) == 0:
+            capi.check(capi.load().rte_project_const(*self._geo(), nq, float(fvals), capi.dptr(out)))
+        else:
+            f = _c(fvals)
+            self._check_points(f, nq)
+            capi.check(capi.load().rte_project(*self._geo(), nq, capi.dptr(f), capi.dptr(out)))
         return out
 
 
@@ -177,9 +186,14 @@ class ProblemDefinition:
 
 
 def _vals(fn, px, py):
+    """Closure values at the cell points; a closure returning one scalar for
+    the whole array (a constant coefficient) stays a scalar."""
     if fn is None:
-        return np.zeros(px.size)
-    return np.ascontiguousarray(np.broadcast_to(np.asarray(fn(px, py), dtype=np.float64), px.shape))
+        return 0.0
+    v = np.asarray(fn(px, py), dtype=np.float64)
+    if v.ndim == 0:
+        return float(v)
+    return np.ascontiguousarray(np.broadcast_to(v, px.shape))
 
 
 # ---------------------------------------------------------------------------
@@ -214,7 +228,7 @@ class TransportBatch:
         for t in problem.terms:
             a = _vals(t.absorption_weight, px, py)
             sc = _vals(t.scattering_weight, px, py)
-            tot = np.zeros(px.size)
+            tot = 0.0  # transport_system.cpp:125-130 (scalars stay scalars)
             if t.absorption_weight is not None:
                 tot = tot + a
             if t.scattering_weight is not None:

@@ -123,3 +123,15 @@ def test_batch_assembly_helpers_match_numpy():
     assert np.array_equal(sc, d0)
     blocks[3, 0, 1] = 1e-6
     assert L.rte_scalar_blocks(50, 4, capi.dptr(np.ascontiguousarray(blocks)), capi.dptr(sc)) == capi.RTE_ERR_UNSUPPORTED
+
+
+def test_constant_weight_helpers_match_array_versions():
+    """rte_weighted_mass_const / rte_project_const == the per-point versions
+    on a constant array, bitwise (slab and XY)."""
+    import numpy as np
+    from paper_2402_10488_b200 import rte
+    for mesh in (rte.Mesh.slab([0.0, 0.1, 0.35, 0.6, 1.0]), rte.Mesh.rect_uniform(0, 1, 5, 0, 2, 3)):
+        px, _ = mesh.cell_points()
+        for c in (0.0, 1.0, 0.3 * 0.999, 12.5):
+            assert np.array_equal(mesh.weighted_mass(c), mesh.weighted_mass(np.full(px.size, c)))
+            assert np.array_equal(mesh.project(c), mesh.project(np.full(px.size, c)))
