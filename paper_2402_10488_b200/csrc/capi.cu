@@ -539,6 +539,55 @@ void guard_release(void* base) {
 }  // namespace rte
 
 namespace rte {
+void pool_init() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  static bool done[64] = {false};
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+void* pool_alloc(size_t bytes) {
+  pool_init();
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, bytes, nullptr);
+  if (e != cudaSuccess) {  // the pool's reserve may be fragmented: hand it back and retry once
+    cudaGetLastError();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    cudaDeviceSynchronize();
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocAsync(&p, bytes, nullptr);
+  }
+  if (e != cudaSuccess)
+    throw Error(RTE_ERR_CUDA, std::string("cudaMallocAsync(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  return p;
+}
+void pool_free(void* p) {
+  if (p) cudaFreeAsync(p, nullptr);
+}
+size_t device_free_bytes() {
+  size_t fr = 0, tot = 0;
+  RTE_CUDA(cudaMemGetInfo(&fr, &tot));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long res = 0, used = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    if (res > used) fr += (size_t)(res - used);
+  }
+  return fr;
+}
+}  // namespace rte
+
+namespace rte {
 __global__ void guard_selftest_kernel(double* p, int n) {
   if (threadIdx.x == 0 && blockIdx.x == 0) p[n] = 1.0;  // one element past the end
 }
@@ -604,8 +653,6 @@ int rte_create(const rte_problem* p, int device, rte_ctx** out) {
                     "rte_create: more than two directions share one (vx, vy) slot");
     }
     const size_t nblk = (size_t)c->S * c->ncells * c->block;
-    c->mt_h.assign(p->mt, p->mt + nblk);
-    c->ms_h.assign(p->ms, p->ms + nblk);
     c->mt.upload(p->mt, nblk);
     c->ms.upload(p->ms, nblk);
     c->g_shared = p->source_shared ? 1 : 0;

@@ -2481,8 +2481,7 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   if (d->warm >= 3 && !d->gram.p) {
     // the history ring takes 2 K vectors of S x 12 x cells doubles (25 GB at
     // C5, K = 8): shorten it to what fits in half of the free device memory
-    size_t fr = 0, tot = 0;
-    RTE_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t fr = device_free_bytes();
     const size_t per = sizeof(double) * (size_t)S * n * 2;
     const int fit = (int)std::min<size_t>(kHist, fr / 2 / per);
     if (fit < d->warm) d->warm = std::max(fit, 1);

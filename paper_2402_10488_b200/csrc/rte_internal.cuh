@@ -45,6 +45,18 @@ bool guard_enabled();
 void guard_register(void* base, size_t user_bytes);
 void guard_release(void* base);
 
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync
+// on the legacy stream) with an unbounded release threshold: memory a released
+// context returns stays mapped for the next one, so per-parameter setups and
+// solves do not pay the driver's page mapping again.  Frees are ordered after
+// all prior work (the private DSA stream is joined back into the caller's
+// stream at the end of every solve).
+void pool_init();
+void* pool_alloc(size_t bytes);
+void pool_free(void* p);
+// free device memory including what the pool holds but does not use
+size_t device_free_bytes();
+
 // Owning device buffer.
 template <typename T>
 struct DBuf {
@@ -75,7 +87,7 @@ struct DBuf {
         guard_release(base);
         cudaFree(base);
       } else {
-        cudaFree(p);
+        pool_free(p);
       }
     }
     p = nullptr;
@@ -94,7 +106,7 @@ struct DBuf {
       guard_register(base, bytes);
       p = reinterpret_cast<T*>(base + kGuardBytes);
     } else {
-      RTE_CUDA(cudaMalloc(&p, count * sizeof(T)));
+      p = static_cast<T*>(pool_alloc(count * sizeof(T)));
     }
     n = count;
   }
@@ -156,7 +168,6 @@ struct rte_ctx {
   int block = 1;
   double hx = 0, hy = 0;
   std::vector<double> bounds;
-  std::vector<double> mt_h, ms_h;  // host copies of the mass blocks (sample-major)
 
   // device problem data
   rte::DBuf<double> width;   // slab widths [N]

@@ -20,6 +20,8 @@
 // One CTA per sample; warps take directions in rounds; the sum
 // rho = sum_j w_j f_j is accumulated in shared memory in the fixed order
 // j = 0..n-1 (deterministic, like transport_system.cpp:398-401).
+#include <cstdlib>
+
 #include "rte_internal.cuh"
 #include "slab_dev.cuh"
 
@@ -133,11 +135,15 @@ int sweep1d_cpl(int N) {
 void slab_cache_ensure(rte_ctx* ctx, cudaStream_t st) {
   if (ctx->slab_cache_tried) return;
   ctx->slab_cache_tried = true;
+  static const bool off = [] {  // RTE_SLAB_CACHE=0: cell blocks on the fly (tests of that path)
+    const char* e = std::getenv("RTE_SLAB_CACHE");
+    return e && std::atoi(e) == 0;
+  }();
+  if (off) return;
   const int cpl = sweep1d_cpl(ctx->ncells);
   if (!cpl) return;
   const size_t n = (size_t)ctx->S * ctx->nv * 5 * 32 * cpl;
-  size_t fr = 0, tot = 0;
-  RTE_CUDA(cudaMemGetInfo(&fr, &tot));
+  const size_t fr = device_free_bytes();
   if (n * sizeof(double) > std::min<size_t>(fr / 4, (size_t)4 << 30)) return;  // on the fly instead
   ctx->slab_cache.alloc(n);
   ctx->slab_sc.alloc(ctx->ncells);

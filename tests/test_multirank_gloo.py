@@ -36,7 +36,7 @@ def _worker(rank, world, port, out):
 def test_two_rank_sharding_and_timing():
     world = 2
     port = _free_port()
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()  # no fork of a multi-threaded (OpenMP) parent
     out = mgr.dict()
     mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
     r0, r1 = out[0], out[1]
