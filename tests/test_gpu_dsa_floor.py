@@ -49,5 +49,5 @@ def test_floor_rule_matches_strict_and_oracle():
         assert rep_o.iterations == K and not rep_o.converged
         assert rel_l2(r1[s], rho_o) < 1e-10
         h_o = np.asarray(rep_o.change_history)
-        above = h_o > 1e-12 * np.abs(rho_o).max()
+        above = h_o > 1e-10 * np.abs(rho_o).max()  # well above the round-off of rho* - rho
         np.testing.assert_allclose(np.asarray(rep1[s].change_history)[above], h_o[above], rtol=1e-5)
