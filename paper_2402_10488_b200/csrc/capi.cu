@@ -1073,25 +1073,51 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
       throw;
     }
 
-    std::vector<double> resid(S, 0.0);
+    // Readback in (at most) two synchronisations: the report state, the
+    // residuals, the DSA status and -- when small -- the full history / log
+    // rows go to pinned staging in one batch; a large history is packed on the
+    // device to the batch's largest iteration count and copied second.
     if (cfg.compute_residual) {
       bits.zero(st);
       transport_apply(ctx, SRC_MS_RHO | SRC_G | SRC_BC, rho, rstar.p, nullptr, rho, delta.p, bits.p, st);
-      std::vector<unsigned long long> hb(2 * S);
-      RTE_CUDA(cudaMemcpy(hb.data(), bits.p, sizeof(unsigned long long) * 2 * S, cudaMemcpyDeviceToHost));
-      for (int s = 0; s < S; ++s) {
-        double v;
-        std::memcpy(&v, &hb[2 * s], sizeof(double));
-        resid[s] = v;
+    }
+    const int* dfail = need_dsa ? dsa_status_dev(ctx) : nullptr;
+    const size_t nrow = (size_t)S * cfg.max_iters;
+    const bool rows_now = (history || log) && nrow * (sizeof(double) + 1) <= ((size_t)1 << 20);
+    const size_t b_bits = sizeof(unsigned long long) * 2 * S, b_int = sizeof(int) * S * 8, b_last = sizeof(double) * S,
+                 b_fail = sizeof(int) * S, b_rows = rows_now ? nrow * (sizeof(double) + 1) : 0;
+    const size_t need0 = b_bits + b_int + b_last + b_fail + b_rows;
+    auto staging = [&](size_t need) -> char* {
+      if (ctx->pinned_hist_bytes < need) {
+        if (ctx->pinned_hist) cudaFreeHost(ctx->pinned_hist);
+        ctx->pinned_hist = nullptr;
+        ctx->pinned_hist_bytes = 0;
+        RTE_CUDA(cudaMallocHost(&ctx->pinned_hist, need));
+        ctx->pinned_hist_bytes = need;
       }
+      return static_cast<char*>(ctx->pinned_hist);
+    };
+    char* h0 = staging(need0);
+    unsigned long long* hb = reinterpret_cast<unsigned long long*>(h0);
+    int* hi = reinterpret_cast<int*>(h0 + b_bits);
+    double* hl = reinterpret_cast<double*>(h0 + b_bits + b_int);
+    int* hf = reinterpret_cast<int*>(h0 + b_bits + b_int + b_last);
+    double* hrow = reinterpret_cast<double*>(h0 + b_bits + b_int + b_last + b_fail);
+    char* lrow = reinterpret_cast<char*>(hrow + (rows_now ? nrow : 0));
+    if (cfg.compute_residual) RTE_CUDA(cudaMemcpyAsync(hb, bits.p, b_bits, cudaMemcpyDeviceToHost, st));
+    RTE_CUDA(cudaMemcpyAsync(hi, ibuf.p, b_int, cudaMemcpyDeviceToHost, st));
+    RTE_CUDA(cudaMemcpyAsync(hl, lastc.p, b_last, cudaMemcpyDeviceToHost, st));
+    if (dfail) RTE_CUDA(cudaMemcpyAsync(hf, dfail, b_fail, cudaMemcpyDeviceToHost, st));
+    if (rows_now) {
+      RTE_CUDA(cudaMemcpyAsync(hrow, hist.p, sizeof(double) * nrow, cudaMemcpyDeviceToHost, st));
+      RTE_CUDA(cudaMemcpyAsync(lrow, lg.p, nrow, cudaMemcpyDeviceToHost, st));
     }
     RTE_CUDA(cudaStreamSynchronize(st));
-    std::vector<int> hi((size_t)S * 8);
-    RTE_CUDA(cudaMemcpy(hi.data(), ibuf.p, sizeof(int) * S * 8, cudaMemcpyDeviceToHost));
-    std::vector<double> hl(S);
-    RTE_CUDA(cudaMemcpy(hl.data(), lastc.p, sizeof(double) * S, cudaMemcpyDeviceToHost));
+    std::vector<double> resid(S, 0.0);
+    if (cfg.compute_residual)
+      for (int s = 0; s < S; ++s) std::memcpy(&resid[s], &hb[2 * s], sizeof(double));
     std::vector<int> dstat(S, RTE_DSA_OK);
-    if (need_dsa) dsa_status_read(ctx, dstat.data(), st);
+    if (dfail) std::copy(hf, hf + S, dstat.begin());
     if (reports) {
       for (int s = 0; s < S; ++s) {
         rte_si_report& r = reports[s];
@@ -1106,37 +1132,43 @@ int rte_si_solve(rte_ctx* ctx, const rte_si_config* cfg_in, double* rho, rte_si_
       }
     }
     // history / log rows: only the first `width` entries (the batch's largest
-    // iteration count) are copied, packed, through pinned staging
+    // iteration count) are written
     int width = 0;
     for (int s = 0; s < S; ++s) width = std::max(width, hi[S + s]);
     if ((history || log) && width > 0) {
-      const size_t nh = (size_t)S * width;
-      DBuf<double>& hc = ctx->si_hist_c;
-      DBuf<char>& lc = ctx->si_log_c;
-      hc.ensure(nh);
-      lc.ensure(nh);
-      compact_rows_kernel<<<(unsigned)((nh + 255) / 256), 256, 0, st>>>(S, cfg.max_iters, width, hist.p, hc.p, lg.p,
-                                                                          lc.p);
-      RTE_CUDA(cudaGetLastError());
-      const size_t need = nh * (sizeof(double) + 1);
-      if (ctx->pinned_hist_bytes < need) {
-        if (ctx->pinned_hist) cudaFreeHost(ctx->pinned_hist);
-        ctx->pinned_hist = nullptr;
-        ctx->pinned_hist_bytes = 0;
-        RTE_CUDA(cudaMallocHost(&ctx->pinned_hist, need));
-        ctx->pinned_hist_bytes = need;
+      const double* hh = hrow;
+      const char* lh = lrow;
+      size_t rstride = (size_t)cfg.max_iters;
+      if (!rows_now) {  // pack on the device, then one more copy
+        const size_t nh = (size_t)S * width;
+        DBuf<double>& hc = ctx->si_hist_c;
+        DBuf<char>& lc = ctx->si_log_c;
+        hc.ensure(nh);
+        lc.ensure(nh);
+        compact_rows_kernel<<<(unsigned)((nh + 255) / 256), 256, 0, st>>>(S, cfg.max_iters, width, hist.p, hc.p,
+                                                                            lg.p, lc.p);
+        RTE_CUDA(cudaGetLastError());
+        char* h1 = staging(nh * (sizeof(double) + 1));  // the first batch has been consumed above
+        double* hp = reinterpret_cast<double*>(h1);
+        char* lp = reinterpret_cast<char*>(hp + nh);
+        RTE_CUDA(cudaMemcpyAsync(hp, hc.p, sizeof(double) * nh, cudaMemcpyDeviceToHost, st));
+        RTE_CUDA(cudaMemcpyAsync(lp, lc.p, nh, cudaMemcpyDeviceToHost, st));
+        RTE_CUDA(cudaStreamSynchronize(st));
+        hh = hp;
+        lh = lp;
+        rstride = (size_t)width;
       }
-      double* hh = reinterpret_cast<double*>(ctx->pinned_hist);
-      char* lh = reinterpret_cast<char*>(hh + nh);
-      RTE_CUDA(cudaMemcpyAsync(hh, hc.p, sizeof(double) * nh, cudaMemcpyDeviceToHost, st));
-      RTE_CUDA(cudaMemcpyAsync(lh, lc.p, nh, cudaMemcpyDeviceToHost, st));
-      RTE_CUDA(cudaStreamSynchronize(st));
       for (int s = 0; s < S; ++s) {
-        if (history) std::memcpy(history + (size_t)s * cfg.max_iters, hh + (size_t)s * width, sizeof(double) * width);
-        if (log) std::memcpy(log + (size_t)s * cfg.max_iters, lh + (size_t)s * width, width);
+        if (history) std::memcpy(history + (size_t)s * cfg.max_iters, hh + (size_t)s * rstride, sizeof(double) * width);
+        if (log) std::memcpy(log + (size_t)s * cfg.max_iters, lh + (size_t)s * rstride, width);
       }
     }
-    if (need_dsa) dsa_status_check(ctx, st, "si_solve: DSA correction");
+    for (int s = 0; s < S; ++s)
+      if (dstat[s] != RTE_DSA_OK) {
+        static const char* why[] = {"ok", "iteration cap reached", "breakdown", "non-finite residual"};
+        throw Error(RTE_ERR_RUNTIME, std::string("si_solve: DSA correction: coupled moment system solve failed at "
+                                                 "sample ") + std::to_string(s) + " (" + why[dstat[s] & 3] + ")");
+      }
   });
 }
 

@@ -414,6 +414,10 @@ void dsa_status_read(rte_ctx* ctx, int* host, cudaStream_t st) {
   else
     std::fill(host, host + ctx->S, 0);
 }
+const int* dsa2d_status_dev(rte_ctx* ctx);
+const int* dsa_status_dev(rte_ctx* ctx) {
+  return ctx->dsa && ctx->dsa->impl2d ? dsa2d_status_dev(ctx) : nullptr;
+}
 void dsa_history_reset(rte_ctx* ctx, cudaStream_t st) {
   if (ctx->dsa && ctx->dsa->impl2d) dsa2d_history_reset(ctx, st);
 }

@@ -2879,6 +2879,11 @@ void dsa2d_status_reset(rte_ctx* ctx, cudaStream_t st) {
   d->fail_init = true;
 }
 
+const int* dsa2d_status_dev(rte_ctx* ctx) {
+  auto* d = static_cast<Dsa2D*>(ctx->dsa->impl2d);
+  return d->fail_init ? d->fail.p : nullptr;
+}
+
 void dsa2d_status_read(rte_ctx* ctx, int* host, cudaStream_t st) {
   auto* d = static_cast<Dsa2D*>(ctx->dsa->impl2d);
   if (!d->fail_init) {

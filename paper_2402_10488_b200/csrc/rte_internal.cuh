@@ -380,6 +380,7 @@ long dsa_coupled_dim(const rte_ctx* ctx);
 void dsa_apply_eliminated(rte_ctx* ctx, const double* x, double* out, cudaStream_t st);
 void dsa_status_reset(rte_ctx* ctx, cudaStream_t st);
 void dsa_status_read(rte_ctx* ctx, int* host, cudaStream_t st);  // [S] rte_dsa_status
+const int* dsa_status_dev(rte_ctx* ctx);  // device [S] rte_dsa_status, or null (all OK / direct slab solve)
 void dsa_status_check(rte_ctx* ctx, cudaStream_t st, const char* what);
 void dsa_history_reset(rte_ctx* ctx, cudaStream_t st);
 
