@@ -91,6 +91,7 @@ struct Dsa2D {
     int maxit;
     cudaGraphExec_t exec;
     long launches;
+    bool loop;  // the whole solve loop: a conditional WHILE node around the iteration
   };
   std::vector<Graph> graphs;
   cudaStream_t gstream = nullptr;
@@ -114,6 +115,7 @@ struct Dsa2D {
   DBuf<int> fail;             // [S] worst rte_dsa_status since the last dsa2d_status_reset
   bool fail_init = false;
   DBuf<int> nact;
+  DBuf<int> itc;              // device iteration counter of the conditional-graph loop
   double tol = 1e-12;
   int maxit = 1000;
   int nu = 6;          // smoothing steps on the finest level
@@ -2462,6 +2464,50 @@ static void vcycle(Dsa2D* d, int l, const float* b, float* x, const int* act, cu
   RTE_CUDA(cudaGetLastError());
 }
 
+// Body tail of the conditional-graph solve loop: count the iteration and keep
+// looping while a sample is active and the cap is not reached.
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* __restrict__ nact, int* __restrict__ itc,
+                            int maxit) {
+  const int it = ++*itc;
+  cudaGraphSetConditional(h, (*nact > 0 && it < maxit) ? 1u : 0u);
+}
+
+// The whole BiCGStab loop as one graph: a WHILE conditional node whose body
+// is one iteration plus k_loop_cond (CUDA 12.4+ device-side loop control), so
+// a solve runs without host polls and stops after exactly the last needed
+// iteration.  Returns false when the driver cannot build it.
+template <typename F>
+static bool build_loop_graph(Dsa2D* d, F&& iteration, cudaGraphExec_t* exec) {
+  cudaGraph_t parent = nullptr;
+  if (cudaGraphCreate(&parent, 0) != cudaSuccess) return false;
+  cudaGraphConditionalHandle h;
+  cudaGraphNodeParams cp = {};
+  cudaGraphNode_t node;
+  bool ok = cudaGraphConditionalHandleCreate(&h, parent, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+  if (ok) {
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    ok = cudaGraphAddNode(&node, parent, nullptr, 0, &cp) == cudaSuccess;
+  }
+  if (ok) {
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    ok = cudaStreamBeginCaptureToGraph(d->gstream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
+         cudaSuccess;
+    if (ok) {
+      iteration(d->gstream);
+      k_loop_cond<<<1, 1, 0, d->gstream>>>(h, d->nact.p, d->itc.p, d->maxit);
+      cudaGraph_t done = nullptr;
+      ok = cudaStreamEndCapture(d->gstream, &done) == cudaSuccess;
+    }
+  }
+  if (ok) ok = cudaGraphInstantiate(exec, parent, 0) == cudaSuccess;
+  cudaGraphDestroy(parent);
+  if (!ok) cudaGetLastError();
+  return ok;
+}
+
 void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, int apply_ms, cudaStream_t st) {
   auto* d = static_cast<Dsa2D*>(ctx->dsa->impl2d);
   RTE_REQUIRE(d, RTE_ERR_INVALID, "dsa: rte_dsa_setup was not called");
@@ -2692,15 +2738,27 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     for (const auto& e : d->graphs)
       if (e.key == d->x.p && e.tols == ctx->dsa_tol_s && e.tol == d->tol && e.maxit == d->maxit) g = &e;
     if (!g) {
-      cudaGraph_t graph;
+      static const bool loop_off = [] {  // RTE_DSA_GRAPH_LOOP=0: host-polled iteration graphs
+        const char* e = std::getenv("RTE_DSA_GRAPH_LOOP");
+        return e && std::atoi(e) == 0;
+      }();
+      if (!d->itc.p) d->itc.alloc(1);
       const long n0 = d->nlaunch;
-      RTE_CUDA(cudaStreamBeginCapture(d->gstream, cudaStreamCaptureModeThreadLocal));
-      iteration(d->gstream);
-      RTE_CUDA(cudaStreamEndCapture(d->gstream, &graph));
-      Dsa2D::Graph e{d->x.p, ctx->dsa_tol_s, d->tol, d->maxit, nullptr, d->nlaunch - n0};
+      Dsa2D::Graph e{d->x.p, ctx->dsa_tol_s, d->tol, d->maxit, nullptr, 0, false};
+      if (!loop_off && build_loop_graph(d, iteration, &e.exec)) {
+        e.loop = true;
+        ++d->nlaunch;  // k_loop_cond
+      } else {
+        d->nlaunch = n0;
+        cudaGraph_t graph;
+        RTE_CUDA(cudaStreamBeginCapture(d->gstream, cudaStreamCaptureModeThreadLocal));
+        iteration(d->gstream);
+        RTE_CUDA(cudaStreamEndCapture(d->gstream, &graph));
+        RTE_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
+        RTE_CUDA(cudaGraphDestroy(graph));
+      }
+      e.launches = d->nlaunch - n0;
       d->nlaunch = n0;
-      RTE_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
-      RTE_CUDA(cudaGraphDestroy(graph));
       if (d->graphs.size() >= 16) d->clear_graphs();
       d->graphs.push_back(e);
       g = &d->graphs.back();
@@ -2709,7 +2767,16 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
     RTE_CUDA(cudaEventRecord(d->ev_in, st));
     RTE_CUDA(cudaStreamWaitEvent(q, d->ev_in, 0));
   }
-  for (; any_active && it < d->maxit; ++it) {
+  if (g && g->loop) {
+    // device-side loop: one launch, one synchronisation for the count
+    RTE_CUDA(cudaMemsetAsync(d->itc.p, 0, sizeof(int), q));
+    RTE_CUDA(cudaGraphLaunch(g->exec, q));
+    RTE_CUDA(cudaMemcpyAsync(nact_h, d->itc.p, sizeof(int), cudaMemcpyDeviceToHost, q));
+    RTE_CUDA(cudaStreamSynchronize(q));
+    it = *nact_h;
+    d->nlaunch += g->launches * it;
+  }
+  for (; any_active && it < d->maxit && !(g && g->loop); ++it) {
     if (g) {
       RTE_CUDA(cudaGraphLaunch(g->exec, q));
       d->nlaunch += g->launches;
