@@ -303,12 +303,20 @@ def run_b200(args, rank, world, device):
                       "kernel": "k_gs_rb<true,*> (finest-level DSA red-black block Gauss-Seidel colour half-sweep, fp32, blocked red-black layout)",
                       "per_launch_ms": gs_ms, "bytes_per_launch": gs_bytes,
                       "share_of_step": ms_k[5] / ms_total, "peak_kind": peak_kind} if gs_ach else None),
-        "sweep_roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic,
-                     "kernel": "sweep2d_kernel", "per_launch_ms": sweep_ms, "bytes_per_update": BYTES_PER_UPDATE,
-                     "share_of_step": ms_k[0] / ms_total, "peak_kind": peak_kind,
-                     "fp64": {"achieved_tflops": fp64_ach, "peak_tflops": tf.value, "frac": fp64_ach / tf.value,
-                              "flop_per_update": FLOP_PER_UPDATE, "peak_kind": "measured DFMA probe"}},
+        # the sweep reuses its operands on chip (one (rho, sigma) load serves 64
+        # directions), so FP64 issue, not HBM, binds it; its DRAM traffic
+        # (ncu) is the 4 quadrant partial fluxes written and read back plus
+        # the operands
+        "sweep_roofline": {"bound": "fp64", "achieved": fp64_ach, "peak": tf.value, "unit": "TFLOP/s",
+                           "frac": fp64_ach / tf.value, "flop_per_update": FLOP_PER_UPDATE,
+                           "peak_kind": "measured DFMA probe", "kernel": "sweep2d_kernel",
+                           "per_launch_ms": sweep_ms, "share_of_step": ms_k[0] / ms_total,
+                           "traffic": traffic,
+                           "operand_stream": {"achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                                              "frac": achieved / hbm_peak, "bytes_per_update": BYTES_PER_UPDATE,
+                                              "peak_kind": peak_kind,
+                                              "note": "SURVEY s8(d) accounting: sigma_t + 4 source moments per "
+                                                      "update, as if streamed per direction"}},
         "kernel_ms": {k: ms_k[i] for i, k in enumerate(capi.PROF_KINDS)},
         "sweep_only_updates_per_s": upd_step / (sweep_ms * 1e-3),
         "kernel_launches": {k: int(n_k[i]) for i, k in enumerate(capi.PROF_KINDS)},
