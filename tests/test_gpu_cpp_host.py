@@ -106,13 +106,15 @@ def test_cpp_problem_setup_c4_pin_cell(tmp_path):
     closures, psi, weighted_mass, project, build_masses combination) and
     solved with SI-DSA: bitwise equal to the Python host mirror's solve of the
     same parameters, identical iteration counts / logs to the oracle
-    (SuperLU DSA) on the first and last sample with flux within 1e-8."""
+    (SuperLU DSA) on the first and last sample with flux within 1e-8; then the
+    offline stage and ROMSAD run in C++ reproduce the Python mirror's
+    iteration counts, logs and switch iterations with fluxes to 1e-12."""
     from paper_2402_10488_b200 import configs, rte
     from tests.tools import parity_workers as pw
     exe = build_demo("pin_cell_demo")
     out = tmp_path / "rho.bin"
     eps = 1e-8
-    r = json.loads(subprocess.run([exe, "128", "64", repr(eps), str(out)], capture_output=True, text=True,
+    r = json.loads(subprocess.run([exe, "128", "64", repr(eps), str(out), "0", "40"], capture_output=True, text=True,
                                   check=True).stdout)
     mus = [s["mu"] for s in r["samples"]]
     assert len(mus) == 64 and r["k_terms"] == 5
@@ -130,3 +132,22 @@ def test_cpp_problem_setup_c4_pin_cell(tmp_path):
         o = pw.solve_sample(("c4", mus[s], ["DSA"], eps, "abs", 3, 0.0, None, None, True))["DSA"]
         assert r["samples"][s]["iterations"] == o["iterations"] and r["samples"][s]["log"] == o["log"]
         assert rel_l2(rho_cpp[s], o["rho"]) < 1e-8
+    # the offline stage (40 training samples, correction POD rank 20) and ROMSAD(theta = 5) in C++ against the
+    # Python mirror's same pipeline
+    train, _ = configs.c4_params(40, 64)
+    tb = rte.TransportBatch(configs.pin_cell(rte)(128), mesh, rte.chebyshev_legendre(16, 8), train)
+    snaps = rte.collect_snapshots(tb, 3, 1e-8)
+    U, sv = rte.pod(rte.snapshot_matrix(tb, snaps, "correction"), 20)
+    cm = rte.build_reduced_model(tb, U, sv, float(np.sum(sv[20:]) / np.sum(sv)), 1e-8, "c")
+    assert r["pod_cols"] == len(sv)
+    np.testing.assert_allclose(r["discarded_fraction"], cm.discarded_fraction, rtol=1e-12)
+    rte.load_rom(b, 1, cm)
+    cfg = rte.SolveConfig(eps_sisa=eps, norm="abs", theta=5, max_iters=500,
+                          eps_romsad=rte.romsad_tolerance(1e-8, cm.discarded_fraction))
+    rho_r, reps_r = rte.sisa_solve(b, "ROMSAD", cfg)
+    rho_r = rho_r.cpu().numpy()
+    rho_rc = np.fromfile(str(out) + ".romsad").reshape(64, -1)
+    for s, (c, p) in enumerate(zip(r["romsad"], reps_r)):
+        assert (c["converged"], c["iterations"], c["switch_iter"], c["log"]) == \
+            (int(p.converged), p.iterations, p.switch_iter, p.correction_log), s
+    assert max(rel_l2(rho_rc[s], rho_r[s]) for s in range(64)) < 1e-12
