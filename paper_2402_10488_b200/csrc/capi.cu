@@ -1304,7 +1304,11 @@ int rte_apply_kinetic(rte_ctx* ctx, const double* u, double* out, void* stream) 
 // ---- measurement ------------------------------------------------------------
 
 int rte_profile_enable(rte_ctx* ctx, int on) {
-  return guarded(ctx, [&] { ctx->prof = on != 0; });
+  return guarded(ctx, [&] {
+    // launches counted while profiling was off do not belong to the profile
+    if (on && !ctx->prof && ctx->geom == RTE_XY2D) dsa2d_take_launches(ctx);
+    ctx->prof = on != 0;
+  });
 }
 
 int rte_profile_read(rte_ctx* ctx, double* ms, long* n) {
