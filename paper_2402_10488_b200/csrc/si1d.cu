@@ -10,11 +10,13 @@
 //   the stop test / strategy choice (si_decide semantics: sisa.cpp:123-127,
 //                           strategies.cpp:55-76 monotone ROMSAD switch)
 //   the correction          DSA: block cyclic reduction of [Ms delta; 0]
-//                           (slab::cr_solve_cta, dsa.cpp:264-277);
-//                           ROMSA: U_rho A_r^{-1} U_iso^T Ms delta
-//                           (strategies.cpp:37-53)
+//                           (slab::cr_solve_compact, dsa.cpp:264-277), the
+//                           sample's factors held in shared memory when they
+//                           fit; ROMSA: U_rho A_r^{-1} U_iso^T Ms delta
+//                           (strategies.cpp:37-53), warp-parallel solve
 //   rho = rho* + correction
-// rho, rho*, delta and the cyclic-reduction vector live in shared memory; the
+// rho, rho*, delta (lane-major layout, slab_dev.cuh) and the cyclic-reduction
+// levels live in shared memory; the
 // per-sample report state (iterations, history, log, switch iteration,
 // convergence) is written to the same SiState arrays the per-kernel loop
 // fills, so rte_si_solve's reporting is shared.  Samples finish
