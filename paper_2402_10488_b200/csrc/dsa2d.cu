@@ -2046,6 +2046,10 @@ void dsa2d_setup(rte_ctx* ctx, cudaStream_t st) {
   const long cells = (long)S * ctx->nx * ctx->ny;
   d->nu = cells < (1l << 19) ? 10 : cells < (4l << 20) ? 6 : 4;
   d->nu_coarse = cells < (4l << 20) ? 1 : 2;
+  // history length of the warm start: each kept solution costs two vector
+  // passes per solve (Gram row, combination); below C5 scale 6 pays best
+  // (C4 SI-DSA 80.0 ms vs 82.0 with 8; C3 flat), at C5 8 (172 ms vs 175 with 6)
+  d->warm = cells < (4l << 20) ? 6 : kHist;
   if (const char* e = std::getenv("RTE_DSA_NU")) d->nu = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_NU_COARSE")) d->nu_coarse = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RTE_DSA_WARM")) d->warm = std::max(0, std::min(kHist, std::atoi(e)));

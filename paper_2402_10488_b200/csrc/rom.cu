@@ -19,6 +19,7 @@ struct RomState {
   DBuf<double> u_rho, u_iso, a_r, b_r;  // column-major as in the reference
   DBuf<double> lu;                      // [S][r][r] row-major factors
   DBuf<int> rp, cp, sing;               // [S][r], [S][r], [S]
+  DBuf<double> part, coef;              // batched correction: [chunks][S][r] partial projections, [S][r]
   bool factored = false;
 };
 
@@ -153,6 +154,109 @@ __global__ void rom_correct_kernel(const RomCorrectArgs a) {
     double t = 0.0;
     for (int k = 0; k < a.r; ++k) t = fma(a.u_rho[(long)k * a.nd + i], c[k], t);
     a.corr[(long)s * a.nd + i] = t;
+  }
+}
+
+// ---- batched ROMSA correction (the S per-sample GEMVs as two passes over the
+// basis: U_iso^T [Ms delta]_S and U_rho C_S) -----------------
+constexpr int kRomRows = 256;  // basis rows per CTA (staged in shared memory)
+
+// partial projections of the chunk's rows: part[c][s][k] = sum_i U_iso[k][i] (Ms delta_s)_i
+__global__ void __launch_bounds__(256) rom_proj_partial(int S, int r, int N, int block, long nd,
+                                                         const double* __restrict__ u_iso,
+                                                         const double* __restrict__ ms,
+                                                         const double* __restrict__ delta, const int* __restrict__ kind,
+                                                         double* __restrict__ part) {
+  extern __shared__ double us[];  // [r][kRomRows]
+  __shared__ double red[8][32];
+  const long i0 = (long)blockIdx.x * kRomRows;
+  const int rows = (int)min((long)kRomRows, nd - i0);
+  for (int e = threadIdx.x; e < r * kRomRows; e += blockDim.x) {
+    const int k = e / kRomRows, t = e - k * kRomRows;
+    us[e] = t < rows ? u_iso[(long)k * nd + i0 + t] : 0.0;
+  }
+  __syncthreads();
+  const int nl = (int)(nd / N);
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  for (int s = 0; s < S; ++s) {
+    if (kind[s] != KIND_ROMSA) continue;  // uniform over the CTA
+    const int t = threadIdx.x;
+    double m = 0.0;
+    if (t < rows) {  // (Ms delta)_i, as block_dots forms it
+      const long i = i0 + t;
+      const double* d = delta + (long)s * nd;
+      if (block == nl * nl) {
+        const long c = i / nl;
+        const int rr = (int)(i - c * nl);
+        const double* mm = ms + ((long)s * N + c) * block + nl * rr;
+        for (int q = 0; q < nl; ++q) m = fma(mm[q], d[nl * c + q], m);
+      } else {
+        m = ms[(long)s * N + i / nl] * d[i];
+      }
+    }
+    for (int k0 = 0; k0 < r; k0 += 32) {
+      // lanes of a warp: the chunk's partial for 32 modes at a time
+      double acc[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) acc[k] = (k0 + k < r) ? us[(k0 + k) * kRomRows + t] * m : 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+      // lane k keeps mode k0 + k of this warp's sum
+      double mine = 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        if (ln == k) mine = acc[k];
+      red[w][ln] = mine;
+      __syncthreads();
+      if (threadIdx.x < 32 && k0 + threadIdx.x < r) {
+        double v = 0.0;
+        for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) v += red[ww][threadIdx.x];
+        part[((long)blockIdx.x * S + s) * r + k0 + threadIdx.x] = v;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// one warp per ROMSA sample: fixed-order sum of the chunk partials, then the
+// reduced solve (r <= 32)
+__global__ void rom_proj_finish(int S, int r, int nchunks, const double* __restrict__ part, const double* lu,
+                                const int* rp, const int* cp, const int* __restrict__ kind, double* __restrict__ coef) {
+  __shared__ double rhs[4][32], cc[4][32];
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  const int s = blockIdx.x * 4 + w;
+  if (s >= S || kind[s] != KIND_ROMSA) return;
+  double v = 0.0;
+  if (ln < r)
+    for (int c = 0; c < nchunks; ++c) v += part[((long)c * S + s) * r + ln];
+  rhs[w][ln] = v;
+  __syncwarp();
+  warp_fullpiv_solve(lu + (long)s * r * r, r, rp + (long)s * r, cp + (long)s * r, rhs[w], cc[w]);
+  __syncwarp();
+  if (ln < r) coef[(long)s * r + ln] = cc[w][ln];
+}
+
+// corr_s = U_rho c_s for the ROMSA samples, the chunk of U_rho staged once
+__global__ void __launch_bounds__(256) rom_lift(int S, int r, long nd, const double* __restrict__ u_rho,
+                                                const double* __restrict__ coef, const int* __restrict__ kind,
+                                                double* __restrict__ corr) {
+  extern __shared__ double us[];  // [r][kRomRows]
+  const long i0 = (long)blockIdx.x * kRomRows;
+  const int rows = (int)min((long)kRomRows, nd - i0);
+  for (int e = threadIdx.x; e < r * kRomRows; e += blockDim.x) {
+    const int k = e / kRomRows, t = e - k * kRomRows;
+    us[e] = t < rows ? u_rho[(long)k * nd + i0 + t] : 0.0;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t >= rows) return;
+  for (int s = 0; s < S; ++s) {
+    if (kind[s] != KIND_ROMSA) continue;
+    const double* c = coef + (long)s * r;
+    double v = 0.0;
+    for (int k = 0; k < r; ++k) v = fma(us[k * kRomRows + t], c[k], v);
+    corr[(long)s * nd + i0 + t] = v;
   }
 }
 
@@ -311,9 +415,24 @@ void rom_setup(rte_ctx* ctx, int which, int* singular_dev, cudaStream_t st) {
 void rom_correct(rte_ctx* ctx, const double* delta, double* corr, const int* kind, cudaStream_t st) {
   RomState* m = ctx->rom[1];
   RTE_REQUIRE(m && m->factored, RTE_ERR_INVALID, "rom: correction model not set up");
-  RomCorrectArgs a{ctx->S, m->r, ctx->ncells, ctx->block, ctx->ndof, m->u_rho.p, m->u_iso.p, m->lu.p, m->rp.p,
+  const int S = ctx->S, r = m->r;
+  const long nd = ctx->ndof;
+  if (r <= 32) {  // batched: the basis is read once per correction, not once per sample
+    const int nchunks = (int)((nd + kRomRows - 1) / kRomRows);
+    m->part.ensure((size_t)nchunks * S * r);
+    m->coef.ensure((size_t)S * r);
+    const size_t smem = sizeof(double) * r * kRomRows;
+    rom_proj_partial<<<nchunks, 256, smem, st>>>(S, r, ctx->ncells, ctx->block, nd, m->u_iso.p, ctx->ms.p, delta,
+                                                 kind, m->part.p);
+    rom_proj_finish<<<(S + 3) / 4, 128, 0, st>>>(S, r, nchunks, m->part.p, m->lu.p, m->rp.p, m->cp.p, kind,
+                                                 m->coef.p);
+    rom_lift<<<nchunks, 256, smem, st>>>(S, r, nd, m->u_rho.p, m->coef.p, kind, corr);
+    RTE_CUDA(cudaGetLastError());
+    return;
+  }
+  RomCorrectArgs a{S, r, ctx->ncells, ctx->block, nd, m->u_rho.p, m->u_iso.p, m->lu.p, m->rp.p,
                    m->cp.p, ctx->ms.p, delta, corr, kind};
-  rom_correct_kernel<<<ctx->S, 256, 0, st>>>(a);
+  rom_correct_kernel<<<S, 256, 0, st>>>(a);
   RTE_CUDA(cudaGetLastError());
 }
 
