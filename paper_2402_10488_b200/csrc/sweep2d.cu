@@ -40,15 +40,38 @@ namespace {
 #ifndef RTE_SWEEP_MINB
 #define RTE_SWEEP_MINB 2
 #endif
+#ifndef RTE_SWEEP_KK_UNROLL
+#define RTE_SWEEP_KK_UNROLL 1
+#endif
+constexpr int kKU = RTE_SWEEP_KK_UNROLL;  // unroll of the step loop inside a chunk
 constexpr int kNW = RTE_SWEEP_NW;  // warps per CTA (direction subgroups)
 constexpr int kC = 4;    // steps per synchronisation chunk
 constexpr int kRC = 40;  // ring slots (columns): >= 31 + 2 * kC
 constexpr int kRP = 162; // ring slot pitch in doubles (5 comps x 32 rows, padded to even)
 
-struct DirConst {
-  double a, b, w, c4b, k1, a2, k2, a12, k6, tb, be, bcx, bcy, pad0;
+// Per-direction constants of the canonical cell solve, 16-byte aligned so the
+// pairs below load as one 128-bit shared-memory access each.
+struct __align__(16) DirConst {
+  double a, b;      // |vx|/hx, |vy|/hy
+  double sa, sb;    // sqrt3 a, sqrt3 b
+  double c4b, k1;   // del = sig (sig + 4b) + 6 (b^2 - a^2)
+  double a2, k2;    // al = 2a sig + 4ab + 4a^2
+  double cA, cB;    // diagonal shifts of G = (sig I + C) r: 3b + a, 3b + 3a
+  double cC, cD;    //                                          b + a,  b + 3a
+  double w, bcx;    // folded weight; unscaled x-face inflow trace (y-mode 0)
+  double bcy, pad0; // unscaled y-face inflow trace (x-mode 0)
   int dir0, dir1, pad1, pad2;
 };
+
+// The constants solve_cell reads, as 128-bit shared-memory loads.
+struct DirK {
+  double a, b, sa, sb, c4b, k1, a2, k2, cA, cB, cC, cD, w;
+};
+__device__ __forceinline__ DirK load_dirk(const DirConst* p) {
+  const double2* v = reinterpret_cast<const double2*>(p);
+  const double2 v0 = v[0], v1 = v[1], v2 = v[2], v3 = v[3], v4 = v[4], v5 = v[5], v6 = v[6];
+  return DirK{v0.x, v0.y, v1.x, v1.y, v2.x, v2.y, v3.x, v3.y, v4.x, v4.y, v5.x, v5.y, v6.x};
+}
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -80,57 +103,56 @@ __device__ __forceinline__ double fast_rcp(double x) {
 }
 
 // Canonical cell solve (see file header).  q: reflected source moments;
-// X: incoming x-face traces per y-mode (pre-scaled by a); Y: incoming
-// y-face traces per x-mode (pre-scaled by b).
-__device__ __forceinline__ void solve_cell(const DirConst& dc, double sig, double sig2, const double q[4], double X0,
-                                           double X1, double Y0, double Y1, double f[4], double& Xo0,
-                                           double& Xo1, double& Yo0, double& Yo1) {
+// x0, x1: incoming x-face traces per y-mode; y0, y1: incoming y-face traces
+// per x-mode (unscaled).  With r = q + face terms, the block is
+// B = sig I + I (x) aK + bK (x) I and B^-1 = E (sig I + C) with C a constant
+// per direction and E = [[e1, -e2], [e2, e3]] on each mode pair, where
+// del = sig (sig + 4b) + 6 (b^2 - a^2), al = 2a sig + 4ab + 4a^2,
+// n1 = del + 3 al, n3 = del + al, det = n1 n3 + 3 al^2,
+// e1 = n1 / det, e3 = n3 / det, e2 = sqrt3 al / det
+// (the closed form of (del I + al K)^-1 applied after (sig I + C); 56 FP64
+// instructions per cell-direction including the weighted accumulation).
+__device__ __forceinline__ void solve_cell(const DirK& dc, double sig, const double q[4], double x0, double x1,
+                                           double y0, double y1, double f[4], double& xo0, double& xo1,
+                                           double& yo0, double& yo1) {
   const double s3 = kSqrt3;
-  const double r00 = (q[0] + Y0) + X0;
-  const double r01 = fma(-s3, X0, q[1] + Y1);
-  const double r10 = fma(-s3, Y0, q[2] + X1);
-  const double r11 = fma(-s3, X1 + Y1, q[3]);
-  // Delta = del I + al K with del = sig^2 + 4 b sig + 6(b^2 - a^2),
-  // al = 2 a sig + 4 a b + 4 a^2; det(Delta) = del (del + 4 al) + 6 al^2.
-  const double del = fma(dc.c4b, sig, sig2 + dc.k1);
+  const double r00 = fma(dc.a, x0, fma(dc.b, y0, q[0]));
+  const double r01 = fma(-dc.sa, x0, fma(dc.b, y1, q[1]));
+  const double r10 = fma(-dc.sb, y0, fma(dc.a, x1, q[2]));
+  const double r11 = fma(-dc.sa, x1, fma(-dc.sb, y1, q[3]));
+  const double del = fma(sig, sig + dc.c4b, dc.k1);
   const double al = fma(dc.a2, sig, dc.k2);
-  const double al6 = fma(dc.a12, sig, dc.k6);
-  const double u4 = fma(4.0, al, del);
-  const double inv = fast_rcp(fma(del, u4, al6 * al));
-  const double c1 = u4 * inv, c2 = -al * inv;
-  const double p = sig + dc.b;
-  const double tt = p + dc.tb;
-  const double k00 = fma(s3, r01, r00), k01 = fma(3.0, r01, -s3 * r00);
-  const double k10 = fma(s3, r11, r10), k11 = fma(3.0, r11, -s3 * r10);
-  const double g00 = fma(tt, r00, fma(dc.a, k00, -dc.be * r10));
-  const double g01 = fma(tt, r01, fma(dc.a, k01, -dc.be * r11));
-  const double g10 = fma(p, r10, fma(dc.a, k10, dc.be * r00));
-  const double g11 = fma(p, r11, fma(dc.a, k11, dc.be * r01));
-  const double h00 = fma(s3, g01, g00), h01 = fma(3.0, g01, -s3 * g00);
-  const double h10 = fma(s3, g11, g10), h11 = fma(3.0, g11, -s3 * g10);
-  f[0] = fma(c1, g00, c2 * h00);
-  f[1] = fma(c1, g01, c2 * h01);
-  f[2] = fma(c1, g10, c2 * h10);
-  f[3] = fma(c1, g11, c2 * h11);
-  Xo0 = dc.a * fma(s3, f[1], f[0]);
-  Xo1 = dc.a * fma(s3, f[3], f[2]);
-  Yo0 = dc.b * fma(s3, f[2], f[0]);
-  Yo1 = dc.b * fma(s3, f[3], f[1]);
+  const double n1 = fma(3.0, al, del);
+  const double n3 = del + al;
+  const double inv = fast_rcp(fma(n1, n3, (3.0 * al) * al));
+  const double e1 = n1 * inv, e3 = n3 * inv, e2 = (s3 * al) * inv;
+  const double g00 = fma(sig + dc.cA, r00, fma(dc.sa, r01, -dc.sb * r10));
+  const double g01 = fma(sig + dc.cB, r01, fma(-dc.sa, r00, -dc.sb * r11));
+  const double g10 = fma(sig + dc.cC, r10, fma(dc.sa, r11, dc.sb * r00));
+  const double g11 = fma(sig + dc.cD, r11, fma(-dc.sa, r10, dc.sb * r01));
+  f[0] = fma(e1, g00, -e2 * g01);
+  f[1] = fma(e3, g01, e2 * g00);
+  f[2] = fma(e1, g10, -e2 * g11);
+  f[3] = fma(e3, g11, e2 * g10);
+  xo0 = fma(s3, f[1], f[0]);
+  xo1 = fma(s3, f[3], f[2]);
+  yo0 = fma(s3, f[2], f[0]);
+  yo1 = fma(s3, f[3], f[1]);
 }
 
 // General cell solve for full per-cell mass blocks (intra-cell-varying
 // coefficients): B = M + I (x) (a K) + (b K) (x) I with M the reflected 4x4
 // total-interaction block; LU without pivoting (the symmetric part of B is
 // positive definite), same face-trace algebra as solve_cell.
-__device__ __forceinline__ void solve_cell_full(const DirConst& dc, const double M[16], const double q[4], double X0,
-                                                double X1, double Y0, double Y1, double f[4], double& Xo0,
-                                                double& Xo1, double& Yo0, double& Yo1) {
+__device__ __forceinline__ void solve_cell_full(const DirK& dc, const double M[16], const double q[4], double x0,
+                                                double x1, double y0, double y1, double f[4], double& xo0,
+                                                double& xo1, double& yo0, double& yo1) {
   const double s3 = kSqrt3;
   double r[4];
-  r[0] = (q[0] + Y0) + X0;
-  r[1] = fma(-s3, X0, q[1] + Y1);
-  r[2] = fma(-s3, Y0, q[2] + X1);
-  r[3] = fma(-s3, X1 + Y1, q[3]);
+  r[0] = fma(dc.a, x0, fma(dc.b, y0, q[0]));
+  r[1] = fma(-dc.sa, x0, fma(dc.b, y1, q[1]));
+  r[2] = fma(-dc.sb, y0, fma(dc.a, x1, q[2]));
+  r[3] = fma(-dc.sa, x1, fma(-dc.sb, y1, q[3]));
   double B[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) B[e] = M[e];
@@ -167,10 +189,10 @@ __device__ __forceinline__ void solve_cell_full(const DirConst& dc, const double
     for (int j = i + 1; j < 4; ++j) v = fma(-B[i * 4 + j], f[j], v);
     f[i] = v * B[i * 4 + i];
   }
-  Xo0 = a * fma(s3, f[1], f[0]);
-  Xo1 = a * fma(s3, f[3], f[2]);
-  Yo0 = b * fma(s3, f[2], f[0]);
-  Yo1 = b * fma(s3, f[3], f[1]);
+  xo0 = fma(s3, f[1], f[0]);
+  xo1 = fma(s3, f[3], f[2]);
+  yo0 = fma(s3, f[2], f[0]);
+  yo1 = fma(s3, f[3], f[1]);
 }
 
 struct Smem {
@@ -216,13 +238,20 @@ __device__ __forceinline__ void issue_chunk_loads(const Sweep2DArgs& a, const Sm
       }
     }
   }
-  // band-boundary traces from the band below
-  if (band > 0) {
+  // band-boundary traces from the band below; the bottom band reads the
+  // inflow traces (y-face, x-mode 0) of its directions instead
+  {
     constexpr int ndir = kNW * D;
     for (int i = t; i < kC * ndir; i += blockDim.x) {
       const int kk = i / ndir, dd = i - kk * ndir;
       const int col = c0 + kk;
-      if (col < nx) cp_async16(sm.ystg + (((ybuf_slot * kC + kk) * ndir + dd) << 1), ybelow + (long)col * ndir + dd);
+      double* dst = sm.ystg + (((ybuf_slot * kC + kk) * ndir + dd) << 1);
+      if (band > 0) {
+        if (col < nx) cp_async16(dst, ybelow + (long)col * ndir + dd);
+      } else {
+        dst[0] = sm.tab[dd].bcy;
+        dst[1] = 0.0;
+      }
     }
   }
   cp_async_commit();
@@ -314,17 +343,21 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
       DirConst d;
       d.a = sl.a;
       d.b = sl.b;
+      d.sa = kSqrt3 * sl.a;
+      d.sb = kSqrt3 * sl.b;
       d.w = sl.w;
       d.c4b = 4.0 * sl.b;
       d.k1 = 6.0 * (sl.b * sl.b - sl.a * sl.a);
       d.a2 = 2.0 * sl.a;
       d.k2 = 4.0 * sl.a * sl.b + 4.0 * sl.a * sl.a;
-      d.a12 = 12.0 * sl.a;
-      d.k6 = 6.0 * d.k2;
-      d.tb = 2.0 * sl.b;
-      d.be = kSqrt3 * sl.b;
-      d.bcx = (a.mode & SRC_BC) ? sl.bcx : 0.0;
-      d.bcy = (a.mode & SRC_BC) ? sl.bcy : 0.0;
+      d.cA = 3.0 * sl.b + sl.a;
+      d.cB = 3.0 * sl.b + 3.0 * sl.a;
+      d.cC = sl.b + sl.a;
+      d.cD = sl.b + 3.0 * sl.a;
+      // Slot2D carries the inflow ghost traces scaled by a (x) / b (y)
+      d.bcx = (a.mode & SRC_BC) && sl.a > 0.0 ? sl.bcx / sl.a : 0.0;
+      d.bcy = (a.mode & SRC_BC) && sl.b > 0.0 ? sl.bcy / sl.b : 0.0;
+      d.pad0 = 0.0;
       d.dir0 = sl.dir0;
       d.dir1 = sl.dir1;
       sm.tab[i] = d;
@@ -336,10 +369,12 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
     const unsigned* prod = progress + ibase * nbands + band - 1;
 
     // prologue: columns [0, kC)
+#ifndef RTE_SWEEP_NOWAIT  // development bound only: drops the band hand-off (wrong answers)
     if (band > 0 && threadIdx.x == 0) {
       const unsigned need = (unsigned)min(nx, kC);
       while (ld_acquire(prod) < need) __nanosleep(64);
     }
+#endif
     __syncthreads();
     issue_chunk_loads<D>(a, sm, 0, band, qx, qy, s, ybelow, 0);
     cp_async_wait_all();
@@ -359,13 +394,15 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
     const int nsteps = nx + 31;
     int ys = 0;  // ystg slot holding the current chunk
     for (int k0 = 0; k0 < nsteps; k0 += kC) {
+#ifndef RTE_SWEEP_NOWAIT
       if (band > 0 && threadIdx.x == 0) {
         const unsigned need = (unsigned)min(nx, k0 + 2 * kC);
         while (ld_acquire(prod) < need) __nanosleep(64);
       }
+#endif
       __syncthreads();
       if (k0 + kC < nx) issue_chunk_loads<D>(a, sm, k0 + kC, band, qx, qy, s, ybelow, ys ^ 1);
-#pragma unroll 1
+#pragma unroll kKU
       for (int kk = 0; kk < kC; ++kk) {
         const int x = k0 + kk - lane;
         const bool ok = row_ok && x >= 0 && x < nx;
@@ -377,7 +414,6 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
         q[3] = rg[96];
         const double sig = ok ? rg[128] : 1.0;
         if (!ok) q[0] = q[1] = q[2] = q[3] = 0.0;
-        const double sig2 = sig * sig;
         double M[FULL ? 16 : 1];
         if (FULL) {
           // reflected full block of this lane's cell: M'_ij = s_i s_j M_ij, s = (1, sx, sy, sx sy)
@@ -390,23 +426,22 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
         }
         const double* yst = sm.ystg + ((ys * kC + kk) * ndir + warp * D) * 2;
         const bool lane0 = lane == 0;
-        const bool from_below = lane0 && band > 0;
         double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
         // Branch-free direction loop: the D chains are independent and the
         // compiler interleaves them (no reconvergence points inside).
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-          const DirConst& dc = sm.tab[warp * D + d];
-          const double ys0 = yst[2 * d], ys1 = yst[2 * d + 1];
+          const DirK dc = load_dirk(sm.tab + warp * D + d);
+          const double2 ysv = *reinterpret_cast<const double2*>(yst + 2 * d);
           double Y0 = __shfl_up_sync(0xffffffffu, Y[d][0], 1);
           double Y1 = __shfl_up_sync(0xffffffffu, Y[d][1], 1);
-          Y0 = lane0 ? (from_below ? ys0 : dc.bcy) : Y0;
-          Y1 = lane0 ? (from_below ? ys1 : 0.0) : Y1;
+          Y0 = lane0 ? ysv.x : Y0;
+          Y1 = lane0 ? ysv.y : Y1;
           double f[4], xo0, xo1, yo0, yo1;
           if (FULL)
             solve_cell_full(dc, M, q, X[d][0], X[d][1], Y0, Y1, f, xo0, xo1, yo0, yo1);
           else
-            solve_cell(dc, sig, sig2, q, X[d][0], X[d][1], Y0, Y1, f, xo0, xo1, yo0, yo1);
+            solve_cell(dc, sig, q, X[d][0], X[d][1], Y0, Y1, f, xo0, xo1, yo0, yo1);
           Y[d][0] = yo0;
           Y[d][1] = yo1;
           X[d][0] = ok ? xo0 : X[d][0];
@@ -421,13 +456,14 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
             const int ix = qx ? nx - 1 - x : x;
             const long pc = (long)(qy ? ny - 1 - yr : yr) * nx + ix;
             const double2 v01 = make_double2(f[0], sx * f[1]), v23 = make_double2(sy * f[2], sx * sy * f[3]);
-            if (dc.dir0 >= 0) {
-              double* o = a.fout + ((long)s * a.nv + dc.dir0) * nd + 4 * pc;
+            const DirConst& dcf = sm.tab[warp * D + d];
+            if (dcf.dir0 >= 0) {
+              double* o = a.fout + ((long)s * a.nv + dcf.dir0) * nd + 4 * pc;
               *reinterpret_cast<double2*>(o) = v01;
               *reinterpret_cast<double2*>(o + 2) = v23;
             }
-            if (dc.dir1 >= 0) {
-              double* o = a.fout + ((long)s * a.nv + dc.dir1) * nd + 4 * pc;
+            if (dcf.dir1 >= 0) {
+              double* o = a.fout + ((long)s * a.nv + dcf.dir1) * nd + 4 * pc;
               *reinterpret_cast<double2*>(o) = v01;
               *reinterpret_cast<double2*>(o + 2) = v23;
             }
