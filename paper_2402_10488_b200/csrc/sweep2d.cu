@@ -30,6 +30,7 @@
 // reciprocal, ~66 FP64 instructions per cell-direction).  It replaces the
 // 16-double cached inverse per slot and cell of the reference.
 #include "rte_internal.cuh"
+#include <type_traits>
 
 namespace rte {
 namespace {
@@ -43,6 +44,21 @@ namespace {
 #ifndef RTE_SWEEP_KK_UNROLL
 #define RTE_SWEEP_KK_UNROLL 1
 #endif
+#ifndef RTE_SWEEP_LEAD
+#define RTE_SWEEP_LEAD 4
+#endif
+#ifndef RTE_SWEEP_PUB
+#define RTE_SWEEP_PUB 1
+#endif
+// Columns the band below must have finished before an item starts (at least
+// one chunk).  Measured at C5 (RTE_SWEEP_DEBUG_WAIT): items spend ~1% of their
+// cycles in this start wait and ~12% in later chunk waits; a lead of 64
+// columns changes neither (2.4% / 12%), 256 moves the wait to the start (26% /
+// 4%) -- consecutive bands of a (sample, quadrant) chain are co-resident (296
+// CTA slots for 64 chains) and a consumer whose SM-mate idles catches up with
+// its producer whatever head start the producer had.
+constexpr int kLead = RTE_SWEEP_LEAD;
+constexpr int kPub = RTE_SWEEP_PUB;  // progress is published every kPub chunks (and at the end)
 constexpr int kKU = RTE_SWEEP_KK_UNROLL;  // unroll of the step loop inside a chunk
 constexpr int kNW = RTE_SWEEP_NW;  // warps per CTA (direction subgroups)
 constexpr int kC = 4;    // steps per synchronisation chunk
@@ -194,6 +210,15 @@ __device__ __forceinline__ void solve_cell_full(const DirK& dc, const double M[1
   yo0 = fma(s3, f[2], f[0]);
   yo1 = fma(s3, f[3], f[1]);
 }
+
+#ifdef RTE_SWEEP_DEBUG_WAIT
+__device__ unsigned long long g_dbg[8];  // [0] prologue wait, [1] chunk waits, [2] item cycles, [3] items, [4] polls
+#define DBG_T0() const long long dbg_t0 = clock64()
+#define DBG_ADD(i) atomicAdd(&g_dbg[i], (unsigned long long)(clock64() - dbg_t0))
+#else
+#define DBG_T0()
+#define DBG_ADD(i)
+#endif
 
 struct Smem {
   double* red;    // [kC][kNW][4][32]
@@ -368,11 +393,19 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
     double* part = a.part + ((long)(qd * a.groups + grp) * a.S + s) * nd;
     const unsigned* prod = progress + ibase * nbands + band - 1;
 
-    // prologue: columns [0, kC)
+    // prologue: columns [0, kC).  Thread 0 keeps the last progress value it
+    // observed (`seen`): once the band below runs ahead, most chunks need no
+    // poll at all.
+    unsigned seen = 0;
 #ifndef RTE_SWEEP_NOWAIT  // development bound only: drops the band hand-off (wrong answers)
+#ifdef RTE_SWEEP_DEBUG_WAIT
+    const long long dbg_item0 = clock64();
+#endif
     if (band > 0 && threadIdx.x == 0) {
-      const unsigned need = (unsigned)min(nx, kC);
-      while (ld_acquire(prod) < need) __nanosleep(64);
+      DBG_T0();
+      const unsigned need = (unsigned)min(nx, max(kC, kLead));
+      while ((seen = ld_acquire(prod)) < need) __nanosleep(64);
+      DBG_ADD(0);
     }
 #endif
     __syncthreads();
@@ -383,6 +416,7 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
 
     const int yr = band * 32 + lane;
     const bool row_ok = yr < ny;
+    const bool band_full = band * 32 + 31 < ny;
     double X[D][2], Y[D][2];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
@@ -397,16 +431,30 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
 #ifndef RTE_SWEEP_NOWAIT
       if (band > 0 && threadIdx.x == 0) {
         const unsigned need = (unsigned)min(nx, k0 + 2 * kC);
-        while (ld_acquire(prod) < need) __nanosleep(64);
+        if (seen < need) {
+          DBG_T0();
+          while ((seen = ld_acquire(prod)) < need) __nanosleep(64);
+          DBG_ADD(1);
+#ifdef RTE_SWEEP_DEBUG_WAIT
+          atomicAdd(&g_dbg[4], 1ull);
+#endif
+        }
       }
 #endif
       __syncthreads();
       if (k0 + kC < nx) issue_chunk_loads<D>(a, sm, k0 + kC, band, qx, qy, s, ybelow, ys ^ 1);
-#pragma unroll kKU
-      for (int kk = 0; kk < kC; ++kk) {
+      // One step of the wavefront for this lane's D directions.  EDGE = false
+      // is the interior version (every lane of the chunk solves a real cell:
+      // no validity selects); EDGE = true handles the fill / drain chunks and
+      // partial bands.  Lane 0's incoming y-traces (the band below's top
+      // traces, or the inflow values) are loaded into lane 31's Y registers,
+      // whose own traces went to `yabove` at the end of the previous step, so a
+      // rotating shuffle delivers every lane's incoming trace without a select.
+      auto step = [&](auto edge_tag, int kk) {
+        constexpr bool EDGE = decltype(edge_tag)::value;
         const int x = k0 + kk - lane;
-        const bool ok = row_ok && x >= 0 && x < nx;
-        const double* rg = sm.ring + (((x % kRC) + kRC) % kRC) * kRP + lane;
+        const bool ok = !EDGE || (row_ok && x >= 0 && x < nx);
+        const double* rg = sm.ring + (EDGE ? ((x % kRC) + kRC) % kRC : x % kRC) * kRP + lane;
         double q[4];
         q[0] = rg[0];
         q[1] = rg[32];
@@ -425,18 +473,19 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
           for (int e = 0; e < 16; ++e) M[e] = ok ? __ldg(m + e) * sg[e >> 2] * sg[e & 3] : (e % 5 == 0 ? 1.0 : 0.0);
         }
         const double* yst = sm.ystg + ((ys * kC + kk) * ndir + warp * D) * 2;
-        const bool lane0 = lane == 0;
         double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
         // Branch-free direction loop: the D chains are independent and the
         // compiler interleaves them (no reconvergence points inside).
 #pragma unroll
         for (int d = 0; d < D; ++d) {
           const DirK dc = load_dirk(sm.tab + warp * D + d);
-          const double2 ysv = *reinterpret_cast<const double2*>(yst + 2 * d);
-          double Y0 = __shfl_up_sync(0xffffffffu, Y[d][0], 1);
-          double Y1 = __shfl_up_sync(0xffffffffu, Y[d][1], 1);
-          Y0 = lane0 ? ysv.x : Y0;
-          Y1 = lane0 ? ysv.y : Y1;
+          if (lane == 31) {
+            const double2 ysv = *reinterpret_cast<const double2*>(yst + 2 * d);
+            Y[d][0] = ysv.x;
+            Y[d][1] = ysv.y;
+          }
+          const double Y0 = __shfl_sync(0xffffffffu, Y[d][0], lane + 31);
+          const double Y1 = __shfl_sync(0xffffffffu, Y[d][1], lane + 31);
           double f[4], xo0, xo1, yo0, yo1;
           if (FULL)
             solve_cell_full(dc, M, q, X[d][0], X[d][1], Y0, Y1, f, xo0, xo1, yo0, yo1);
@@ -478,6 +527,13 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
         rr[32] = acc1;
         rr[64] = acc2;
         rr[96] = acc3;
+      };
+      if (band_full && k0 >= 31 && k0 + kC <= nx) {
+#pragma unroll kKU
+        for (int kk = 0; kk < kC; ++kk) step(std::false_type{}, kk);
+      } else {
+#pragma unroll 1
+        for (int kk = 0; kk < kC; ++kk) step(std::true_type{}, kk);
       }
       cp_async_wait_all();
       __syncthreads();
@@ -507,12 +563,19 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
       }
       if (k0 + kC < nx) convert_chunk<FULL>(a, sm, k0 + kC, band, sx, sy, s, qx, qy);
       ys ^= 1;
-      if (threadIdx.x == 0 && band + 1 < nbands) {
+      if (threadIdx.x == 0 && band + 1 < nbands &&
+          (kPub == 1 || (k0 / kC) % kPub == kPub - 1 || k0 + kC >= nsteps)) {
         __threadfence();
         const int avail = min(nx, max(0, k0 + kC - 31));
         st_release(progress + ibase * nbands + band, (unsigned)avail);
       }
     }
+#ifdef RTE_SWEEP_DEBUG_WAIT
+    if (threadIdx.x == 0) {
+      atomicAdd(&g_dbg[2], (unsigned long long)(clock64() - dbg_item0));
+      atomicAdd(&g_dbg[3], 1ull);
+    }
+#endif
     __syncthreads();
   }
 }
@@ -542,6 +605,17 @@ void launch_d(const Sweep2DArgs& a, cudaStream_t st) {
   const int grid = (int)std::min<long>(total, max_ctas);
   sweep2d_kernel<D, KIN, FULL><<<grid, kNW * 32, smem, st>>>(a);
   RTE_CUDA(cudaGetLastError());
+#ifdef RTE_SWEEP_DEBUG_WAIT
+  {
+    unsigned long long h[8];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_dbg, sizeof(h));
+    fprintf(stderr, "sweep dbg: items %llu item-cycles %.3e prologue-wait %.3e (%.1f%%) chunk-wait %.3e (%.1f%%) polls/item %.1f\n",
+            h[3], (double)h[2], (double)h[0], 100.0 * h[0] / h[2], (double)h[1], 100.0 * h[1] / h[2], (double)h[4] / h[3]);
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_dbg, z, sizeof(z));
+  }
+#endif
 }
 
 __global__ void reduce_partials_kernel(int S, long nd, int nparts, const double* __restrict__ part,
