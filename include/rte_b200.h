@@ -260,6 +260,11 @@ int rte_dsa_correct(rte_ctx* ctx, const double* delta_dev, double* out_dev, void
 int rte_dsa_set_tolerance(rte_ctx* ctx, double tol, int max_iters);
 /* Krylov iterations of the last XY DSA solve (0 for slab: direct). */
 int rte_dsa_last_iterations(const rte_ctx* ctx);
+/* Krylov iteration counts (max over the samples) of the XY DSA solves since
+ * the start of the last rte_si_solve / rte_gmres_solve (or since the last
+ * direct DSA call): returns the number of solves logged (0 for slabs, < 0 on
+ * a device error) and writes the first min(that, cap) counts to out. */
+int rte_dsa_iteration_log(const rte_ctx* ctx, int* out, int cap);
 /* The XY solve starts from the minimal-residual combination of the sample's
  * last solutions (a warm start; the history holds up to 8 solution vectors and
  * their operator images, up to half of the free device memory, for the

@@ -406,6 +406,13 @@ class DsaOperator {  // dsa.hpp:29-56
     check(rte_dsa_set_tolerance(b_->handle(), tol, max_iters), b_->handle());
   }
   int last_iterations() const { return rte_dsa_last_iterations(b_->handle()); }
+  /* Krylov iteration counts of the XY DSA solves of the last solve call, one per correction */
+  std::vector<int> iteration_log() const {
+    std::vector<int> v(4096);
+    const int n = rte_dsa_iteration_log(b_->handle(), v.data(), (int)v.size());
+    v.resize(n < 0 ? 0 : std::min<size_t>((size_t)n, v.size()));
+    return v;
+  }
 
  private:
   TransportBatch* b_;

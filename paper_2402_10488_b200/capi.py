@@ -106,6 +106,7 @@ SIGNATURES = [
     ("rte_dsa_apply_eliminated", ctypes.c_int, [_vp, _vp, _vp, _vp]),
     ("rte_dsa_set_tolerance", ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_int]),
     ("rte_dsa_last_iterations", ctypes.c_int, [_vp]),
+    ("rte_dsa_iteration_log", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int), ctypes.c_int]),
     ("rte_dsa_reset_history", ctypes.c_int, [_vp, _vp]),
     ("rte_rom_load", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(Rom)]),
     ("rte_romig", ctypes.c_int, [_vp, _vp, _ip, _vp]),

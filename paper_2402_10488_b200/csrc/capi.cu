@@ -845,6 +845,11 @@ int rte_dsa_set_tolerance(rte_ctx* ctx, double tol, int max_iters) {
 
 int rte_dsa_last_iterations(const rte_ctx* ctx) { return ctx->geom == RTE_XY2D ? dsa2d_last_iters(ctx) : 0; }
 
+int rte_dsa_iteration_log(const rte_ctx* ctx, int* out, int cap) {
+  if (!ctx || ctx->geom != RTE_XY2D || (cap > 0 && !out)) return 0;
+  return dsa2d_iteration_log(ctx, out, cap);
+}
+
 int rte_rom_load(rte_ctx* ctx, int which, const rte_rom* rom) {
   return guarded(ctx, [&] {
     DeviceGuard dg(ctx->device);

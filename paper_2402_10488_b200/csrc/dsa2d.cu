@@ -61,6 +61,8 @@ struct Level {
   std::vector<double> nbr_h;
 };
 
+constexpr int kItLog = 4096;  // solves kept in the iteration log
+
 struct Dsa2D {
   int S = 0;
   std::vector<Level> L;
@@ -113,6 +115,7 @@ struct Dsa2D {
   DBuf<double> part, part2;   // dot partials [S][nblk][4] (two sets: producer / consumer overlap)
   DBuf<int> act;              // per-sample active flag
   DBuf<int> fail;             // [S] worst rte_dsa_status since the last dsa2d_status_reset
+  DBuf<int> itlog;            // [1 + kItLog] solves since the last reset and their BiCGStab iteration counts
   bool fail_init = false;
   DBuf<int> nact;
   DBuf<int> itc;              // device iteration counter of the conditional-graph loop
@@ -1662,9 +1665,18 @@ __global__ void k_bicg_init_warm(int S, int nblk, const double* part, const doub
 
 // per-sample failure codes of this solve folded into the running status
 // (the worst code since the last dsa2d_status_reset)
-__global__ void k_fail_accum(int S, const double* scal, int* fail) {
+// and the solve's iteration count (max over the samples) appended to the
+// context's solve log (itlog[0] = solves logged, itlog[1 + i] = count of solve i)
+__global__ void k_fail_accum(int S, const double* scal, int* fail, int* itlog, int cap) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s < S) fail[s] = max(fail[s], (int)scal[s * 16 + SC_FAIL]);
+  if (s == 0 && itlog) {
+    double mx = 0.0;
+    for (int k = 0; k < S; ++k) mx = fmax(mx, scal[k * 16 + SC_ITERS]);
+    const int i = itlog[0];
+    if (i < cap) itlog[1 + i] = (int)mx;
+    itlog[0] = i + 1;
+  }
 }
 
 __global__ void k_mark_prev(int S, const double* scal, int* has_prev) {
@@ -2828,10 +2840,12 @@ void dsa2d_solve(rte_ctx* ctx, const double* rhs, double* out, const int* kind, 
   if (!d->fail_init) {
     d->fail.ensure(S);
     d->fail.zero(st);
+    d->itlog.ensure(1 + kItLog);
+    d->itlog.zero(st);
     d->fail_init = true;
   }
   ++d->nlaunch;
-  k_fail_accum<<<(S + 127) / 128, 128, 0, st>>>(S, d->scal.p, d->fail.p);
+  k_fail_accum<<<(S + 127) / 128, 128, 0, st>>>(S, d->scal.p, d->fail.p, d->itlog.p, kItLog);
   ++d->nlaunch;
   k_unpack<<<nblocks((long)S * l0.nc), 256, 0, st>>>(S, l0.nc, d->x.p, out, kind);
   RTE_CUDA(cudaGetLastError());
@@ -2943,10 +2957,28 @@ int dsa2d_last_iters(const rte_ctx* ctx) {
   return (int)mx;
 }
 
+// BiCGStab iteration counts (max over the samples) of the solves since the
+// last dsa2d_status_reset (the start of the last rte_si_solve / rte_gmres_solve
+// or direct DSA call): returns the number of solves, writes up to cap counts
+int dsa2d_iteration_log(const rte_ctx* ctx, int* out, int cap) {
+  if (!ctx->dsa || !ctx->dsa->impl2d) return 0;
+  const auto* d = static_cast<const Dsa2D*>(ctx->dsa->impl2d);
+  if (!d->itlog.p) return 0;
+  std::vector<int> h(1 + kItLog);
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpy(h.data(), d->itlog.p, sizeof(int) * h.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  const int n = h[0];
+  for (int i = 0; i < n && i < cap && i < kItLog; ++i) out[i] = h[1 + i];
+  return n;
+}
+
 void dsa2d_status_reset(rte_ctx* ctx, cudaStream_t st) {
   auto* d = static_cast<Dsa2D*>(ctx->dsa->impl2d);
   d->fail.ensure(d->S);
   d->fail.zero(st);
+  d->itlog.ensure(1 + kItLog);
+  d->itlog.zero(st);
   d->fail_init = true;
 }
 

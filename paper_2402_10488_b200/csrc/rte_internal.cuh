@@ -374,6 +374,7 @@ void dsa_setup(rte_ctx* ctx, cudaStream_t st);
 void dsa_solve_density(rte_ctx* ctx, const double* rhs, double* out, const int* kind_mask, cudaStream_t st);
 void dsa_destroy(DsaState* d);
 int dsa2d_last_iters(const rte_ctx* ctx);
+int dsa2d_iteration_log(const rte_ctx* ctx, int* out, int cap);
 long dsa2d_take_launches(rte_ctx* ctx);
 void dsa2d_set_tolerance(rte_ctx* ctx, double tol, int maxit);
 long dsa_coupled_dim(const rte_ctx* ctx);

@@ -65,6 +65,48 @@ constexpr int kC = 4;    // steps per synchronisation chunk
 constexpr int kRC = 40;  // ring slots (columns): >= 31 + 2 * kC
 constexpr int kRP = 162; // ring slot pitch in doubles (5 comps x 32 rows, padded to even)
 
+// Bulk staging (TMA bulk copies, used when nx is a multiple of kC so every row
+// segment is 16-byte aligned): each band row's kC cells of rho / G / sigma_t /
+// sigma_s and the chunk's band-below traces are contiguous in global memory
+// and arrive by cp.async.bulk into row-major stage arrays (padded pitches
+// against bank conflicts), completion counted on an mbarrier.
+constexpr int kSP4 = 4 * kC + 2;  // row pitch (doubles) of the staged rho / G rows
+constexpr int kSP1 = kC + 2;      // row pitch of the staged sigma_t / sigma_s rows
+constexpr int kStageDoubles = 2 * 32 * kSP4 + 2 * 32 * kSP1;  // >= kC * 32 * 10 of the cp.async layout
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_inval(unsigned long long* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  const unsigned addr = smem_u32(bar);
+  unsigned done = 0;
+  for (unsigned spins = 0; !done; ++spins) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (!done && spins > (1u << 24)) __trap();  // a lost bulk copy must not hang the device
+  }
+}
+// global -> shared bulk copy (bytes and both addresses multiples of 16), completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // Per-direction constants of the canonical cell solve, 16-byte aligned so the
 // pairs below load as one 128-bit shared-memory access each.
 struct __align__(16) DirConst {
@@ -223,7 +265,9 @@ __device__ unsigned long long g_dbg[8];  // [0] prologue wait, [1] chunk waits, 
 struct Smem {
   double* red;    // [kC][kNW][4][32]
   double* ring;   // [kRC][kRP]: comps 0..3 = reflected q, 4 = sigma_t; row fastest
-  double* stage;  // [kC*32][10]: raw rho(4), G(4), sigma_t, sigma_s of the next columns
+  double* stage;  // cp.async path: [kC*32][10] raw rho(4), G(4), sigma_t, sigma_s of the next columns;
+                  // bulk path: rho rows [32][kSP4], G rows [32][kSP4], sigma_t rows [32][kSP1], sigma_s rows [32][kSP1]
+  unsigned long long* bar;  // mbarrier of the bulk staging
   double* ystg;   // [2][kC][ndir][2]
   DirConst* tab;  // [ndir]
 };
@@ -282,15 +326,83 @@ __device__ __forceinline__ void issue_chunk_loads(const Sweep2DArgs& a, const Sm
   cp_async_commit();
 }
 
+// Bulk-copy version of issue_chunk_loads (nx % kC == 0): one copy per band row
+// and array (threads 0..127: row = t % 32, array = t / 32), one for the chunk's
+// band-below traces; thread 0 posts the expected byte count first.
+template <int D>
+__device__ __forceinline__ void issue_chunk_bulk(const Sweep2DArgs& a, const Smem& sm, int c0, int band, int qx,
+                                                 int qy, int s, const double2* ybelow, int ybuf_slot) {
+  constexpr int ndir = kNW * D;
+  const int nx = a.nx, ny = a.ny;
+  const long ncell = (long)nx * ny, nd = 4 * ncell;
+  const int t = threadIdx.x;
+  const bool want_rho = (a.mode & (SRC_MS_RHO | SRC_RAW)) != 0, want_g = (a.mode & SRC_G) != 0;
+  if (t == 0) {
+    const int rows = min(32, ny - band * 32);
+    unsigned bytes = (unsigned)rows * (2u * kC * 8u + (want_rho ? 4u * kC * 8u : 0u) + (want_g ? 4u * kC * 8u : 0u));
+    if (band > 0) bytes += (unsigned)(kC * ndir * sizeof(double2));
+    mbar_arrive_expect_tx(sm.bar, bytes);
+  }
+  __syncwarp();
+  if (t < 128) {
+    const int row = t & 31, arr = t >> 5;
+    const int yrow = band * 32 + row;
+    if (yrow < ny) {
+      const int ix0 = qx ? nx - c0 - kC : c0;  // the chunk's kC cells are contiguous along x (reversed when reflected)
+      const long pc = (long)(qy ? ny - 1 - yrow : yrow) * nx + ix0;
+      if (arr == 0) {
+        if (want_rho) bulk_g2s(sm.stage + row * kSP4, a.rho + (long)s * nd + 4 * pc, 4 * kC * 8, sm.bar);
+      } else if (arr == 1) {
+        if (want_g)
+          bulk_g2s(sm.stage + 32 * kSP4 + row * kSP4, a.g + (a.g_shared ? 0 : (long)s * nd) + 4 * pc, 4 * kC * 8,
+                   sm.bar);
+      } else if (arr == 2) {
+        bulk_g2s(sm.stage + 64 * kSP4 + row * kSP1, a.sig_t + (long)s * ncell + pc, kC * 8, sm.bar);
+      } else {
+        bulk_g2s(sm.stage + 64 * kSP4 + 32 * kSP1 + row * kSP1, a.sig_s + (long)s * ncell + pc, kC * 8, sm.bar);
+      }
+    }
+  } else if (t == 128 && band > 0) {
+    bulk_g2s(sm.ystg + (size_t)ybuf_slot * kC * ndir * 2, ybelow + (long)c0 * ndir, kC * ndir * sizeof(double2),
+             sm.bar);
+  }
+  if (band == 0) {
+    // the bottom band reads the inflow traces (y-face, x-mode 0) of its directions
+    for (int i = t; i < kC * ndir; i += blockDim.x) {
+      const int dd = i % ndir;
+      double* dst = sm.ystg + (((size_t)ybuf_slot * kC * ndir + i) << 1);
+      dst[0] = sm.tab[dd].bcy;
+      dst[1] = 0.0;
+    }
+  }
+}
+
 // stage -> ring (reflected source moments + sigma_t) for columns c0..c0+kC-1
-template <bool FULL>
+template <bool FULL, bool BULK>
 __device__ __forceinline__ void convert_chunk(const Sweep2DArgs& a, const Smem& sm, int c0, int band, double sx,
                                               double sy, int s, int qx, int qy) {
   const int t = threadIdx.x;
   if (t >= kC * 32) return;
   const int col = c0 + (t >> 5), row = t & 31;
   const bool ok = col < a.nx && band * 32 + row < a.ny;
-  const double* r = sm.stage + t * 10;
+  double r[10];
+  if (BULK) {
+    // row-major staged rows; the cells of a reflected chunk arrive in reverse order
+    const int j = qx ? kC - 1 - (t >> 5) : (t >> 5);
+    const double* pr = sm.stage + row * kSP4 + 4 * j;
+    const double* pg = pr + 32 * kSP4;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      r[e] = pr[e];
+      r[4 + e] = pg[e];
+    }
+    r[8] = sm.stage[64 * kSP4 + row * kSP1 + j];
+    r[9] = sm.stage[64 * kSP4 + 32 * kSP1 + row * kSP1 + j];
+  } else {
+    const double* pr = sm.stage + t * 10;
+#pragma unroll
+    for (int e = 0; e < 10; ++e) r[e] = pr[e];
+  }
   double q0 = 0, q1 = 0, q2 = 0, q3 = 0, sg = 1.0;
   if (ok) {
     sg = r[8];
@@ -333,7 +445,14 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
   sm.red = smraw;
   sm.ring = sm.red + kC * kNW * 4 * 32;
   sm.stage = sm.ring + kRC * kRP;
-  sm.ystg = sm.stage + kC * 32 * 10;
+  sm.ystg = sm.stage + kStageDoubles;
+  __shared__ __align__(8) unsigned long long stage_bar;
+  sm.bar = &stage_bar;
+#ifdef RTE_SWEEP_NOBULK
+  const bool bulk = false;
+#else
+  const bool bulk = a.nx % kC == 0;
+#endif
   sm.tab = reinterpret_cast<DirConst*>(sm.ystg + 2 * kC * ndir * 2);
   __shared__ int item_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -363,6 +482,8 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
     }
     const int qx = qd & 1, qy = qd >> 1;
     const double sx = qx ? -1.0 : 1.0, sy = qy ? -1.0 : 1.0;
+    // every item starts the staging barrier at phase 0 (one arrival: thread 0's expect_tx)
+    if (bulk && threadIdx.x == 0) mbar_init(sm.bar, 1);
     for (int i = threadIdx.x; i < ndir; i += blockDim.x) {
       const Slot2D sl = a.slots[qd * a.nq_pad + grp * ndir + i];
       DirConst d;
@@ -409,10 +530,18 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
     }
 #endif
     __syncthreads();
-    issue_chunk_loads<D>(a, sm, 0, band, qx, qy, s, ybelow, 0);
-    cp_async_wait_all();
+    if (bulk) {
+      issue_chunk_bulk<D>(a, sm, 0, band, qx, qy, s, ybelow, 0);
+      mbar_wait(sm.bar, 0);
+    } else {
+      issue_chunk_loads<D>(a, sm, 0, band, qx, qy, s, ybelow, 0);
+      cp_async_wait_all();
+    }
     __syncthreads();
-    convert_chunk<FULL>(a, sm, 0, band, sx, sy, s, qx, qy);
+    if (bulk)
+      convert_chunk<FULL, true>(a, sm, 0, band, sx, sy, s, qx, qy);
+    else
+      convert_chunk<FULL, false>(a, sm, 0, band, sx, sy, s, qx, qy);
 
     const int yr = band * 32 + lane;
     const bool row_ok = yr < ny;
@@ -442,7 +571,12 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
       }
 #endif
       __syncthreads();
-      if (k0 + kC < nx) issue_chunk_loads<D>(a, sm, k0 + kC, band, qx, qy, s, ybelow, ys ^ 1);
+      if (k0 + kC < nx) {
+        if (bulk)
+          issue_chunk_bulk<D>(a, sm, k0 + kC, band, qx, qy, s, ybelow, ys ^ 1);
+        else
+          issue_chunk_loads<D>(a, sm, k0 + kC, band, qx, qy, s, ybelow, ys ^ 1);
+      }
       // One step of the wavefront for this lane's D directions.  EDGE = false
       // is the interior version (every lane of the chunk solves a real cell:
       // no validity selects); EDGE = true handles the fill / drain chunks and
@@ -535,7 +669,13 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
 #pragma unroll 1
         for (int kk = 0; kk < kC; ++kk) step(std::true_type{}, kk);
       }
-      cp_async_wait_all();
+      // the next chunk's staged data: bulk copies complete on the mbarrier
+      // (phase parity = chunk index), cp.async copies on the thread's group
+      if (bulk) {
+        if (k0 + kC < nx) mbar_wait(sm.bar, ((k0 + kC) / kC) & 1);
+      } else {
+        cp_async_wait_all();
+      }
       __syncthreads();
       // fixed-order reduction over the warps (direction subgroups) of the chunk
       {
@@ -561,7 +701,12 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
           }
         }
       }
-      if (k0 + kC < nx) convert_chunk<FULL>(a, sm, k0 + kC, band, sx, sy, s, qx, qy);
+      if (k0 + kC < nx) {
+        if (bulk)
+          convert_chunk<FULL, true>(a, sm, k0 + kC, band, sx, sy, s, qx, qy);
+        else
+          convert_chunk<FULL, false>(a, sm, k0 + kC, band, sx, sy, s, qx, qy);
+      }
       ys ^= 1;
       if (threadIdx.x == 0 && band + 1 < nbands &&
           (kPub == 1 || (k0 / kC) % kPub == kPub - 1 || k0 + kC >= nsteps)) {
@@ -576,13 +721,14 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
       atomicAdd(&g_dbg[3], 1ull);
     }
 #endif
+    if (bulk && threadIdx.x == 0) mbar_inval(sm.bar);  // every phase was waited for before the last chunk barrier
     __syncthreads();
   }
 }
 
 template <int D>
 size_t smem_bytes() {  // NOLINT
-  return sizeof(double) * ((size_t)kC * kNW * 4 * 32 + (size_t)kRC * kRP + (size_t)kC * 32 * 10 +
+  return sizeof(double) * ((size_t)kC * kNW * 4 * 32 + (size_t)kRC * kRP + (size_t)kStageDoubles +
                            (size_t)2 * kC * kNW * D * 2) +
          sizeof(DirConst) * kNW * D;
 }

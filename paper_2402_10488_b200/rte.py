@@ -479,6 +479,16 @@ class DsaOperator:
     def last_iterations(self) -> int:
         return capi.load().rte_dsa_last_iterations(self.batch._h)
 
+    def iteration_log(self, cap: int = 4096):
+        """Krylov iteration counts (max over the samples) of the XY DSA solves
+        of the last sisa_solve / gmres_solve, one per correction."""
+        import ctypes
+        buf = (ctypes.c_int * cap)()
+        n = capi.load().rte_dsa_iteration_log(self.batch._h, buf, cap)
+        if n < 0:
+            raise capi.RteError("rte_dsa_iteration_log failed")
+        return [int(buf[i]) for i in range(min(n, cap))]
+
     def solve_density(self, rhs):
         b = self.batch
         rhs = b._dev(rhs, (b.S, b.nd))
