@@ -256,7 +256,24 @@ def run_b200(args, rank, world, device):
         strict = {"ms_per_step": ms_s / args.steps, "value": aggregate_value(upd_step, args.steps, world, ms_s),
                   "final_flux_max_rel_l2_vs_floor_rule": rel,
                   "dsa": "every DSA solve to rel. residual %g" % args.dsa_tol}
-        del rho_s
+        # and with the DSA solved inexactly (relative residual 1e-2, a common
+        # production choice: the outer iteration contracts by ~0.1 + 1e-2 instead
+        # of ~0.1 per step, so 20 iterations still end at the same flux; the
+        # intermediate iterates differ from the exact-DSA ones, so this is a
+        # reported comparison, not the headline)
+        dsa.set_tolerance(1e-2, 2000)
+        torch.cuda.synchronize()
+        e0.record()
+        rho_i, _ = solve(args.steps, rho_start, floor=0.0)
+        e1.record()
+        torch.cuda.synchronize()
+        ms_i = max_over_ranks(e0.elapsed_time(e1), world, device)
+        strict["inexact_dsa_1e-2"] = {
+            "ms_per_step": ms_i / args.steps, "value": aggregate_value(upd_step, args.steps, world, ms_i),
+            "final_flux_max_rel_l2_vs_strict": ((rho_i - rho_s).norm(dim=1) / rho_s.norm(dim=1)).max().item(),
+            "bicgstab_iterations_per_step": dsa.iteration_log()}
+        dsa.set_tolerance(args.dsa_tol, 2000)
+        del rho_s, rho_i
     value = aggregate_value(upd_step, args.steps, world, ms_max)
     n_dof = batch.n_dof()
     batch = rho = reps = dsa = None  # release the timed context (~55 GB at C5) before the e2e one

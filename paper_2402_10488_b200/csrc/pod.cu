@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "rte_internal.cuh"
+#include <cstdlib>
 
 namespace rte {
 namespace {
@@ -98,8 +99,9 @@ __global__ void k_rmul(long m, int n, int k, const double* __restrict__ A, const
 // ---- blocked kernels for p, q, n, k <= 128 (all POD shapes of the configs) ----
 // One CTA reads each row chunk of A and B once and accumulates the whole
 // p x q product (16 x 16 threads, 8 x 8 outputs each, columns strided by 16
-// so shared-memory reads are conflict-free).  FP64 on the CUDA cores: the
-// B200 FP64 tensor rate is not higher than the DFMA rate for this shape.
+// so shared-memory reads are conflict-free).  CUDA-core FP64 version, kept as
+// the RTE_POD_DMMA=0 comparison: 21.5 ms for the C4 correction matrix
+// (8.4M x 120) against 9.0 ms for the tensor-core kernel k_gram_dmma below.
 constexpr int kW = 128;         // max columns
 constexpr int kGR = 16;         // rows per shared-memory stage
 constexpr int kGChunk = 16384;  // rows per CTA
@@ -169,6 +171,95 @@ __global__ void __launch_bounds__(512) k_gram_wide(long m, int p, int q, const d
     for (int b = 0; b < 8; ++b) o[(ty + 32 * a) * kW + tx + 16 * b] = acc[a][b];
 }
 
+// ---- FP64 tensor-core Gram (DMMA: mma.sync m8n8k4 f64) --------------------
+// C = A^T B for p, q <= 128: a CTA of 16 warps (4 x 4) accumulates the whole
+// 128 x 128 product of its row range; each warp owns a 32 x 32 block as 4 x 4
+// m8n8 accumulator tiles (32 doubles per lane) and per 4 rows issues 16 DMMAs
+// from 8 fragment loads (the CUDA-core version needs 12 shared-memory loads
+// per 32 DFMAs and reached a third of the FP64 peak).  Rows are staged column
+// by column (the matrices are column-major, rows contiguous) with a pitch of
+// kDR + 4 doubles, which makes the (row, column) fragment reads of every
+// half-warp hit 16 distinct banks.  Partial products per CTA, summed by
+// k_gram_wide_reduce in a fixed order (deterministic).
+constexpr int kDR = 32;       // rows per shared-memory stage
+constexpr int kDP = kDR + 4;  // staged column pitch in doubles
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(512, 1) k_gram_dmma(long m, long rows_per_cta, int p, int q,
+                                                      const double* __restrict__ A, const double* __restrict__ B,
+                                                      double* __restrict__ part) {
+  extern __shared__ double gsm[];
+  double* sa = gsm;                  // [2][kW][kDP]
+  double* sb = gsm + 2 * kW * kDP;   // [2][kW][kDP]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wi = warp >> 2, wj = warp & 3, g = lane >> 2, t4 = lane & 3;
+  const long r0 = (long)blockIdx.x * rows_per_cta;
+  const long r1 = min(m, r0 + rows_per_cta);
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  constexpr int kPer = kDR * kW / 512;  // elements per thread per matrix and stage
+  double ra[kPer], rb_[kPer];
+  auto load = [&](long rb) {
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int e = threadIdx.x + t * 512;
+      const int rr = e % kDR, cc = e / kDR;  // a warp reads kDR consecutive rows of one column
+      const long row = rb + rr;
+      ra[t] = (row < r1 && cc < p) ? __ldg(A + (long)cc * m + row) : 0.0;
+      rb_[t] = (row < r1 && cc < q) ? __ldg(B + (long)cc * m + row) : 0.0;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int e = threadIdx.x + t * 512;
+      sa[(buf * kW + e / kDR) * kDP + e % kDR] = ra[t];
+      sb[(buf * kW + e / kDR) * kDP + e % kDR] = rb_[t];
+    }
+  };
+  int buf = 0;
+  load(r0);
+  store(0);
+  __syncthreads();
+  for (long rb = r0; rb < r1; rb += kDR) {
+    const bool more = rb + kDR < r1;
+    if (more) load(rb + kDR);
+    const double* pa = sa + (buf * kW + 32 * wi + g) * kDP + t4;
+    const double* pb = sb + (buf * kW + 32 * wj + g) * kDP + t4;
+#pragma unroll
+    for (int kk = 0; kk < kDR / 4; ++kk) {
+      double va[4], vb[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) va[a] = pa[8 * a * kDP + 4 * kk];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) vb[b] = pb[8 * b * kDP + 4 * kk];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], va[a], vb[b]);
+    }
+    if (more) store(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+  double* o = part + (long)blockIdx.x * kW * kW;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = 32 * wi + 8 * a + g, j = 32 * wj + 8 * b + 2 * t4;
+      *reinterpret_cast<double2*>(o + i * kW + j) = make_double2(acc[a][b][0], acc[a][b][1]);
+    }
+}
+
 __global__ void k_gram_wide_reduce(int nchunks, int p, int q, const double* __restrict__ part,
                                    double* __restrict__ C) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -230,6 +321,88 @@ __global__ void __launch_bounds__(256) k_rmul_wide(long m, int n, int k, const d
   }
 }
 
+// Y (m x k) = A (m x n) M (n x k) on the FP64 tensor cores, n, k <= 128:
+// 64-row tiles; M (zero-padded to 128 columns) stays in shared memory, the A
+// tile is staged column by column (the next tile prefetched into registers
+// while this one multiplies); 16 warps = 2 row blocks x 8 column blocks, each
+// 32 rows x 16 columns (4 x 2 m8n8 tiles: 8 DMMAs per 6 fragment loads).  The
+// product tile goes back through shared memory so the global stores are
+// whole 512-byte column segments.
+constexpr int kRT = 64;        // rows per tile
+constexpr int kRPA = kRT + 4;  // pitch of a staged A / Y column (conflict-free fragment reads)
+constexpr int kRPM = kW + 4;   // pitch of a row of M
+
+__global__ void __launch_bounds__(512, 1) k_rmul_dmma(long m, int n, int k, const double* __restrict__ A,
+                                                      const double* __restrict__ M, double* __restrict__ Y) {
+  extern __shared__ double sm[];
+  double* Ms = sm;               // [kW][kRPM]: M[l][j], zero outside n x k
+  double* At = sm + kW * kRPM;   // [kW][kRPA]: A tile by column, then the Y tile by column
+  for (int e = threadIdx.x; e < kW * kW; e += blockDim.x) {
+    const int l = e / kW, j = e % kW;
+    Ms[l * kRPM + j] = (l < n && j < k) ? M[(long)j * n + l] : 0.0;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = warp & 1, wc = warp >> 1, g = lane >> 2, t4 = lane & 3;
+  const int n4 = (n + 3) / 4;
+  constexpr int kPer = kRT * kW / 512;
+  double ra[kPer];
+  auto load = [&](long rb) {
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int e = threadIdx.x + t * 512;
+      const int rr = e % kRT, l = e / kRT;
+      const long row = rb + rr;
+      ra[t] = (row < m && l < n) ? __ldg(A + (long)l * m + row) : 0.0;
+    }
+  };
+  long rb = (long)blockIdx.x * kRT;
+  if (rb < m) load(rb);
+  for (; rb < m; rb += (long)gridDim.x * kRT) {
+    __syncthreads();  // the previous tile's Y columns have been written out
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int e = threadIdx.x + t * 512;
+      At[(e / kRT) * kRPA + e % kRT] = ra[t];
+    }
+    __syncthreads();
+    const long nxt = rb + (long)gridDim.x * kRT;
+    if (nxt < m) load(nxt);
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    const double* pa = At + t4 * kRPA + 32 * wr + g;
+    const double* pb = Ms + t4 * kRPM + 16 * wc + g;
+    for (int kk = 0; kk < n4; ++kk) {
+      double va[4], vb[2];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) va[a] = pa[4 * kk * kRPA + 8 * a];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) vb[b] = pb[4 * kk * kRPM + 8 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma884(acc[a][b][0], acc[a][b][1], va[a], vb[b]);
+    }
+    __syncthreads();  // every warp is done reading the A tile
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int row = 32 * wr + 8 * a + g, j = 16 * wc + 8 * b + 2 * t4;
+        At[j * kRPA + row] = acc[a][b][0];
+        At[(j + 1) * kRPA + row] = acc[a][b][1];
+      }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kRT * k; e += blockDim.x) {
+      const int rr = e % kRT, j = e / kRT;
+      const long row = rb + rr;
+      if (row < m) Y[(long)j * m + row] = At[j * kRPA + rr];
+    }
+  }
+}
+
 // u_rho / u_iso: out[c][i] = sum_j wj U[c][j][i]
 __global__ void k_block_sum(int r, int nv, long nd, const double* __restrict__ U, const double* __restrict__ w,
                             double* __restrict__ out) {
@@ -242,6 +415,30 @@ __global__ void k_block_sum(int r, int nv, long nd, const double* __restrict__ U
 }
 
 void gram(long m, int p, int q, const double* A, const double* B, double* C_dev, cudaStream_t st) {
+  static const bool use_dmma = !(std::getenv("RTE_POD_DMMA") && std::atoi(std::getenv("RTE_POD_DMMA")) == 0);
+  if (p <= kW && q <= kW && use_dmma) {
+    // row ranges sized so the CTAs fill whole waves of the device (one CTA per SM)
+    int sms = 148, dev = 0;
+    RTE_CUDA(cudaGetDevice(&dev));
+    RTE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const long waves = std::max<long>(1, (m + (long)sms * 8192 - 1) / ((long)sms * 8192));
+    long rows = (m + sms * waves - 1) / (sms * waves);
+    rows = std::max<long>(kDR, (rows + kDR - 1) / kDR * kDR);
+    const int nch = (int)((m + rows - 1) / rows);
+    DBuf<double> part;
+    part.alloc((size_t)nch * kW * kW);
+    const int gsmem = (int)(sizeof(double) * 4 * kW * kDP);
+    static bool dcfg = false;
+    if (!dcfg) {
+      RTE_CUDA(cudaFuncSetAttribute(k_gram_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem));
+      dcfg = true;
+    }
+    k_gram_dmma<<<nch, 512, gsmem, st>>>(m, rows, p, q, A, B, part.p);
+    k_gram_wide_reduce<<<kW * kW / 256, 256, 0, st>>>(nch, p, q, part.p, C_dev);
+    RTE_CUDA(cudaGetLastError());
+    RTE_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
   if (p <= kW && q <= kW) {
     const int nch = (int)((m + kGChunk - 1) / kGChunk);
     DBuf<double> part;
@@ -280,6 +477,23 @@ std::vector<double> gram_host(long m, int p, int q, const double* A, const doubl
 void rmul(long m, int n, int k, const double* A, const std::vector<double>& M, double* Y, cudaStream_t st) {
   DBuf<double> dM;
   dM.upload(M.data(), M.size());
+  static const bool use_dmma = !(std::getenv("RTE_POD_DMMA") && std::atoi(std::getenv("RTE_POD_DMMA")) == 0);
+  if (n <= kW && k <= kW && use_dmma) {
+    const size_t smem3 = sizeof(double) * ((size_t)kW * kRPM + (size_t)kW * kRPA);
+    static bool cfg3 = false;
+    if (!cfg3) {
+      RTE_CUDA(cudaFuncSetAttribute(k_rmul_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+      cfg3 = true;
+    }
+    int sms = 148, dev = 0;
+    RTE_CUDA(cudaGetDevice(&dev));
+    RTE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const long tiles = (m + kRT - 1) / kRT;
+    k_rmul_dmma<<<(int)std::min<long>(tiles, (long)sms), 512, smem3, st>>>(m, n, k, A, dM.p, Y);
+    RTE_CUDA(cudaGetLastError());
+    RTE_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
   if (n <= kW && k <= kW) {
     const size_t smem2 = sizeof(double) * ((size_t)n * kW + (size_t)n * 64);
     static bool cfg2 = false;
