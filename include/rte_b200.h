@@ -263,7 +263,10 @@ int rte_dsa_last_iterations(const rte_ctx* ctx);
 /* Krylov iteration counts (max over the samples) of the XY DSA solves since
  * the start of the last rte_si_solve / rte_gmres_solve (or since the last
  * direct DSA call): returns the number of solves logged (0 for slabs, < 0 on
- * a device error) and writes the first min(that, cap) counts to out. */
+ * a device error) and writes the first min(that, cap) counts to out.  Inside
+ * rte_si_solve there is one entry per trip of the device loop; trips after
+ * the last sample stopped (the host polls the active count every check_every
+ * iterations) are masked and log 0. */
 int rte_dsa_iteration_log(const rte_ctx* ctx, int* out, int cap);
 /* The XY solve starts from the minimal-residual combination of the sample's
  * last solutions (a warm start; the history holds up to 8 solution vectors and

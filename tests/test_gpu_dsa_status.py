@@ -63,3 +63,24 @@ def test_fixed_iters_above_max_iters_rejected():
     R = rte()
     with pytest.raises(ValueError):
         R.si_config(R.SolveConfig(fixed_iters=5, max_iters=4), 1)
+
+
+def test_iteration_log_has_one_entry_per_correction():
+    """rte_dsa_iteration_log: the Krylov iteration count of every XY DSA solve
+    of the last rte_si_solve, one per SI iteration that applied a correction
+    (the converging iteration returns rho* without one, sisa.cpp:36-44).  The
+    device loop runs on to the next host poll of the active count
+    (check_every); those masked trips log 0."""
+    R = rte()
+    b = batch(mus=([], []))
+    d = R.DsaOperator(b)
+    d.set_tolerance(1e-10, 1000)
+    _, reps = R.sisa_solve(b, "DSA", R.SolveConfig(eps_sisa=1e-8, max_iters=100))
+    log = d.iteration_log()
+    its = max(r.iterations for r in reps)
+    assert len(log) >= its - 1
+    assert all(1 <= v <= 1000 for v in log[:its - 1]) and all(v == 0 for v in log[its - 1:])
+    # a second solve starts a new log
+    R.sisa_solve(b, "DSA", R.SolveConfig(fixed_iters=3, max_iters=3, compute_residual=False))
+    log3 = d.iteration_log()
+    assert len(log3) == 3 and all(v >= 1 for v in log3)
