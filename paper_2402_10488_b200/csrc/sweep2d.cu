@@ -710,9 +710,15 @@ __global__ void __launch_bounds__(kNW * 32, RTE_SWEEP_MINB) sweep2d_kernel(const
       ys ^= 1;
       if (threadIdx.x == 0 && band + 1 < nbands &&
           (kPub == 1 || (k0 / kC) % kPub == kPub - 1 || k0 + kC >= nsteps)) {
+        DBG_T0();
+        // the release store orders the CTA's top traces (stored before the
+        // chunk barrier above) before the new progress value
+#ifdef RTE_SWEEP_DOUBLE_FENCE
         __threadfence();
+#endif
         const int avail = min(nx, max(0, k0 + kC - 31));
         st_release(progress + ibase * nbands + band, (unsigned)avail);
+        DBG_ADD(5);
       }
     }
 #ifdef RTE_SWEEP_DEBUG_WAIT
@@ -756,8 +762,9 @@ void launch_d(const Sweep2DArgs& a, cudaStream_t st) {
     unsigned long long h[8];
     cudaStreamSynchronize(st);
     cudaMemcpyFromSymbol(h, g_dbg, sizeof(h));
-    fprintf(stderr, "sweep dbg: items %llu item-cycles %.3e prologue-wait %.3e (%.1f%%) chunk-wait %.3e (%.1f%%) polls/item %.1f\n",
-            h[3], (double)h[2], (double)h[0], 100.0 * h[0] / h[2], (double)h[1], 100.0 * h[1] / h[2], (double)h[4] / h[3]);
+    fprintf(stderr, "sweep dbg: items %llu item-cycles %.3e prologue-wait %.3e (%.1f%%) chunk-wait %.3e (%.1f%%) polls/item %.1f publish %.3e (%.1f%%)\n",
+            h[3], (double)h[2], (double)h[0], 100.0 * h[0] / h[2], (double)h[1], 100.0 * h[1] / h[2], (double)h[4] / h[3],
+            (double)h[5], 100.0 * h[5] / h[2]);
     unsigned long long z[8] = {0};
     cudaMemcpyToSymbol(g_dbg, z, sizeof(z));
   }
