@@ -147,6 +147,10 @@ CASES_2D = [
         m.CoefficientTerm(psi=lambda mu: mu[0], scattering_weight=lambda x, y: 1.0)],
         lambda x, y: np.exp(-10 * ((x - .5) ** 2 + (y - .5) ** 2))),
      70, 65, (8, 2), [[0.3], [1.5], [4.0]], (0.0, 1.0, 0.0, 1.0)),
+    # nx a multiple of the chunk width: the TMA bulk-copy staging, with inflow on all sides and a ragged top band
+    ("bulk_inflow_ragged", lambda m: prob2d_const(m, 0.6, 1.4, lambda x, y: 0.5 + x * y, inflow_left=0.9,
+                                                  inflow_bottom=0.4, inflow_right=0.6, inflow_top=0.1),
+     44, 37, (8, 4), [[]], (0.0, 1.0, 0.0, 0.8)),
 ]
 
 
