@@ -44,7 +44,10 @@ constexpr int NB = 12;  // unknowns per cell
 constexpr int NB2 = NB * NB;
 constexpr int kMaxCoarseCells = 16;
 constexpr int kMaxLevels = 16;
-constexpr int kHist = 8;  // max ring length of the K-vector warm start
+#ifndef RTE_DSA_HIST
+#define RTE_DSA_HIST 8
+#endif
+constexpr int kHist = RTE_DSA_HIST;  // max ring length of the K-vector warm start
 #ifdef RTE_DSA_FAC64
 using FacT = double;
 #else

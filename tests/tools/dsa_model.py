@@ -6,7 +6,7 @@ and a red-black 12x12 block Gauss-Seidel V-cycle mirroring dsa2d.cu, then
 measures BiCGStab/GMRES preconditioner applications and analyses the slow
 modes.  DESIGN.md section 6 quotes its results.
 
-  python tests/tools/dsa_model.py NX LEVELS [plain|aux] [mode|gmres|lines N|smoothedP W|spectrum|semicoarse|patch N|bicgstabl]
+  python tests/tools/dsa_model.py NX LEVELS [plain|aux] [mode|gmres|lines N|smoothedP W|spectrum|semicoarse|patch N|bicgstabl|idrs]
 """
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
@@ -225,6 +225,51 @@ if len(sys.argv) > 4 and sys.argv[4] == "bicgstabl":
         xv = vcycle(0, yv)
         print("BiCGStab(%d): %d preconditioner applications, true relres %.2e" %
               (ell, napp, np.linalg.norm(b - A @ xv) / np.linalg.norm(b)), flush=True)
+
+def idrs(Bop, b, s, tol=1e-8, maxit=400):
+    """IDR(s), bi-orthogonal variant (van Gijzen & Sonneveld 2011) on B y = b; returns (y, B applications)."""
+    nloc = b.size
+    y = np.zeros(nloc); r = b.copy(); nb = np.linalg.norm(b)
+    Pm = np.linalg.qr(np.random.default_rng(5).standard_normal((nloc, s)))[0]
+    G = np.zeros((nloc, s)); U = np.zeros((nloc, s)); Mm = np.eye(s); om = 1.0
+    napp = 0
+    while np.linalg.norm(r) > tol * nb and napp < maxit:
+        f = Pm.T @ r
+        done = False
+        for k in range(s):
+            cvec = np.linalg.solve(Mm[k:, k:], f[k:])
+            v = r - G[:, k:] @ cvec
+            U[:, k] = U[:, k:] @ cvec + om * v
+            G[:, k] = Bop(U[:, k]); napp += 1
+            for i in range(k):
+                al = (Pm[:, i] @ G[:, k]) / Mm[i, i]
+                G[:, k] -= al * G[:, i]; U[:, k] -= al * U[:, i]
+            Mm[k:, k] = Pm[:, k:].T @ G[:, k]
+            beta = f[k] / Mm[k, k]
+            r = r - beta * G[:, k]; y = y + beta * U[:, k]
+            if np.linalg.norm(r) <= tol * nb:
+                done = True
+                break
+            if k + 1 < s:
+                f[k + 1:] = f[k + 1:] - beta * Mm[k + 1:, k]
+        if done:
+            break
+        t = Bop(r); napp += 1
+        tr = t @ r; tn = np.linalg.norm(t); rn = np.linalg.norm(r)
+        om = tr / (tn * tn)
+        rho = abs(tr) / (tn * rn)
+        if rho < 0.7:
+            om *= 0.7 / rho
+        y = y + om * r; r = r - om * t
+    return y, napp
+
+if len(sys.argv) > 4 and sys.argv[4] == "idrs":
+    Bop = lambda v: A @ vcycle(0, v)
+    for sdim in (1, 2, 4, 8):
+        yv, napp = idrs(Bop, b, sdim)
+        xv = vcycle(0, yv)
+        print("IDR(%d): %d preconditioner applications, true relres %.2e" %
+              (sdim, napp, np.linalg.norm(b - A @ xv) / np.linalg.norm(b)), flush=True)
 
 if len(sys.argv) > 4 and sys.argv[4] == "mode":
     e = rng.standard_normal(N)
