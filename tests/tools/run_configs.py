@@ -20,6 +20,12 @@ from paper_2402_10488_b200 import configs, reports, rte
 from tests.problems import homog, pin_cell, rel_l2, two_region_slab
 
 
+# XY DSA inner tolerance of the "dsa_inner" legs (rte_si_config.dsa_inner): 1e-3 keeps every
+# C3 / C4 flux within 1e-8 of the oracle's exact-DSA solve (the bench's choice); 1e-2 matches the iteration
+# counts too but leaves 3 of 16 checked C4 fluxes at 2-3e-8
+INNER = 1e-3
+
+
 def timed(fn):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -165,8 +171,8 @@ def c3(args):
     out = {"iterations": r.iterations, "n_sweep": r.n_sweep, "final_residual": r.final_residual,
            "time_to_tol_s": t, "time_to_tol_cold_s": tc, "setup_s": tset + tdsa, "history": r.change_history}
     ((_, ireps), _, ti) = timed_warm(lambda: rte.sisa_solve(b, "DSA", rte.SolveConfig(eps_sisa=1e-8, norm="rel",
-                                                                                      dsa_inner=1e-2)), reps=1)
-    out["dsa_inner=0.01"] = {"iterations": ireps[0].iterations, "time_to_tol_s": ti,
+                                                                                      dsa_inner=INNER)), reps=1)
+    out["dsa_inner=%g" % INNER] = {"iterations": ireps[0].iterations, "time_to_tol_s": ti,
                              "history_max_rel_diff": float(np.max(np.abs(np.array(ireps[0].change_history) -
                                                                          np.array(r.change_history)) /
                                                                   np.array(r.change_history)))}
@@ -214,7 +220,7 @@ def c4(args):
     idx = list(range(0, S, max(1, S // args.parity4)))[:args.parity4] if args.parity4 > 0 else []
     table = reports.MetricsTable("c4_xy_pin_cell", [], [("snapshot_seconds", t_snap), ("pod_seconds", t_pod),
                                                          ("projection_seconds", t_b)])
-    for method, inner in (("DSA", 0.0), ("ROMSAD", 0.0), ("DSA", 1e-2), ("ROMSAD", 1e-2)):
+    for method, inner in (("DSA", 0.0), ("ROMSAD", 0.0), ("DSA", INNER), ("ROMSAD", INNER)):
         cfg = rte.SolveConfig(eps_sisa=1e-8, theta=theta, eps_romsad=eps_r, max_iters=500, dsa_inner=inner)
         ((rho, reps), tc, t) = timed_warm(lambda: rte.sisa_solve(b, method, cfg), reps=1)
         if method == "DSA" and inner == 0:
