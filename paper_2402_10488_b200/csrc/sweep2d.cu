@@ -30,6 +30,7 @@
 // reciprocal, ~66 FP64 instructions per cell-direction).  It replaces the
 // 16-double cached inverse per slot and cell of the reference.
 #include "rte_internal.cuh"
+#include <cstdint>
 #include <type_traits>
 
 namespace rte {
@@ -841,6 +842,10 @@ void launch_full(const Sweep2DArgs& a, cudaStream_t st, int dpc) {
 }
 
 void launch_sweep2d(const Sweep2DArgs& a, cudaStream_t st) {
+  // the staging copies (cp.async.bulk / 16-byte cp.async) need 16-byte aligned vectors
+  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  RTE_REQUIRE(aligned(a.rho) && aligned(a.g) && aligned(a.sig_t) && aligned(a.sig_s), RTE_ERR_INVALID,
+              "sweep2d: device vectors must be 16-byte aligned");
   const int dpc = a.nq_pad / a.groups / kNW;  // directions per lane
   if (a.mt_blk)
     launch_full<true>(a, st, dpc);

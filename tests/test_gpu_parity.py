@@ -326,3 +326,19 @@ def test_2d_dsa_history_warm_start():
     assert d.last_iterations() <= 1
     for b, x in ((b1, x1), (b2, x2), (b1, x1b), (b3, x3)):
         assert rel_l2(x[0], od.solve_density(b[0])) < 1e-9
+
+
+def test_2d_sweep_rejects_misaligned_vectors():
+    """The sweep stages its operands with 16-byte copies (TMA bulk / cp.async):
+    a device vector that is not 16-byte aligned is an invalid argument, not a
+    device fault."""
+    import torch
+    from paper_2402_10488_b200 import capi
+    name, fn, nx, ny, cl, mus, ext = CASES_2D[3]
+    _, batch = pair_2d(fn, nx, ny, cl, mus, ext)
+    buf = torch.zeros(batch.S * batch.nd + 1, dtype=torch.float64, device="cuda")
+    out = torch.zeros(batch.S * batch.nd, dtype=torch.float64, device="cuda")
+    with pytest.raises(capi.RteError, match="aligned"):
+        batch._call(capi.load().rte_apply_L, buf.data_ptr() + 8, out.data_ptr(), batch._stream())
+    batch._call(capi.load().rte_apply_L, buf.data_ptr(), out.data_ptr(), batch._stream())  # aligned: fine
+    torch.cuda.synchronize()
