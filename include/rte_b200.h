@@ -175,6 +175,9 @@ int rte_n_slots(const rte_ctx* ctx); /* unique (vx,vy) sweep slots (transport_sy
 int rte_sweep_plan(rte_ctx* ctx, int* dirs_per_lane, int* groups);
 
 /* ---- transport operator (batched over samples) -------------------------- */
+/* Device vectors are [n_samples][n_dof] doubles, contiguous, 16-byte aligned
+ * (the XY sweep stages them with 16-byte bulk copies; a misaligned pointer is
+ * RTE_ERR_INVALID). */
 /* TransportSystem::apply_L (transport_system.cpp:393-404): out = L rho. */
 int rte_apply_L(rte_ctx* ctx, const double* rho_dev, double* out_dev, void* stream);
 /* TransportSystem::assemble_rhs (transport_system.cpp:406-418): bbar. */
